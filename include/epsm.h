@@ -1,0 +1,164 @@
+/*
+ * epsm.h -- C ABI of the B200-native exact packed string matcher.
+ *
+ * Operation (Sec. 1): given a byte text t[0..n-1] and a pattern
+ * p[0..m-1] (Sec. 2), report *all* occurrences of p in t:
+ *
+ *     Occ(p, t) = { s : 0 <= s <= n-m and t[s+j] = p[j] for all 0 <= j < m }
+ *
+ * as strictly increasing uint64 start offsets, overlapping occurrences included.
+ * EPSM's procedures (EPSMa/b, Sec. 3.2-3.3) filter with a packed
+ * compare of alpha = 16 alignments per 128-bit word and then "naively check"
+ * candidates; every entry point here returns exactly Occ(p, t).
+ * Readings where the paper is silent are listed in DESIGN.md (R1-R13).
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Return value: >= 0 is success (an occurrence count where the call returns
+ *    one); < 0 is one of the EPSM_E* codes below.  epsm_strerror() names a code,
+ *    epsm_last_error() gives the calling thread's last detailed message.
+ *  - Device pointers (d_*) are caller-owned CUDA global memory on the current
+ *    device; the library never frees them.  d_text may have any alignment; it is
+ *    read only in [d_text, d_text + n) (plus, at most, the bytes of the 16-byte
+ *    aligned blocks that contain its first and last byte).  d_pos and d_occ
+ *    must be 8-byte aligned.
+ *  - Positions are written as uint64 in ascending order.  With cap < occ only
+ *    the cap smallest positions are written and the full occ is still returned
+ *    (snprintf-style), so a caller can resize and retry.  cap = 0 behaves like a
+ *    count and d_pos may then be NULL.
+ *  - stream is a cudaStream_t (NULL = the legacy default stream).  All device
+ *    work is enqueued on it.  The *_async calls return without synchronising;
+ *    the others end with one cudaStreamSynchronize(stream).
+ *  - A plan owns a small device workspace (look-back status words, 8 bytes per
+ *    16 KiB tile of text, and scratch).  One plan must not be used by two
+ *    searches that may run concurrently (e.g. on two streams); use one plan
+ *    per stream.  Plans are bound to the device of their first search.
+ *  - Maximum n: 2^38 bytes (256 GiB) per call.
+ */
+#ifndef EPSM_H
+#define EPSM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EPSM_OK       0
+#define EPSM_EINVAL  (-1)   /* NULL argument, m = 0, d_pos NULL with cap > 0, n too large */
+#define EPSM_EUNSUP  (-2)   /* m > 32 (long patterns, EPSMc territory: not built yet)    */
+#define EPSM_EALIGN  (-3)   /* d_pos or d_occ not 8-byte aligned                          */
+#define EPSM_ECUDA   (-4)   /* a CUDA runtime call or kernel launch failed                */
+#define EPSM_ENCCL   (-5)   /* NCCL missing or an NCCL call failed (sharded search)       */
+#define EPSM_ENOMEM  (-6)   /* device or pinned-host allocation failed                    */
+
+#define EPSM_MAX_M   32u
+
+typedef struct epsm_plan_s epsm_plan_t;   /* opaque, host-owned */
+typedef void *epsm_stream_t;              /* a cudaStream_t     */
+
+/*
+ * epsm_plan -- preprocessing (Sec. 3.2: B[i] = (p_i)^alpha for
+ * i < m' = min(m, 4); Sec. 3.3: the filter prefix p'; dispatch by m,
+ * PAPER.md:150-152).  Copies pattern[0..m-1] (1 <= m <= 32) into a new plan,
+ * builds the broadcast words and selects the kernel variant for m.  No device
+ * work.  *out receives the plan (caller frees with epsm_plan_free).
+ * Returns EPSM_OK, EPSM_EINVAL (NULL pattern/out, m = 0) or EPSM_EUNSUP (m > 32).
+ */
+int epsm_plan(const uint8_t *pattern, uint32_t m, epsm_plan_t **out);
+
+/* epsm_plan_free -- release a plan and its device workspace.  NULL-safe.
+ * Synchronises the plan's device before freeing device memory. */
+void epsm_plan_free(epsm_plan_t *plan);
+
+/* epsm_plan_m -- the pattern length a plan was built for (0 for NULL). */
+uint32_t epsm_plan_m(const epsm_plan_t *plan);
+
+/*
+ * epsm_count -- occ = |Occ(p, t)| (the popcount of every match mask,
+ * PAPER.md:437-439, Sec. 3.1.5) for the device text d_text[0..n-1].
+ * Returns occ >= 0 or a negative error.  Synchronises stream.
+ */
+int64_t epsm_count(epsm_plan_t *plan, const uint8_t *d_text, uint64_t n,
+                   epsm_stream_t stream);
+
+/* epsm_count_async -- as epsm_count, but leaves occ in the device uint64
+ * *d_occ and does not synchronise.  Returns EPSM_OK or a negative error. */
+int epsm_count_async(epsm_plan_t *plan, const uint8_t *d_text, uint64_t n,
+                     uint64_t *d_occ, epsm_stream_t stream);
+
+/*
+ * epsm_search -- report Occ(p, t) (the occurrences at i*alpha + {r} of
+ * PAPER.md:470 and Fig. 1, in block order) for the device text
+ * d_text[0..n-1] into d_pos[0 .. min(occ, cap)), ascending.  One pass over the
+ * text; tiles are ordered by a single-pass decoupled look-back scan.
+ * Returns occ >= 0 or a negative error.  Synchronises stream.
+ */
+int64_t epsm_search(epsm_plan_t *plan, const uint8_t *d_text, uint64_t n,
+                    uint64_t *d_pos, uint64_t cap, epsm_stream_t stream);
+
+/* epsm_search_async -- as epsm_search, but leaves occ in the device uint64
+ * *d_occ (required, 8-byte aligned) and does not synchronise. */
+int epsm_search_async(epsm_plan_t *plan, const uint8_t *d_text, uint64_t n,
+                      uint64_t *d_pos, uint64_t cap, uint64_t *d_occ,
+                      epsm_stream_t stream);
+
+/*
+ * epsm_search_host -- end-to-end convenience: h_text[0..n-1] and h_pos are HOST
+ * buffers (pinned memory gives full PCIe bandwidth; pageable works).  Copies
+ * the text to a plan-owned device buffer, runs epsm_search, and copies the
+ * first min(occ, cap) positions back into h_pos.  Returns occ or an error.
+ */
+int64_t epsm_search_host(epsm_plan_t *plan, const uint8_t *h_text, uint64_t n,
+                         uint64_t *h_pos, uint64_t cap, epsm_stream_t stream);
+
+/*
+ * epsm_search_sharded -- collective over the NCCL communicator nccl_comm
+ * (an ncclComm_t; every rank calls it with a plan for the same pattern).
+ * The global text has n_total bytes.  This rank's buffer d_shard holds global
+ * bytes [base, base + shard_len) and the rank OWNS the starts
+ * [base, base + owned_len); shard_len must be >= min(owned_len + m - 1,
+ * n_total - base) so that every owned window is inside the shard (the
+ * (m-1)-byte overlap).  Owned ranges of the ranks must partition [0, n_total).
+ * Each rank scans only its shard, the per-rank counts are all-gathered, and
+ * the positions are all-gathered (grouped ncclBroadcast, one root per rank) so
+ * that every rank's d_pos receives the first min(occ, cap) GLOBAL positions,
+ * ascending.  Returns the global occ on every rank, or a negative error.
+ * NCCL is loaded at run time (libnccl.so.2, the copy PyTorch already loaded).
+ * Synchronises stream.
+ */
+int64_t epsm_search_sharded(epsm_plan_t *plan, const uint8_t *d_shard,
+                            uint64_t base, uint64_t owned_len,
+                            uint64_t shard_len, uint64_t n_total,
+                            uint64_t *d_pos, uint64_t cap, void *nccl_comm,
+                            epsm_stream_t stream);
+
+/*
+ * epsm_search_range_async -- the local step of the sharded search, exposed so
+ * that a host runtime (e.g. torch.distributed) can do the exchange itself:
+ * scans d_shard[0..shard_len-1], reports only starts s < owned_len, and writes
+ * s + base into d_pos (first min(occ_local, cap)); occ_local goes to *d_occ.
+ */
+int epsm_search_range_async(epsm_plan_t *plan, const uint8_t *d_shard,
+                            uint64_t shard_len, uint64_t owned_len,
+                            uint64_t base, uint64_t *d_pos, uint64_t cap,
+                            uint64_t *d_occ, epsm_stream_t stream);
+
+/* epsm_strerror -- static name/description of an EPSM_E* code. */
+const char *epsm_strerror(int64_t code);
+
+/* epsm_last_error -- the calling thread's last detailed error message ("" if none). */
+const char *epsm_last_error(void);
+
+/* epsm_launch_count -- number of CUDA kernels this library has launched in the
+ * process so far (all plans, all threads); used by benchmarks to report how many
+ * of the library's kernels ran in a timed region. */
+uint64_t epsm_launch_count(void);
+
+/* epsm_version -- ABI version (major * 10000 + minor * 100 + patch). */
+int epsm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPSM_H */

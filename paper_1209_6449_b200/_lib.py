@@ -1,0 +1,303 @@
+"""Thin ctypes binding of the C ABI in include/epsm.h (argument marshalling only).
+
+Every step of the search runs in libepsm.so's sm_100a kernels; this module only
+converts torch tensors / numpy arrays / CUDA streams into the pointers and sizes
+the C calls take.  There is no CPU fallback: if libepsm.so is missing the import
+fails, and on a machine without a GPU the calls raise EpsmError(EPSM_ECUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libepsm.so")
+
+EPSM_OK = 0
+EPSM_EINVAL = -1
+EPSM_EUNSUP = -2
+EPSM_EALIGN = -3
+EPSM_ECUDA = -4
+EPSM_ENCCL = -5
+EPSM_ENOMEM = -6
+MAX_M = 32
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: the CUDA extension was not built "
+        "(run `python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_u64 = ctypes.c_uint64
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+_lib.epsm_plan.argtypes = [_vp, ctypes.c_uint32, ctypes.POINTER(_vp)]
+_lib.epsm_plan.restype = ctypes.c_int
+_lib.epsm_plan_free.argtypes = [_vp]
+_lib.epsm_plan_free.restype = None
+_lib.epsm_plan_m.argtypes = [_vp]
+_lib.epsm_plan_m.restype = ctypes.c_uint32
+_lib.epsm_count.argtypes = [_vp, _vp, _u64, _vp]
+_lib.epsm_count.restype = _i64
+_lib.epsm_count_async.argtypes = [_vp, _vp, _u64, _vp, _vp]
+_lib.epsm_count_async.restype = ctypes.c_int
+_lib.epsm_search.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
+_lib.epsm_search.restype = _i64
+_lib.epsm_search_async.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp, _vp]
+_lib.epsm_search_async.restype = ctypes.c_int
+_lib.epsm_search_host.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
+_lib.epsm_search_host.restype = _i64
+_lib.epsm_search_sharded.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _u64, _vp, _vp]
+_lib.epsm_search_sharded.restype = _i64
+_lib.epsm_search_range_async.argtypes = [_vp, _vp, _u64, _u64, _u64, _vp, _u64, _vp, _vp]
+_lib.epsm_search_range_async.restype = ctypes.c_int
+_lib.epsm_strerror.argtypes = [_i64]
+_lib.epsm_strerror.restype = ctypes.c_char_p
+_lib.epsm_last_error.argtypes = []
+_lib.epsm_last_error.restype = ctypes.c_char_p
+_lib.epsm_launch_count.argtypes = []
+_lib.epsm_launch_count.restype = _u64
+_lib.epsm_version.argtypes = []
+_lib.epsm_version.restype = ctypes.c_int
+
+EXPORTED_SYMBOLS = (
+    "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
+    "epsm_search", "epsm_search_async", "epsm_search_host", "epsm_search_sharded",
+    "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
+    "epsm_version",
+)
+
+
+class EpsmError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = int(code)
+        detail = _lib.epsm_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {strerror(code)}" + (f" ({detail})" if detail else ""))
+
+
+def strerror(code: int) -> str:
+    return _lib.epsm_strerror(int(code)).decode()
+
+
+def launch_count() -> int:
+    """Kernels libepsm.so has launched in this process so far."""
+    return int(_lib.epsm_launch_count())
+
+
+def version() -> int:
+    return int(_lib.epsm_version())
+
+
+def _check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise EpsmError(rc, where)
+    return rc
+
+
+def _pattern_bytes(pattern) -> bytes:
+    if isinstance(pattern, (bytes, bytearray, memoryview)):
+        return bytes(pattern)
+    if isinstance(pattern, str):
+        return pattern.encode()
+    if isinstance(pattern, torch.Tensor):
+        return pattern.detach().cpu().contiguous().numpy().astype(np.uint8).tobytes()
+    return np.asarray(pattern, dtype=np.uint8).tobytes()
+
+
+class Plan:
+    """epsm_plan(): the preprocessed pattern plus workspace."""
+
+    def __init__(self, pattern):
+        self.pattern = _pattern_bytes(pattern)
+        h = _vp()
+        buf = ctypes.create_string_buffer(self.pattern, max(len(self.pattern), 1))
+        _check(_lib.epsm_plan(buf if self.pattern else None, len(self.pattern), ctypes.byref(h)), "epsm_plan")
+        self._h = h
+
+    @property
+    def m(self) -> int:
+        return len(self.pattern)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("plan is closed")
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.epsm_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def plan(pattern) -> Plan:
+    return Plan(pattern)
+
+
+def _as_plan(p) -> Plan:
+    return p if isinstance(p, Plan) else Plan(p)
+
+
+def _stream_handle(stream, device) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _check_text(text: torch.Tensor):
+    if not isinstance(text, torch.Tensor) or text.dtype != torch.uint8 or not text.is_cuda:
+        raise TypeError("text must be a CUDA torch.uint8 tensor")
+    if not text.is_contiguous():
+        raise ValueError("text must be contiguous")
+
+
+def _check_out(out: torch.Tensor | None, name: str):
+    if out is None:
+        return
+    if not isinstance(out, torch.Tensor) or out.dtype not in (torch.int64, torch.uint64) or not out.is_cuda:
+        raise TypeError(f"{name} must be a CUDA int64/uint64 tensor")
+    if not out.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def count(p, text: torch.Tensor, stream=None) -> int:
+    """|Occ(p, text)| for a CUDA uint8 text (synchronises the stream)."""
+    pl = _as_plan(p)
+    _check_text(text)
+    return _check(_lib.epsm_count(pl.handle, text.data_ptr(), text.numel(),
+                                  _stream_handle(stream, text.device)), "epsm_count")
+
+
+def count_async(p: Plan, text: torch.Tensor, occ_out: torch.Tensor, stream=None) -> None:
+    _check_text(text)
+    _check_out(occ_out, "occ_out")
+    _check(_lib.epsm_count_async(p.handle, text.data_ptr(), text.numel(), occ_out.data_ptr(),
+                                 _stream_handle(stream, text.device)), "epsm_count_async")
+
+
+def search(p, text: torch.Tensor, out: torch.Tensor | None = None, cap: int | None = None, stream=None):
+    """Occurrences of the plan's pattern in ``text``.
+
+    Returns ``(positions, occ)``: ``positions`` is the int64 CUDA tensor view
+    ``out[:min(occ, cap)]`` (ascending), ``occ`` the full count.  Without ``out``
+    a buffer is allocated (and grown once if it was too small)."""
+    pl = _as_plan(p)
+    _check_text(text)
+    n = text.numel()
+    strm = _stream_handle(stream, text.device)
+    auto = out is None
+    if auto:
+        nst = max(0, n - pl.m + 1)
+        size = min(nst, int(cap)) if cap is not None else min(nst, 1 << 16)
+        out = torch.empty(size, dtype=torch.int64, device=text.device)
+    _check_out(out, "out")
+    c = out.numel() if cap is None else min(int(cap), out.numel())
+    occ = _check(_lib.epsm_search(pl.handle, text.data_ptr(), n, out.data_ptr() if c else None, c, strm),
+                 "epsm_search")
+    if auto and cap is None and occ > c:
+        out = torch.empty(occ, dtype=torch.int64, device=text.device)
+        c = occ
+        occ = _check(_lib.epsm_search(pl.handle, text.data_ptr(), n, out.data_ptr(), c, strm), "epsm_search")
+    return out[: min(occ, c)], occ
+
+
+def find_all(pattern, text: torch.Tensor) -> torch.Tensor:
+    """All occurrence positions (int64 CUDA tensor, ascending)."""
+    pos, _ = search(pattern, text)
+    return pos
+
+
+def search_async(p: Plan, text: torch.Tensor, out: torch.Tensor | None, occ_out: torch.Tensor,
+                 cap: int | None = None, stream=None) -> None:
+    """Enqueue a search; occ lands in occ_out[0] (device), positions in out."""
+    _check_text(text)
+    _check_out(out, "out")
+    _check_out(occ_out, "occ_out")
+    c = 0 if out is None else (out.numel() if cap is None else min(int(cap), out.numel()))
+    _check(_lib.epsm_search_async(p.handle, text.data_ptr(), text.numel(),
+                                  out.data_ptr() if (out is not None and c) else None, c,
+                                  occ_out.data_ptr(), _stream_handle(stream, text.device)),
+           "epsm_search_async")
+
+
+def search_range_async(p: Plan, shard: torch.Tensor, owned_len: int, base: int,
+                       out: torch.Tensor | None, occ_out: torch.Tensor, cap: int | None = None,
+                       stream=None) -> None:
+    """Local step of a sharded search: starts s < owned_len of ``shard``, reported as s + base."""
+    _check_text(shard)
+    _check_out(out, "out")
+    _check_out(occ_out, "occ_out")
+    c = 0 if out is None else (out.numel() if cap is None else min(int(cap), out.numel()))
+    _check(_lib.epsm_search_range_async(p.handle, shard.data_ptr(), shard.numel(), int(owned_len), int(base),
+                                        out.data_ptr() if (out is not None and c) else None, c,
+                                        occ_out.data_ptr(), _stream_handle(stream, shard.device)),
+           "epsm_search_range_async")
+
+
+def _host_ptr_len(a, dtype):
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or not a.is_contiguous():
+            raise TypeError("host buffers must be contiguous CPU tensors or numpy arrays")
+        return a.data_ptr(), a.numel()
+    arr = np.asarray(a)
+    if arr.dtype != dtype or not arr.flags["C_CONTIGUOUS"]:
+        raise TypeError(f"host buffer must be a contiguous {dtype} array")
+    return arr.ctypes.data, arr.size
+
+
+def search_host(p, host_text, host_out=None, cap: int | None = None, stream=None) -> int:
+    """epsm_search_host: host text in, host positions out (copies inside).  Returns occ."""
+    pl = _as_plan(p)
+    tp, n = _host_ptr_len(host_text, np.uint8)
+    if host_out is None:
+        op, c = None, 0
+    else:
+        op, c = _host_ptr_len(host_out, np.uint64)
+        if cap is not None:
+            c = min(c, int(cap))
+    strm = _stream_handle(stream, None) if torch.cuda.is_available() else (stream or 0)
+    return _check(_lib.epsm_search_host(pl.handle, tp, n, op if c else None, c, strm), "epsm_search_host")
+
+
+def nccl_comm_ptr(group=None) -> int:
+    """The ncclComm_t behind a torch.distributed NCCL process group."""
+    import torch.distributed as dist
+    g = group or dist.group.WORLD
+    backend = g._get_backend(torch.device("cuda"))
+    return int(backend._comm_ptr())
+
+
+def search_sharded(p, shard: torch.Tensor, base: int, owned_len: int, n_total: int,
+                   out: torch.Tensor | None = None, cap: int | None = None, group=None,
+                   nccl_comm: int | None = None, stream=None) -> int:
+    """epsm_search_sharded over a torch.distributed NCCL group (collective).
+
+    Every rank ends with the first min(occ, cap) global positions in ``out``."""
+    pl = _as_plan(p)
+    _check_text(shard)
+    _check_out(out, "out")
+    comm = nccl_comm if nccl_comm is not None else nccl_comm_ptr(group)
+    c = 0 if out is None else (out.numel() if cap is None else min(int(cap), out.numel()))
+    return _check(_lib.epsm_search_sharded(pl.handle, shard.data_ptr(), int(base), int(owned_len),
+                                           shard.numel(), int(n_total),
+                                           out.data_ptr() if (out is not None and c) else None, c,
+                                           comm, _stream_handle(stream, shard.device)),
+                  "epsm_search_sharded")

@@ -1,0 +1,434 @@
+// epsm.cu -- host side of the C ABI declared in include/epsm.h.
+//
+// Plan construction (preprocessing, PAPER.md:453-457 / 492, dispatch by m
+// PAPER.md:150-152), workspace management, kernel dispatch and the host-buffer
+// convenience call.  The sharded (NCCL) call lives in epsm_sharded.cu.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <new>
+
+#include "epsm.h"
+#include "epsm_internal.h"
+#include "epsm_kernels.cuh"
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+std::atomic<uint64_t> g_launches{0};
+
+using KernelFn = void (*)(epsm::KParams);
+
+template <int F, int MW>
+constexpr KernelFn pick(bool search) {
+  return search ? &epsm::epsm_scan_kernel<F, MW, true> : &epsm::epsm_scan_kernel<F, MW, false>;
+}
+
+// Kernel variant for a pattern of length m: F = min(m, 4) filter bytes, MW = ceil(m/4)
+// words checked (no verification when m <= 4: the filter is exact).
+KernelFn kernel_for(uint32_t m, bool search) {
+  switch (m) {
+    case 1: return pick<1, 1>(search);
+    case 2: return pick<2, 1>(search);
+    case 3: return pick<3, 1>(search);
+    case 4: return pick<4, 1>(search);
+    default: break;
+  }
+  switch ((m + 3) / 4) {
+    case 2: return pick<4, 2>(search);
+    case 3: return pick<4, 3>(search);
+    case 4: return pick<4, 4>(search);
+    case 5: return pick<4, 5>(search);
+    case 6: return pick<4, 6>(search);
+    case 7: return pick<4, 7>(search);
+    default: return pick<4, 8>(search);
+  }
+}
+
+}  // namespace
+
+void epsm_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+int epsm_cuda_fail(cudaError_t e, const char* what) {
+  epsm_set_error("%s: %s", what, cudaGetErrorString(e));
+  return EPSM_ECUDA;
+}
+
+void epsm_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Bind the calling thread to the device that owns ptr (torch and this library each
+// carry their own CUDA runtime; the pointer is the unambiguous source of truth).
+int epsm_bind_device(epsm_plan_t* plan, const void* dptr) {
+  int dev = -1;
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, dptr);
+  if (e == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+    dev = attr.device;
+  } else {
+    cudaGetLastError();
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaGetDevice");
+  }
+  if (plan->device < 0) plan->device = dev;
+  if (plan->device != dev) {
+    epsm_set_error("plan is bound to device %d but the buffer is on device %d", plan->device, dev);
+    return EPSM_EINVAL;
+  }
+  e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaSetDevice");
+  return EPSM_OK;
+}
+
+static int ensure_status(epsm_plan_t* plan, uint64_t tiles, cudaStream_t s) {
+  if (tiles > plan->status_cap) {
+    if (plan->d_status) {
+      cudaStreamSynchronize(s);
+      cudaFree(plan->d_status);
+      plan->d_status = nullptr;
+      plan->status_cap = 0;
+    }
+    uint64_t cap = tiles < 4096 ? 4096 : tiles;
+    cudaError_t e = cudaMalloc(&plan->d_status, cap * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+      epsm_set_error("cudaMalloc(status, %llu tiles): %s", (unsigned long long)cap, cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    e = cudaMemsetAsync(plan->d_status, 0, cap * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
+    plan->status_cap = cap;
+    plan->epoch = 0;
+  }
+  // next epoch; on wrap clear the words so stale tags can never match
+  plan->epoch = (plan->epoch + 1) & 0xFFFFFFu;
+  if (plan->epoch == 0) {
+    cudaError_t e = cudaMemsetAsync(plan->d_status, 0, plan->status_cap * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
+    plan->epoch = 1;
+  }
+  return EPSM_OK;
+}
+
+int epsm_ensure_occ(epsm_plan_t* plan) {
+  if (plan->d_occ) return EPSM_OK;
+  cudaError_t e = cudaMalloc(&plan->d_occ, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    epsm_set_error("cudaMalloc(occ): %s", cudaGetErrorString(e));
+    return EPSM_ENOMEM;
+  }
+  e = cudaMallocHost(&plan->h_occ, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    epsm_set_error("cudaMallocHost(occ): %s", cudaGetErrorString(e));
+    return EPSM_ENOMEM;
+  }
+  return EPSM_OK;
+}
+
+// Core launcher.  The device text is d_text[0..nbytes-1]; starts [0, nstarts) are
+// reported (nstarts <= nbytes - m + 1), each shifted by `base`.
+int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
+                uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s) {
+  if (nstarts == 0) {
+    cudaError_t e = cudaMemsetAsync(d_occ, 0, sizeof(unsigned long long), s);
+    return e == cudaSuccess ? EPSM_OK : epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
+  }
+  const uint64_t mis = reinterpret_cast<uintptr_t>(d_text) & 15u;
+  epsm::KParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.text = d_text - mis;
+  P.nbytes = nbytes + mis;
+  P.s_lo = mis;
+  P.s_hi = mis + nstarts;
+  P.pos_bias = base - mis;
+  P.pos = d_pos;
+  P.cap = d_pos ? cap : 0;
+  P.occ = d_occ;
+  std::memcpy(P.bcast, plan->bcast, sizeof(P.bcast));
+  std::memcpy(P.pat, plan->pat, sizeof(P.pat));
+  std::memcpy(P.pmask, plan->pmask, sizeof(P.pmask));
+  const uint64_t tiles = (P.s_hi + epsm::kTileBytes - 1) / epsm::kTileBytes;
+  if (tiles > 0x7FFFFFFFull) {
+    epsm_set_error("text too large: %llu tiles", (unsigned long long)tiles);
+    return EPSM_EINVAL;
+  }
+  int rc;
+  if (search) {
+    rc = ensure_status(plan, tiles, s);
+    if (rc) return rc;
+    P.status = plan->d_status;
+    P.tag = static_cast<unsigned long long>(plan->epoch) << epsm::kEpochShift;
+  } else {
+    cudaError_t e = cudaMemsetAsync(d_occ, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
+  }
+  KernelFn fn = kernel_for(plan->m, search);
+  fn<<<static_cast<unsigned>(tiles), epsm::kThreads, epsm::kSmemBytes, s>>>(P);
+  epsm_count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
+  return EPSM_OK;
+}
+
+static bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+static int check_common(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n) {
+  if (!plan) {
+    epsm_set_error("NULL plan");
+    return EPSM_EINVAL;
+  }
+  if (!d_text && n > 0) {
+    epsm_set_error("NULL text with n > 0");
+    return EPSM_EINVAL;
+  }
+  if (n > (1ull << 38)) {
+    epsm_set_error("n = %llu exceeds 2^38", (unsigned long long)n);
+    return EPSM_EINVAL;
+  }
+  return EPSM_OK;
+}
+
+static uint64_t n_starts(uint32_t m, uint64_t n) { return n >= m ? n - m + 1 : 0; }
+
+extern "C" {
+
+int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
+  if (!out) {
+    epsm_set_error("NULL out");
+    return EPSM_EINVAL;
+  }
+  *out = nullptr;
+  if (!pattern || m == 0) {
+    epsm_set_error("pattern must be non-NULL with m >= 1");
+    return EPSM_EINVAL;
+  }
+  if (m > EPSM_MAX_M) {
+    epsm_set_error("m = %u > %u is not supported (long-pattern filter not built)", m, EPSM_MAX_M);
+    return EPSM_EUNSUP;
+  }
+  epsm_plan_t* p = new (std::nothrow) epsm_plan_t();
+  if (!p) return EPSM_ENOMEM;
+  p->m = m;
+  std::memcpy(p->pattern, pattern, m);
+  // B[i] = (p_i)^alpha restricted to one 32-bit lane, i < min(m, 4)
+  for (uint32_t i = 0; i < 4; ++i) p->bcast[i] = i < m ? 0x01010101u * pattern[i] : 0u;
+  // P_i blocks, zero padded, as little-endian words + byte masks
+  for (uint32_t q = 0; q < 9; ++q) {
+    uint32_t w = 0, mk = 0;
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t idx = 4 * q + b;
+      if (idx < m) {
+        w |= static_cast<uint32_t>(pattern[idx]) << (8 * b);
+        mk |= 0xFFu << (8 * b);
+      }
+    }
+    p->pat[q] = w;
+    p->pmask[q] = mk;
+  }
+  p->device = -1;
+  *out = p;
+  return EPSM_OK;
+}
+
+void epsm_plan_free(epsm_plan_t* plan) {
+  if (!plan) return;
+  if (plan->device >= 0) {
+    cudaSetDevice(plan->device);
+    cudaDeviceSynchronize();
+  }
+  if (plan->d_status) cudaFree(plan->d_status);
+  if (plan->d_occ) cudaFree(plan->d_occ);
+  if (plan->h_occ) cudaFreeHost(plan->h_occ);
+  if (plan->d_text_buf) cudaFree(plan->d_text_buf);
+  if (plan->d_pos_buf) cudaFree(plan->d_pos_buf);
+  if (plan->d_scratch) cudaFree(plan->d_scratch);
+  if (plan->d_counts) cudaFree(plan->d_counts);
+  if (plan->h_counts) cudaFreeHost(plan->h_counts);
+  delete plan;
+}
+
+uint32_t epsm_plan_m(const epsm_plan_t* plan) { return plan ? plan->m : 0; }
+
+int epsm_count_async(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint64_t* d_occ, epsm_stream_t stream) {
+  int rc = check_common(plan, d_text, n);
+  if (rc) return rc;
+  if (!d_occ || !aligned8(d_occ)) {
+    epsm_set_error("d_occ must be a non-NULL 8-byte aligned device pointer");
+    return d_occ ? EPSM_EALIGN : EPSM_EINVAL;
+  }
+  rc = epsm_bind_device(plan, d_occ);
+  if (rc) return rc;
+  return epsm_launch(plan, d_text, n, n_starts(plan->m, n), 0, nullptr, 0,
+                     reinterpret_cast<unsigned long long*>(d_occ), false, static_cast<cudaStream_t>(stream));
+}
+
+int64_t epsm_count(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, epsm_stream_t stream) {
+  int rc = check_common(plan, d_text, n);
+  if (rc) return rc;
+  rc = epsm_bind_device(plan, d_text ? (const void*)d_text : nullptr);
+  if (rc) return rc;
+  rc = epsm_ensure_occ(plan);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rc = epsm_launch(plan, d_text, n, n_starts(plan->m, n), 0, nullptr, 0, plan->d_occ, false, s);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(plan->h_occ, plan->d_occ, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_count");
+  return static_cast<int64_t>(plan->h_occ[0]);
+}
+
+int epsm_search_async(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint64_t* d_pos, uint64_t cap,
+                      uint64_t* d_occ, epsm_stream_t stream) {
+  int rc = check_common(plan, d_text, n);
+  if (rc) return rc;
+  if (!d_occ || (cap > 0 && !d_pos)) {
+    epsm_set_error("d_occ required; d_pos required when cap > 0");
+    return EPSM_EINVAL;
+  }
+  if (!aligned8(d_occ) || (d_pos && !aligned8(d_pos))) {
+    epsm_set_error("d_pos and d_occ must be 8-byte aligned");
+    return EPSM_EALIGN;
+  }
+  rc = epsm_bind_device(plan, d_occ);
+  if (rc) return rc;
+  return epsm_launch(plan, d_text, n, n_starts(plan->m, n), 0, cap ? d_pos : nullptr, cap,
+                     reinterpret_cast<unsigned long long*>(d_occ), true, static_cast<cudaStream_t>(stream));
+}
+
+int epsm_search_range_async(epsm_plan_t* plan, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,
+                            uint64_t base, uint64_t* d_pos, uint64_t cap, uint64_t* d_occ, epsm_stream_t stream) {
+  int rc = check_common(plan, d_shard, shard_len);
+  if (rc) return rc;
+  if (!d_occ || (cap > 0 && !d_pos)) {
+    epsm_set_error("d_occ required; d_pos required when cap > 0");
+    return EPSM_EINVAL;
+  }
+  if (!aligned8(d_occ) || (d_pos && !aligned8(d_pos))) {
+    epsm_set_error("d_pos and d_occ must be 8-byte aligned");
+    return EPSM_EALIGN;
+  }
+  rc = epsm_bind_device(plan, d_occ);
+  if (rc) return rc;
+  uint64_t ns = n_starts(plan->m, shard_len);
+  if (owned_len < ns) ns = owned_len;
+  return epsm_launch(plan, d_shard, shard_len, ns, base, cap ? d_pos : nullptr, cap,
+                     reinterpret_cast<unsigned long long*>(d_occ), true, static_cast<cudaStream_t>(stream));
+}
+
+int64_t epsm_search(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint64_t* d_pos, uint64_t cap,
+                    epsm_stream_t stream) {
+  int rc = check_common(plan, d_text, n);
+  if (rc) return rc;
+  if (cap > 0 && !d_pos) {
+    epsm_set_error("d_pos required when cap > 0");
+    return EPSM_EINVAL;
+  }
+  if (d_pos && !aligned8(d_pos)) {
+    epsm_set_error("d_pos must be 8-byte aligned");
+    return EPSM_EALIGN;
+  }
+  rc = epsm_bind_device(plan, d_text ? (const void*)d_text : (const void*)d_pos);
+  if (rc) return rc;
+  rc = epsm_ensure_occ(plan);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rc = epsm_launch(plan, d_text, n, n_starts(plan->m, n), 0, cap ? d_pos : nullptr, cap, plan->d_occ, true, s);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(plan->h_occ, plan->d_occ, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_search");
+  return static_cast<int64_t>(plan->h_occ[0]);
+}
+
+int64_t epsm_search_host(epsm_plan_t* plan, const uint8_t* h_text, uint64_t n, uint64_t* h_pos, uint64_t cap,
+                         epsm_stream_t stream) {
+  int rc = check_common(plan, h_text, n);
+  if (rc) return rc;
+  if (cap > 0 && !h_pos) {
+    epsm_set_error("h_pos required when cap > 0");
+    return EPSM_EINVAL;
+  }
+  if (plan->device < 0) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaGetDevice");
+    plan->device = dev;
+  }
+  cudaError_t e = cudaSetDevice(plan->device);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaSetDevice");
+  rc = epsm_ensure_occ(plan);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n > plan->text_cap) {
+    if (plan->d_text_buf) {
+      cudaStreamSynchronize(s);
+      cudaFree(plan->d_text_buf);
+      plan->d_text_buf = nullptr;
+      plan->text_cap = 0;
+    }
+    e = cudaMalloc(&plan->d_text_buf, n);
+    if (e != cudaSuccess) {
+      epsm_set_error("cudaMalloc(text, %llu): %s", (unsigned long long)n, cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    plan->text_cap = n;
+  }
+  if (cap > plan->pos_cap) {
+    if (plan->d_pos_buf) {
+      cudaStreamSynchronize(s);
+      cudaFree(plan->d_pos_buf);
+      plan->d_pos_buf = nullptr;
+      plan->pos_cap = 0;
+    }
+    e = cudaMalloc(&plan->d_pos_buf, cap * sizeof(uint64_t));
+    if (e != cudaSuccess) {
+      epsm_set_error("cudaMalloc(pos, %llu): %s", (unsigned long long)cap, cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    plan->pos_cap = cap;
+  }
+  if (n) {
+    e = cudaMemcpyAsync(plan->d_text_buf, h_text, n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(H2D text)");
+  }
+  rc = epsm_launch(plan, plan->d_text_buf, n, n_starts(plan->m, n), 0, cap ? plan->d_pos_buf : nullptr, cap,
+                   plan->d_occ, true, s);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(plan->h_occ, plan->d_occ, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_search_host");
+  const uint64_t occ = plan->h_occ[0];
+  const uint64_t k = occ < cap ? occ : cap;
+  if (k) {
+    e = cudaMemcpyAsync(h_pos, plan->d_pos_buf, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(D2H positions)");
+  }
+  return static_cast<int64_t>(occ);
+}
+
+const char* epsm_strerror(int64_t code) {
+  switch (code) {
+    case EPSM_OK: return "EPSM_OK: success";
+    case EPSM_EINVAL: return "EPSM_EINVAL: invalid argument";
+    case EPSM_EUNSUP: return "EPSM_EUNSUP: unsupported pattern length (m > 32)";
+    case EPSM_EALIGN: return "EPSM_EALIGN: misaligned output pointer (needs 8-byte alignment)";
+    case EPSM_ECUDA: return "EPSM_ECUDA: CUDA error";
+    case EPSM_ENCCL: return "EPSM_ENCCL: NCCL error";
+    case EPSM_ENOMEM: return "EPSM_ENOMEM: out of memory";
+    default: return code > 0 ? "success (count)" : "unknown error";
+  }
+}
+
+const char* epsm_last_error(void) { return g_last_error; }
+
+uint64_t epsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int epsm_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// epsm_internal.h -- plan layout and helpers shared by the host translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "epsm.h"
+
+struct epsm_plan_s {
+  uint32_t m = 0;
+  uint8_t pattern[EPSM_MAX_M] = {};
+  uint32_t bcast[4] = {};   // B_i = p_i * 0x01010101
+  uint32_t pat[9] = {};     // zero-padded pattern words
+  uint32_t pmask[9] = {};   // byte masks of the words
+  int device = -1;          // bound on first device use
+  // look-back workspace (one status word per tile), epoch-tagged
+  unsigned long long* d_status = nullptr;
+  uint64_t status_cap = 0;
+  uint32_t epoch = 0;
+  // occ readback for the synchronous calls
+  unsigned long long* d_occ = nullptr;
+  unsigned long long* h_occ = nullptr;
+  // epsm_search_host buffers
+  uint8_t* d_text_buf = nullptr;
+  uint64_t text_cap = 0;
+  uint64_t* d_pos_buf = nullptr;
+  uint64_t pos_cap = 0;
+  // epsm_search_sharded scratch
+  uint64_t* d_scratch = nullptr;
+  uint64_t scratch_cap = 0;
+  unsigned long long* d_counts = nullptr;   // [nranks] + [1] local occ
+  unsigned long long* h_counts = nullptr;
+  int counts_cap = 0;
+};
+
+void epsm_set_error(const char* fmt, ...);
+int epsm_cuda_fail(cudaError_t e, const char* what);
+int epsm_bind_device(epsm_plan_t* plan, const void* dptr);
+int epsm_ensure_occ(epsm_plan_t* plan);
+int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
+                uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s);

@@ -1,0 +1,105 @@
+"""Data parallelism over the text (BASELINE.json north_star multi-GPU path).
+
+The paper is single-threaded; sharding is this build's reading R11:
+
+* the text of n bytes is cut into P contiguous pieces at 16-byte aligned
+  boundaries base_r = round_down_16(r * n / P) (base_P = n);
+* rank r OWNS the starts [base_r, base_{r+1}) and holds the bytes
+  [base_r, min(n, base_{r+1} + halo)) with halo >= m - 1 (a fixed 31-byte halo
+  serves every m <= 32), so every owned window lies inside its shard;
+* every start belongs to exactly one rank, so the union of the per-rank
+  occurrence sets is Occ(p, t) with no duplicates and no misses, and
+  concatenating them in rank order keeps them sorted.
+
+The exchange (counts, then positions) is the only collective.  This module
+implements it with torch.distributed, so the same host logic runs over NCCL on
+GPUs and over gloo on CPUs (tests/test_sharding.py).  The C ABI's
+epsm_search_sharded does the same exchange natively with NCCL.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+ALIGN = 16
+MAX_HALO = 31   # m - 1 for the largest supported m (32)
+
+
+def shard_base(n_total: int, world: int, rank: int) -> int:
+    if rank >= world:
+        return n_total
+    return (rank * n_total // world) // ALIGN * ALIGN
+
+
+def shard_layout(n_total: int, world: int, rank: int, halo: int = MAX_HALO):
+    """(base, owned_len, shard_len) of ``rank``: owned starts [base, base+owned_len),
+    bytes [base, base+shard_len)."""
+    base = shard_base(n_total, world, rank)
+    nxt = shard_base(n_total, world, rank + 1)
+    owned = nxt - base
+    shard_len = min(n_total - base, owned + halo)
+    return base, owned, shard_len
+
+
+def all_layouts(n_total: int, world: int, halo: int = MAX_HALO):
+    return [shard_layout(n_total, world, r, halo) for r in range(world)]
+
+
+def exchange_positions(local_pos: torch.Tensor, local_occ: int, group=None, cap: int | None = None):
+    """All-gather per-rank counts, then the per-rank position lists.
+
+    ``local_pos`` holds this rank's first min(local_occ, len) GLOBAL positions
+    (ascending).  Returns (positions, occ) with positions = the first
+    min(occ, cap) global positions in rank order, identical on every rank."""
+    world = dist.get_world_size(group)
+    dev = local_pos.device
+    cnt = torch.tensor([int(local_occ)], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    occ = sum(counts)
+    cap = occ if cap is None else min(int(cap), occ)
+    keep, off = [], 0
+    for c in counts:
+        keep.append(max(0, min(c, cap - off)))
+        off += c
+    width = max(keep) if keep else 0
+    if width == 0:
+        return local_pos.new_empty(0), occ
+    me = dist.get_rank(group)
+    send = torch.zeros(width, dtype=torch.int64, device=dev)
+    if keep[me]:
+        send[: keep[me]] = local_pos[: keep[me]].to(torch.int64)
+    recv = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(recv, send, group=group)
+    out = torch.cat([r[:k] for r, k in zip(recv, keep)])
+    return out, occ
+
+
+def search_sharded_torch(shard: torch.Tensor, base: int, owned_len: int, n_total: int, local_search,
+                         group=None, cap: int | None = None):
+    """Sharded search with the exchange done by torch.distributed.
+
+    ``local_search(shard, owned_len, base) -> (global_positions, occ_local)`` is the
+    per-rank scan (the CUDA path via ``local_search_cuda``; tests may inject the
+    oracle to exercise this host logic on CPU)."""
+    pos, occ_local = local_search(shard, owned_len, base)
+    return exchange_positions(pos, occ_local, group=group, cap=cap)
+
+
+def local_search_cuda(plan):
+    """The per-rank scan through the C ABI (epsm_search_range_async)."""
+    from . import _lib
+
+    def run(shard: torch.Tensor, owned_len: int, base: int):
+        occ_dev = torch.zeros(1, dtype=torch.int64, device=shard.device)
+        nst = max(0, min(owned_len, shard.numel() - plan.m + 1))
+        out = torch.empty(min(nst, 1 << 20), dtype=torch.int64, device=shard.device)
+        _lib.search_range_async(plan, shard, owned_len, base, out, occ_dev)
+        occ = int(occ_dev.item())
+        if occ > out.numel():
+            out = torch.empty(occ, dtype=torch.int64, device=shard.device)
+            _lib.search_range_async(plan, shard, owned_len, base, out, occ_dev)
+        return out[:occ], occ
+
+    return run

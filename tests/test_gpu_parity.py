@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: bit-exact positions and counts (integer/index work).  Sizes span several
+16 KiB tiles with ragged tails; every unit/tile alignment is hit by rotating the
+text's base address; edge cases cover n < m, n = 0, m = 1 and 32, dense output,
+cap truncation and misaligned text pointers.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TILE = 16384
+
+
+@pytest.fixture(scope="module")
+def epsm():
+    import paper_1209_6449_b200 as e
+    return e
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda:0")
+
+
+def gpu_search(epsm, pattern, text_dev, cap=None):
+    pos, occ = epsm.search(pattern, text_dev, cap=cap)
+    return pos.cpu().numpy().astype(np.uint64), occ
+
+
+def check(epsm, pattern, text_np, text_dev, label=""):
+    got, occ = gpu_search(epsm, pattern, text_dev)
+    want = oracle.search(pattern, text_np)
+    assert occ == want.size, (label, pattern, occ, want.size)
+    if not np.array_equal(got, want):
+        bad = np.flatnonzero(got[: min(got.size, want.size)] != want[: min(got.size, want.size)])
+        raise AssertionError(f"{label} m={len(pattern)} first mismatch at index {bad[:5]}")
+    return occ
+
+
+def test_paper_wsmatch_figure_on_gpu(epsm, dev):
+    """b = [1010,0111,1010] occurs in a at {1, 5}."""
+    a = bytes([0b0110, 0b1010, 0b0111, 0b1010, 0b0100, 0b1010, 0b0111, 0b1010, 0b0000, 0b1010, 0b0100, 0b0010])
+    b = bytes([0b1010, 0b0111, 0b1010])
+    t = torch.tensor(list(a), dtype=torch.uint8, device=dev)
+    got, occ = gpu_search(epsm, b, t)
+    assert got.tolist() == [1, 5] and occ == 2
+
+
+def test_exhaustive_binary_concatenated_all_alignments(epsm, dev):
+    """Every binary pattern of length 1..12 against every binary text of length <= 10
+    (joined by 0x02 separators), at every base-address rotation mod 16."""
+    pieces = [b"\x02"]
+    for n in range(1, 11):
+        for bits in itertools.product(b"\x00\x01", repeat=n):
+            pieces.append(bytes(bits))
+            pieces.append(b"\x02")
+    big = np.frombuffer(b"".join(pieces), dtype=np.uint8)
+    buf = torch.zeros(big.size + 64, dtype=torch.uint8, device=dev)
+    pats = [bytes(b) for m in range(1, 13) for b in itertools.product(b"\x00\x01", repeat=m)]
+    rng = np.random.default_rng(3)
+    for rot in range(16):
+        buf[rot:rot + big.size] = torch.from_numpy(big).to(dev)
+        t = buf[rot:rot + big.size]
+        sel = pats if rot in (0, 5) else [pats[i] for i in rng.choice(len(pats), 300, replace=False)]
+        for p in sel:
+            got, occ = gpu_search(epsm, p, t)
+            want = oracle.search(p, big)
+            assert occ == want.size and np.array_equal(got, want), (rot, p)
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 20, 27, 64, 256])
+def test_random_fuzz_with_planted_boundaries(epsm, dev, sigma):
+    rng = np.random.default_rng(100 + sigma)
+    sizes = [0, 1, 15, 16, 17, 31, 33, 1000, TILE - 1, TILE, TILE + 1, 3 * TILE + 777, 5 * TILE + 31]
+    for n in sizes:
+        t = rng.integers(0, sigma, size=n, dtype=np.uint8)
+        for m in (1, 2, 3, 4, 5, 7, 8, 9, 12, 15, 16, 17, 24, 31, 32):
+            if n >= m and rng.random() < 0.8:
+                p = rng.integers(0, sigma, size=m, dtype=np.uint8)
+                # plant at 0, n-m, unit and tile edges (s = -1, 0 mod 16 and mod TILE)
+                for s in {0, n - m, 15, 16, TILE - 1, TILE, TILE - m + 1, 2 * TILE - 3}:
+                    if 0 <= s <= n - m:
+                        t[s:s + m] = p
+                p = p.tobytes()
+            else:
+                p = rng.integers(0, sigma, size=m, dtype=np.uint8).tobytes()
+            td = torch.from_numpy(t.copy()).to(dev)
+            check(epsm, p, t, td, label=f"sigma={sigma} n={n}")
+
+
+@pytest.mark.parametrize("offset", [1, 3, 7, 8, 13, 15])
+def test_misaligned_text_pointer(epsm, dev, offset):
+    rng = np.random.default_rng(offset)
+    full = rng.integers(0, 4, size=3 * TILE + 100, dtype=np.uint8)
+    fd = torch.from_numpy(full).to(dev)
+    t = full[offset: offset + 2 * TILE + 41]
+    td = fd[offset: offset + 2 * TILE + 41]
+    for m in (1, 2, 4, 6, 11, 32):
+        p = t[TILE - 2: TILE - 2 + m].tobytes()
+        check(epsm, p, t, td, label=f"offset={offset}")
+
+
+def test_dense_unary_closed_form(epsm, dev):
+    """'a'^m in 'a'^n: positions are exactly 0..n-m (dense output, many staging rounds)."""
+    n = 3 * TILE + 123
+    td = torch.full((n,), ord("a"), dtype=torch.uint8, device=dev)
+    for m in (1, 2, 4, 5, 16, 17, 32):
+        pos, occ = epsm.search(b"a" * m, td)
+        assert occ == n - m + 1
+        assert torch.equal(pos, torch.arange(n - m + 1, device=dev, dtype=torch.int64))
+        assert epsm.count(b"a" * m, td) == n - m + 1
+
+
+def test_periodic_text(epsm, dev):
+    u = b"ACGTTGCA"
+    t = np.frombuffer(u * 5000, dtype=np.uint8)
+    td = torch.from_numpy(t.copy()).to(dev)
+    for c in range(len(u)):
+        for m in (8, 9, 16, 31):
+            p = (u * 10)[c:c + m]
+            got, occ = gpu_search(epsm, p, td)
+            assert got.tolist() == list(range(c, t.size - m + 1, len(u)))
+
+
+def test_cap_truncation_and_count(epsm, dev):
+    rng = np.random.default_rng(11)
+    t = rng.integers(0, 2, size=4 * TILE + 5, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    p = bytes([0, 1, 1])
+    want = oracle.search(p, t)
+    for cap in (0, 1, 7, 1000, want.size - 1, want.size, want.size + 10):
+        got, occ = gpu_search(epsm, p, td, cap=cap)
+        assert occ == want.size
+        assert np.array_equal(got, want[:cap])
+    assert epsm.count(p, td) == want.size
+
+
+def test_edge_cases(epsm, dev):
+    td = torch.tensor([1, 2, 3], dtype=torch.uint8, device=dev)
+    assert gpu_search(epsm, b"\x01\x02\x03\x04", td)[1] == 0        # m > n
+    assert gpu_search(epsm, b"\x01\x02\x03", td)[0].tolist() == [0]  # p = t
+    empty = torch.empty(0, dtype=torch.uint8, device=dev)
+    assert gpu_search(epsm, b"\x01", empty)[1] == 0
+    assert epsm.count(b"\x01", empty) == 0
+    with pytest.raises(epsm.EpsmError):
+        epsm.plan(b"")
+    with pytest.raises(epsm.EpsmError) as ei:
+        epsm.plan(b"x" * 33)
+    assert ei.value.code == epsm.EPSM_EUNSUP
+
+
+def test_nul_pattern_never_matches_padding(epsm, dev):
+    """Zero bytes are symbols; the kernel's zero-filled staging past the text end
+    must never produce a match."""
+    for n in (1, 5, 16, 17, TILE + 3):
+        t = np.zeros(n, dtype=np.uint8)
+        td = torch.from_numpy(t).to(dev)
+        for m in (1, 2, 4, 8, 32):
+            check(epsm, b"\x00" * m, t, td, label=f"nul n={n}")
+
+
+def test_async_and_host_apis(epsm, dev):
+    rng = np.random.default_rng(5)
+    t = rng.integers(0, 4, size=5 * TILE + 9, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    p = t[1000:1006].tobytes()
+    want = oracle.search(p, t)
+    pl = epsm.plan(p)
+    out = torch.empty(want.size + 5, dtype=torch.int64, device=dev)
+    occ_d = torch.zeros(1, dtype=torch.int64, device=dev)
+    for _ in range(3):   # plan reuse: epochs advance, status words never leak across calls
+        epsm.search_async(pl, td, out, occ_d)
+        torch.cuda.synchronize()
+        assert int(occ_d.item()) == want.size
+        assert np.array_equal(out[: want.size].cpu().numpy().astype(np.uint64), want)
+    epsm.count_async(pl, td, occ_d)
+    assert int(occ_d.item()) == want.size
+    hout = np.zeros(want.size, dtype=np.uint64)
+    occ = epsm.search_host(pl, t, hout)
+    assert occ == want.size and np.array_equal(hout, want)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_emulated_shards_compose(epsm, dev, world):
+    """Production ownership/halo rules, shards scanned one after another on one GPU."""
+    from paper_1209_6449_b200 import sharding
+    rng = np.random.default_rng(world)
+    n = 7 * TILE + 1234
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    for m in (2, 8, 32):
+        p = t[500:500 + m].copy()
+        for r in range(1, world):                       # straddle every cut
+            b = sharding.shard_base(n, world, r)
+            s = max(0, b - m // 2)
+            if s + m <= n:
+                t[s:s + m] = p
+        td = torch.from_numpy(t).to(dev)
+        pl = epsm.plan(p.tobytes())
+        run = sharding.local_search_cuda(pl)
+        parts, total = [], 0
+        for r in range(world):
+            base, owned, slen = sharding.shard_layout(n, world, r)
+            pos, occ = run(td[base:base + slen], owned, base)
+            parts.append(pos.cpu().numpy().astype(np.uint64))
+            total += occ
+        want = oracle.search(p.tobytes(), t)
+        assert total == want.size
+        assert np.array_equal(np.concatenate(parts), want)
+
+
+def test_launch_counter_moves(epsm, dev):
+    td = torch.zeros(100, dtype=torch.uint8, device=dev)
+    before = epsm.launch_count()
+    epsm.search(b"\x00\x00", td)
+    assert epsm.launch_count() > before

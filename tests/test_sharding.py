@@ -1,0 +1,93 @@
+"""Multi-rank host logic of the sharded search, world_size 2 (and 3) over gloo on
+CPU.  The per-rank scan is the oracle here (no GPU); the layout, ownership,
+halo and the counts/positions exchange are the production code."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1209_6449_b200 import sharding
+
+
+def test_layout_partitions_starts():
+    for n in (0, 1, 15, 16, 17, 1000, 1 << 20, (1 << 20) + 7):
+        for world in (1, 2, 3, 4, 8):
+            lay = sharding.all_layouts(n, world)
+            assert lay[0][0] == 0
+            covered = 0
+            for r, (base, owned, slen) in enumerate(lay):
+                assert base % 16 == 0
+                assert base == covered
+                covered += owned
+                assert slen == min(n - base, owned + sharding.MAX_HALO)
+            assert covered == n
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        results = []
+        for text, pattern, cap in cases:
+            n = text.size
+            base, owned, slen = sharding.shard_layout(n, world, rank)
+            shard = torch.from_numpy(text[base:base + slen].copy())
+
+            def local(sh, owned_len, b, p=pattern):
+                # oracle over the shard, owned starts only, shifted to global
+                pos = oracle.search(p, sh.numpy())
+                pos = pos[pos < owned_len].astype(np.int64) + b
+                return torch.from_numpy(pos), int(pos.size)
+
+            pos, occ = sharding.search_sharded_torch(shard, base, owned, n, local, cap=cap)
+            results.append((pos.numpy().copy(), occ))
+        q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_search_equals_unsharded(world):
+    import oracle
+    rng = np.random.default_rng(world)
+    cases = []
+    for n, sigma, m in [(5000, 2, 3), (40_000, 4, 8), (40_000, 4, 32), (33, 2, 2), (17, 256, 4)]:
+        t = rng.integers(0, sigma, size=n, dtype=np.uint8)
+        p = t[n // 3: n // 3 + m].copy()
+        for r in range(1, world):   # occurrences straddling every cut
+            b = sharding.shard_base(n, world, r)
+            s = max(0, b - m // 2)
+            if s + m <= n:
+                t[s:s + m] = p
+        cases.append((t, p.tobytes(), None))
+        cases.append((t, p.tobytes(), 5))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for i, (t, p, cap) in enumerate(cases):
+        want = oracle.search(p, t)
+        for r in range(world):
+            pos, occ = got[r][i]
+            assert occ == want.size
+            assert np.array_equal(pos.astype(np.uint64), want[:cap] if cap else want)
