@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: exact matching of short patterns (m = 2..32).
+
+Workload (N = 1): BASELINE.json configs[1], the random-alphabet sweep --
+n = 256 MiB texts i.i.d. uniform over byte values 0..sigma-1 for sigma in
+{2,4,...,256}; for every (sigma, m in {2,4,8,16,32}) 100 patterns extracted from
+the text at seeded uniform positions; every search reports all positions.
+One STEP = the whole sweep: 8 texts x 5 m x 100 patterns = 4000 searches.
+
+Metric: text GB/s scanned (1e9 bytes of text per second), positions bit-exact
+(the tests check parity; the bench checks every search's count against the
+count kernel on the first step).  Each text (256 MiB) is larger than the
+126 MB L2, so no L2 flush is inserted between searches.
+
+N > 1 (torchrun): weak scaling -- each rank holds a 256 MiB shard (+31-byte
+halo) of an N x 256 MiB text per sigma and every search is the full collective
+epsm_search_sharded (local scan + NCCL all-gather of counts and positions).
+
+--impl reference: the CPU oracle (brute force, oracle/) timed on this box's host
+cores over a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "text GB/s scanned (bit-exact positions) vs HBM peak, m=2..32, 1/2/4/8 B200"
+UNIT = "GB/s"
+SIGMAS = (2, 4, 8, 16, 32, 64, 128, 256)
+MS = (2, 4, 8, 16, 32)
+N_PER_RANK = 256 * synth.MiB
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="epsm", choices=["epsm", "reference"])
+    ap.add_argument("--patterns", type=int, default=100, help="patterns per (sigma, m)")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-bytes", type=int, default=256 * synth.MiB, help="oracle sample bytes per search")
+    ap.add_argument("--sigmas", default=",".join(map(str, SIGMAS)))
+    ap.add_argument("--ms", default=",".join(map(str, MS)))
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"epsm_clocks_{os.getpid()}_{index}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        try:
+            os.remove(self.path)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+                if any(r[2].replace(".", "").isdigit() for r in rows) else None}
+
+
+# ----------------------------------------------------------------- distributed
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "epsm":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, dev) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------- workload
+
+def make_texts(sigmas, world, rank, dev):
+    """Per sigma: (spec, n_total, base, owned, shard tensor on dev)."""
+    from paper_1209_6449_b200 import sharding
+    out = []
+    n_total = N_PER_RANK * world
+    for s in sigmas:
+        spec = synth.raw_sigma_spec(s, (2, s))
+        base, owned, slen = sharding.shard_layout(n_total, world, rank)
+        t = synth.text_torch(spec, base, slen, device=dev)
+        out.append((s, spec, n_total, base, owned, t))
+    return out
+
+
+def make_patterns(texts, ms, count):
+    pats = {}
+    for s, spec, n_total, base, owned, t in texts:
+        for m in ms:
+            if base == 0 and t.numel() == n_total:
+                p, _ = synth.extract_patterns_torch(t, (2, s, m), m, count)
+            else:
+                p, _ = synth.extract_patterns_spec(spec, n_total, (2, s, m), m, count)
+            pats[(s, m)] = p
+    return pats
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def run_epsm(args, world, rank, local):
+    import paper_1209_6449_b200 as epsm
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    sigmas = [int(x) for x in args.sigmas.split(",")]
+    ms = [int(x) for x in args.ms.split(",")]
+    texts = make_texts(sigmas, world, rank, dev)
+    pats = make_patterns(texts, ms, args.patterns)
+    jobs = []   # (text index, plan)
+    for ti, (s, spec, n_total, base, owned, t) in enumerate(texts):
+        for m in ms:
+            for p in pats[(s, m)]:
+                jobs.append((ti, epsm.plan(p)))
+    cap = N_PER_RANK * world if world > 1 else N_PER_RANK
+    pos_buf = torch.empty(cap, dtype=torch.int64, device=dev)
+    occ_buf = torch.zeros(len(jobs), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    comm = epsm.nccl_comm_ptr() if world > 1 else None
+    n_text_step = sum(texts[ti][2] for ti, _ in jobs)        # global text bytes per step
+
+    def one_step(events=None):
+        for j, (ti, pl) in enumerate(jobs):
+            s, spec, n_total, base, owned, t = texts[ti]
+            if events is not None:
+                events[2 * j].record(stream)
+            if world == 1:
+                epsm.search_async(pl, t, pos_buf, occ_buf[j:j + 1], stream=stream)
+            else:
+                occ = epsm.search_sharded(pl, t, base, owned, n_total, out=pos_buf, nccl_comm=comm, stream=stream)
+                occ_buf[j] = occ
+            if events is not None:
+                events[2 * j + 1].record(stream)
+
+    # warm-up (also the correctness spot check: count kernel == search occ, step 0)
+    for w in range(args.warmup):
+        one_step()
+        if w == 0 and world == 1:
+            torch.cuda.synchronize()
+            occ0 = occ_buf.cpu().numpy()
+            chk = list(range(0, len(jobs), max(1, len(jobs) // 40)))
+            for j in chk:
+                ti, pl = jobs[j]
+                assert epsm.count(pl, texts[ti][5]) == occ0[j], "count != search occ"
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(jobs))] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = epsm.launch_count()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        start.record(stream)
+        for k in range(args.steps):
+            one_step(ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = epsm.launch_count() - launches0
+    ms_total = max_over_ranks(start.elapsed_time(stop), world, dev)
+    ms_step = ms_total / args.steps
+    value = n_text_step * args.steps / (ms_total * 1e-3) / 1e9
+
+    # roofline of the scan kernel: algorithmic bytes = n + 8 * min(occ, cap) per launch
+    occ = occ_buf.cpu().numpy().astype(np.int64)
+    kernel_ms = 0.0
+    for k in range(args.steps):
+        for j in range(len(jobs)):
+            kernel_ms += ev[k][2 * j].elapsed_time(ev[k][2 * j + 1])
+    local_bytes = [texts[ti][5].numel() for ti, _ in jobs]
+    alg_bytes = sum(nb + 8 * min(int(o), cap) for nb, o in zip(local_bytes, occ)) * args.steps
+    hbm_peak, peak_src = peaks()
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    clocks = clk.summary()
+
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "BASELINE configs[1]: random-alphabet sweep, n=256 MiB per text"
+                               + (f" per rank (text n={world}x256 MiB, sharded +31 B halo)" if world > 1 else ""),
+                   "sigmas": sigmas, "ms": ms, "patterns_per_sigma_m": args.patterns,
+                   "searches_per_step": len(jobs), "text_bytes_per_step": n_text_step,
+                   "l2": "no flush: every text (256 MiB) is larger than the 126 MB L2",
+                   "parallelism": f"dp{world} over text shards" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "peak_source": peak_src, "kernel": "epsm_scan_kernel (search)",
+                     "per_launch_ms": round(kernel_ms / (args.steps * len(jobs)), 5),
+                     "kernel_share_of_step": round(kernel_ms / ms_total, 4)},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "total_occ_per_step": int(occ.sum()),
+    }
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, epsm, texts, pats, jobs, world, dev)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_sample(args, texts, pats, ms)
+    for _, pl in jobs:
+        pl.close()
+    return res
+
+
+def run_e2e(args, epsm, texts, pats, jobs, world, dev):
+    """Same sweep through the public API with HOST buffers: per step every text is
+    copied host->device (pinned), every search returns occ (8 B D2H) and its
+    positions are copied device->host (pinned).  Plans are built in warm-up."""
+    if world > 1:
+        return None
+    stream = torch.cuda.current_stream(dev)
+    host_texts = [t.cpu().pin_memory() for (_, _, _, _, _, t) in texts]
+    dev_text = torch.empty(max(t.numel() for t in host_texts), dtype=torch.uint8, device=dev)
+    pos_dev = torch.empty(N_PER_RANK, dtype=torch.int64, device=dev)
+    pos_host = torch.empty(N_PER_RANK, dtype=torch.int64).pin_memory()
+    by_text = {}
+    for ti, pl in jobs:
+        by_text.setdefault(ti, []).append(pl)
+
+    def step():
+        h2d = d2h = 0
+        for ti, plans in by_text.items():
+            ht = host_texts[ti]
+            dt = dev_text[: ht.numel()]
+            dt.copy_(ht, non_blocking=True)
+            h2d += ht.numel()
+            for pl in plans:
+                _, occ = epsm.search(pl, dt, out=pos_dev, stream=stream)   # syncs; returns occ
+                k = min(occ, pos_dev.numel())
+                if k:
+                    pos_host[:k].copy_(pos_dev[:k], non_blocking=True)
+                d2h += 8 + 8 * k
+        torch.cuda.synchronize()
+        return h2d, d2h
+
+    step()   # warm-up
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        h2d, d2h = step()
+    dt_s = (time.perf_counter() - t0) / args.e2e_steps
+    n_step = sum(texts[ti][2] for ti, _ in jobs)
+    return {"value": round(n_step / dt_s / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt_s * 1e3, 2), "steps": args.e2e_steps,
+            "note": "public API (epsm.search) with pinned host text in / positions out; plans prebuilt"}
+
+
+# ----------------------------------------------------------------- CPU oracle
+
+def cpu_sample(args, texts, pats, ms, sample_bytes=None):
+    """The oracle (brute force, never tuned) on the host cores: one pattern per
+    (sigma, m) over the first `cpu-bytes` of each text, one pattern per thread."""
+    import oracle
+    sample_bytes = sample_bytes or args.cpu_bytes
+    cores = len(os.sched_getaffinity(0))
+    tasks = []
+    for s, spec, n_total, base, owned, t in texts:
+        host = t[:sample_bytes].cpu().numpy() if isinstance(t, torch.Tensor) else t[:sample_bytes]
+        for m in ms:
+            tasks.append((pats[(s, m)][0], host))
+    from concurrent.futures import ThreadPoolExecutor
+    oracle.count(b"x", np.zeros(1, np.uint8))   # load the library outside the timed region
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(lambda a: oracle.count(a[0], a[1]), tasks))
+    dt = time.perf_counter() - t0
+    scanned = sum(h.size for _, h in tasks)
+    return {"value": round(scanned / dt / 1e9, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 pattern per (sigma, m) = {len(tasks)} searches over the first "
+                      f"{sample_bytes // synth.MiB} MiB of each text ({scanned / 1e9:.2f} GB scanned, "
+                      f"{dt:.2f} s wall, one pattern per thread)"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle as it stands, each step a bounded sample."""
+    if rank != 0:
+        return None
+    sigmas = [int(x) for x in args.sigmas.split(",")]
+    ms = [int(x) for x in args.ms.split(",")]
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    texts = []
+    for s in sigmas:
+        spec = synth.raw_sigma_spec(s, (2, s))
+        t = synth.text_torch(spec, 0, N_PER_RANK, device=dev).cpu().numpy()
+        texts.append((s, spec, N_PER_RANK, 0, N_PER_RANK, t))
+    pats = {}
+    for s, spec, n, _, _, t in texts:
+        for m in ms:
+            pats[(s, m)] = synth.extract_patterns_np(t, (2, s, m), m, 1)[0]
+    sample = min(args.cpu_bytes, 64 * synth.MiB)
+    for _ in range(args.warmup):
+        cpu_sample(args, texts, pats, ms, sample)
+    vals = [cpu_sample(args, texts, pats, ms, sample) for _ in range(args.steps)]
+    v = float(np.mean([x["value"] for x in vals]))
+    per_step_bytes = sample * len(sigmas) * len(ms)
+    cb = dict(vals[-1])
+    cb["value"] = round(v, 3)
+    return {"metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(per_step_bytes / (v * 1e9) * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "BASELINE configs[1] random-alphabet sweep (bounded sample)",
+                       "sigmas": sigmas, "ms": ms, "sample_bytes_per_search": sample},
+            "cpu_baseline": cb,
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        res = run_reference(args, world, rank)
+    else:
+        res = run_epsm(args, world, rank, local)
+    if rank == 0 and res is not None:
+        line = json.dumps(res)
+        print(line, flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                f.write(line + "\n")
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
