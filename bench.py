@@ -255,6 +255,23 @@ def run_epsm(args, world, rank, local):
         for j in range(len(jobs)):
             kernel_ms += ev[k][2 * j].elapsed_time(ev[k][2 * j + 1])
     local_bytes = [texts[ti][5].numel() for ti, _ in jobs]
+    per = {}
+    for j, (ti, pl) in enumerate(jobs):
+        key = (texts[ti][0], pl.m)
+        d = sum(ev[k][2 * j].elapsed_time(ev[k][2 * j + 1]) for k in range(args.steps)) / args.steps
+        a = per.setdefault(key, [0.0, 0, 0])
+        a[0] += d
+        a[1] += 1
+        a[2] += local_bytes[j] + 8 * min(int(occ[j]), cap)
+    breakdown = []
+    for (s, m), (d, c, b) in sorted(per.items()):
+        us = d / c * 1e3
+        breakdown.append([s, m, round(us, 2), round(local_bytes[0] / (us * 1e-6) / 1e9, 1),
+                          round(b / c / (us * 1e-6) / 1e9, 1)])
+    if rank == 0:
+        print("sigma m  us/search  text_GB/s  alg_GB/s", file=sys.stderr)
+        for row in breakdown:
+            print("%5d %2d %10.2f %10.1f %9.1f" % tuple(row), file=sys.stderr)
     alg_bytes = sum(nb + 8 * min(int(o), cap) for nb, o in zip(local_bytes, occ)) * args.steps
     hbm_peak, peak_src = peaks()
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
@@ -278,6 +295,7 @@ def run_epsm(args, world, rank, local):
         "clocks": clocks,
         "gpu_launches": int(launches),
         "total_occ_per_step": int(occ.sum()),
+        "breakdown": {"cols": ["sigma", "m", "us_per_search", "text_GBps", "alg_GBps"], "rows": breakdown},
     }
     if not args.no_e2e:
         res["e2e"] = run_e2e(args, epsm, texts, pats, jobs, world, dev)

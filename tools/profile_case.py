@@ -1,0 +1,40 @@
+"""Run one (sigma, m) search of the bench workload a few times (for ncu / quick timing)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1209_6449_b200 as epsm  # noqa: E402
+import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--sigma", type=int, default=256)
+ap.add_argument("--m", type=int, default=8)
+ap.add_argument("--n", type=int, default=256 * synth.MiB)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--count", action="store_true")
+a = ap.parse_args()
+dev = torch.device("cuda:0")
+t = synth.text_torch(synth.raw_sigma_spec(a.sigma, (2, a.sigma)), 0, a.n, device=dev)
+pats, _ = synth.extract_patterns_torch(t, (2, a.sigma, a.m), a.m, a.reps)
+out = torch.empty(a.n, dtype=torch.int64, device=dev)
+occ = torch.zeros(1, dtype=torch.int64, device=dev)
+plans = [epsm.plan(p) for p in pats]
+torch.cuda.synchronize()
+evs = []
+for pl in plans:
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if a.count:
+        epsm.count_async(pl, t, occ)
+    else:
+        epsm.search_async(pl, t, out, occ)
+    e1.record()
+    evs.append((e0, e1))
+torch.cuda.synchronize()
+for (e0, e1) in evs:
+    us = e0.elapsed_time(e1) * 1e3
+    print(f"sigma={a.sigma} m={a.m} {'count' if a.count else 'search'} {us:.1f} us  {a.n / us / 1e3:.1f} GB/s text")
+print("occ", int(occ.item()))
