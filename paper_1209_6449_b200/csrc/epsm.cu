@@ -85,18 +85,33 @@ int epsm_bind_device(epsm_plan_t* plan, const void* dptr) {
   return EPSM_OK;
 }
 
-static int ensure_status(epsm_plan_t* plan, uint64_t tiles, cudaStream_t s) {
-  if (tiles > plan->status_cap) {
+static int ensure_workspace(epsm_plan_t* plan, uint64_t chunks, bool search, cudaStream_t s) {
+  if (!plan->d_ctr) {
+    cudaError_t e = cudaMalloc(&plan->d_ctr, sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+      epsm_set_error("cudaMalloc(ctr): %s", cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    e = cudaMemsetAsync(plan->d_ctr, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(ctr)");
+    plan->ctr_base = 0;
+  }
+  if (plan->num_sms <= 0) {
+    cudaError_t e = cudaDeviceGetAttribute(&plan->num_sms, cudaDevAttrMultiProcessorCount, plan->device);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  }
+  if (!search) return EPSM_OK;
+  if (chunks > plan->status_cap) {
     if (plan->d_status) {
       cudaStreamSynchronize(s);
       cudaFree(plan->d_status);
       plan->d_status = nullptr;
       plan->status_cap = 0;
     }
-    uint64_t cap = tiles < 4096 ? 4096 : tiles;
+    uint64_t cap = chunks < 1024 ? 1024 : chunks;
     cudaError_t e = cudaMalloc(&plan->d_status, cap * sizeof(unsigned long long));
     if (e != cudaSuccess) {
-      epsm_set_error("cudaMalloc(status, %llu tiles): %s", (unsigned long long)cap, cudaGetErrorString(e));
+      epsm_set_error("cudaMalloc(status, %llu chunks): %s", (unsigned long long)cap, cudaGetErrorString(e));
       return EPSM_ENOMEM;
     }
     e = cudaMemsetAsync(plan->d_status, 0, cap * sizeof(unsigned long long), s);
@@ -129,6 +144,25 @@ int epsm_ensure_occ(epsm_plan_t* plan) {
   return EPSM_OK;
 }
 
+// One-time per (device, kernel variant): opt in to > 48 KiB of dynamic shared memory.
+static int set_smem_attr(KernelFn fn, int device) {
+  static std::atomic<KernelFn> done[16][32];
+  if (device < 0 || device >= 16) device = 15;
+  for (auto& slot : done[device]) {
+    KernelFn f = slot.load(std::memory_order_acquire);
+    if (f == fn) return EPSM_OK;
+    if (f == nullptr) break;
+  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(epsm::SmemLayout)));
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(max dynamic smem)");
+  for (auto& slot : done[device]) {
+    KernelFn expected = nullptr;
+    if (slot.compare_exchange_strong(expected, fn) || expected == fn) break;
+  }
+  return EPSM_OK;
+}
+
 // Core launcher.  The device text is d_text[0..nbytes-1]; starts [0, nstarts) are
 // reported (nstarts <= nbytes - m + 1), each shifted by `base`.
 int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
@@ -151,15 +185,19 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   std::memcpy(P.bcast, plan->bcast, sizeof(P.bcast));
   std::memcpy(P.pat, plan->pat, sizeof(P.pat));
   std::memcpy(P.pmask, plan->pmask, sizeof(P.pmask));
-  const uint64_t tiles = (P.s_hi + epsm::kTileBytes - 1) / epsm::kTileBytes;
+  const uint64_t tiles = (P.s_hi + epsm::kTile - 1) / epsm::kTile;
+  const uint64_t chunks = (tiles + epsm::kChunkTiles - 1) / epsm::kChunkTiles;
   if (tiles > 0x7FFFFFFFull) {
     epsm_set_error("text too large: %llu tiles", (unsigned long long)tiles);
     return EPSM_EINVAL;
   }
-  int rc;
+  int rc = ensure_workspace(plan, chunks, search, s);
+  if (rc) return rc;
+  P.ntiles = static_cast<uint32_t>(tiles);
+  P.nchunks = static_cast<uint32_t>(chunks);
+  P.ctr = plan->d_ctr;
+  P.ctr_base = plan->ctr_base;
   if (search) {
-    rc = ensure_status(plan, tiles, s);
-    if (rc) return rc;
     P.status = plan->d_status;
     P.tag = static_cast<unsigned long long>(plan->epoch) << epsm::kEpochShift;
   } else {
@@ -167,10 +205,15 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
   }
   KernelFn fn = kernel_for(plan->m, search);
-  fn<<<static_cast<unsigned>(tiles), epsm::kThreads, epsm::kSmemBytes, s>>>(P);
+  rc = set_smem_attr(fn, plan->device);
+  if (rc) return rc;
+  const uint64_t grid = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
+  fn<<<static_cast<unsigned>(grid), epsm::kThreads, sizeof(epsm::SmemLayout), s>>>(P);
   epsm_count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
+  // every CTA fetches chunk ids until it draws one past the end: chunks + grid draws
+  plan->ctr_base += chunks + grid;
   return EPSM_OK;
 }
 
@@ -241,6 +284,7 @@ void epsm_plan_free(epsm_plan_t* plan) {
     cudaDeviceSynchronize();
   }
   if (plan->d_status) cudaFree(plan->d_status);
+  if (plan->d_ctr) cudaFree(plan->d_ctr);
   if (plan->d_occ) cudaFree(plan->d_occ);
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);

@@ -12,10 +12,14 @@ struct epsm_plan_s {
   uint32_t pat[9] = {};     // zero-padded pattern words
   uint32_t pmask[9] = {};   // byte masks of the words
   int device = -1;          // bound on first device use
-  // look-back workspace (one status word per tile), epoch-tagged
+  int num_sms = 0;
+  // look-back workspace (one status word per 128 KiB chunk), epoch-tagged
   unsigned long long* d_status = nullptr;
   uint64_t status_cap = 0;
   uint32_t epoch = 0;
+  // chunk-id counter: monotonic across launches; ctr_base = its value at the next launch
+  unsigned long long* d_ctr = nullptr;
+  unsigned long long ctr_base = 0;
   // occ readback for the synchronous calls
   unsigned long long* d_occ = nullptr;
   unsigned long long* h_occ = nullptr;

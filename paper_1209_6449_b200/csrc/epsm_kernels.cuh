@@ -1,40 +1,63 @@
 // epsm_kernels.cuh -- sm_100a kernels of the exact packed string matcher.
 //
-// One CTA scans one 16 KiB tile of text (1024 "units" of alpha = 16 bytes,
-// PAPER.md:166-168, Sec. 3.1).  The tile plus a 32-byte halo (>= m-1 for every
-// m <= 32) is staged into shared memory by ONE TMA bulk copy
-// (cp.async.bulk ... mbarrier::complete_tx) -- the GPU analogue of EPSMb's
-// wsblend, which exists only to avoid unaligned loads; shared
-// memory is byte addressable, so every alignment is read directly.
+// One persistent CTA per SM, warp-specialised:
 //
-// Per thread and unit (16 candidate starts u..u+15):
-//   filter  (EPSMa's shift-AND, PAPER.md:461-469 / Fig. 1 lines 5-9):
-//           Z_k = OR_{i<F} ( S_i[k] XOR B_i ),  S_i = the text shifted by i bytes
-//           (funnel shifts of the unit's words), B_i = p_i * 0x01010101.
-//           A zero byte j of Z_k  <=>  t[u+4k+j+i] = p_i for all i < F.
-//   verify  (the "naive check"): for m > F each candidate
-//           window is compared word by word with the zero-padded pattern P_i
-//           (PAPER.md:124-128), masking the last partial word.
-//   count   popcount of the 16-bit mask r.
-//   report  positions tile_base + unit + {r} (Fig. 1 line 11),
-//           ordered across tiles by a decoupled look-back over 64-bit epoch-tagged
-//           status words, staged in shared memory and stored coalesced.
+//   warp 0      producer   fetches CHUNK ids (8 consecutive 16 KiB tiles = 128 KiB)
+//                          from a global counter and streams every tile plus a
+//                          32-byte halo (>= m-1 for m <= 32) into an 8-stage shared
+//                          memory ring with ONE TMA bulk copy per tile
+//                          (cp.async.bulk ... mbarrier::complete_tx).  The halo is
+//                          the GPU analogue of EPSMb's wsblend, which only exists to
+//                          avoid unaligned loads: shared memory is
+//                          byte addressable, so every alignment is read directly.
+//   warps 2-17  consumers  16 candidate starts ("alpha = 16") per
+//                          thread and unit:
+//       filter   EPSMa's shift-AND (Fig. 1 lines 5-9), packed:
+//                Z_k = OR_{i<F} ( S_i[k] XOR B_i ), S_i = the text shifted by i bytes
+//                (funnel shifts), B_i = p_i * 0x01010101.
+//                A zero byte j of Z_k <=> t[u+4k+j+i] = p_i for all i < F = min(m,4).
+//       verify   the "naive check" of each candidate for
+//                m > 4: word compares against the zero-padded pattern blocks P_i
+//                (PAPER.md:124-128), last partial word masked.
+//       count    popcount of the 16-bit match mask r.
+//       masks    r is parked in a per-chunk shared-memory buffer (2 bytes / 16 text
+//                bytes) so the chunk's positions can be written later, once its
+//                global offset is known, without re-reading the text.
+//   warp 1      look-back  per chunk: publish the chunk's count, walk predecessors
+//                          128 at a time until an inclusive prefix is found
+//                          (decoupled look-back over 64-bit epoch-tagged status
+//                          words), publish the inclusive prefix.  Runs concurrently
+//                          with the consumers, which only wait for it one chunk later.
+//   report       consumers turn a finished chunk's masks into positions
+//                chunk_base + unit*16 + {r} (Fig. 1 line 11) in text
+//                order, stage them in shared memory and store them coalesced at
+//                pos[prefix ...].
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace epsm {
 
-constexpr int kThreads = 256;
-constexpr int kUnitsPerThread = 4;
-constexpr int kUnitBytes = 16;                                            // alpha
-constexpr int kTileBytes = kThreads * kUnitsPerThread * kUnitBytes;      // 16 KiB
-constexpr int kHaloBytes = 32;                                            // >= m-1, x16
-constexpr int kSmemBytes = kTileBytes + kHaloBytes + 32;                  // + verify slack
-constexpr int kStageCap = kTileBytes / 8;                                 // u64 per round
-constexpr int kWarps = kThreads / 32;
+constexpr int kUnitBytes = 16;                                   // alpha
+constexpr int kTile = 16384;                                     // bytes per TMA stage
+constexpr int kHalo = 32;                                        // >= m-1, multiple of 16
+constexpr int kStageBytes = kTile + 64;                          // tile + halo + verify slack
+constexpr int kStages = 8;
+constexpr int kChunkTiles = 8;                                   // 128 KiB look-back granularity
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;                  // 512
+constexpr int kThreads = kConsumers + 64;                        // + producer + look-back warps
+constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 1024
+constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 2
+constexpr int kChunkUnits = kChunkTiles * kUnitsPerTile;         // 8192
+constexpr int kWriteUnits = kChunkUnits / kConsumers;            // 16 per thread
+constexpr int kMaskBufs = 2;
+constexpr int kOutStage = 1024;                                  // positions per staging round
+constexpr int kLookbackWindow = 128;                             // statuses per look-back round
 
-// Tile status word: [63:40] epoch, [39:38] flag, [37:0] value.
+constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
+
+// Chunk status word: [63:40] epoch, [39:38] flag, [37:0] value.
 constexpr int kEpochShift = 40;
 constexpr unsigned long long kFlagAgg = 1ull << 38;
 constexpr unsigned long long kFlagInc = 2ull << 38;
@@ -49,12 +72,38 @@ struct KParams {
   uint64_t pos_bias;            // reported = virtual start + pos_bias (mod 2^64)
   uint64_t* pos;                // output positions (search)
   uint64_t cap;                 // capacity of pos
-  unsigned long long* occ;      // device occ (search: written by the last tile; count: atomics)
-  unsigned long long* status;   // one word per tile (search)
+  unsigned long long* occ;      // device occ
+  unsigned long long* status;   // one word per chunk (search)
+  unsigned long long* ctr;      // chunk-id counter (monotonic across launches)
+  unsigned long long ctr_base;  // value of *ctr when this launch starts
   unsigned long long tag;       // epoch << 40
+  uint32_t ntiles;              // tiles covering [0, s_hi)
+  uint32_t nchunks;
   uint32_t bcast[4];            // B_i = p_i * 0x01010101
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
   uint32_t pmask[9];            // per-word byte masks (partial last word)
+};
+
+struct ChunkSlot {
+  uint32_t chunk;               // chunk id, or kInfoEnd
+  uint32_t total;               // occurrences in the chunk
+  uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
+  uint32_t pad;
+  unsigned long long prefix;    // exclusive prefix (written by the look-back warp)
+};
+
+struct __align__(128) SmemLayout {
+  uint8_t ring[kStages][kStageBytes];
+  uint16_t masks[kMaskBufs][kChunkUnits];
+  uint64_t out[kOutStage];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t lb_full[kMaskBufs];
+  uint64_t lb_done[kMaskBufs];
+  ChunkSlot slot[kMaskBufs];
+  uint32_t info[kStages];       // tile index | (last-of-chunk << 31), or kInfoEnd
+  uint32_t red[kConsumerWarps];
+  uint32_t scan[kConsumerWarps];
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -69,6 +118,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -118,6 +171,10 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
 
 __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void consumer_sync() {   // named barrier 1: the 512 consumer threads
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
 // ------------------------------------------------------------------ packed filter
@@ -198,42 +255,124 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
-// Decoupled look-back (single pass): publish this tile's aggregate, walk the
-// predecessors 32 at a time until an inclusive prefix is found, publish the
-// inclusive prefix.  Called by one full warp; returns the exclusive prefix.
-__device__ __forceinline__ unsigned long long lookback(const KParams& P, uint64_t tile, uint32_t total,
+// Decoupled look-back over chunk status words (single pass).  One full warp;
+// returns the exclusive prefix of `chunk`.  Window: 128 predecessors per round,
+// lane l / slot i reads predecessor pred - (32 i + l), nearest first.
+__device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_t chunk, uint32_t total,
                                                        uint32_t lane) {
   const unsigned long long tag = P.tag;
-  if (tile == 0) {
+  if (chunk == 0) {
     if (lane == 0) st_relaxed(P.status, tag | kFlagInc | total);
     return 0;
   }
-  if (lane == 0) st_relaxed(P.status + tile, tag | kFlagAgg | total);
+  if (lane == 0) st_relaxed(P.status + chunk, tag | kFlagAgg | total);
   unsigned long long prefix = 0;
-  long long pred = static_cast<long long>(tile) - 1;
+  long long pred = static_cast<long long>(chunk) - 1;
   uint32_t spins = 0;
+  constexpr int kPer = kLookbackWindow / 32;
   while (true) {
-    const long long idx = pred - static_cast<long long>(lane);
-    unsigned long long s;
+    unsigned long long s[kPer];
     while (true) {
-      s = idx >= 0 ? ld_relaxed(P.status + idx) : (tag | kFlagInc);
-      const bool valid = ((s & kEpochMask) == tag) && (s & kFlagMask);
+      bool valid = true;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const long long idx = pred - (32 * i + static_cast<long long>(lane));
+        s[i] = idx >= 0 ? ld_relaxed(P.status + idx) : (tag | kFlagInc);
+        valid &= ((s[i] & kEpochMask) == tag) && (s[i] & kFlagMask);
+      }
       if (__all_sync(0xffffffffu, valid)) break;
-      __nanosleep(64);
+      __nanosleep(32);
       if (++spins > (1u << 24)) __trap();   // a predecessor never published: fail loudly, never hang
     }
-    const uint32_t inc = __ballot_sync(0xffffffffu, (s & kFlagMask) == kFlagInc);
-    unsigned long long v = s & kValueMask;
-    if (inc) {
-      const uint32_t k = __ffs(inc) - 1;
-      prefix += warp_sum_u64(lane <= k ? v : 0ull);
-      break;
-    }
+    // nearest inclusive predecessor: smallest distance d = 32 i + lane with flag INC
+    uint32_t dmin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = kPer - 1; i >= 0; --i)
+      if ((s[i] & kFlagMask) == kFlagInc) dmin = 32u * i + lane;
+    dmin = __reduce_min_sync(0xffffffffu, dmin);
+    unsigned long long v = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+      if (32u * i + lane <= dmin) v += s[i] & kValueMask;
     prefix += warp_sum_u64(v);
-    pred -= 32;
+    if (dmin != 0xFFFFFFFFu) break;
+    pred -= kLookbackWindow;
   }
-  if (lane == 0) st_relaxed(P.status + tile, tag | kFlagInc | (prefix + total));
+  if (lane == 0) st_relaxed(P.status + chunk, tag | kFlagInc | (prefix + total));
   return prefix;
+}
+
+// Consumer-block exclusive scan of one u32 per thread (512 threads); returns the
+// exclusive prefix and writes the block total to *total.
+__device__ __forceinline__ uint32_t consumer_exclusive_scan(uint32_t x, uint32_t ctid, SmemLayout& S,
+                                                            uint32_t* total) {
+  const uint32_t lane = ctid & 31u, w = ctid >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= static_cast<uint32_t>(d)) inc += y;
+  }
+  if (lane == 31) S.scan[w] = inc;
+  consumer_sync();
+  uint32_t base = 0, tot = 0;
+#pragma unroll
+  for (int i = 0; i < kConsumerWarps; ++i) {
+    const uint32_t v = S.scan[i];
+    base += (static_cast<uint32_t>(i) < w) ? v : 0u;
+    tot += v;
+  }
+  consumer_sync();   // S.scan may be reused right after
+  *total = tot;
+  return base + inc - x;
+}
+
+// Write the positions of a finished chunk (masks in S.masks[b]) at pos[prefix ...].
+__device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, int b, uint32_t ctid) {
+  const ChunkSlot slot = S.slot[b];
+  if (slot.total == 0 || slot.prefix >= P.cap) return;   // block-uniform
+  const uint32_t nunits = slot.ntiles * kUnitsPerTile;
+  const uint32_t u0 = ctid * kWriteUnits;
+  uint32_t mk[kWriteUnits];
+  const uint4* src = reinterpret_cast<const uint4*>(&S.masks[b][u0]);
+  const uint4 a = src[0], c = src[1];
+  const uint32_t packed[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int i = 0; i < kWriteUnits; ++i) {
+    uint32_t v = (packed[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+    if (u0 + i >= nunits) v = 0;
+    mk[i] = v;
+    cnt += __popc(v);
+  }
+  uint32_t tot;
+  const uint32_t off = consumer_exclusive_scan(cnt, ctid, S, &tot);
+  const unsigned long long prefix = slot.prefix;
+  const uint64_t room = P.cap - prefix;
+  const uint64_t limit = room < tot ? room : static_cast<uint64_t>(tot);
+  const uint64_t cbase = static_cast<uint64_t>(slot.chunk) * (kChunkTiles * kTile) + P.pos_bias;
+  for (uint64_t R = 0; R < limit; R += kOutStage) {
+    if (cnt && off < R + kOutStage && off + cnt > R) {
+      uint32_t idx = off;
+#pragma unroll
+      for (int i = 0; i < kWriteUnits; ++i) {
+        uint32_t v = mk[i];
+        const uint64_t ub = cbase + static_cast<uint64_t>(u0 + i) * kUnitBytes;
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          if (idx >= R && idx < R + kOutStage) S.out[idx - R] = ub + bit;
+          ++idx;
+        }
+      }
+    }
+    consumer_sync();
+    const uint64_t left = limit - R;
+    const uint32_t n_out = left < kOutStage ? static_cast<uint32_t>(left) : static_cast<uint32_t>(kOutStage);
+    uint64_t* dst = P.pos + prefix + R;
+    for (uint32_t i = ctid; i < n_out; i += kConsumers) st_stream_u64(dst + i, S.out[i]);
+    consumer_sync();
+  }
 }
 
 // ------------------------------------------------------------------ the scan kernel
@@ -241,150 +380,183 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint64_
 // F  = filter bytes (min(m, 4));  MW = ceil(m/4) pattern words (MW <= 1: no verify);
 // SEARCH = report positions (else count only).
 template <int F, int MW, bool SEARCH>
-__global__ void __launch_bounds__(kThreads) epsm_scan_kernel(const __grid_constant__ KParams P) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t warp_cnt[kWarps];
-  __shared__ uint32_t warp_tot[kUnitsPerThread * kWarps];
-  __shared__ unsigned long long s_prefix;
-
+__global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  SmemLayout& S = *reinterpret_cast<SmemLayout*>(smem_raw);
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
   const uint32_t warp = tid >> 5;
-  const uint64_t tile = blockIdx.x;
-  const uint64_t base = tile * static_cast<uint64_t>(kTileBytes);
-  const uint64_t want_end = base + static_cast<uint64_t>(kTileBytes + kHaloBytes);
-  const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
-  const uint32_t bulk = static_cast<uint32_t>((end & ~15ull) - base);   // 16-byte multiple
 
-  // ---- stage tile + halo: one TMA bulk copy, scalar tail, zero fill beyond `end`
   if (tid == 0) {
-    mbar_init(&bar, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], kConsumerWarps);
+    }
+    for (int b = 0; b < kMaskBufs; ++b) {
+      mbar_init(&S.lb_full[b], 1);
+      mbar_init(&S.lb_done[b], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && bulk) {
-    mbar_arrive_expect_tx(&bar, bulk);
-    bulk_g2s(smem, P.text + base, bulk, &bar, policy_evict_first());
-  }
-  for (uint32_t i = bulk + tid; i < static_cast<uint32_t>(kSmemBytes); i += kThreads) {
-    const uint64_t g = base + i;
-    smem[i] = g < end ? P.text[g] : static_cast<uint8_t>(0);
-  }
-  if (bulk) mbar_wait(&bar, 0);
-  __syncthreads();
 
-  // ---- filter + verify: 16 alignments per unit, 4 units per thread
-  const uint32_t B[4] = {P.bcast[0], P.bcast[1], P.bcast[2], P.bcast[3]};
-  uint32_t r[kUnitsPerThread];
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int j = 0; j < kUnitsPerThread; ++j) {
-    const uint32_t o = (j * kThreads + tid) * kUnitBytes;
-    const uint4 v = *reinterpret_cast<const uint4*>(smem + o);
-    const uint32_t w[5] = {v.x, v.y, v.z, v.w, *reinterpret_cast<const uint32_t*>(smem + o + 16)};
-    uint32_t Z[4];
-    filter_words<F>(w, B, Z);
-    const uint32_t hz = has_zero_byte(Z[0]) | has_zero_byte(Z[1]) | has_zero_byte(Z[2]) | has_zero_byte(Z[3]);
-    uint32_t mask = 0;
-    if (__any_sync(0xffffffffu, hz)) {
-      mask = movemask4(zero_byte_flags(Z[0])) | (movemask4(zero_byte_flags(Z[1])) << 4) |
-             (movemask4(zero_byte_flags(Z[2])) << 8) | (movemask4(zero_byte_flags(Z[3])) << 12);
-      const uint64_t us = base + o;
-      if (us < P.s_lo || us + 16 > P.s_hi) mask &= range_mask(us, P.s_lo, P.s_hi);
-      if (MW > 1 && mask) mask = verify_candidates<MW>(mask, smem, o, P);
-    }
-    r[j] = mask;
-    cnt += __popc(mask);
-  }
-
-  // ---- tile total
-  const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);
-  if (lane == 0) warp_cnt[warp] = wsum;
-  __syncthreads();
-  uint32_t total = 0;
-#pragma unroll
-  for (int i = 0; i < kWarps; ++i) total += warp_cnt[i];
-
-  if (!SEARCH) {
-    if (tid == 0 && total) atomicAdd(P.occ, static_cast<unsigned long long>(total));
-    return;
-  }
-
-  const bool last_tile = tile + 1 == gridDim.x;
-  if (total == 0) {
-    // nothing to write: warp 0 still resolves the inclusive prefix for successors
-    if (warp == 0) {
-      const unsigned long long pre = lookback(P, tile, 0, lane);
-      if (last_tile && lane == 0) *P.occ = pre;
-    }
-    return;
-  }
-
-  // ---- ordered offsets within the tile (unit order u = j*256 + tid)
-  uint32_t off[kUnitsPerThread];
-#pragma unroll
-  for (int j = 0; j < kUnitsPerThread; ++j) {
-    const uint32_t c = __popc(r[j]);
-    uint32_t x = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= static_cast<uint32_t>(d)) x += y;
-    }
-    off[j] = x - c;   // exclusive within the warp
-    if (lane == 31) warp_tot[j * kWarps + warp] = x;
-  }
   if (warp == 0) {
-    const unsigned long long pre = lookback(P, tile, total, lane);
-    if (lane == 0) {
-      s_prefix = pre;
-      if (last_tile) *P.occ = pre + total;
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {   // exclusive scan of the 32 (unit-slot, warp) totals in unit order
-    const uint32_t c = warp_tot[lane];
-    uint32_t x = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= static_cast<uint32_t>(d)) x += y;
-    }
-    warp_tot[lane] = x - c;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kUnitsPerThread; ++j) off[j] += warp_tot[j * kWarps + warp];
-
-  // ---- staged, coalesced stores of this tile's positions into pos[prefix ...]
-  const unsigned long long prefix = s_prefix;
-  if (prefix >= P.cap) return;
-  const uint64_t room = P.cap - prefix;
-  const uint64_t limit = room < total ? room : static_cast<uint64_t>(total);
-  uint64_t* stage = reinterpret_cast<uint64_t*>(smem);   // text is no longer needed
-  for (uint64_t R = 0; R < limit; R += kStageCap) {
-#pragma unroll
-    for (int j = 0; j < kUnitsPerThread; ++j) {
-      const uint32_t c = __popc(r[j]);
-      if (c && off[j] < R + kStageCap && off[j] + c > R) {
-        uint32_t mm = r[j];
-        uint32_t idx = off[j];
-        const uint64_t ubase = base + (j * kThreads + tid) * kUnitBytes + P.pos_bias;
-        while (mm) {
-          const int b = __ffs(mm) - 1;
-          mm &= mm - 1;
-          if (idx >= R && idx < R + kStageCap) stage[idx - R] = ubase + b;
-          ++idx;
+    // ================================================================ producer
+    const uint64_t policy = policy_evict_first();
+    uint32_t stage = 0, phase = 0;
+    unsigned long long next = 0;
+    if (lane == 0) next = atomicAdd(P.ctr, 1ull) - P.ctr_base;
+    next = __shfl_sync(0xffffffffu, next, 0);
+    while (true) {
+      const unsigned long long chunk = next;
+      if (chunk >= P.nchunks) {
+        mbar_wait(&S.empty[stage], phase ^ 1u);
+        if (lane == 0) {
+          S.info[stage] = kInfoEnd;
+          mbar_arrive(&S.full[stage]);
+        }
+        break;
+      }
+      if (lane == 0) next = atomicAdd(P.ctr, 1ull) - P.ctr_base;   // prefetch the next chunk id
+      const uint32_t t0 = static_cast<uint32_t>(chunk) * kChunkTiles;
+      const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
+      for (uint32_t t = t0; t < t1; ++t) {
+        mbar_wait(&S.empty[stage], phase ^ 1u);
+        const uint64_t base = static_cast<uint64_t>(t) * kTile;
+        const uint64_t want_end = base + kTile + kHalo;
+        const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
+        const uint32_t bulk = static_cast<uint32_t>((end & ~15ull) - base);
+        const uint32_t tail = static_cast<uint32_t>(end - base) - bulk;   // < 16 bytes
+        if (lane < tail) S.ring[stage][bulk + lane] = P.text[base + bulk + lane];
+        __syncwarp();
+        if (lane == 0) {
+          S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
+          if (bulk) {
+            mbar_arrive_expect_tx(&S.full[stage], bulk);
+            bulk_g2s(S.ring[stage], P.text + base, bulk, &S.full[stage], policy);
+          } else {
+            mbar_arrive(&S.full[stage]);
+          }
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1u;
         }
       }
+      next = __shfl_sync(0xffffffffu, next, 0);
     }
-    __syncthreads();
-    const uint64_t left = limit - R;
-    const uint32_t n_out = left < kStageCap ? static_cast<uint32_t>(left) : static_cast<uint32_t>(kStageCap);
-    uint64_t* dst = P.pos + prefix + R;
-    for (uint32_t i = tid; i < n_out; i += kThreads) st_stream_u64(dst + i, stage[i]);
-    __syncthreads();
+  } else if (warp == 1) {
+    // ================================================================ look-back
+    if (!SEARCH) return;
+    uint32_t b = 0, par = 0;
+    while (true) {
+      mbar_wait(&S.lb_full[b], par);
+      const uint32_t chunk = S.slot[b].chunk;
+      if (chunk == kInfoEnd) break;
+      const uint32_t total = S.slot[b].total;
+      const unsigned long long pre = lookback(P, chunk, total, lane);
+      if (lane == 0) {
+        S.slot[b].prefix = pre;
+        if (chunk + 1 == P.nchunks) *P.occ = pre + total;
+        mbar_arrive(&S.lb_done[b]);
+      }
+      __syncwarp();
+      if (++b == kMaskBufs) {
+        b = 0;
+        par ^= 1u;
+      }
+    }
+  } else {
+    // ================================================================ consumers
+    const uint32_t ctid = tid - 64;
+    const uint32_t cw = ctid >> 5;
+    const uint32_t B[4] = {P.bcast[0], P.bcast[1], P.bcast[2], P.bcast[3]};
+    uint32_t stage = 0, phase = 0;
+    uint32_t mb = 0;                        // mask buffer being filled
+    uint32_t pend = 0;                      // bit b: buffer b handed to look-back, not flushed
+    uint32_t upar = 0;                      // bit b: parity of buffer b's next lb_done phase
+    uint32_t acc = 0;                       // this thread's count in the current chunk
+    uint32_t tpos = 0;                      // tile index inside the current chunk
+    while (true) {
+      mbar_wait(&S.full[stage], phase);
+      const uint32_t info = S.info[stage];
+      if (info == kInfoEnd) break;
+      const uint32_t tile = info & 0x7FFFFFFFu;
+      const bool last_in_chunk = info >> 31;
+      const uint8_t* ts = S.ring[stage];
+      const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
+#pragma unroll
+      for (int j = 0; j < kUnitsPerThread; ++j) {
+        const uint32_t u = j * kConsumers + ctid;
+        const uint32_t o = u * kUnitBytes;
+        const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
+        const uint32_t w[5] = {v.x, v.y, v.z, v.w, *reinterpret_cast<const uint32_t*>(ts + o + 16)};
+        uint32_t Z[4];
+        filter_words<F>(w, B, Z);
+        const uint32_t hz = has_zero_byte(Z[0]) | has_zero_byte(Z[1]) | has_zero_byte(Z[2]) | has_zero_byte(Z[3]);
+        uint32_t mask = 0;
+        if (__any_sync(0xffffffffu, hz)) {
+          mask = movemask4(zero_byte_flags(Z[0])) | (movemask4(zero_byte_flags(Z[1])) << 4) |
+                 (movemask4(zero_byte_flags(Z[2])) << 8) | (movemask4(zero_byte_flags(Z[3])) << 12);
+          const uint64_t us = tbase + o;
+          if (us < P.s_lo || us + 16 > P.s_hi) mask &= range_mask(us, P.s_lo, P.s_hi);
+          if (MW > 1 && mask) mask = verify_candidates<MW>(mask, ts, o, P);
+        }
+        if (SEARCH) S.masks[mb][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
+        acc += __popc(mask);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[stage]);
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      ++tpos;
+      if (!SEARCH || !last_in_chunk) continue;
+
+      // ---- chunk complete: hand it to the look-back warp, then flush the older buffer
+      const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
+      if (lane == 0) S.red[cw] = wsum;
+      consumer_sync();
+      if (ctid == 0) {
+        uint32_t tot = 0;
+        for (int i = 0; i < kConsumerWarps; ++i) tot += S.red[i];
+        S.slot[mb].chunk = tile / kChunkTiles;
+        S.slot[mb].total = tot;
+        S.slot[mb].ntiles = tpos;
+        mbar_arrive(&S.lb_full[mb]);
+      }
+      pend |= 1u << mb;
+      acc = 0;
+      tpos = 0;
+      mb = (mb + 1 == kMaskBufs) ? 0u : mb + 1;
+      if ((pend >> mb) & 1u) {
+        mbar_wait(&S.lb_done[mb], (upar >> mb) & 1u);
+        upar ^= 1u << mb;
+        pend &= ~(1u << mb);
+        flush_chunk(P, S, mb, ctid);
+      }
+      consumer_sync();   // S.red / S.slot reuse; mask buffer mb free for the next chunk
+    }
+    if constexpr (!SEARCH) {
+      const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
+      if (lane == 0 && wsum) atomicAdd(P.occ, static_cast<unsigned long long>(wsum));
+    } else {
+    // ---- drain: flush the remaining handed-off chunks in order, then stop the look-back warp
+    for (uint32_t k = 0, b = mb; k < kMaskBufs; ++k, b = (b + 1 == kMaskBufs) ? 0u : b + 1) {
+      if ((pend >> b) & 1u) {
+        mbar_wait(&S.lb_done[b], (upar >> b) & 1u);
+        upar ^= 1u << b;
+        pend &= ~(1u << b);
+        flush_chunk(P, S, b, ctid);
+        consumer_sync();
+      }
+    }
+    if (ctid == 0) {
+      S.slot[mb].chunk = kInfoEnd;
+      mbar_arrive(&S.lb_full[mb]);
+    }
+    }
   }
 }
 
