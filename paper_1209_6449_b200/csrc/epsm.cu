@@ -182,6 +182,9 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   P.pos = d_pos;
   P.cap = d_pos ? cap : 0;
   P.occ = d_occ;
+  P.mul8 = 1u << 24;
+  P.mul24 = 1u << 8;
+  P.movemask_mul = 0x00204081u;
   std::memcpy(P.bcast, plan->bcast, sizeof(P.bcast));
   std::memcpy(P.pat, plan->pat, sizeof(P.pat));
   std::memcpy(P.pmask, plan->pmask, sizeof(P.pmask));

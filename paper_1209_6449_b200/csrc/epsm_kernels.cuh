@@ -2,36 +2,39 @@
 //
 // One persistent CTA per SM, warp-specialised:
 //
-//   warp 0      producer   fetches CHUNK ids (8 consecutive 16 KiB tiles = 128 KiB)
+//   warp 0      producer   fetches CHUNK ids (4 consecutive 32 KiB tiles = 128 KiB)
 //                          from a global counter and streams every tile plus a
-//                          32-byte halo (>= m-1 for m <= 32) into an 8-stage shared
+//                          32-byte halo (>= m-1 for m <= 32) into a 4-stage shared
 //                          memory ring with ONE TMA bulk copy per tile
 //                          (cp.async.bulk ... mbarrier::complete_tx).  The halo is
 //                          the GPU analogue of EPSMb's wsblend, which only exists to
 //                          avoid unaligned loads: shared memory is
 //                          byte addressable, so every alignment is read directly.
 //   warps 2-17  consumers  16 candidate starts ("alpha = 16") per
-//                          thread and unit:
+//                          thread and unit, 4 units per thread and tile:
 //       filter   EPSMa's shift-AND (Fig. 1 lines 5-9), packed:
-//                Z_k = OR_{i<F} ( S_i[k] XOR B_i ), S_i = the text shifted by i bytes
-//                (funnel shifts), B_i = p_i * 0x01010101.
-//                A zero byte j of Z_k <=> t[u+4k+j+i] = p_i for all i < F = min(m,4).
+//                Z_k = OR_{i<F} ( S_i[k] XOR B_i ), S_i = the text shifted by i bytes,
+//                B_i = p_i * 0x01010101.  A zero byte j of Z_k
+//                <=> t[u+4k+j+i] = p_i for all i < F = min(m, 4).  The byte shifts by
+//                8 and 24 bits run as IMAD pairs on the FMA pipe, the rest on the ALU
+//                pipe, so the two integer pipes share the work.
 //       verify   the "naive check" of each candidate for
 //                m > 4: word compares against the zero-padded pattern blocks P_i
 //                (PAPER.md:124-128), last partial word masked.
 //       count    popcount of the 16-bit match mask r.
-//       masks    r is parked in a per-chunk shared-memory buffer (2 bytes / 16 text
-//                bytes) so the chunk's positions can be written later, once its
-//                global offset is known, without re-reading the text.
+//       masks    r is parked in a per-chunk shared-memory buffer (2 bytes per 16 text
+//                bytes) so the chunk's positions can be written once its global
+//                offset is known, without re-reading the text.  Chunks without any
+//                occurrence release their buffer at once.
 //   warp 1      look-back  per chunk: publish the chunk's count, walk predecessors
 //                          128 at a time until an inclusive prefix is found
 //                          (decoupled look-back over 64-bit epoch-tagged status
 //                          words), publish the inclusive prefix.  Runs concurrently
-//                          with the consumers, which only wait for it one chunk later.
-//   report       consumers turn a finished chunk's masks into positions
-//                chunk_base + unit*16 + {r} (Fig. 1 line 11) in text
-//                order, stage them in shared memory and store them coalesced at
-//                pos[prefix ...].
+//                          with the consumers through an 8-deep slot queue.
+//   report       each consumer warp turns its 512 units of a finished chunk into
+//                positions chunk_base + unit*16 + {r} (Fig. 1
+//                line 11) in text order, stages them in its own shared-memory buffer
+//                and stores them coalesced at pos[prefix + ...].
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -39,23 +42,28 @@
 namespace epsm {
 
 constexpr int kUnitBytes = 16;                                   // alpha
-constexpr int kTile = 16384;                                     // bytes per TMA stage
+constexpr int kTile = 32768;                                     // bytes per TMA stage
 constexpr int kHalo = 32;                                        // >= m-1, multiple of 16
 constexpr int kStageBytes = kTile + 64;                          // tile + halo + verify slack
-constexpr int kStages = 8;
-constexpr int kChunkTiles = 8;                                   // 128 KiB look-back granularity
+constexpr int kStages = 4;
+constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
+constexpr int kChunkBytes = kChunkTiles * kTile;
 constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = kConsumerWarps * 32;                  // 512
 constexpr int kThreads = kConsumers + 64;                        // + producer + look-back warps
-constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 1024
-constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 2
+constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 2048
+constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 4
 constexpr int kChunkUnits = kChunkTiles * kUnitsPerTile;         // 8192
-constexpr int kWriteUnits = kChunkUnits / kConsumers;            // 16 per thread
+constexpr int kWarpUnits = kChunkUnits / kConsumerWarps;         // 512 units per warp in a flush
+constexpr int kGroups = kWarpUnits / 32;                         // 16 groups of 32 units
 constexpr int kMaskBufs = 2;
-constexpr int kOutStage = 1024;                                  // positions per staging round
+constexpr int kSlots = 8;                                        // look-back queue depth
+constexpr int kWarpStage = 256;                                  // positions per warp round
+constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
 constexpr int kLookbackWindow = 128;                             // statuses per look-back round
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
+constexpr uint32_t kNoSlot = 0xFFu;
 
 // Chunk status word: [63:40] epoch, [39:38] flag, [37:0] value.
 constexpr int kEpochShift = 40;
@@ -79,6 +87,9 @@ struct KParams {
   unsigned long long tag;       // epoch << 40
   uint32_t ntiles;              // tiles covering [0, s_hi)
   uint32_t nchunks;
+  uint32_t mul8;                // 1 << 24: funnel shift by  8 bits as an IMAD pair
+  uint32_t mul24;               // 1 << 8 : funnel shift by 24 bits as an IMAD pair
+  uint32_t movemask_mul;        // 0x00204081
   uint32_t bcast[4];            // B_i = p_i * 0x01010101
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
   uint32_t pmask[9];            // per-word byte masks (partial last word)
@@ -95,12 +106,12 @@ struct ChunkSlot {
 struct __align__(128) SmemLayout {
   uint8_t ring[kStages][kStageBytes];
   uint16_t masks[kMaskBufs][kChunkUnits];
-  uint64_t out[kOutStage];
+  uint64_t wstage[kConsumerWarps][kWarpStagePad];
   uint64_t full[kStages];
   uint64_t empty[kStages];
-  uint64_t lb_full[kMaskBufs];
-  uint64_t lb_done[kMaskBufs];
-  ChunkSlot slot[kMaskBufs];
+  uint64_t lb_full[kSlots];
+  uint64_t lb_done[kSlots];
+  ChunkSlot slot[kSlots];
   uint32_t info[kStages];       // tile index | (last-of-chunk << 31), or kInfoEnd
   uint32_t red[kConsumerWarps];
   uint32_t scan[kConsumerWarps];
@@ -179,33 +190,45 @@ __device__ __forceinline__ void consumer_sync() {   // named barrier 1: the 512 
 
 // ------------------------------------------------------------------ packed filter
 
-// Exact "byte is zero" flags: bit 8j+7 set iff byte j of z is 0x00.
-__device__ __forceinline__ uint32_t zero_byte_flags(uint32_t z) {
-  return ~(((z | 0x80808080u) - 0x01010101u) | z) & 0x80808080u;
-}
-
-// Nonzero iff some byte of z is zero (the classic has-zero test; exact as a boolean).
-__device__ __forceinline__ uint32_t has_zero_byte(uint32_t z) {
-  return (z - 0x01010101u) & ~z & 0x80808080u;
-}
-
-// movemask: flags at bits 7,15,23,31 -> 4-bit mask, bit j <=> byte j.
-__device__ __forceinline__ uint32_t movemask4(uint32_t flags) {
-  return (((flags >> 7) * 0x00204081u) >> 21) & 0xFu;
+// funnel shift right of the pair (hi:lo) by s bits, as two IMADs on the FMA pipe:
+// mul = 2^(32-s) (a run-time value, so ptxas keeps the multiplies).
+__device__ __forceinline__ uint32_t funnel_fma(uint32_t lo, uint32_t hi, uint32_t mul) {
+  uint32_t r;
+  asm("{\n.reg .u32 t;\nmul.lo.u32 t, %2, %3;\nmad.hi.u32 %0, %1, %3, t;\n}" : "=r"(r) : "r"(lo), "r"(hi), "r"(mul));
+  return r;
 }
 
 // Z words of one unit for an F-byte filter: byte j of Z[k] is zero iff the
 // F bytes starting at unit offset 4k+j equal p_0..p_{F-1}.
 template <int F>
-__device__ __forceinline__ void filter_words(const uint32_t (&w)[5], const uint32_t (&B)[4], uint32_t (&Z)[4]) {
+__device__ __forceinline__ void filter_words(const uint32_t (&w)[5], const KParams& P, uint32_t (&Z)[4]) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    uint32_t z = w[k] ^ B[0];
-    if (F > 1) z |= __funnelshift_r(w[k], w[k + 1], 8) ^ B[1];
-    if (F > 2) z |= __funnelshift_r(w[k], w[k + 1], 16) ^ B[2];
-    if (F > 3) z |= __funnelshift_r(w[k], w[k + 1], 24) ^ B[3];
+    uint32_t z = w[k] ^ P.bcast[0];
+    if (F > 1) z |= funnel_fma(w[k], w[k + 1], P.mul8) ^ P.bcast[1];
+    if (F > 2) z |= __funnelshift_r(w[k], w[k + 1], 16) ^ P.bcast[2];
+    if (F > 3) z |= funnel_fma(w[k], w[k + 1], P.mul24) ^ P.bcast[3];
     Z[k] = z;
   }
+}
+
+// Nonzero (bit 8j+7 set) iff some byte of some Z[k] is zero (has-zero test, exact as a boolean).
+__device__ __forceinline__ uint32_t any_zero_byte(const uint32_t (&Z)[4]) {
+  uint32_t h = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h |= (Z[k] - 0x01010101u) & ~Z[k];
+  return h & 0x80808080u;
+}
+
+// Exact 16-bit mask: bit 4k+j set iff byte j of Z[k] is zero.
+__device__ __forceinline__ uint32_t zero_byte_mask16(const uint32_t (&Z)[4], uint32_t mm) {
+  uint32_t t[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t f = ~(((Z[k] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | Z[k]) & 0x80808080u;   // flags at 8j+7
+    t[k] = f * mm;                                                                      // gathered at 28..31
+  }
+  return (t[0] >> 28) | ((t[1] >> 24) & 0xF0u) | ((t[2] >> 20) & 0xF00u) | ((t[3] >> 16) & 0xF000u);
 }
 
 // Bits j of a 16-bit unit mask whose start (ustart + j) lies in [lo, hi).
@@ -255,6 +278,15 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
+__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, uint32_t lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= static_cast<uint32_t>(d)) x += y;
+  }
+  return x;
+}
+
 // Decoupled look-back over chunk status words (single pass).  One full warp;
 // returns the exclusive prefix of `chunk`.  Window: 128 predecessors per round,
 // lane l / slot i reads predecessor pred - (32 i + l), nearest first.
@@ -302,76 +334,63 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
   return prefix;
 }
 
-// Consumer-block exclusive scan of one u32 per thread (512 threads); returns the
-// exclusive prefix and writes the block total to *total.
-__device__ __forceinline__ uint32_t consumer_exclusive_scan(uint32_t x, uint32_t ctid, SmemLayout& S,
-                                                            uint32_t* total) {
-  const uint32_t lane = ctid & 31u, w = ctid >> 5;
-  uint32_t inc = x;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= static_cast<uint32_t>(d)) inc += y;
-  }
-  if (lane == 31) S.scan[w] = inc;
-  consumer_sync();
-  uint32_t base = 0, tot = 0;
-#pragma unroll
-  for (int i = 0; i < kConsumerWarps; ++i) {
-    const uint32_t v = S.scan[i];
-    base += (static_cast<uint32_t>(i) < w) ? v : 0u;
-    tot += v;
-  }
-  consumer_sync();   // S.scan may be reused right after
-  *total = tot;
-  return base + inc - x;
-}
-
-// Write the positions of a finished chunk (masks in S.masks[b]) at pos[prefix ...].
-__device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, int b, uint32_t ctid) {
-  const ChunkSlot slot = S.slot[b];
+// Write the positions of a finished chunk (masks in S.masks[b], look-back result in
+// S.slot[q]) at pos[prefix ...].  Warp w owns units [512 w, 512 w + 512) of the chunk,
+// i.e. a contiguous slice of the chunk's output.
+__device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, uint32_t b, uint32_t q,
+                                            uint32_t ctid) {
+  const ChunkSlot slot = S.slot[q];
   if (slot.total == 0 || slot.prefix >= P.cap) return;   // block-uniform
+  const uint32_t lane = ctid & 31u, w = ctid >> 5;
   const uint32_t nunits = slot.ntiles * kUnitsPerTile;
-  const uint32_t u0 = ctid * kWriteUnits;
-  uint32_t mk[kWriteUnits];
-  const uint4* src = reinterpret_cast<const uint4*>(&S.masks[b][u0]);
-  const uint4 a = src[0], c = src[1];
-  const uint32_t packed[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  const uint16_t* mrow = &S.masks[b][w * kWarpUnits + lane];
+  const uint32_t ulim = nunits > w * kWarpUnits + lane ? nunits - (w * kWarpUnits + lane) : 0u;
   uint32_t cnt = 0;
 #pragma unroll
-  for (int i = 0; i < kWriteUnits; ++i) {
-    uint32_t v = (packed[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-    if (u0 + i >= nunits) v = 0;
-    mk[i] = v;
-    cnt += __popc(v);
-  }
-  uint32_t tot;
-  const uint32_t off = consumer_exclusive_scan(cnt, ctid, S, &tot);
-  const unsigned long long prefix = slot.prefix;
-  const uint64_t room = P.cap - prefix;
-  const uint64_t limit = room < tot ? room : static_cast<uint64_t>(tot);
-  const uint64_t cbase = static_cast<uint64_t>(slot.chunk) * (kChunkTiles * kTile) + P.pos_bias;
-  for (uint64_t R = 0; R < limit; R += kOutStage) {
-    if (cnt && off < R + kOutStage && off + cnt > R) {
-      uint32_t idx = off;
+  for (int g = 0; g < kGroups; ++g) cnt += (g * 32u < ulim) ? __popc(mrow[g * 32]) : 0u;
+  const uint32_t wtot = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) S.scan[w] = wtot;
+  consumer_sync();
+  uint32_t wbase = 0;
 #pragma unroll
-      for (int i = 0; i < kWriteUnits; ++i) {
-        uint32_t v = mk[i];
-        const uint64_t ub = cbase + static_cast<uint64_t>(u0 + i) * kUnitBytes;
+  for (int i = 0; i < kConsumerWarps; ++i) wbase += (static_cast<uint32_t>(i) < w) ? S.scan[i] : 0u;
+  consumer_sync();                                   // S.scan is reused by the next flush
+  if (wtot == 0) return;
+  uint64_t gidx = slot.prefix + wbase;               // global index of this warp's first position
+  const uint64_t cbase = static_cast<uint64_t>(slot.chunk) * kChunkBytes + P.pos_bias;
+  uint64_t* stage = S.wstage[w];
+#pragma unroll 1
+  for (int g = 0; g < kGroups; ++g) {
+    const uint32_t mkg = (g * 32u < ulim) ? mrow[g * 32] : 0u;
+    const uint32_t c = __popc(mkg);
+    const uint32_t tg = __reduce_add_sync(0xffffffffu, c);
+    if (tg == 0) continue;
+    if (gidx >= P.cap) return;
+    const uint32_t off = warp_inclusive_scan(c, lane) - c;
+    const uint64_t ub = cbase + static_cast<uint64_t>(w * kWarpUnits + g * 32 + lane) * kUnitBytes;
+    for (uint32_t R = 0; R < tg; R += kWarpStage) {
+      if (c && off < R + kWarpStage && off + c > R) {
+        uint32_t v = mkg;
+        uint32_t idx = off;
         while (v) {
           const int bit = __ffs(v) - 1;
           v &= v - 1;
-          if (idx >= R && idx < R + kOutStage) S.out[idx - R] = ub + bit;
+          if (idx >= R && idx < R + kWarpStage) {
+            const uint32_t i = idx - R;
+            stage[i + (i >> 4)] = ub + bit;
+          }
           ++idx;
         }
       }
+      __syncwarp();
+      uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
+      if (gidx + R >= P.cap) n = 0;
+      else if (P.cap - (gidx + R) < n) n = static_cast<uint32_t>(P.cap - (gidx + R));
+      uint64_t* dst = P.pos + gidx + R;
+      for (uint32_t i = lane; i < n; i += 32) st_stream_u64(dst + i, stage[i + (i >> 4)]);
+      __syncwarp();
     }
-    consumer_sync();
-    const uint64_t left = limit - R;
-    const uint32_t n_out = left < kOutStage ? static_cast<uint32_t>(left) : static_cast<uint32_t>(kOutStage);
-    uint64_t* dst = P.pos + prefix + R;
-    for (uint32_t i = ctid; i < n_out; i += kConsumers) st_stream_u64(dst + i, S.out[i]);
-    consumer_sync();
+    gidx += tg;
   }
 }
 
@@ -392,9 +411,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       mbar_init(&S.full[s], 1);
       mbar_init(&S.empty[s], kConsumerWarps);
     }
-    for (int b = 0; b < kMaskBufs; ++b) {
-      mbar_init(&S.lb_full[b], 1);
-      mbar_init(&S.lb_done[b], 1);
+    for (int q = 0; q < kSlots; ++q) {
+      mbar_init(&S.lb_full[q], 1);
+      mbar_init(&S.lb_done[q], 1);
     }
     fence_mbar_init();
   }
@@ -448,21 +467,21 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   } else if (warp == 1) {
     // ================================================================ look-back
     if (!SEARCH) return;
-    uint32_t b = 0, par = 0;
+    uint32_t q = 0, par = 0;
     while (true) {
-      mbar_wait(&S.lb_full[b], par);
-      const uint32_t chunk = S.slot[b].chunk;
+      mbar_wait(&S.lb_full[q], par);
+      const uint32_t chunk = S.slot[q].chunk;
       if (chunk == kInfoEnd) break;
-      const uint32_t total = S.slot[b].total;
+      const uint32_t total = S.slot[q].total;
       const unsigned long long pre = lookback(P, chunk, total, lane);
       if (lane == 0) {
-        S.slot[b].prefix = pre;
+        S.slot[q].prefix = pre;
         if (chunk + 1 == P.nchunks) *P.occ = pre + total;
-        mbar_arrive(&S.lb_done[b]);
+        mbar_arrive(&S.lb_done[q]);
       }
       __syncwarp();
-      if (++b == kMaskBufs) {
-        b = 0;
+      if (++q == kSlots) {
+        q = 0;
         par ^= 1u;
       }
     }
@@ -470,13 +489,35 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // ================================================================ consumers
     const uint32_t ctid = tid - 64;
     const uint32_t cw = ctid >> 5;
-    const uint32_t B[4] = {P.bcast[0], P.bcast[1], P.bcast[2], P.bcast[3]};
     uint32_t stage = 0, phase = 0;
-    uint32_t mb = 0;                        // mask buffer being filled
-    uint32_t pend = 0;                      // bit b: buffer b handed to look-back, not flushed
-    uint32_t upar = 0;                      // bit b: parity of buffer b's next lb_done phase
-    uint32_t acc = 0;                       // this thread's count in the current chunk
-    uint32_t tpos = 0;                      // tile index inside the current chunk
+    uint32_t mb = 0;                           // mask buffer being filled
+    uint32_t bufq = kNoSlot | (kNoSlot << 8);  // byte b: slot of the unflushed chunk in buffer b
+    uint32_t qh = 0;                           // next look-back slot
+    uint32_t need = 0;                         // bit q: lb_done[q] phase not consumed yet
+    uint32_t qpar = 0;                         // bit q: parity of lb_done[q]'s next phase
+    uint32_t acc = 0;                          // this thread's count in the current chunk
+    uint32_t tpos = 0;                         // tile index inside the current chunk
+
+    auto wait_slot = [&](uint32_t q) {
+      if ((need >> q) & 1u) {
+        mbar_wait(&S.lb_done[q], (qpar >> q) & 1u);
+        qpar ^= 1u << q;
+        need &= ~(1u << q);
+      }
+    };
+    auto flush_buf = [&](uint32_t b) {
+      const uint32_t q = (bufq >> (8 * b)) & 0xFFu;
+      if (q == kNoSlot) return;
+      wait_slot(q);
+      flush_chunk(P, S, b, q, ctid);
+      bufq |= kNoSlot << (8 * b);
+    };
+    auto take_slot = [&](uint32_t q) {          // make slot q reusable
+      for (uint32_t b = 0; b < kMaskBufs; ++b)
+        if (((bufq >> (8 * b)) & 0xFFu) == q) flush_buf(b);
+      wait_slot(q);
+    };
+
     while (true) {
       mbar_wait(&S.full[stage], phase);
       const uint32_t info = S.info[stage];
@@ -492,15 +533,13 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
         const uint32_t w[5] = {v.x, v.y, v.z, v.w, *reinterpret_cast<const uint32_t*>(ts + o + 16)};
         uint32_t Z[4];
-        filter_words<F>(w, B, Z);
-        const uint32_t hz = has_zero_byte(Z[0]) | has_zero_byte(Z[1]) | has_zero_byte(Z[2]) | has_zero_byte(Z[3]);
+        filter_words<F>(w, P, Z);
         uint32_t mask = 0;
-        if (__any_sync(0xffffffffu, hz)) {
-          mask = movemask4(zero_byte_flags(Z[0])) | (movemask4(zero_byte_flags(Z[1])) << 4) |
-                 (movemask4(zero_byte_flags(Z[2])) << 8) | (movemask4(zero_byte_flags(Z[3])) << 12);
+        if (__any_sync(0xffffffffu, any_zero_byte(Z))) {
+          mask = zero_byte_mask16(Z, P.movemask_mul);
           const uint64_t us = tbase + o;
           if (us < P.s_lo || us + 16 > P.s_hi) mask &= range_mask(us, P.s_lo, P.s_hi);
-          if (MW > 1 && mask) mask = verify_candidates<MW>(mask, ts, o, P);
+          if (MW > 1 && __any_sync(0xffffffffu, mask)) mask = verify_candidates<MW>(mask, ts, o, P);
         }
         if (SEARCH) S.masks[mb][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
         acc += __popc(mask);
@@ -514,48 +553,43 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       ++tpos;
       if (!SEARCH || !last_in_chunk) continue;
 
-      // ---- chunk complete: hand it to the look-back warp, then flush the older buffer
+      // ---- chunk complete: hand it to the look-back warp through slot qh
       const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
       if (lane == 0) S.red[cw] = wsum;
+      take_slot(qh);                    // (may flush an older chunk that still references qh)
       consumer_sync();
+      uint32_t tot = 0;
+#pragma unroll
+      for (int i = 0; i < kConsumerWarps; ++i) tot += S.red[i];
       if (ctid == 0) {
-        uint32_t tot = 0;
-        for (int i = 0; i < kConsumerWarps; ++i) tot += S.red[i];
-        S.slot[mb].chunk = tile / kChunkTiles;
-        S.slot[mb].total = tot;
-        S.slot[mb].ntiles = tpos;
-        mbar_arrive(&S.lb_full[mb]);
+        S.slot[qh].chunk = tile / kChunkTiles;
+        S.slot[qh].total = tot;
+        S.slot[qh].ntiles = tpos;
+        mbar_arrive(&S.lb_full[qh]);
       }
-      pend |= 1u << mb;
+      need |= 1u << qh;
+      if (tot) {                         // keep the masks until the prefix is known
+        bufq = (bufq & ~(0xFFu << (8 * mb))) | (qh << (8 * mb));
+        mb ^= 1u;
+        flush_buf(mb);                   // the other buffer's chunk (if any) goes out now
+      }
+      qh = (qh + 1 == kSlots) ? 0u : qh + 1;
       acc = 0;
       tpos = 0;
-      mb = (mb + 1 == kMaskBufs) ? 0u : mb + 1;
-      if ((pend >> mb) & 1u) {
-        mbar_wait(&S.lb_done[mb], (upar >> mb) & 1u);
-        upar ^= 1u << mb;
-        pend &= ~(1u << mb);
-        flush_chunk(P, S, mb, ctid);
-      }
-      consumer_sync();   // S.red / S.slot reuse; mask buffer mb free for the next chunk
+      consumer_sync();                   // S.red reuse; mask buffer mb free for the next chunk
     }
     if constexpr (!SEARCH) {
       const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
       if (lane == 0 && wsum) atomicAdd(P.occ, static_cast<unsigned long long>(wsum));
     } else {
-    // ---- drain: flush the remaining handed-off chunks in order, then stop the look-back warp
-    for (uint32_t k = 0, b = mb; k < kMaskBufs; ++k, b = (b + 1 == kMaskBufs) ? 0u : b + 1) {
-      if ((pend >> b) & 1u) {
-        mbar_wait(&S.lb_done[b], (upar >> b) & 1u);
-        upar ^= 1u << b;
-        pend &= ~(1u << b);
-        flush_chunk(P, S, b, ctid);
-        consumer_sync();
+      // ---- drain: flush the chunks still parked in mask buffers, then stop the look-back warp
+      flush_buf(mb ^ 1u);
+      flush_buf(mb);
+      take_slot(qh);
+      if (ctid == 0) {
+        S.slot[qh].chunk = kInfoEnd;
+        mbar_arrive(&S.lb_full[qh]);
       }
-    }
-    if (ctid == 0) {
-      S.slot[mb].chunk = kInfoEnd;
-      mbar_arrive(&S.lb_full[mb]);
-    }
     }
   }
 }
