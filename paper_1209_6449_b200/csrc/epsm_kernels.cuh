@@ -56,6 +56,8 @@ constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 4
 constexpr int kChunkUnits = kChunkTiles * kUnitsPerTile;         // 8192
 constexpr int kWarpUnits = kChunkUnits / kConsumerWarps;         // 512 units per warp in a flush
 constexpr int kGroups = kWarpUnits / 32;                         // 16 groups of 32 units
+static_assert(kGroups == kConsumerWarps, "flush group g is filled by consumer warp g");
+static_assert(kUnitsPerTile % kWarpUnits == 0, "a flush warp covers part of one tile");
 constexpr int kMaskBufs = 2;
 constexpr int kSlots = 8;                                        // look-back queue depth
 constexpr int kWarpStage = 256;                                  // positions per warp round
@@ -113,6 +115,7 @@ struct __align__(128) SmemLayout {
   uint64_t lb_done[kSlots];
   ChunkSlot slot[kSlots];
   uint32_t info[kStages];       // tile index | (last-of-chunk << 31), or kInfoEnd
+  uint8_t wflag[kMaskBufs][kChunkTiles][kConsumerWarps];   // 1: the warp stored masks for the tile
   uint32_t red[kConsumerWarps];
   uint32_t scan[kConsumerWarps];
 };
@@ -346,8 +349,9 @@ __device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, uin
   const uint16_t* mrow = &S.masks[b][w * kWarpUnits + lane];
   const uint32_t ulim = nunits > w * kWarpUnits + lane ? nunits - (w * kWarpUnits + lane) : 0u;
   uint32_t cnt = 0;
+  const uint8_t* flag = S.wflag[b][w / (kUnitsPerTile / kWarpUnits)];   // group g <- filter warp g
 #pragma unroll
-  for (int g = 0; g < kGroups; ++g) cnt += (g * 32u < ulim) ? __popc(mrow[g * 32]) : 0u;
+  for (int g = 0; g < kGroups; ++g) cnt += (g * 32u < ulim && flag[g]) ? __popc(mrow[g * 32]) : 0u;
   const uint32_t wtot = __reduce_add_sync(0xffffffffu, cnt);
   if (lane == 0) S.scan[w] = wtot;
   consumer_sync();
@@ -361,7 +365,7 @@ __device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, uin
   uint64_t* stage = S.wstage[w];
 #pragma unroll 1
   for (int g = 0; g < kGroups; ++g) {
-    const uint32_t mkg = (g * 32u < ulim) ? mrow[g * 32] : 0u;
+    const uint32_t mkg = (g * 32u < ulim && flag[g]) ? mrow[g * 32] : 0u;
     const uint32_t c = __popc(mkg);
     const uint32_t tg = __reduce_add_sync(0xffffffffu, c);
     if (tg == 0) continue;
@@ -526,24 +530,32 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       const bool last_in_chunk = info >> 31;
       const uint8_t* ts = S.ring[stage];
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
+      // filter all units first (independent chains), then one warp vote for the tile
+      uint32_t Z[kUnitsPerThread][4];
+      uint32_t hz = 0;
 #pragma unroll
       for (int j = 0; j < kUnitsPerThread; ++j) {
-        const uint32_t u = j * kConsumers + ctid;
-        const uint32_t o = u * kUnitBytes;
+        const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
         const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
         const uint32_t w[5] = {v.x, v.y, v.z, v.w, *reinterpret_cast<const uint32_t*>(ts + o + 16)};
-        uint32_t Z[4];
-        filter_words<F>(w, P, Z);
-        uint32_t mask = 0;
-        if (__any_sync(0xffffffffu, any_zero_byte(Z))) {
-          mask = zero_byte_mask16(Z, P.movemask_mul);
+        filter_words<F>(w, P, Z[j]);
+        hz |= any_zero_byte(Z[j]);
+      }
+      const bool slow = __any_sync(0xffffffffu, hz);
+      if (slow) {
+#pragma unroll
+        for (int j = 0; j < kUnitsPerThread; ++j) {
+          const uint32_t u = j * kConsumers + ctid;
+          const uint32_t o = u * kUnitBytes;
+          uint32_t mask = zero_byte_mask16(Z[j], P.movemask_mul);
           const uint64_t us = tbase + o;
           if (us < P.s_lo || us + 16 > P.s_hi) mask &= range_mask(us, P.s_lo, P.s_hi);
           if (MW > 1 && __any_sync(0xffffffffu, mask)) mask = verify_candidates<MW>(mask, ts, o, P);
+          if (SEARCH) S.masks[mb][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
+          acc += __popc(mask);
         }
-        if (SEARCH) S.masks[mb][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
-        acc += __popc(mask);
       }
+      if (SEARCH && lane == 0) S.wflag[mb][tpos][cw] = slow;   // masks of this warp/tile are valid
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[stage]);
       if (++stage == kStages) {
