@@ -291,7 +291,8 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, uint32_t lan
 }
 
 // Decoupled look-back over chunk status words (single pass).  One full warp;
-// returns the exclusive prefix of `chunk`.  Window: 128 predecessors per round,
+// returns the exclusive prefix of `chunk` and publishes its inclusive prefix (its
+// aggregate was published by the consumers).  Window: 128 predecessors per round,
 // lane l / slot i reads predecessor pred - (32 i + l), nearest first.
 __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_t chunk, uint32_t total,
                                                        uint32_t lane) {
@@ -300,7 +301,7 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
     if (lane == 0) st_relaxed(P.status, tag | kFlagInc | total);
     return 0;
   }
-  if (lane == 0) st_relaxed(P.status + chunk, tag | kFlagAgg | total);
+  // (the chunk's aggregate was already published by the consumers when they finished it)
   unsigned long long prefix = 0;
   long long pred = static_cast<long long>(chunk) - 1;
   uint32_t spins = 0;
@@ -372,6 +373,22 @@ __device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, uin
     if (gidx >= P.cap) return;
     const uint32_t off = warp_inclusive_scan(c, lane) - c;
     const uint64_t ub = cbase + static_cast<uint64_t>(w * kWarpUnits + g * 32 + lane) * kUnitBytes;
+    if (tg <= kWarpStage) {            // common case: the group fits one staging round
+      uint32_t v = mkg, i = off;
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        v &= v - 1;
+        stage[i + (i >> 4)] = ub + bit;
+        ++i;
+      }
+      __syncwarp();
+      const uint32_t n = P.cap - gidx < tg ? static_cast<uint32_t>(P.cap - gidx) : tg;
+      uint64_t* dst = P.pos + gidx;
+      for (uint32_t k = lane; k < n; k += 32) st_stream_u64(dst + k, stage[k + (k >> 4)]);
+      __syncwarp();
+      gidx += tg;
+      continue;
+    }
     for (uint32_t R = 0; R < tg; R += kWarpStage) {
       if (c && off < R + kWarpStage && off + c > R) {
         uint32_t v = mkg;
@@ -574,6 +591,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 #pragma unroll
       for (int i = 0; i < kConsumerWarps; ++i) tot += S.red[i];
       if (ctid == 0) {
+        // publish the aggregate at once so successors' look-backs never wait for our queue
+        const uint32_t chunk = tile / kChunkTiles;
+        st_relaxed(P.status + chunk, P.tag | (chunk == 0 ? kFlagInc : kFlagAgg) | tot);
         S.slot[qh].chunk = tile / kChunkTiles;
         S.slot[qh].total = tot;
         S.slot[qh].ntiles = tpos;
