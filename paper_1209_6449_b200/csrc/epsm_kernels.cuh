@@ -58,12 +58,13 @@ constexpr int kWarpUnits = kChunkUnits / kConsumerWarps;         // 512 units pe
 constexpr int kGroups = kWarpUnits / 32;                         // 16 groups of 32 units
 static_assert(kGroups == kConsumerWarps, "flush group g is filled by consumer warp g");
 static_assert(kUnitsPerTile % kWarpUnits == 0, "a flush warp covers part of one tile");
-constexpr int kMaskBufs = 2;
+constexpr int kMaskBufs = 4;                                     // chunks parked awaiting their prefix
 constexpr int kSlots = 8;                                        // look-back queue depth
-constexpr int kWarpStage = 256;                                  // positions per warp round
+constexpr int kWarpStage = 128;                                  // positions per warp round
 constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
-constexpr int kLookbackWindow = 128;                             // statuses per look-back round
+constexpr int kLookbackWindow = 256;                             // statuses per look-back round
 
+static_assert(kMaskBufs <= 4 && kSlots <= 32, "bufq packs 4 slot ids; need/qpar are 32-bit masks");
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 constexpr uint32_t kNoSlot = 0xFFu;
 
@@ -291,8 +292,9 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, uint32_t lan
 }
 
 // Decoupled look-back over chunk status words (single pass).  One full warp;
+// window: kLookbackWindow statuses per round (kLookbackWindow / 32 loads per lane in flight).
 // returns the exclusive prefix of `chunk` and publishes its inclusive prefix (its
-// aggregate was published by the consumers).  Window: 128 predecessors per round,
+// aggregate was published by the consumers).  Window: kLookbackWindow predecessors per round,
 // lane l / slot i reads predecessor pred - (32 i + l), nearest first.
 __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_t chunk, uint32_t total,
                                                        uint32_t lane) {
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     const uint32_t cw = ctid >> 5;
     uint32_t stage = 0, phase = 0;
     uint32_t mb = 0;                           // mask buffer being filled
-    uint32_t bufq = kNoSlot | (kNoSlot << 8);  // byte b: slot of the unflushed chunk in buffer b
+    uint32_t bufq = 0xFFFFFFFFu;               // byte b: slot of the unflushed chunk in buffer b (FF: none)
     uint32_t qh = 0;                           // next look-back slot
     uint32_t need = 0;                         // bit q: lb_done[q] phase not consumed yet
     uint32_t qpar = 0;                         // bit q: parity of lb_done[q]'s next phase
@@ -602,8 +604,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       need |= 1u << qh;
       if (tot) {                         // keep the masks until the prefix is known
         bufq = (bufq & ~(0xFFu << (8 * mb))) | (qh << (8 * mb));
-        mb ^= 1u;
-        flush_buf(mb);                   // the other buffer's chunk (if any) goes out now
+        mb = (mb + 1) % kMaskBufs;
+        flush_buf(mb);                   // the oldest parked chunk (if any) goes out now
       }
       qh = (qh + 1 == kSlots) ? 0u : qh + 1;
       acc = 0;
@@ -615,8 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (lane == 0 && wsum) atomicAdd(P.occ, static_cast<unsigned long long>(wsum));
     } else {
       // ---- drain: flush the chunks still parked in mask buffers, then stop the look-back warp
-      flush_buf(mb ^ 1u);
-      flush_buf(mb);
+      for (uint32_t k = 0; k < kMaskBufs; ++k) flush_buf((mb + k) % kMaskBufs);
       take_slot(qh);
       if (ctid == 0) {
         S.slot[qh].chunk = kInfoEnd;
