@@ -11,7 +11,10 @@
 //                          avoid unaligned loads: shared memory is
 //                          byte addressable, so every alignment is read directly.
 //   warps 2-17  consumers  16 candidate starts ("alpha = 16") per
-//                          thread and unit, 4 units per thread and tile:
+//                          thread and unit, 4 units per thread and tile.  The 16
+//                          consumer warps never wait for each other (no block
+//                          barrier): per-chunk bookkeeping is one shared-memory
+//                          atomic, and each warp writes out its own slices:
 //       filter   EPSMa's shift-AND (Fig. 1 lines 5-9), packed:
 //                Z_k = OR_{i<F} ( S_i[k] XOR B_i ), S_i = the text shifted by i bytes,
 //                B_i = p_i * 0x01010101.  A zero byte j of Z_k
@@ -23,18 +26,17 @@
 //                (PAPER.md:124-128), last partial word masked.
 //       count    popcount of the 16-bit match mask r.
 //       masks    r is parked in a per-chunk shared-memory buffer (2 bytes per 16 text
-//                bytes) so the chunk's positions can be written once its global
-//                offset is known, without re-reading the text.  Chunks without any
-//                occurrence release their buffer at once.
+//                bytes; 4 buffers round robin) so the chunk's positions can be written
+//                once its global offset is known, without re-reading the text.
 //   warp 1      look-back  per chunk: publish the chunk's count, walk predecessors
 //                          128 at a time until an inclusive prefix is found
 //                          (decoupled look-back over 64-bit epoch-tagged status
 //                          words), publish the inclusive prefix.  Runs concurrently
 //                          with the consumers through an 8-deep slot queue.
-//   report       each consumer warp turns its 512 units of a finished chunk into
-//                positions chunk_base + unit*16 + {r} (Fig. 1
-//                line 11) in text order, stages them in its own shared-memory buffer
-//                and stores them coalesced at pos[prefix + ...].
+//   report       four chunks later each consumer warp turns ITS 16 slices (32 units
+//                each) of the parked chunk into positions chunk_base + unit*16 + {r}
+//                (Fig. 1 line 11), stages them in its own shared-
+//                memory buffer and stores them coalesced at pos[prefix + slice offset].
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -54,19 +56,19 @@ constexpr int kThreads = kConsumers + 64;                        // + producer +
 constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 2048
 constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 4
 constexpr int kChunkUnits = kChunkTiles * kUnitsPerTile;         // 8192
-constexpr int kWarpUnits = kChunkUnits / kConsumerWarps;         // 512 units per warp in a flush
-constexpr int kGroups = kWarpUnits / 32;                         // 16 groups of 32 units
-static_assert(kGroups == kConsumerWarps, "flush group g is filled by consumer warp g");
-static_assert(kUnitsPerTile % kWarpUnits == 0, "a flush warp covers part of one tile");
+// A slice = the 32 consecutive units (512 text bytes) one warp filters in one
+// (tile, j) step: unit = tile*2048 + j*512 + warp*32 + lane.  Text order of slices
+// is (tile, j, warp).
+constexpr int kSlices = kChunkTiles * kUnitsPerThread * kConsumerWarps;   // 256 per chunk
 constexpr int kMaskBufs = 4;                                     // chunks parked awaiting their prefix
 constexpr int kSlots = 8;                                        // look-back queue depth
 constexpr int kWarpStage = 128;                                  // positions per warp round
 constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
 constexpr int kLookbackWindow = 256;                             // statuses per look-back round
+static_assert(kSlots % kMaskBufs == 0 && kSlots >= 2 * kMaskBufs, "slot / buffer rotation");
+static_assert(kSlices == 256, "the hand-off scan gives 8 slices to each lane");
 
-static_assert(kMaskBufs <= 4 && kSlots <= 32, "bufq packs 4 slot ids; need/qpar are 32-bit masks");
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
-constexpr uint32_t kNoSlot = 0xFFu;
 
 // Chunk status word: [63:40] epoch, [39:38] flag, [37:0] value.
 constexpr int kEpochShift = 40;
@@ -98,27 +100,35 @@ struct KParams {
   uint32_t pmask[9];            // per-word byte masks (partial last word)
 };
 
-struct ChunkSlot {
+struct ChunkSlot {              // consumers -> look-back warp
   uint32_t chunk;               // chunk id, or kInfoEnd
   uint32_t total;               // occurrences in the chunk
-  uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
+  uint32_t buf;                 // mask buffer holding the chunk
   uint32_t pad;
-  unsigned long long prefix;    // exclusive prefix (written by the look-back warp)
+};
+
+struct ParkedChunk {            // per mask buffer
+  uint32_t chunk;               // chunk id
+  uint32_t total;               // occurrences (hand-off warp)
+  uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
+  uint32_t done;                // consumer warps finished with the chunk (smem atomic)
+  unsigned long long prefix;    // exclusive prefix (look-back warp)
+  uint32_t cnt[kSlices];        // per-slice counts (each warp its own), then exclusive offsets
 };
 
 struct __align__(128) SmemLayout {
   uint8_t ring[kStages][kStageBytes];
   uint16_t masks[kMaskBufs][kChunkUnits];
   uint64_t wstage[kConsumerWarps][kWarpStagePad];
+  ParkedChunk park[kMaskBufs];
+  uint32_t off[kMaskBufs][kSlices];   // exclusive slice offsets inside the chunk
   uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t lb_full[kSlots];
   uint64_t lb_done[kSlots];
   ChunkSlot slot[kSlots];
   uint32_t info[kStages];       // tile index | (last-of-chunk << 31), or kInfoEnd
-  uint8_t wflag[kMaskBufs][kChunkTiles][kConsumerWarps];   // 1: the warp stored masks for the tile
-  uint32_t red[kConsumerWarps];
-  uint32_t scan[kConsumerWarps];
+  uint32_t fin;                 // consumer warps that reached the end
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -188,9 +198,6 @@ __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ void consumer_sync() {   // named barrier 1: the 512 consumer threads
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
-}
 
 // ------------------------------------------------------------------ packed filter
 
@@ -340,80 +347,54 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
   return prefix;
 }
 
-// Write the positions of a finished chunk (masks in S.masks[b], look-back result in
-// S.slot[q]) at pos[prefix ...].  Warp w owns units [512 w, 512 w + 512) of the chunk,
-// i.e. a contiguous slice of the chunk's output.
-__device__ __forceinline__ void flush_chunk(const KParams& P, SmemLayout& S, uint32_t b, uint32_t q,
-                                            uint32_t ctid) {
-  const ChunkSlot slot = S.slot[q];
-  if (slot.total == 0 || slot.prefix >= P.cap) return;   // block-uniform
-  const uint32_t lane = ctid & 31u, w = ctid >> 5;
-  const uint32_t nunits = slot.ntiles * kUnitsPerTile;
-  const uint16_t* mrow = &S.masks[b][w * kWarpUnits + lane];
-  const uint32_t ulim = nunits > w * kWarpUnits + lane ? nunits - (w * kWarpUnits + lane) : 0u;
-  uint32_t cnt = 0;
-  const uint8_t* flag = S.wflag[b][w / (kUnitsPerTile / kWarpUnits)];   // group g <- filter warp g
-#pragma unroll
-  for (int g = 0; g < kGroups; ++g) cnt += (g * 32u < ulim && flag[g]) ? __popc(mrow[g * 32]) : 0u;
-  const uint32_t wtot = __reduce_add_sync(0xffffffffu, cnt);
-  if (lane == 0) S.scan[w] = wtot;
-  consumer_sync();
-  uint32_t wbase = 0;
-#pragma unroll
-  for (int i = 0; i < kConsumerWarps; ++i) wbase += (static_cast<uint32_t>(i) < w) ? S.scan[i] : 0u;
-  consumer_sync();                                   // S.scan is reused by the next flush
-  if (wtot == 0) return;
-  uint64_t gidx = slot.prefix + wbase;               // global index of this warp's first position
-  const uint64_t cbase = static_cast<uint64_t>(slot.chunk) * kChunkBytes + P.pos_bias;
-  uint64_t* stage = S.wstage[w];
+// Write this warp's slices of the chunk parked in buffer b (its masks, the slice
+// offsets computed at hand-off, the prefix from the look-back warp) at pos[...].
+// `slow` bit t: this warp stored masks for tile t of the chunk (else all zero).
+__device__ __forceinline__ void flush_slices(const KParams& P, SmemLayout& S, uint32_t b, uint32_t slow,
+                                             uint32_t cw, uint32_t lane) {
+  const ParkedChunk& pk = S.park[b];
+  if (pk.total == 0) return;                                  // warp-uniform
+  const unsigned long long prefix = pk.prefix;
+  if (prefix >= P.cap) return;
+  const uint64_t cbase = static_cast<uint64_t>(pk.chunk) * kChunkBytes + P.pos_bias;
+  uint64_t* stage = S.wstage[cw];
+  const uint32_t nt = pk.ntiles;
 #pragma unroll 1
-  for (int g = 0; g < kGroups; ++g) {
-    const uint32_t mkg = (g * 32u < ulim && flag[g]) ? mrow[g * 32] : 0u;
-    const uint32_t c = __popc(mkg);
-    const uint32_t tg = __reduce_add_sync(0xffffffffu, c);
-    if (tg == 0) continue;
-    if (gidx >= P.cap) return;
-    const uint32_t off = warp_inclusive_scan(c, lane) - c;
-    const uint64_t ub = cbase + static_cast<uint64_t>(w * kWarpUnits + g * 32 + lane) * kUnitBytes;
-    if (tg <= kWarpStage) {            // common case: the group fits one staging round
-      uint32_t v = mkg, i = off;
-      while (v) {
-        const int bit = __ffs(v) - 1;
-        v &= v - 1;
-        stage[i + (i >> 4)] = ub + bit;
-        ++i;
-      }
-      __syncwarp();
-      const uint32_t n = P.cap - gidx < tg ? static_cast<uint32_t>(P.cap - gidx) : tg;
-      uint64_t* dst = P.pos + gidx;
-      for (uint32_t k = lane; k < n; k += 32) st_stream_u64(dst + k, stage[k + (k >> 4)]);
-      __syncwarp();
-      gidx += tg;
-      continue;
-    }
-    for (uint32_t R = 0; R < tg; R += kWarpStage) {
-      if (c && off < R + kWarpStage && off + c > R) {
-        uint32_t v = mkg;
-        uint32_t idx = off;
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          if (idx >= R && idx < R + kWarpStage) {
-            const uint32_t i = idx - R;
-            stage[i + (i >> 4)] = ub + bit;
+  for (uint32_t t = 0; t < nt; ++t) {
+    if (!((slow >> t) & 1u)) continue;
+#pragma unroll 1
+    for (uint32_t j = 0; j < kUnitsPerThread; ++j) {
+      const uint32_t unit = t * kUnitsPerTile + j * kConsumers + cw * 32 + lane;
+      const uint32_t mk = S.masks[b][unit];
+      const uint32_t c = __popc(mk);
+      const uint32_t tg = __reduce_add_sync(0xffffffffu, c);
+      if (tg == 0) continue;
+      const uint64_t gidx = prefix + S.off[b][(t * kUnitsPerThread + j) * kConsumerWarps + cw];
+      if (gidx >= P.cap) return;                              // later slices are even further out
+      const uint32_t off = warp_inclusive_scan(c, lane) - c;
+      const uint64_t ub = cbase + static_cast<uint64_t>(unit) * kUnitBytes;
+      for (uint32_t R = 0; R < tg; R += kWarpStage) {
+        if (c && off < R + kWarpStage && off + c > R) {
+          uint32_t v = mk, idx = off;
+          while (v) {
+            const int bit = __ffs(v) - 1;
+            v &= v - 1;
+            if (idx >= R && idx < R + kWarpStage) {
+              const uint32_t i = idx - R;
+              stage[i + (i >> 4)] = ub + bit;
+            }
+            ++idx;
           }
-          ++idx;
         }
+        __syncwarp();
+        uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
+        if (gidx + R >= P.cap) n = 0;
+        else if (P.cap - (gidx + R) < n) n = static_cast<uint32_t>(P.cap - (gidx + R));
+        uint64_t* dst = P.pos + gidx + R;
+        for (uint32_t i = lane; i < n; i += 32) st_stream_u64(dst + i, stage[i + (i >> 4)]);
+        __syncwarp();
       }
-      __syncwarp();
-      uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
-      if (gidx + R >= P.cap) n = 0;
-      else if (P.cap - (gidx + R) < n) n = static_cast<uint32_t>(P.cap - (gidx + R));
-      uint64_t* dst = P.pos + gidx + R;
-      for (uint32_t i = lane; i < n; i += 32) st_stream_u64(dst + i, stage[i + (i >> 4)]);
-      __syncwarp();
     }
-    gidx += tg;
   }
 }
 
@@ -438,6 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       mbar_init(&S.lb_full[q], 1);
       mbar_init(&S.lb_done[q], 1);
     }
+    for (int b = 0; b < kMaskBufs; ++b) S.park[b].done = 0;
+    S.fin = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -493,13 +476,12 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     uint32_t q = 0, par = 0;
     while (true) {
       mbar_wait(&S.lb_full[q], par);
-      const uint32_t chunk = S.slot[q].chunk;
-      if (chunk == kInfoEnd) break;
-      const uint32_t total = S.slot[q].total;
-      const unsigned long long pre = lookback(P, chunk, total, lane);
+      const ChunkSlot sl = S.slot[q];
+      if (sl.chunk == kInfoEnd) break;
+      const unsigned long long pre = lookback(P, sl.chunk, sl.total, lane);
       if (lane == 0) {
-        S.slot[q].prefix = pre;
-        if (chunk + 1 == P.nchunks) *P.occ = pre + total;
+        S.park[sl.buf].prefix = pre;
+        if (sl.chunk + 1 == P.nchunks) *P.occ = pre + sl.total;
         mbar_arrive(&S.lb_done[q]);
       }
       __syncwarp();
@@ -510,35 +492,25 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     }
   } else {
     // ================================================================ consumers
+    const uint32_t cw = warp - 2;
     const uint32_t ctid = tid - 64;
-    const uint32_t cw = ctid >> 5;
     uint32_t stage = 0, phase = 0;
-    uint32_t mb = 0;                           // mask buffer being filled
-    uint32_t bufq = 0xFFFFFFFFu;               // byte b: slot of the unflushed chunk in buffer b (FF: none)
-    uint32_t qh = 0;                           // next look-back slot
-    uint32_t need = 0;                         // bit q: lb_done[q] phase not consumed yet
-    uint32_t qpar = 0;                         // bit q: parity of lb_done[q]'s next phase
-    uint32_t acc = 0;                          // this thread's count in the current chunk
+    uint32_t seq = 0;                          // chunks this warp has started (same for all warps)
     uint32_t tpos = 0;                         // tile index inside the current chunk
+    uint32_t slowbits = 0;                     // bit 4b+t: masks stored for tile t of buffer b
+    uint32_t acc = 0;                          // count mode: this thread's occurrences
 
-    auto wait_slot = [&](uint32_t q) {
-      if ((need >> q) & 1u) {
-        mbar_wait(&S.lb_done[q], (qpar >> q) & 1u);
-        qpar ^= 1u << q;
-        need &= ~(1u << q);
-      }
+    // lb_done[q] completes once per chunk routed through slot q: chunk #k uses slot k % kSlots
+    // and phase parity (k / kSlots) & 1.
+    auto wait_done = [&](uint32_t k) {
+      mbar_wait(&S.lb_done[k % kSlots], (k / kSlots) & 1u);
     };
-    auto flush_buf = [&](uint32_t b) {
-      const uint32_t q = (bufq >> (8 * b)) & 0xFFu;
-      if (q == kNoSlot) return;
-      wait_slot(q);
-      flush_chunk(P, S, b, q, ctid);
-      bufq |= kNoSlot << (8 * b);
-    };
-    auto take_slot = [&](uint32_t q) {          // make slot q reusable
-      for (uint32_t b = 0; b < kMaskBufs; ++b)
-        if (((bufq >> (8 * b)) & 0xFFu) == q) flush_buf(b);
-      wait_slot(q);
+    // write out chunk #k's slices (parked in buffer k % kMaskBufs) once its prefix is known
+    auto flush_chunk_seq = [&](uint32_t k) {
+      const uint32_t b = k % kMaskBufs;
+      wait_done(k);
+      flush_slices(P, S, b, (slowbits >> (4 * b)) & 0xFu, cw, lane);
+      slowbits &= ~(0xFu << (4 * b));
     };
 
     while (true) {
@@ -547,8 +519,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (info == kInfoEnd) break;
       const uint32_t tile = info & 0x7FFFFFFFu;
       const bool last_in_chunk = info >> 31;
+      const uint32_t b = seq % kMaskBufs;
+      if (SEARCH && tpos == 0 && seq >= kMaskBufs) flush_chunk_seq(seq - kMaskBufs);   // free buffer b
       const uint8_t* ts = S.ring[stage];
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
+
       // filter all units first (independent chains), then one warp vote for the tile
       uint32_t Z[kUnitsPerThread][4];
       uint32_t hz = 0;
@@ -560,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         filter_words<F>(w, P, Z[j]);
         hz |= any_zero_byte(Z[j]);
       }
+      uint32_t cnt[kUnitsPerThread] = {};
       const bool slow = __any_sync(0xffffffffu, hz);
       if (slow) {
 #pragma unroll
@@ -570,58 +546,94 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           const uint64_t us = tbase + o;
           if (us < P.s_lo || us + 16 > P.s_hi) mask &= range_mask(us, P.s_lo, P.s_hi);
           if (MW > 1 && __any_sync(0xffffffffu, mask)) mask = verify_candidates<MW>(mask, ts, o, P);
-          if (SEARCH) S.masks[mb][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
-          acc += __popc(mask);
+          if (SEARCH) S.masks[b][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
+          cnt[j] = __popc(mask);
+          acc += cnt[j];
         }
       }
-      if (SEARCH && lane == 0) S.wflag[mb][tpos][cw] = slow;   // masks of this warp/tile are valid
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[stage]);
+      if (lane == 0) mbar_arrive(&S.empty[stage]);   // the text of this stage is no longer needed
       if (++stage == kStages) {
         stage = 0;
         phase ^= 1u;
       }
-      ++tpos;
-      if (!SEARCH || !last_in_chunk) continue;
+      if (!SEARCH) continue;
 
-      // ---- chunk complete: hand it to the look-back warp through slot qh
-      const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
-      if (lane == 0) S.red[cw] = wsum;
-      take_slot(qh);                    // (may flush an older chunk that still references qh)
-      consumer_sync();
-      uint32_t tot = 0;
+      // per-slice counts of this warp for this tile (zero unless the slow path ran)
+      uint32_t sc[kUnitsPerThread];
 #pragma unroll
-      for (int i = 0; i < kConsumerWarps; ++i) tot += S.red[i];
-      if (ctid == 0) {
-        // publish the aggregate at once so successors' look-backs never wait for our queue
-        const uint32_t chunk = tile / kChunkTiles;
-        st_relaxed(P.status + chunk, P.tag | (chunk == 0 ? kFlagInc : kFlagAgg) | tot);
-        S.slot[qh].chunk = tile / kChunkTiles;
-        S.slot[qh].total = tot;
-        S.slot[qh].ntiles = tpos;
-        mbar_arrive(&S.lb_full[qh]);
+      for (int j = 0; j < kUnitsPerThread; ++j) sc[j] = slow ? __reduce_add_sync(0xffffffffu, cnt[j]) : 0u;
+      if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < kUnitsPerThread; ++j) S.park[b].cnt[(tpos * kUnitsPerThread + j) * kConsumerWarps + cw] = sc[j];
       }
-      need |= 1u << qh;
-      if (tot) {                         // keep the masks until the prefix is known
-        bufq = (bufq & ~(0xFFu << (8 * mb))) | (qh << (8 * mb));
-        mb = (mb + 1) % kMaskBufs;
-        flush_buf(mb);                   // the oldest parked chunk (if any) goes out now
+      if (slow) slowbits |= 1u << (4 * b + tpos);
+      ++tpos;
+      if (!last_in_chunk) continue;
+
+      // ---- this warp is done with chunk #seq; the last warp to finish hands it off
+      const uint32_t chunk = tile / kChunkTiles;
+      const uint32_t ntiles = tpos;
+      __syncwarp();
+      uint32_t prev = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        prev = atomicAdd(&S.park[b].done, 1u);
       }
-      qh = (qh + 1 == kSlots) ? 0u : qh + 1;
-      acc = 0;
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == kConsumerWarps - 1) {
+        __threadfence_block();
+        // exclusive prefix over the 256 slice counts, text order (tile, j, warp); tiles
+        // beyond the chunk's end count zero
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t s = lane * 8 + i;
+          v[i] = (s / (kUnitsPerThread * kConsumerWarps) < ntiles) ? S.park[b].cnt[s] : 0u;
+          sum += v[i];
+        }
+        const uint32_t incl = warp_inclusive_scan(sum, lane);
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          S.off[b][lane * 8 + i] = run;
+          run += v[i];
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (seq >= kSlots) wait_done(seq - kSlots);          // slot seq % kSlots is free again
+        if (lane == 0) {
+          S.park[b].done = 0;
+          S.park[b].chunk = chunk;
+          S.park[b].total = total;
+          S.park[b].ntiles = ntiles;
+          // publish the aggregate at once so successors' look-backs never wait for our queue
+          st_relaxed(P.status + chunk, P.tag | (chunk == 0 ? kFlagInc : kFlagAgg) | total);
+          const uint32_t q = seq % kSlots;
+          S.slot[q].chunk = chunk;
+          S.slot[q].total = total;
+          S.slot[q].buf = b;
+          mbar_arrive(&S.lb_full[q]);
+        }
+        __syncwarp();
+      }
+      ++seq;
       tpos = 0;
-      consumer_sync();                   // S.red reuse; mask buffer mb free for the next chunk
     }
+
     if constexpr (!SEARCH) {
       const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
       if (lane == 0 && wsum) atomicAdd(P.occ, static_cast<unsigned long long>(wsum));
     } else {
-      // ---- drain: flush the chunks still parked in mask buffers, then stop the look-back warp
-      for (uint32_t k = 0; k < kMaskBufs; ++k) flush_buf((mb + k) % kMaskBufs);
-      take_slot(qh);
-      if (ctid == 0) {
-        S.slot[qh].chunk = kInfoEnd;
-        mbar_arrive(&S.lb_full[qh]);
+      // ---- drain: write out the chunks still parked, then (last warp) stop the look-back warp
+      for (uint32_t k = seq > kMaskBufs ? seq - kMaskBufs : 0; k < seq; ++k) flush_chunk_seq(k);
+      uint32_t prev = 0;
+      if (lane == 0) prev = atomicAdd(&S.fin, 1u);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == kConsumerWarps - 1 && lane == 0) {
+        if (seq >= kSlots) mbar_wait(&S.lb_done[(seq - kSlots) % kSlots], ((seq - kSlots) / kSlots) & 1u);
+        const uint32_t q = seq % kSlots;
+        S.slot[q].chunk = kInfoEnd;
+        mbar_arrive(&S.lb_full[q]);
       }
     }
   }
