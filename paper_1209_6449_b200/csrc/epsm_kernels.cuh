@@ -174,6 +174,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
+// Bulk prefetch of global memory into L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // TMA bulk copy global -> shared, completion counted on an mbarrier (UBLKCP in SASS).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
@@ -442,7 +447,20 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
         break;
       }
-      if (lane == 0) next = atomicAdd(P.ctr, 1ull) - P.ctr_base;   // prefetch the next chunk id
+      if (lane == 0) {
+        next = atomicAdd(P.ctr, 1ull) - P.ctr_base;   // the next chunk id, one chunk ahead
+        if (next < P.nchunks) {
+          // pull the next chunk towards L2 now, so its TMA loads later hit L2: this deepens the
+          // pipeline beyond the shared-memory ring at no shared-memory cost
+          const uint64_t pb = next * static_cast<unsigned long long>(kChunkBytes);
+          const uint64_t pe_want = pb + kChunkBytes + kHalo;
+          const uint64_t pe = (pe_want < P.nbytes ? pe_want : P.nbytes) & ~15ull;
+          for (uint64_t a = pb; a < pe; a += kTile) {
+            const uint64_t e = a + kTile < pe ? a + kTile : pe;
+            bulk_prefetch_l2(P.text + a, static_cast<uint32_t>(e - a));
+          }
+        }
+      }
       const uint32_t t0 = static_cast<uint32_t>(chunk) * kChunkTiles;
       const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
       for (uint32_t t = t0; t < t1; ++t) {
