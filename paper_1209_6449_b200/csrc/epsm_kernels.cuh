@@ -92,8 +92,8 @@ struct KParams {
   unsigned long long tag;       // epoch << 40
   uint32_t ntiles;              // tiles covering [0, s_hi)
   uint32_t nchunks;
-  uint32_t mul8;                // 1 << 24: funnel shift by  8 bits as an IMAD pair
-  uint32_t mul24;               // 1 << 8 : funnel shift by 24 bits as an IMAD pair
+  uint32_t mul8;                // 1 << 24: byte shift by 1 through one IMAD.WIDE
+  uint32_t mul24;               // 1 << 8 : byte shift by 3 through one IMAD.WIDE
   uint32_t movemask_mul;        // 0x00204081
   uint32_t bcast[4];            // B_i = p_i * 0x01010101
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
@@ -206,25 +206,43 @@ __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
 
 // ------------------------------------------------------------------ packed filter
 
-// funnel shift right of the pair (hi:lo) by s bits, as two IMADs on the FMA pipe:
-// mul = 2^(32-s) (a run-time value, so ptxas keeps the multiplies).
-__device__ __forceinline__ uint32_t funnel_fma(uint32_t lo, uint32_t hi, uint32_t mul) {
-  uint32_t r;
-  asm("{\n.reg .u32 t;\nmul.lo.u32 t, %2, %3;\nmad.hi.u32 %0, %1, %3, t;\n}" : "=r"(r) : "r"(lo), "r"(hi), "r"(mul));
-  return r;
+// Filter words of one unit, in two stages (EPSMa's shift-AND):
+//   stage 1 (pair):   Z[k] = (S_0[k] ^ B_0) | (S_1[k] ^ B_1)
+//   stage 2 (extend): Z[k] |= (S_2[k] ^ B_2) | (S_3[k] ^ B_3)      (F > 2, F > 3)
+// so that byte j of Z[k] is zero iff t[u+4k+j+i] = p_i for all i < F.  S_i is the text
+// shifted by i bytes.  The shifts by 8 and 24 bits come from one 32x32->64 IMAD.WIDE per
+// word (FMA pipe): w*2^(32-s) holds w >> s in its high half and w << (32-s) in its low
+// half, so S_i[k] = hi(w_k * 2^(32-8i)) | lo(w_{k+1} * 2^(32-8i)); the two halves have
+// disjoint bits, so the OR is folded into the 3-input XOR with B_i.
+template <int F>
+__device__ __forceinline__ void filter_pair(const uint32_t (&w)[5], const KParams& P, uint32_t (&Z)[4]) {
+  if (F == 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) Z[k] = w[k] ^ P.bcast[0];
+    return;
+  }
+  uint64_t p8[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) p8[k] = static_cast<uint64_t>(w[k]) * P.mul8;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    Z[k] = (w[k] ^ P.bcast[0]) |
+           (static_cast<uint32_t>(p8[k] >> 32) ^ static_cast<uint32_t>(p8[k + 1]) ^ P.bcast[1]);
 }
 
-// Z words of one unit for an F-byte filter: byte j of Z[k] is zero iff the
-// F bytes starting at unit offset 4k+j equal p_0..p_{F-1}.
 template <int F>
-__device__ __forceinline__ void filter_words(const uint32_t (&w)[5], const KParams& P, uint32_t (&Z)[4]) {
+__device__ __forceinline__ void filter_extend(const uint32_t (&w)[5], const KParams& P, uint32_t (&Z)[4]) {
+  if (F > 2) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t z = w[k] ^ P.bcast[0];
-    if (F > 1) z |= funnel_fma(w[k], w[k + 1], P.mul8) ^ P.bcast[1];
-    if (F > 2) z |= __funnelshift_r(w[k], w[k + 1], 16) ^ P.bcast[2];
-    if (F > 3) z |= funnel_fma(w[k], w[k + 1], P.mul24) ^ P.bcast[3];
-    Z[k] = z;
+    for (int k = 0; k < 4; ++k) Z[k] |= __funnelshift_r(w[k], w[k + 1], 16) ^ P.bcast[2];
+  }
+  if (F > 3) {
+    uint64_t p24[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) p24[k] = static_cast<uint64_t>(w[k]) * P.mul24;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      Z[k] |= static_cast<uint32_t>(p24[k] >> 32) ^ static_cast<uint32_t>(p24[k + 1]) ^ P.bcast[3];
   }
 }
 
@@ -517,6 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     uint32_t tpos = 0;                         // tile index inside the current chunk
     uint32_t slowbits = 0;                     // bit 4b+t: masks stored for tile t of buffer b
     uint32_t acc = 0;                          // count mode: this thread's occurrences
+    bool try_pair = true;                      // test the pair stage on its own (adaptive)
+    uint32_t tiles_seen = 0;
 
     // lb_done[q] completes once per chunk routed through slot q: chunk #k uses slot k % kSlots
     // and phase parity (k / kSlots) & 1.
@@ -542,19 +562,50 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       const uint8_t* ts = S.ring[stage];
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
 
-      // filter all units first (independent chains), then one warp vote for the tile
+      // filter all units first (independent chains), then one warp vote per stage.  The pair
+      // stage is tested on its own only while it pays off (large alphabets: almost never a
+      // candidate); otherwise the words are extended to F bytes straight away.  Both paths
+      // give the same Z, so the adaptation never changes the result.
+      uint32_t W[kUnitsPerThread][5];
       uint32_t Z[kUnitsPerThread][4];
-      uint32_t hz = 0;
 #pragma unroll
       for (int j = 0; j < kUnitsPerThread; ++j) {
         const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
         const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
-        const uint32_t w[5] = {v.x, v.y, v.z, v.w, *reinterpret_cast<const uint32_t*>(ts + o + 16)};
-        filter_words<F>(w, P, Z[j]);
-        hz |= any_zero_byte(Z[j]);
+        W[j][0] = v.x;
+        W[j][1] = v.y;
+        W[j][2] = v.z;
+        W[j][3] = v.w;
+        W[j][4] = *reinterpret_cast<const uint32_t*>(ts + o + 16);
+        filter_pair<F>(W[j], P, Z[j]);
+      }
+      bool slow;
+      if constexpr (F > 2) {
+        bool need_extend = true;
+        if (try_pair) {
+          uint32_t hz = 0;
+#pragma unroll
+          for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
+          need_extend = __any_sync(0xffffffffu, hz);
+        }
+        try_pair = !need_extend || ((++tiles_seen & 15u) == 0);
+        slow = false;
+        if (need_extend) {
+          uint32_t hz = 0;
+#pragma unroll
+          for (int j = 0; j < kUnitsPerThread; ++j) {
+            filter_extend<F>(W[j], P, Z[j]);
+            hz |= any_zero_byte(Z[j]);
+          }
+          slow = __any_sync(0xffffffffu, hz);
+        }
+      } else {
+        uint32_t hz = 0;
+#pragma unroll
+        for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
+        slow = __any_sync(0xffffffffu, hz);
       }
       uint32_t cnt[kUnitsPerThread] = {};
-      const bool slow = __any_sync(0xffffffffu, hz);
       if (slow) {
 #pragma unroll
         for (int j = 0; j < kUnitsPerThread; ++j) {
