@@ -145,7 +145,7 @@ int epsm_ensure_occ(epsm_plan_t* plan) {
 }
 
 // One-time per (device, kernel variant): opt in to > 48 KiB of dynamic shared memory.
-static int set_smem_attr(KernelFn fn, int device) {
+static int set_smem_attr(KernelFn fn, int device, int smem) {
   static std::atomic<KernelFn> done[16][32];
   if (device < 0 || device >= 16) device = 15;
   for (auto& slot : done[device]) {
@@ -154,7 +154,7 @@ static int set_smem_attr(KernelFn fn, int device) {
     if (f == nullptr) break;
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sizeof(epsm::SmemLayout)));
+                                       smem);
   if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(max dynamic smem)");
   for (auto& slot : done[device]) {
     KernelFn expected = nullptr;
@@ -208,10 +208,11 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
   }
   KernelFn fn = kernel_for(plan->m, search);
-  rc = set_smem_attr(fn, plan->device);
+  const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
+  rc = set_smem_attr(fn, plan->device, smem);
   if (rc) return rc;
   const uint64_t grid = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
-  fn<<<static_cast<unsigned>(grid), epsm::kThreads, sizeof(epsm::SmemLayout), s>>>(P);
+  fn<<<static_cast<unsigned>(grid), epsm::kThreads, smem, s>>>(P);
   epsm_count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");

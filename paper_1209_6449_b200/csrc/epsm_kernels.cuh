@@ -39,6 +39,7 @@
 //                memory buffer and stores them coalesced at pos[prefix + slice offset].
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace epsm {
@@ -47,7 +48,8 @@ constexpr int kUnitBytes = 16;                                   // alpha
 constexpr int kTile = 32768;                                     // bytes per TMA stage
 constexpr int kHalo = 32;                                        // >= m-1, multiple of 16
 constexpr int kStageBytes = kTile + 64;                          // tile + halo + verify slack
-constexpr int kStages = 4;
+constexpr int kStagesSearch = 4;                                 // search: ring + 4 parked mask buffers
+constexpr int kStagesCount = 6;                                  // count: no mask buffers, deeper ring
 constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
 constexpr int kChunkBytes = kChunkTiles * kTile;
 constexpr int kConsumerWarps = 16;
@@ -60,7 +62,7 @@ constexpr int kChunkUnits = kChunkTiles * kUnitsPerTile;         // 8192
 // (tile, j) step: unit = tile*2048 + j*512 + warp*32 + lane.  Text order of slices
 // is (tile, j, warp).
 constexpr int kSlices = kChunkTiles * kUnitsPerThread * kConsumerWarps;   // 256 per chunk
-constexpr int kMaskBufs = 4;                                     // chunks parked awaiting their prefix
+constexpr int kMaskBufs = 4;                                     // chunks parked awaiting their prefix (search)
 constexpr int kSlots = 8;                                        // look-back queue depth
 constexpr int kWarpStage = 128;                                  // positions per warp round
 constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
@@ -116,20 +118,26 @@ struct ParkedChunk {            // per mask buffer
   uint32_t cnt[kSlices];        // per-slice counts (each warp its own), then exclusive offsets
 };
 
-struct __align__(128) SmemLayout {
-  uint8_t ring[kStages][kStageBytes];
-  uint16_t masks[kMaskBufs][kChunkUnits];
-  uint64_t wstage[kConsumerWarps][kWarpStagePad];
-  ParkedChunk park[kMaskBufs];
-  uint32_t off[kMaskBufs][kSlices];   // exclusive slice offsets inside the chunk
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+template <int STAGES, int MASKBUFS>
+struct __align__(128) SmemLayoutT {
+  static constexpr int kStages = STAGES;
+  uint8_t ring[STAGES][kStageBytes];
+  uint16_t masks[MASKBUFS][kChunkUnits];
+  uint64_t wstage[MASKBUFS ? kConsumerWarps : 1][kWarpStagePad];
+  ParkedChunk park[MASKBUFS ? MASKBUFS : 1];
+  uint32_t off[MASKBUFS ? MASKBUFS : 1][kSlices];   // exclusive slice offsets inside the chunk
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
   uint64_t lb_full[kSlots];
   uint64_t lb_done[kSlots];
   ChunkSlot slot[kSlots];
-  uint32_t info[kStages];       // tile index | (last-of-chunk << 31), or kInfoEnd
+  uint32_t info[STAGES];        // tile index | (last-of-chunk << 31), or kInfoEnd
   uint32_t fin;                 // consumer warps that reached the end
 };
+using SearchSmem = SmemLayoutT<kStagesSearch, kMaskBufs>;
+using CountSmem = SmemLayoutT<kStagesCount, 0>;
+template <bool SEARCH>
+using SmemFor = typename std::conditional<SEARCH, SearchSmem, CountSmem>::type;
 
 // ------------------------------------------------------------------ PTX helpers
 
@@ -373,7 +381,8 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
 // Write this warp's slices of the chunk parked in buffer b (its masks, the slice
 // offsets computed at hand-off, the prefix from the look-back warp) at pos[...].
 // `slow` bit t: this warp stored masks for tile t of the chunk (else all zero).
-__device__ __forceinline__ void flush_slices(const KParams& P, SmemLayout& S, uint32_t b, uint32_t slow,
+template <class Smem>
+__device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, uint32_t b, uint32_t slow,
                                              uint32_t cw, uint32_t lane) {
   const ParkedChunk& pk = S.park[b];
   if (pk.total == 0) return;                                  // warp-uniform
@@ -428,7 +437,9 @@ __device__ __forceinline__ void flush_slices(const KParams& P, SmemLayout& S, ui
 template <int F, int MW, bool SEARCH>
 __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  SmemLayout& S = *reinterpret_cast<SmemLayout*>(smem_raw);
+  using Smem = SmemFor<SEARCH>;
+  constexpr int kStages = Smem::kStages;
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
   const uint32_t warp = tid >> 5;
