@@ -121,6 +121,7 @@ struct ParkedChunk {            // per mask buffer
 template <int STAGES, int MASKBUFS>
 struct __align__(128) SmemLayoutT {
   static constexpr int kStages = STAGES;
+  static constexpr int kBufs = MASKBUFS;
   uint8_t ring[STAGES][kStageBytes];
   uint16_t masks[MASKBUFS][kChunkUnits];
   uint64_t wstage[MASKBUFS ? kConsumerWarps : 1][kWarpStagePad];
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       mbar_init(&S.lb_full[q], 1);
       mbar_init(&S.lb_done[q], 1);
     }
-    for (int b = 0; b < kMaskBufs; ++b) S.park[b].done = 0;
+    for (int b = 0; b < Smem::kBufs; ++b) S.park[b].done = 0;
     S.fin = 0;
     fence_mbar_init();
   }
