@@ -216,8 +216,9 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   epsm_count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
-  // every CTA fetches chunk ids until it draws one past the end: chunks + grid draws
-  plan->ctr_base += chunks + grid;
+  // CTAs start on chunks [0, grid) and draw the rest from the counter until one draw is past
+  // the end: (chunks - grid) useful draws + grid final draws
+  plan->ctr_base += chunks;
   return EPSM_OK;
 }
 

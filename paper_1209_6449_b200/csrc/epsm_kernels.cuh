@@ -464,9 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // ================================================================ producer
     const uint64_t policy = policy_evict_first();
     uint32_t stage = 0, phase = 0;
-    unsigned long long next = 0;
-    if (lane == 0) next = atomicAdd(P.ctr, 1ull) - P.ctr_base;
-    next = __shfl_sync(0xffffffffu, next, 0);
+    // chunk ids: the first one is static (blockIdx.x: no atomic on the start-up path), the
+    // rest come from a monotonic counter: gridDim.x + (atomicAdd(ctr) - ctr_base).  Every CTA
+    // draws until it gets an id >= nchunks, so a launch advances the counter by nchunks.
+    unsigned long long next = blockIdx.x;
     while (true) {
       const unsigned long long chunk = next;
       if (chunk >= P.nchunks) {
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         break;
       }
       if (lane == 0) {
-        next = atomicAdd(P.ctr, 1ull) - P.ctr_base;   // the next chunk id, one chunk ahead
+        next = gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base);   // the next chunk id, one chunk ahead
         if (next < P.nchunks) {
           // pull the next chunk towards L2 now, so its TMA loads later hit L2: this deepens the
           // pipeline beyond the shared-memory ring at no shared-memory cost
