@@ -5,6 +5,7 @@
 // convenience call.  The sharded (NCCL) call lives in epsm_sharded.cu.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <new>
@@ -87,12 +88,12 @@ int epsm_bind_device(epsm_plan_t* plan, const void* dptr) {
 
 static int ensure_workspace(epsm_plan_t* plan, uint64_t chunks, bool search, cudaStream_t s) {
   if (!plan->d_ctr) {
-    cudaError_t e = cudaMalloc(&plan->d_ctr, sizeof(unsigned long long));
+    cudaError_t e = cudaMalloc(&plan->d_ctr, 4 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
       epsm_set_error("cudaMalloc(ctr): %s", cudaGetErrorString(e));
       return EPSM_ENOMEM;
     }
-    e = cudaMemsetAsync(plan->d_ctr, 0, sizeof(unsigned long long), s);
+    e = cudaMemsetAsync(plan->d_ctr, 0, 4 * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(ctr)");
     plan->ctr_base = 0;
   }
@@ -163,6 +164,15 @@ static int set_smem_attr(KernelFn fn, int device, int smem) {
   return EPSM_OK;
 }
 
+// PDL on by default; EPSM_NO_PDL=1 turns it off (debugging / A-B timing).
+static bool plan_pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("EPSM_NO_PDL");
+    return !(v && v[0] && v[0] != '0');
+  }();
+  return on;
+}
+
 // Core launcher.  The device text is d_text[0..nbytes-1]; starts [0, nstarts) are
 // reported (nstarts <= nbytes - m + 1), each shifted by `base`.
 int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
@@ -203,18 +213,28 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   if (search) {
     P.status = plan->d_status;
     P.tag = static_cast<unsigned long long>(plan->epoch) << epsm::kEpochShift;
-  } else {
-    cudaError_t e = cudaMemsetAsync(d_occ, 0, sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
   }
   KernelFn fn = kernel_for(plan->m, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan->device, smem);
   if (rc) return rc;
   const uint64_t grid = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
-  fn<<<static_cast<unsigned>(grid), epsm::kThreads, smem, s>>>(P);
+  // programmatic dependent launch: the kernel's prologue (barrier setup, first chunk's TMA
+  // loads and filtering) overlaps the previous grid's tail; it waits (griddepcontrol.wait)
+  // before touching the workspace or any output
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(epsm::kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = plan_pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, P);
   epsm_count_launch();
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
   // CTAs start on chunks [0, grid) and draw the rest from the counter until one draw is past
   // the end: (chunks - grid) useful draws + grid final draws

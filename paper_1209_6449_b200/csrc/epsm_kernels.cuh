@@ -89,7 +89,8 @@ struct KParams {
   uint64_t cap;                 // capacity of pos
   unsigned long long* occ;      // device occ
   unsigned long long* status;   // one word per chunk (search)
-  unsigned long long* ctr;      // chunk-id counter (monotonic across launches)
+  unsigned long long* ctr;      // [0] chunk-id counter (monotonic across launches),
+                                // [1] count accumulator, [2] CTA ticket (both re-armed to 0)
   unsigned long long ctr_base;  // value of *ctr when this launch starts
   unsigned long long tag;       // epoch << 40
   uint32_t ntiles;              // tiles covering [0, s_hi)
@@ -181,6 +182,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+
+// Programmatic dependent launch (PDL): let the next grid in the stream start its prologue as
+// our CTAs retire, and wait for the previous grid before touching memory it may write.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Bulk prefetch of global memory into L2 (no shared memory, no completion tracking).
@@ -457,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     for (int b = 0; b < Smem::kBufs; ++b) S.park[b].done = 0;
     S.fin = 0;
     fence_mbar_init();
+    griddep_launch_dependents();   // the next grid may start its prologue as our CTAs retire
   }
   __syncthreads();
 
@@ -468,18 +479,12 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // rest come from a monotonic counter: gridDim.x + (atomicAdd(ctr) - ctr_base).  Every CTA
     // draws until it gets an id >= nchunks, so a launch advances the counter by nchunks.
     unsigned long long next = blockIdx.x;
-    while (true) {
-      const unsigned long long chunk = next;
-      if (chunk >= P.nchunks) {
-        mbar_wait(&S.empty[stage], phase ^ 1u);
-        if (lane == 0) {
-          S.info[stage] = kInfoEnd;
-          mbar_arrive(&S.full[stage]);
-        }
-        break;
-      }
+    bool first = true;
+    auto fetch_next = [&]() {
+      if (first) griddep_wait();   // the counter (and everything below) belongs to the previous grid
+      first = false;
       if (lane == 0) {
-        next = gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base);   // the next chunk id, one chunk ahead
+        next = gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base);   // the next chunk id
         if (next < P.nchunks) {
           // pull the next chunk towards L2 now, so its TMA loads later hit L2: this deepens the
           // pipeline beyond the shared-memory ring at no shared-memory cost
@@ -492,8 +497,23 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           }
         }
       }
+      next = __shfl_sync(0xffffffffu, next, 0);
+    };
+    while (true) {
+      const unsigned long long chunk = next;
+      if (chunk >= P.nchunks) {
+        mbar_wait(&S.empty[stage], phase ^ 1u);
+        if (lane == 0) {
+          S.info[stage] = kInfoEnd;
+          mbar_arrive(&S.full[stage]);
+        }
+        break;
+      }
       const uint32_t t0 = static_cast<uint32_t>(chunk) * kChunkTiles;
       const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
+      // the first chunk's loads are all issued before the (PDL) wait on the previous grid;
+      // afterwards the next id is fetched right after a chunk's first tile, one chunk ahead
+      const uint32_t fetch_after = first ? t1 - 1 : t0;
       for (uint32_t t = t0; t < t1; ++t) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
         const uint64_t base = static_cast<uint64_t>(t) * kTile;
@@ -516,12 +536,13 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           stage = 0;
           phase ^= 1u;
         }
+        if (t == fetch_after) fetch_next();
       }
-      next = __shfl_sync(0xffffffffu, next, 0);
     }
   } else if (warp == 1) {
     // ================================================================ look-back
     if (!SEARCH) return;
+    griddep_wait();
     uint32_t q = 0, par = 0;
     while (true) {
       mbar_wait(&S.lb_full[q], par);
@@ -549,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     uint32_t slowbits = 0;                     // bit 4b+t: masks stored for tile t of buffer b
     uint32_t acc = 0;                          // count mode: this thread's occurrences
     bool try_pair = true;                      // test the pair stage on its own (adaptive)
+    uint32_t pair_streak = 0;                  // consecutive pair tests that found candidates
     uint32_t tiles_seen = 0;
 
     // lb_done[q] completes once per chunk routed through slot q: chunk #k uses slot k % kSlots
@@ -601,7 +623,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
           need_extend = __any_sync(0xffffffffu, hz);
         }
-        try_pair = !need_extend || ((++tiles_seen & 15u) == 0);
+        // hysteresis: stop testing the pair stage alone after two hits in a row (small
+        // alphabets), retry every 16th tile
+        if (try_pair) pair_streak = need_extend ? pair_streak + 1 : 0u;
+        try_pair = pair_streak < 2 || ((++tiles_seen & 15u) == 0);
         slow = false;
         if (need_extend) {
           uint32_t hz = 0;
@@ -654,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (!last_in_chunk) continue;
 
       // ---- this warp is done with chunk #seq; the last warp to finish hands it off
+      if (seq == 0) griddep_wait();   // status words / outputs may still belong to the previous grid
       const uint32_t chunk = tile / kChunkTiles;
       const uint32_t ntiles = tpos;
       __syncwarp();
@@ -703,8 +729,24 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     }
 
     if constexpr (!SEARCH) {
+      // count: per-warp partials into the workspace accumulator; the CTA's last warp takes a
+      // ticket, and the last CTA publishes occ and re-arms the workspace (no memset per call)
+      griddep_wait();
       const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
-      if (lane == 0 && wsum) atomicAdd(P.occ, static_cast<unsigned long long>(wsum));
+      uint32_t prev = 0;
+      if (lane == 0) {
+        if (wsum) atomicAdd(P.ctr + 1, static_cast<unsigned long long>(wsum));
+        __threadfence();
+        prev = atomicAdd(&S.fin, 1u);
+        if (prev == kConsumerWarps - 1) {
+          const unsigned long long ticket = atomicAdd(P.ctr + 2, 1ull);
+          if (ticket == gridDim.x - 1) {
+            __threadfence();
+            *P.occ = atomicExch(P.ctr + 1, 0ull);
+            P.ctr[2] = 0;
+          }
+        }
+      }
     } else {
       // ---- drain: write out the chunks still parked, then (last warp) stop the look-back warp
       for (uint32_t k = seq > kMaskBufs ? seq - kMaskBufs : 0; k < seq; ++k) flush_chunk_seq(k);
