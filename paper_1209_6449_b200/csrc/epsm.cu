@@ -102,6 +102,14 @@ static int ensure_workspace(epsm_plan_t* plan, uint64_t chunks, bool search, cud
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
   }
   if (!search) return EPSM_OK;
+  if (!plan->d_park) {
+    const size_t bytes = static_cast<size_t>(plan->num_sms) * epsm::kScratchPerCta * sizeof(uint64_t);
+    cudaError_t e = cudaMalloc(&plan->d_park, bytes);
+    if (e != cudaSuccess) {
+      epsm_set_error("cudaMalloc(parked masks, %zu bytes): %s", bytes, cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+  }
   if (chunks > plan->status_cap) {
     if (plan->d_status) {
       cudaStreamSynchronize(s);
@@ -212,6 +220,7 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   P.ctr_base = plan->ctr_base;
   if (search) {
     P.status = plan->d_status;
+    P.scratch = plan->d_park;
     P.tag = static_cast<unsigned long long>(plan->epoch) << epsm::kEpochShift;
   }
   KernelFn fn = kernel_for(plan->m, search);
@@ -310,6 +319,7 @@ void epsm_plan_free(epsm_plan_t* plan) {
   }
   if (plan->d_status) cudaFree(plan->d_status);
   if (plan->d_ctr) cudaFree(plan->d_ctr);
+  if (plan->d_park) cudaFree(plan->d_park);
   if (plan->d_occ) cudaFree(plan->d_occ);
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);

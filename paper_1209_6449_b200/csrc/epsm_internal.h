@@ -20,6 +20,8 @@ struct epsm_plan_s {
   // chunk-id counter: monotonic across launches; ctr_base = its value at the next launch
   unsigned long long* d_ctr = nullptr;
   unsigned long long ctr_base = 0;
+  // parked match masks of the search kernel (per CTA, L2-resident), allocated on first search
+  uint64_t* d_park = nullptr;
   // occ readback for the synchronous calls
   unsigned long long* d_occ = nullptr;
   unsigned long long* h_occ = nullptr;

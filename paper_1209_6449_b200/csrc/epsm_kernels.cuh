@@ -2,13 +2,14 @@
 //
 // One persistent CTA per SM, warp-specialised:
 //
-//   warp 0      producer   fetches CHUNK ids (4 consecutive 32 KiB tiles = 128 KiB)
-//                          from a global counter and streams every tile plus a
-//                          32-byte halo (>= m-1 for m <= 32) into a 4-stage shared
-//                          memory ring with ONE TMA bulk copy per tile
-//                          (cp.async.bulk ... mbarrier::complete_tx).  The halo is
-//                          the GPU analogue of EPSMb's wsblend, which only exists to
-//                          avoid unaligned loads: shared memory is
+//   warp 0      producer   fetches CHUNK ids (4 consecutive 32 KiB tiles = 128 KiB; the
+//                          first one is static, the rest come from a global counter) and
+//                          streams every tile plus a 32-byte halo (>= m-1 for m <= 32)
+//                          into a shared-memory ring with ONE TMA bulk copy per tile
+//                          (cp.async.bulk ... mbarrier::complete_tx), and pulls the next
+//                          chunk into L2 ahead of time (cp.async.bulk.prefetch.L2).  The
+//                          halo is the GPU analogue of EPSMb's wsblend, which only exists
+//                          to avoid unaligned loads: shared memory is
 //                          byte addressable, so every alignment is read directly.
 //   warps 2-17  consumers  16 candidate starts ("alpha = 16") per
 //                          thread and unit, 4 units per thread and tile.  The 16
@@ -18,25 +19,30 @@
 //       filter   EPSMa's shift-AND (Fig. 1 lines 5-9), packed:
 //                Z_k = OR_{i<F} ( S_i[k] XOR B_i ), S_i = the text shifted by i bytes,
 //                B_i = p_i * 0x01010101.  A zero byte j of Z_k
-//                <=> t[u+4k+j+i] = p_i for all i < F = min(m, 4).  The byte shifts by
-//                8 and 24 bits run as IMAD pairs on the FMA pipe, the rest on the ALU
-//                pipe, so the two integer pipes share the work.
+//                <=> t[u+4k+j+i] = p_i for all i < F = min(m, 4).  Pair stage first,
+//                extended to F bytes only where the pair has candidates.
 //       verify   the "naive check" of each candidate for
 //                m > 4: word compares against the zero-padded pattern blocks P_i
 //                (PAPER.md:124-128), last partial word masked.
 //       count    popcount of the 16-bit match mask r.
-//       masks    r is parked in a per-chunk shared-memory buffer (2 bytes per 16 text
-//                bytes; 4 buffers round robin) so the chunk's positions can be written
-//                once its global offset is known, without re-reading the text.
-//   warp 1      look-back  per chunk: publish the chunk's count, walk predecessors
-//                          128 at a time until an inclusive prefix is found
-//                          (decoupled look-back over 64-bit epoch-tagged status
-//                          words), publish the inclusive prefix.  Runs concurrently
-//                          with the consumers through an 8-deep slot queue.
-//   report       four chunks later each consumer warp turns ITS 16 slices (32 units
+//       masks    tiles with candidates park their masks r (2 bytes per 16 text bytes)
+//                in a small per-CTA global scratch that stays in L2 (8 chunks, round
+//                robin), so the chunk's positions can be written once its global
+//                offset is known, without re-reading the text.
+//   warp 1      look-back  per chunk: walk the predecessors' status words 256 at a time
+//                          until an inclusive prefix is found (decoupled look-back over
+//                          64-bit epoch-tagged words), publish the inclusive prefix.  It
+//                          runs concurrently with the consumers through a 16-deep slot
+//                          queue; the consumers published the chunk's aggregate already.
+//   report       eight chunks later each consumer warp turns ITS 16 slices (32 units
 //                each) of the parked chunk into positions chunk_base + unit*16 + {r}
 //                (Fig. 1 line 11), stages them in its own shared-
-//                memory buffer and stores them coalesced at pos[prefix + slice offset].
+//                memory buffer and stores them coalesced (16-byte stores) at
+//                pos[prefix + slice offset].
+//
+// Launches use programmatic dependent launch: the prologue and the first chunk's loads
+// and filtering overlap the previous grid; griddepcontrol.wait precedes every access
+// to memory the previous grid may write (workspace, parked masks, outputs).
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -48,8 +54,8 @@ constexpr int kUnitBytes = 16;                                   // alpha
 constexpr int kTile = 32768;                                     // bytes per TMA stage
 constexpr int kHalo = 32;                                        // >= m-1, multiple of 16
 constexpr int kStageBytes = kTile + 64;                          // tile + halo + verify slack
-constexpr int kStagesSearch = 4;                                 // search: ring + 4 parked mask buffers
-constexpr int kStagesCount = 6;                                  // count: no mask buffers, deeper ring
+constexpr int kStagesSearch = 5;
+constexpr int kStagesCount = 6;
 constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
 constexpr int kChunkBytes = kChunkTiles * kTile;
 constexpr int kConsumerWarps = 16;
@@ -57,18 +63,20 @@ constexpr int kConsumers = kConsumerWarps * 32;                  // 512
 constexpr int kThreads = kConsumers + 64;                        // + producer + look-back warps
 constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 2048
 constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 4
-constexpr int kChunkUnits = kChunkTiles * kUnitsPerTile;         // 8192
 // A slice = the 32 consecutive units (512 text bytes) one warp filters in one
 // (tile, j) step: unit = tile*2048 + j*512 + warp*32 + lane.  Text order of slices
 // is (tile, j, warp).
 constexpr int kSlices = kChunkTiles * kUnitsPerThread * kConsumerWarps;   // 256 per chunk
-constexpr int kMaskBufs = 4;                                     // chunks parked awaiting their prefix (search)
-constexpr int kSlots = 8;                                        // look-back queue depth
-constexpr int kWarpStage = 128;                                  // positions per warp round
+constexpr int kParked = 8;                                       // chunks parked awaiting their prefix
+constexpr int kSlots = 16;                                       // look-back queue depth
+constexpr int kWarpStage = 256;                                  // positions per warp round
 constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
 constexpr int kLookbackWindow = 256;                             // statuses per look-back round
-static_assert(kSlots % kMaskBufs == 0 && kSlots >= 2 * kMaskBufs, "slot / buffer rotation");
-static_assert(kSlices == 256, "the hand-off scan gives 8 slices to each lane");
+// parked masks in global scratch: one u64 (4 units x 16 bits) per (chunk slot, tile, warp, lane)
+constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
+static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking rotation");
+static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
+static_assert(kSlices == 256 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 
@@ -91,7 +99,8 @@ struct KParams {
   unsigned long long* status;   // one word per chunk (search)
   unsigned long long* ctr;      // [0] chunk-id counter (monotonic across launches),
                                 // [1] count accumulator, [2] CTA ticket (both re-armed to 0)
-  unsigned long long ctr_base;  // value of *ctr when this launch starts
+  uint64_t* scratch;            // parked masks, kScratchPerCta u64 per CTA (search)
+  unsigned long long ctr_base;  // value of ctr[0] when this launch starts
   unsigned long long tag;       // epoch << 40
   uint32_t ntiles;              // tiles covering [0, s_hi)
   uint32_t nchunks;
@@ -106,28 +115,28 @@ struct KParams {
 struct ChunkSlot {              // consumers -> look-back warp
   uint32_t chunk;               // chunk id, or kInfoEnd
   uint32_t total;               // occurrences in the chunk
-  uint32_t buf;                 // mask buffer holding the chunk
+  uint32_t park;                // parking slot holding the chunk
   uint32_t pad;
 };
 
-struct ParkedChunk {            // per mask buffer
+struct ParkedChunk {            // per parking slot
   uint32_t chunk;               // chunk id
   uint32_t total;               // occurrences (hand-off warp)
   uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
   uint32_t done;                // consumer warps finished with the chunk (smem atomic)
   unsigned long long prefix;    // exclusive prefix (look-back warp)
-  uint32_t cnt[kSlices];        // per-slice counts (each warp its own), then exclusive offsets
+  uint8_t slow[kConsumerWarps]; // bit t: the warp parked masks for tile t (else all zero)
+  uint32_t cnt[kSlices];        // per-slice counts, layout [warp][tile][j] (valid where slow)
+  uint32_t off[kSlices];        // exclusive slice offsets inside the chunk, text order (hand-off)
 };
 
-template <int STAGES, int MASKBUFS>
+template <int STAGES, bool SEARCH>
 struct __align__(128) SmemLayoutT {
   static constexpr int kStages = STAGES;
-  static constexpr int kBufs = MASKBUFS;
+  static constexpr int kPark = SEARCH ? kParked : 1;
   uint8_t ring[STAGES][kStageBytes];
-  uint16_t masks[MASKBUFS][kChunkUnits];
-  uint64_t wstage[MASKBUFS ? kConsumerWarps : 1][kWarpStagePad];
-  ParkedChunk park[MASKBUFS ? MASKBUFS : 1];
-  uint32_t off[MASKBUFS ? MASKBUFS : 1][kSlices];   // exclusive slice offsets inside the chunk
+  uint64_t wstage[SEARCH ? kConsumerWarps : 1][SEARCH ? kWarpStagePad : 1];
+  ParkedChunk park[kPark];
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t lb_full[kSlots];
@@ -136,8 +145,8 @@ struct __align__(128) SmemLayoutT {
   uint32_t info[STAGES];        // tile index | (last-of-chunk << 31), or kInfoEnd
   uint32_t fin;                 // consumer warps that reached the end
 };
-using SearchSmem = SmemLayoutT<kStagesSearch, kMaskBufs>;
-using CountSmem = SmemLayoutT<kStagesCount, 0>;
+using SearchSmem = SmemLayoutT<kStagesSearch, true>;
+using CountSmem = SmemLayoutT<kStagesCount, false>;
 template <bool SEARCH>
 using SmemFor = typename std::conditional<SEARCH, SearchSmem, CountSmem>::type;
 
@@ -220,6 +229,26 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
 
 __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_stream_u64x2(uint64_t* p, uint64_t a, uint64_t b) {   // 16-byte aligned p
+  asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// parked match masks live in a small per-CTA global scratch that stays in L2
+__device__ __forceinline__ void st_keep_u64(uint64_t* p, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_keep_u64(const uint64_t* p, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
 }
 
 
@@ -389,54 +418,99 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
   return prefix;
 }
 
-// Write this warp's slices of the chunk parked in buffer b (its masks, the slice
-// offsets computed at hand-off, the prefix from the look-back warp) at pos[...].
-// `slow` bit t: this warp stored masks for tile t of the chunk (else all zero).
+// Stage the positions of one slice (lane: unit mask mk, c = popc(mk), off = exclusive
+// offset of the lane inside the slice, tg = slice total) in the warp's shared buffer and
+// store them coalesced at dst[0 .. min(tg, room)).  Positions of a unit are ub + bit.
+__device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint64_t room, uint32_t mk,
+                                            uint32_t c, uint32_t off, uint32_t tg, uint64_t ub,
+                                            uint32_t lane) {
+  for (uint32_t R = 0; R < tg; R += kWarpStage) {
+    if (tg <= kWarpStage) {
+      if (tg > 8 * 32) {
+        // dense slice: fixed 16-step loop, no divergence; rank of bit b = popc(mk below b)
+#pragma unroll
+        for (int bit = 0; bit < 16; ++bit) {
+          if ((mk >> bit) & 1u) {
+            const uint32_t i = off + __popc(mk & ((1u << bit) - 1u));
+            stage[i + (i >> 4)] = ub + static_cast<uint64_t>(bit);
+          }
+        }
+      } else {
+        uint32_t v = mk, i = off;
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          stage[i + (i >> 4)] = ub + static_cast<uint64_t>(bit);
+          ++i;
+        }
+      }
+    } else if (c && off < R + kWarpStage && off + c > R) {   // > 256 positions: two rounds
+      uint32_t v = mk, idx = off;
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        v &= v - 1;
+        if (idx >= R && idx < R + kWarpStage) {
+          const uint32_t i = idx - R;
+          stage[i + (i >> 4)] = ub + static_cast<uint64_t>(bit);
+        }
+        ++idx;
+      }
+    }
+    __syncwarp();
+    uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
+    if (room <= R) n = 0;
+    else if (room - R < n) n = static_cast<uint32_t>(room - R);
+    uint64_t* d = dst + R;
+    if (n) {
+      // 16-byte stores: peel one entry if d is only 8-byte aligned
+      const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
+      if (lead && lane == 0) st_stream_u64(d, stage[0]);
+      const uint32_t npairs = (n - lead) >> 1;
+      for (uint32_t k = lane; k < npairs; k += 32) {
+        const uint32_t e = lead + 2 * k;
+        st_stream_u64x2(d + e, stage[e + (e >> 4)], stage[(e + 1) + ((e + 1) >> 4)]);
+      }
+      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, stage[(n - 1) + ((n - 1) >> 4)]);
+    }
+    __syncwarp();
+  }
+}
+
+// Write this warp's slices of the chunk parked in slot b (its masks in the global
+// scratch, the slice offsets computed at hand-off, the prefix from the look-back warp)
+// at pos[...].  `slow` bit t: this warp parked masks for tile t (else all zero).
 template <class Smem>
-__device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, uint32_t b, uint32_t slow,
-                                             uint32_t cw, uint32_t lane) {
+__device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const uint64_t* scratch_cta,
+                                             uint32_t b, uint32_t slow, uint32_t cw, uint32_t lane,
+                                             uint64_t keep_pol) {
   const ParkedChunk& pk = S.park[b];
-  if (pk.total == 0) return;                                  // warp-uniform
+  if (pk.total == 0 || slow == 0) return;                      // warp-uniform
   const unsigned long long prefix = pk.prefix;
   if (prefix >= P.cap) return;
   const uint64_t cbase = static_cast<uint64_t>(pk.chunk) * kChunkBytes + P.pos_bias;
   uint64_t* stage = S.wstage[cw];
   const uint32_t nt = pk.ntiles;
-#pragma unroll 1
-  for (uint32_t t = 0; t < nt; ++t) {
-    if (!((slow >> t) & 1u)) continue;
+  uint64_t mk4[kChunkTiles];
+#pragma unroll
+  for (int t = 0; t < kChunkTiles; ++t)   // all loads first (L2 latency overlaps)
+    mk4[t] = (t < static_cast<int>(nt) && ((slow >> t) & 1u))
+                 ? ld_keep_u64(scratch_cta + ((b * kChunkTiles + t) * kConsumerWarps + cw) * 32 + lane, keep_pol)
+                 : 0ull;
+#pragma unroll
+  for (int t = 0; t < kChunkTiles; ++t) {
+    if (!((slow >> t) & 1u) || t >= static_cast<int>(nt)) continue;
 #pragma unroll 1
     for (uint32_t j = 0; j < kUnitsPerThread; ++j) {
-      const uint32_t unit = t * kUnitsPerTile + j * kConsumers + cw * 32 + lane;
-      const uint32_t mk = S.masks[b][unit];
+      const uint32_t mk = static_cast<uint32_t>(mk4[t] >> (16 * j)) & 0xFFFFu;
       const uint32_t c = __popc(mk);
       const uint32_t tg = __reduce_add_sync(0xffffffffu, c);
       if (tg == 0) continue;
-      const uint64_t gidx = prefix + S.off[b][(t * kUnitsPerThread + j) * kConsumerWarps + cw];
+      const uint64_t gidx = prefix + pk.off[(t * kUnitsPerThread + j) * kConsumerWarps + cw];
       if (gidx >= P.cap) return;                              // later slices are even further out
       const uint32_t off = warp_inclusive_scan(c, lane) - c;
-      const uint64_t ub = cbase + static_cast<uint64_t>(unit) * kUnitBytes;
-      for (uint32_t R = 0; R < tg; R += kWarpStage) {
-        if (c && off < R + kWarpStage && off + c > R) {
-          uint32_t v = mk, idx = off;
-          while (v) {
-            const int bit = __ffs(v) - 1;
-            v &= v - 1;
-            if (idx >= R && idx < R + kWarpStage) {
-              const uint32_t i = idx - R;
-              stage[i + (i >> 4)] = ub + bit;
-            }
-            ++idx;
-          }
-        }
-        __syncwarp();
-        uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
-        if (gidx + R >= P.cap) n = 0;
-        else if (P.cap - (gidx + R) < n) n = static_cast<uint32_t>(P.cap - (gidx + R));
-        uint64_t* dst = P.pos + gidx + R;
-        for (uint32_t i = lane; i < n; i += 32) st_stream_u64(dst + i, stage[i + (i >> 4)]);
-        __syncwarp();
-      }
+      const uint32_t unit = t * kUnitsPerTile + j * kConsumers + cw * 32 + lane;
+      write_slice(stage, P.pos + gidx, P.cap - gidx, mk, c, off, tg,
+                  cbase + static_cast<uint64_t>(unit) * kUnitBytes, lane);
     }
   }
 }
@@ -464,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       mbar_init(&S.lb_full[q], 1);
       mbar_init(&S.lb_done[q], 1);
     }
-    for (int b = 0; b < Smem::kBufs; ++b) S.park[b].done = 0;
+    for (int b = 0; b < Smem::kPark; ++b) S.park[b].done = 0;
     S.fin = 0;
     fence_mbar_init();
     griddep_launch_dependents();   // the next grid may start its prologue as our CTAs retire
@@ -481,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     unsigned long long next = blockIdx.x;
     bool first = true;
     auto fetch_next = [&]() {
-      if (first) griddep_wait();   // the counter (and everything below) belongs to the previous grid
+      if (first) griddep_wait();   // the counter belongs to the previous grid until it ends
       first = false;
       if (lane == 0) {
         next = gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base);   // the next chunk id
@@ -541,23 +615,24 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ================================================================ look-back
-    if (!SEARCH) return;
-    griddep_wait();
-    uint32_t q = 0, par = 0;
-    while (true) {
-      mbar_wait(&S.lb_full[q], par);
-      const ChunkSlot sl = S.slot[q];
-      if (sl.chunk == kInfoEnd) break;
-      const unsigned long long pre = lookback(P, sl.chunk, sl.total, lane);
-      if (lane == 0) {
-        S.park[sl.buf].prefix = pre;
-        if (sl.chunk + 1 == P.nchunks) *P.occ = pre + sl.total;
-        mbar_arrive(&S.lb_done[q]);
-      }
-      __syncwarp();
-      if (++q == kSlots) {
-        q = 0;
-        par ^= 1u;
+    if constexpr (SEARCH) {
+      griddep_wait();
+      uint32_t q = 0, par = 0;
+      while (true) {
+        mbar_wait(&S.lb_full[q], par);
+        const ChunkSlot sl = S.slot[q];
+        if (sl.chunk == kInfoEnd) break;
+        const unsigned long long pre = lookback(P, sl.chunk, sl.total, lane);
+        if (lane == 0) {
+          S.park[sl.park].prefix = pre;
+          if (sl.chunk + 1 == P.nchunks) *P.occ = pre + sl.total;
+          mbar_arrive(&S.lb_done[q]);
+        }
+        __syncwarp();
+        if (++q == kSlots) {
+          q = 0;
+          par ^= 1u;
+        }
       }
     }
   } else {
@@ -567,22 +642,25 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     uint32_t stage = 0, phase = 0;
     uint32_t seq = 0;                          // chunks this warp has started (same for all warps)
     uint32_t tpos = 0;                         // tile index inside the current chunk
-    uint32_t slowbits = 0;                     // bit 4b+t: masks stored for tile t of buffer b
+    uint32_t slowbits = 0;                     // bit 4b+t: masks parked for tile t of slot b
     uint32_t acc = 0;                          // count mode: this thread's occurrences
     bool try_pair = true;                      // test the pair stage on its own (adaptive)
     uint32_t pair_streak = 0;                  // consecutive pair tests that found candidates
     uint32_t tiles_seen = 0;
+    bool waited = false;                       // griddepcontrol.wait done
+    uint64_t* scratch_cta = SEARCH ? P.scratch + static_cast<uint64_t>(blockIdx.x) * kScratchPerCta : nullptr;
+    const uint64_t keep_pol = policy_evict_last();
 
     // lb_done[q] completes once per chunk routed through slot q: chunk #k uses slot k % kSlots
     // and phase parity (k / kSlots) & 1.
     auto wait_done = [&](uint32_t k) {
       mbar_wait(&S.lb_done[k % kSlots], (k / kSlots) & 1u);
     };
-    // write out chunk #k's slices (parked in buffer k % kMaskBufs) once its prefix is known
+    // write out chunk #k's slices (parked in slot k % kParked) once its prefix is known
     auto flush_chunk_seq = [&](uint32_t k) {
-      const uint32_t b = k % kMaskBufs;
+      const uint32_t b = k % kParked;
       wait_done(k);
-      flush_slices(P, S, b, (slowbits >> (4 * b)) & 0xFu, cw, lane);
+      flush_slices(P, S, scratch_cta, b, (slowbits >> (4 * b)) & 0xFu, cw, lane, keep_pol);
       slowbits &= ~(0xFu << (4 * b));
     };
 
@@ -592,8 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (info == kInfoEnd) break;
       const uint32_t tile = info & 0x7FFFFFFFu;
       const bool last_in_chunk = info >> 31;
-      const uint32_t b = seq % kMaskBufs;
-      if (SEARCH && tpos == 0 && seq >= kMaskBufs) flush_chunk_seq(seq - kMaskBufs);   // free buffer b
+      const uint32_t b = seq % kParked;
+      if (SEARCH && tpos == 0 && seq >= kParked) flush_chunk_seq(seq - kParked);   // free slot b
       const uint8_t* ts = S.ring[stage];
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
 
@@ -622,10 +700,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 #pragma unroll
           for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
           need_extend = __any_sync(0xffffffffu, hz);
+          // hysteresis: stop testing the pair stage alone after two hits in a row (small
+          // alphabets), retry every 16th tile
+          pair_streak = need_extend ? pair_streak + 1 : 0u;
         }
-        // hysteresis: stop testing the pair stage alone after two hits in a row (small
-        // alphabets), retry every 16th tile
-        if (try_pair) pair_streak = need_extend ? pair_streak + 1 : 0u;
         try_pair = pair_streak < 2 || ((++tiles_seen & 15u) == 0);
         slow = false;
         if (need_extend) {
@@ -643,19 +721,32 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
         slow = __any_sync(0xffffffffu, hz);
       }
-      uint32_t cnt[kUnitsPerThread] = {};
       if (slow) {
+        uint32_t mask[kUnitsPerThread];
 #pragma unroll
         for (int j = 0; j < kUnitsPerThread; ++j) {
-          const uint32_t u = j * kConsumers + ctid;
-          const uint32_t o = u * kUnitBytes;
-          uint32_t mask = zero_byte_mask16(Z[j], P.movemask_mul);
+          const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+          mask[j] = zero_byte_mask16(Z[j], P.movemask_mul);
           const uint64_t us = tbase + o;
-          if (us < P.s_lo || us + 16 > P.s_hi) mask &= range_mask(us, P.s_lo, P.s_hi);
-          if (MW > 1 && __any_sync(0xffffffffu, mask)) mask = verify_candidates<MW>(mask, ts, o, P);
-          if (SEARCH) S.masks[b][tpos * kUnitsPerTile + u] = static_cast<uint16_t>(mask);
-          cnt[j] = __popc(mask);
-          acc += cnt[j];
+          if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
+          if (MW > 1 && __any_sync(0xffffffffu, mask[j])) mask[j] = verify_candidates<MW>(mask[j], ts, o, P);
+          acc += __popc(mask[j]);
+        }
+        if constexpr (SEARCH) {
+          if (!waited) {                       // the scratch may still be read by the previous grid
+            griddep_wait();
+            waited = true;
+          }
+          const uint64_t packed = static_cast<uint64_t>(mask[0]) | (static_cast<uint64_t>(mask[1]) << 16) |
+                                  (static_cast<uint64_t>(mask[2]) << 32) | (static_cast<uint64_t>(mask[3]) << 48);
+          st_keep_u64(scratch_cta + ((b * kChunkTiles + tpos) * kConsumerWarps + cw) * 32 + lane, packed, keep_pol);
+          uint4 sc;
+          sc.x = __reduce_add_sync(0xffffffffu, __popc(mask[0]));
+          sc.y = __reduce_add_sync(0xffffffffu, __popc(mask[1]));
+          sc.z = __reduce_add_sync(0xffffffffu, __popc(mask[2]));
+          sc.w = __reduce_add_sync(0xffffffffu, __popc(mask[3]));
+          if (lane == 0) *reinterpret_cast<uint4*>(&S.park[b].cnt[(cw * kChunkTiles + tpos) * kUnitsPerThread]) = sc;
+          slowbits |= 1u << (4 * b + tpos);
         }
       }
       __syncwarp();
@@ -664,24 +755,18 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         stage = 0;
         phase ^= 1u;
       }
-      if (!SEARCH) continue;
-
-      // per-slice counts of this warp for this tile (zero unless the slow path ran)
-      uint32_t sc[kUnitsPerThread];
-#pragma unroll
-      for (int j = 0; j < kUnitsPerThread; ++j) sc[j] = slow ? __reduce_add_sync(0xffffffffu, cnt[j]) : 0u;
-      if (lane == 0) {
-#pragma unroll
-        for (int j = 0; j < kUnitsPerThread; ++j) S.park[b].cnt[(tpos * kUnitsPerThread + j) * kConsumerWarps + cw] = sc[j];
-      }
-      if (slow) slowbits |= 1u << (4 * b + tpos);
+      if constexpr (!SEARCH) continue;
       ++tpos;
       if (!last_in_chunk) continue;
 
       // ---- this warp is done with chunk #seq; the last warp to finish hands it off
-      if (seq == 0) griddep_wait();   // status words / outputs may still belong to the previous grid
+      if (!waited) {                           // status words may still belong to the previous grid
+        griddep_wait();
+        waited = true;
+      }
       const uint32_t chunk = tile / kChunkTiles;
       const uint32_t ntiles = tpos;
+      if (lane == 0) S.park[b].slow[cw] = static_cast<uint8_t>((slowbits >> (4 * b)) & 0xFu);
       __syncwarp();
       uint32_t prev = 0;
       if (lane == 0) {
@@ -691,20 +776,24 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       prev = __shfl_sync(0xffffffffu, prev, 0);
       if (prev == kConsumerWarps - 1) {
         __threadfence_block();
-        // exclusive prefix over the 256 slice counts, text order (tile, j, warp); tiles
-        // beyond the chunk's end count zero
+        // exclusive prefix over the 256 slice counts in text order (tile, j, warp); slices of
+        // warps that parked nothing for a tile count zero
         uint32_t v[8], sum = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const uint32_t s = lane * 8 + i;
-          v[i] = (s / (kUnitsPerThread * kConsumerWarps) < ntiles) ? S.park[b].cnt[s] : 0u;
+          const uint32_t s = lane * 8 + i;                      // text order
+          const uint32_t t = s / (kUnitsPerThread * kConsumerWarps);
+          const uint32_t j = (s / kConsumerWarps) % kUnitsPerThread;
+          const uint32_t w = s % kConsumerWarps;
+          v[i] = (t < ntiles && ((S.park[b].slow[w] >> t) & 1u))
+                     ? S.park[b].cnt[(w * kChunkTiles + t) * kUnitsPerThread + j] : 0u;
           sum += v[i];
         }
         const uint32_t incl = warp_inclusive_scan(sum, lane);
         uint32_t run = incl - sum;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          S.off[b][lane * 8 + i] = run;
+          S.park[b].off[lane * 8 + i] = run;
           run += v[i];
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
@@ -719,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           const uint32_t q = seq % kSlots;
           S.slot[q].chunk = chunk;
           S.slot[q].total = total;
-          S.slot[q].buf = b;
+          S.slot[q].park = b;
           mbar_arrive(&S.lb_full[q]);
         }
         __syncwarp();
@@ -733,11 +822,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       // ticket, and the last CTA publishes occ and re-arms the workspace (no memset per call)
       griddep_wait();
       const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
-      uint32_t prev = 0;
       if (lane == 0) {
         if (wsum) atomicAdd(P.ctr + 1, static_cast<unsigned long long>(wsum));
         __threadfence();
-        prev = atomicAdd(&S.fin, 1u);
+        const uint32_t prev = atomicAdd(&S.fin, 1u);
         if (prev == kConsumerWarps - 1) {
           const unsigned long long ticket = atomicAdd(P.ctr + 2, 1ull);
           if (ticket == gridDim.x - 1) {
@@ -749,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
     } else {
       // ---- drain: write out the chunks still parked, then (last warp) stop the look-back warp
-      for (uint32_t k = seq > kMaskBufs ? seq - kMaskBufs : 0; k < seq; ++k) flush_chunk_seq(k);
+      for (uint32_t k = seq > kParked ? seq - kParked : 0; k < seq; ++k) flush_chunk_seq(k);
       uint32_t prev = 0;
       if (lane == 0) prev = atomicAdd(&S.fin, 1u);
       prev = __shfl_sync(0xffffffffu, prev, 0);
