@@ -119,15 +119,15 @@ struct ChunkSlot {              // consumers -> look-back warp
   uint32_t pad;
 };
 
-struct ParkedChunk {            // per parking slot
+struct __align__(16) ParkedChunk {   // per parking slot
+  uint32_t cnt[kSlices];        // per-slice counts, layout [warp][tile][j] (valid where slow)
+  uint32_t off[kSlices];        // exclusive slice offsets inside the chunk, text order (hand-off)
+  unsigned long long prefix;    // exclusive prefix (look-back warp)
   uint32_t chunk;               // chunk id
   uint32_t total;               // occurrences (hand-off warp)
   uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
   uint32_t done;                // consumer warps finished with the chunk (smem atomic)
-  unsigned long long prefix;    // exclusive prefix (look-back warp)
   uint8_t slow[kConsumerWarps]; // bit t: the warp parked masks for tile t (else all zero)
-  uint32_t cnt[kSlices];        // per-slice counts, layout [warp][tile][j] (valid where slow)
-  uint32_t off[kSlices];        // exclusive slice offsets inside the chunk, text order (hand-off)
 };
 
 template <int STAGES, bool SEARCH>
@@ -137,7 +137,7 @@ struct __align__(128) SmemLayoutT {
   uint8_t ring[STAGES][kStageBytes];
   uint64_t wstage[SEARCH ? kConsumerWarps : 1][SEARCH ? kWarpStagePad : 1];
   ParkedChunk park[kPark];
-  uint64_t full[STAGES];
+  alignas(8) uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t lb_full[kSlots];
   uint64_t lb_done[kSlots];
