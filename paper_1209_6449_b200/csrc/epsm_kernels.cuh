@@ -187,6 +187,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same, for waiters off the critical path (idle look-back warp, producer with a full ring):
+// the suspend-time hint lets the warp sleep in hardware instead of re-polling, which keeps
+// issue slots for the consumer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -503,14 +520,41 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
     for (uint32_t j = 0; j < kUnitsPerThread; ++j) {
       const uint32_t mk = static_cast<uint32_t>(mk4[t] >> (16 * j)) & 0xFFFFu;
       const uint32_t c = __popc(mk);
-      const uint32_t tg = __reduce_add_sync(0xffffffffu, c);
-      if (tg == 0) continue;
+      const uint32_t any = __ballot_sync(0xffffffffu, c != 0);
+      if (any == 0) continue;
       const uint64_t gidx = prefix + pk.off[(t * kUnitsPerThread + j) * kConsumerWarps + cw];
       if (gidx >= P.cap) return;                              // later slices are even further out
-      const uint32_t off = warp_inclusive_scan(c, lane) - c;
+      const uint64_t room = P.cap - gidx;
       const uint32_t unit = t * kUnitsPerTile + j * kConsumers + cw * 32 + lane;
-      write_slice(stage, P.pos + gidx, P.cap - gidx, mk, c, off, tg,
-                  cbase + static_cast<uint64_t>(unit) * kUnitBytes, lane);
+      const uint64_t ub = cbase + static_cast<uint64_t>(unit) * kUnitBytes;
+      const uint32_t lt = (1u << lane) - 1u;
+      if (__ballot_sync(0xffffffffu, c > 1) == 0) {
+        // sparse slice (<= 1 position per unit): lanes store straight to consecutive slots,
+        // which one warp store coalesces -- no staging, no scan
+        const uint32_t off = __popc(any & lt);
+        if (c && off < room) st_stream_u64(P.pos + gidx + off, ub + static_cast<uint64_t>(__ffs(mk) - 1));
+        continue;
+      }
+      // exclusive offsets from 5 bit-sliced ballots (c <= 16): independent ops, no shuffle chain
+      uint32_t off = 0, tg = 0;
+#pragma unroll
+      for (int bb = 0; bb < 5; ++bb) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (c >> bb) & 1u);
+        off += __popc(bal & lt) << bb;
+        tg += __popc(bal) << bb;
+      }
+      if (tg <= 64) {
+        // moderately sparse: direct stores, lane by lane in bit order
+        uint32_t v = mk, i = off;
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          if (i < room) st_stream_u64(P.pos + gidx + i, ub + static_cast<uint64_t>(bit));
+          ++i;
+        }
+        continue;
+      }
+      write_slice(stage, P.pos + gidx, room, mk, c, off, tg, ub, lane);
     }
   }
 }
@@ -589,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       // afterwards the next id is fetched right after a chunk's first tile, one chunk ahead
       const uint32_t fetch_after = first ? t1 - 1 : t0;
       for (uint32_t t = t0; t < t1; ++t) {
-        mbar_wait(&S.empty[stage], phase ^ 1u);
+        mbar_wait_sleep(&S.empty[stage], phase ^ 1u, 200);
         const uint64_t base = static_cast<uint64_t>(t) * kTile;
         const uint64_t want_end = base + kTile + kHalo;
         const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
@@ -619,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       griddep_wait();
       uint32_t q = 0, par = 0;
       while (true) {
-        mbar_wait(&S.lb_full[q], par);
+        mbar_wait_sleep(&S.lb_full[q], par, 500);
         const ChunkSlot sl = S.slot[q];
         if (sl.chunk == kInfoEnd) break;
         const unsigned long long pre = lookback(P, sl.chunk, sl.total, lane);

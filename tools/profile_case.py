@@ -22,6 +22,11 @@ pats, _ = synth.extract_patterns_torch(t, (2, a.sigma, a.m), a.m, a.reps)
 out = torch.empty(a.n, dtype=torch.int64, device=dev)
 occ = torch.zeros(1, dtype=torch.int64, device=dev)
 plans = [epsm.plan(p) for p in pats]
+for pl in plans:   # warm-up: workspace allocation happens on a plan's first call
+    if a.count:
+        epsm.count_async(pl, t, occ)
+    else:
+        epsm.search_async(pl, t, out, occ)
 torch.cuda.synchronize()
 evs = []
 for pl in plans:
