@@ -58,7 +58,18 @@ def parse():
     ap.add_argument("--sigmas", default=",".join(map(str, SIGMAS)))
     ap.add_argument("--ms", default=",".join(map(str, MS)))
     ap.add_argument("--out", default=None, help="also write the JSON line here")
+    ap.add_argument("--breakdown", action="store_true", help="per-(sigma, m) timing pass (stderr)")
     return ap.parse_args()
+
+
+def traffic_per_launch():
+    """DRAM bytes (read + write) per launch of the search kernel over the bench's launch mix,
+    from the committed ncu capture summary (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
 
 
 def peaks():
@@ -231,7 +242,8 @@ def run_epsm(args, world, rank, local):
                 assert epsm.count(pl, texts[ti][5]) == occ0[j], "count != search occ"
     torch.cuda.synchronize()
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(jobs))] for _ in range(args.steps)]
+    # timed region: K steps of back-to-back launches on one stream, nothing in between (the
+    # kernels chain with programmatic dependent launch); CUDA events bracket the region
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = epsm.launch_count()
     with ClockSampler(local) as clk:
@@ -239,7 +251,7 @@ def run_epsm(args, world, rank, local):
         torch.cuda.synchronize()
         start.record(stream)
         for k in range(args.steps):
-            one_step(ev[k])
+            one_step()
         stop.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -248,34 +260,40 @@ def run_epsm(args, world, rank, local):
     ms_step = ms_total / args.steps
     value = n_text_step * args.steps / (ms_total * 1e-3) / 1e9
 
-    # roofline of the scan kernel: algorithmic bytes = n + 8 * min(occ, cap) per launch
+    # roofline of the scan kernel (the only kernel in the region): algorithmic bytes =
+    # n + 8 * min(occ, cap) per launch; average launch duration = region time / launches
     occ = occ_buf.cpu().numpy().astype(np.int64)
-    kernel_ms = 0.0
-    for k in range(args.steps):
-        for j in range(len(jobs)):
-            kernel_ms += ev[k][2 * j].elapsed_time(ev[k][2 * j + 1])
     local_bytes = [texts[ti][5].numel() for ti, _ in jobs]
-    per = {}
-    for j, (ti, pl) in enumerate(jobs):
-        key = (texts[ti][0], pl.m)
-        d = sum(ev[k][2 * j].elapsed_time(ev[k][2 * j + 1]) for k in range(args.steps)) / args.steps
-        a = per.setdefault(key, [0.0, 0, 0])
-        a[0] += d
-        a[1] += 1
-        a[2] += local_bytes[j] + 8 * min(int(occ[j]), cap)
-    breakdown = []
-    for (s, m), (d, c, b) in sorted(per.items()):
-        us = d / c * 1e3
-        breakdown.append([s, m, round(us, 2), round(local_bytes[0] / (us * 1e-6) / 1e9, 1),
-                          round(b / c / (us * 1e-6) / 1e9, 1)])
-    if rank == 0:
-        print("sigma m  us/search  text_GB/s  alg_GB/s", file=sys.stderr)
-        for row in breakdown:
-            print("%5d %2d %10.2f %10.1f %9.1f" % tuple(row), file=sys.stderr)
     alg_bytes = sum(nb + 8 * min(int(o), cap) for nb, o in zip(local_bytes, occ)) * args.steps
+    kernel_ms = ms_total
     hbm_peak, peak_src = peaks()
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
     clocks = clk.summary()
+
+    # per-(sigma, m) breakdown, outside the timed region (events between launches stop the
+    # launches from overlapping, so these per-search times are slightly pessimistic)
+    breakdown = []
+    if args.breakdown:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(jobs))]
+        one_step(ev)
+        torch.cuda.synchronize()
+        per = {}
+        for j, (ti, pl) in enumerate(jobs):
+            key = (texts[ti][0], pl.m)
+            d = ev[2 * j].elapsed_time(ev[2 * j + 1])
+            a = per.setdefault(key, [0.0, 0, 0])
+            a[0] += d
+            a[1] += 1
+            a[2] += local_bytes[j] + 8 * min(int(occ[j]), cap)
+        for (s_, m), (d, c, b_) in sorted(per.items()):
+            us = d / c * 1e3
+            breakdown.append([s_, m, round(us, 2), round(local_bytes[0] / (us * 1e-6) / 1e9, 1),
+                              round(b_ / c / (us * 1e-6) / 1e9, 1)])
+        if rank == 0:
+            print("sigma m  us/search  text_GB/s  alg_GB/s", file=sys.stderr)
+            for row in breakdown:
+                print("%5d %2d %10.2f %10.1f %9.1f" % tuple(row), file=sys.stderr)
+    traffic = traffic_per_launch()
 
     res = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -288,14 +306,17 @@ def run_epsm(args, world, rank, local):
                    "l2": "no flush: every text (256 MiB) is larger than the 126 MB L2",
                    "parallelism": f"dp{world} over text shards" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                     "peak_source": peak_src, "kernel": "epsm_scan_kernel (search)",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, copy read+write)",
+                     "kernel": "epsm_scan_kernel (search), the only kernel in the timed region",
                      "per_launch_ms": round(kernel_ms / (args.steps * len(jobs)), 5),
-                     "kernel_share_of_step": round(kernel_ms / ms_total, 4)},
+                     "alg_bytes_per_launch": int(alg_bytes / (args.steps * len(jobs))),
+                     "kernel_share_of_step": 1.0},
         "clocks": clocks,
         "gpu_launches": int(launches),
         "total_occ_per_step": int(occ.sum()),
-        "breakdown": {"cols": ["sigma", "m", "us_per_search", "text_GBps", "alg_GBps"], "rows": breakdown},
+        "breakdown": ({"cols": ["sigma", "m", "us_per_search", "text_GBps", "alg_GBps"], "rows": breakdown}
+                      if breakdown else None),
     }
     if not args.no_e2e:
         res["e2e"] = run_e2e(args, epsm, texts, pats, jobs, world, dev)

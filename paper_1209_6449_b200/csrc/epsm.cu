@@ -102,13 +102,22 @@ static int ensure_workspace(epsm_plan_t* plan, uint64_t chunks, bool search, cud
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
   }
   if (!search) return EPSM_OK;
-  if (!plan->d_park) {
-    const size_t bytes = static_cast<size_t>(plan->num_sms) * epsm::kScratchPerCta * sizeof(uint64_t);
+  // parked-mask scratch: 128 KiB per CTA of the grid this launch uses
+  const uint64_t ctas = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
+  if (ctas > plan->park_ctas) {
+    if (plan->d_park) {
+      cudaStreamSynchronize(s);
+      cudaFree(plan->d_park);
+      plan->d_park = nullptr;
+      plan->park_ctas = 0;
+    }
+    const size_t bytes = static_cast<size_t>(ctas) * epsm::kScratchPerCta * sizeof(uint64_t);
     cudaError_t e = cudaMalloc(&plan->d_park, bytes);
     if (e != cudaSuccess) {
       epsm_set_error("cudaMalloc(parked masks, %zu bytes): %s", bytes, cudaGetErrorString(e));
       return EPSM_ENOMEM;
     }
+    plan->park_ctas = ctas;
   }
   if (chunks > plan->status_cap) {
     if (plan->d_status) {

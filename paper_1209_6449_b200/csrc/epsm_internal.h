@@ -22,6 +22,7 @@ struct epsm_plan_s {
   unsigned long long ctr_base = 0;
   // parked match masks of the search kernel (per CTA, L2-resident), allocated on first search
   uint64_t* d_park = nullptr;
+  uint64_t park_ctas = 0;
   // occ readback for the synchronous calls
   unsigned long long* d_occ = nullptr;
   unsigned long long* h_occ = nullptr;
