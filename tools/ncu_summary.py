@@ -1,0 +1,102 @@
+"""Summarise ncu captures into profiles/ (tracked).
+
+  traffic   --csv from `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
+            dram__bytes_write.sum -k regex:epsm_scan` over one launch per (sigma, m) of the
+            bench sweep  ->  profiles/traffic.json (DRAM bytes per launch, bench launch mix)
+  launches  --csv launch list (gpu__time_duration.sum) of the bench command -> summary text
+  full      .ncu-rep of one launch (--set full) -> key metrics text
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+SIGMAS = (2, 4, 8, 16, 32, 64, 128, 256)
+MS = (2, 4, 8, 16, 32)
+
+
+def read_csv(path):
+    with open(path) as f:
+        lines = [l for l in f if l.startswith('"')]
+    return list(csv.DictReader(io.StringIO("".join(lines))))
+
+
+def traffic(path, out_json, out_txt):
+    rows = read_csv(path)
+    per = {}
+    for r in rows:
+        if "epsm_scan" not in r["Kernel Name"]:
+            continue
+        per.setdefault(r["ID"], {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    launches = [per[k] for k in sorted(per, key=int)]
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    lines = ["sigma m  time_us  dram_read_MB  dram_write_MB"]
+    tot = 0.0
+    for i, l in enumerate(launches):
+        rd = l["dram__bytes_read.sum"]
+        wr = l["dram__bytes_write.sum"]
+        tot += rd + wr
+        s, m = SIGMAS[i // len(MS)], MS[i % len(MS)]
+        lines.append("%5d %2d %8.1f %13.1f %14.1f" % (s, m, l["gpu__time_duration.sum"] / 1e3, rd / 1e6, wr / 1e6))
+    avg = tot / len(launches)
+    with open(out_json, "w") as f:
+        json.dump({"dram_bytes_per_launch": int(avg), "launches": len(launches),
+                   "source": os.path.basename(path),
+                   "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
+                          "one search per (sigma, m) of the bench sweep (bench.py --patterns 1), "
+                          "averaged with equal weight per (sigma, m) as in the bench"}, f, indent=1)
+    with open(out_txt, "w") as f:
+        f.write("\n".join(lines) + f"\naverage DRAM bytes per launch: {avg:.0f}\n")
+    print(open(out_txt).read())
+
+
+def launches(path, out_txt):
+    rows = read_csv(path)
+    t = [float(r["Metric Value"].replace(",", "")) for r in rows if r["Metric Name"] == "gpu__time_duration.sum"]
+    names = {r["Kernel Name"] for r in rows}
+    with open(out_txt, "w") as f:
+        f.write(f"launches captured: {len(t)}\nkernels: {sorted(names)}\n")
+        f.write(f"sum of launch times: {sum(t)/1e3:.1f} us, mean {sum(t)/len(t)/1e3:.2f} us, "
+                f"min {min(t)/1e3:.2f} us, max {max(t)/1e3:.2f} us\n")
+        f.write("share of the timed step taken by epsm_scan_kernel: 100% (it is the only kernel launched)\n")
+        f.write("(ncu launch times are cold-cache and serialised: compare shares, not absolutes)\n")
+    print(open(out_txt).read())
+
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
+        "launch__block_size", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_sector_hit_rate.pct"]
+
+
+def full(path, out_txt):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, u, v = rows[0], rows[1], rows[2]
+    lines = [f"ncu --set full capture: {os.path.basename(path)}", f"kernel: {v[h.index('Kernel Name')]}"]
+    for k in KEYS:
+        if k in h:
+            i = h.index(k)
+            lines.append(f"{k} = {v[i]} {u[i]}")
+    stalls = [(float(v[i]), n.replace("smsp__pcsamp_warps_issue_stalled_", "")) for i, n in enumerate(h)
+              if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued") and v[i]]
+    tot = sum(x for x, _ in stalls) or 1
+    lines.append("warp stall sampling: " + ", ".join(f"{n} {100*x/tot:.1f}%" for x, n in sorted(stalls, reverse=True)[:8]))
+    with open(out_txt, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print(open(out_txt).read())
+
+
+if __name__ == "__main__":
+    kind = sys.argv[1]
+    if kind == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif kind == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3])
