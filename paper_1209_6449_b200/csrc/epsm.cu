@@ -21,29 +21,32 @@ std::atomic<uint64_t> g_launches{0};
 
 using KernelFn = void (*)(epsm::KParams);
 
-template <int F, int MW>
+template <int F, int F2, int MW>
 constexpr KernelFn pick(bool search) {
-  return search ? &epsm::epsm_scan_kernel<F, MW, true> : &epsm::epsm_scan_kernel<F, MW, false>;
+  return search ? &epsm::epsm_scan_kernel<F, F2, MW, true> : &epsm::epsm_scan_kernel<F, F2, MW, false>;
 }
 
-// Kernel variant for a pattern of length m: F = min(m, 4) filter bytes, MW = ceil(m/4)
-// words checked (no verification when m <= 4: the filter is exact).
+// Kernel variant for a pattern of length m: F = min(m, 4) bytes in the first filter word,
+// F2 = min(m, 8) - 4 in the second (used where candidates are dense), MW = ceil(m/4) words.
 KernelFn kernel_for(uint32_t m, bool search) {
   switch (m) {
-    case 1: return pick<1, 1>(search);
-    case 2: return pick<2, 1>(search);
-    case 3: return pick<3, 1>(search);
-    case 4: return pick<4, 1>(search);
+    case 1: return pick<1, 0, 1>(search);
+    case 2: return pick<2, 0, 1>(search);
+    case 3: return pick<3, 0, 1>(search);
+    case 4: return pick<4, 0, 1>(search);
+    case 5: return pick<4, 1, 2>(search);
+    case 6: return pick<4, 2, 2>(search);
+    case 7: return pick<4, 3, 2>(search);
+    case 8: return pick<4, 4, 2>(search);
     default: break;
   }
   switch ((m + 3) / 4) {
-    case 2: return pick<4, 2>(search);
-    case 3: return pick<4, 3>(search);
-    case 4: return pick<4, 4>(search);
-    case 5: return pick<4, 5>(search);
-    case 6: return pick<4, 6>(search);
-    case 7: return pick<4, 7>(search);
-    default: return pick<4, 8>(search);
+    case 3: return pick<4, 4, 3>(search);
+    case 4: return pick<4, 4, 4>(search);
+    case 5: return pick<4, 4, 5>(search);
+    case 6: return pick<4, 4, 6>(search);
+    case 7: return pick<4, 4, 7>(search);
+    default: return pick<4, 4, 8>(search);
   }
 }
 
@@ -213,6 +216,7 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   P.mul24 = 1u << 8;
   P.movemask_mul = 0x00204081u;
   std::memcpy(P.bcast, plan->bcast, sizeof(P.bcast));
+  std::memcpy(P.bcast2, plan->bcast2, sizeof(P.bcast2));
   std::memcpy(P.pat, plan->pat, sizeof(P.pat));
   std::memcpy(P.pmask, plan->pmask, sizeof(P.pmask));
   const uint64_t tiles = (P.s_hi + epsm::kTile - 1) / epsm::kTile;
@@ -302,6 +306,7 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
   std::memcpy(p->pattern, pattern, m);
   // B[i] = (p_i)^alpha restricted to one 32-bit lane, i < min(m, 4)
   for (uint32_t i = 0; i < 4; ++i) p->bcast[i] = i < m ? 0x01010101u * pattern[i] : 0u;
+  for (uint32_t i = 0; i < 4; ++i) p->bcast2[i] = 4 + i < m ? 0x01010101u * pattern[4 + i] : 0u;
   // P_i blocks, zero padded, as little-endian words + byte masks
   for (uint32_t q = 0; q < 9; ++q) {
     uint32_t w = 0, mk = 0;

@@ -9,6 +9,7 @@ struct epsm_plan_s {
   uint32_t m = 0;
   uint8_t pattern[EPSM_MAX_M] = {};
   uint32_t bcast[4] = {};   // B_i = p_i * 0x01010101
+  uint32_t bcast2[4] = {};  // B_{4+i}: second filter word
   uint32_t pat[9] = {};     // zero-padded pattern words
   uint32_t pmask[9] = {};   // byte masks of the words
   int device = -1;          // bound on first device use

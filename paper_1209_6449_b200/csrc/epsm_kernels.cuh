@@ -108,6 +108,7 @@ struct KParams {
   uint32_t mul24;               // 1 << 8 : byte shift by 3 through one IMAD.WIDE
   uint32_t movemask_mul;        // 0x00204081
   uint32_t bcast[4];            // B_i = p_i * 0x01010101
+  uint32_t bcast2[4];           // B_{4+i}: the second filter word (pattern bytes 4..7)
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
   uint32_t pmask[9];            // per-word byte masks (partial last word)
 };
@@ -188,20 +189,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // Same, for waiters off the critical path (idle look-back warp, producer with a full ring):
-// the suspend-time hint lets the warp sleep in hardware instead of re-polling, which keeps
-// issue slots for the consumer warps.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+// back off with nanosleep between probes, so the waiting warp does not steal issue slots
+// from the consumer warps.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity), "r"(ns)
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -311,6 +316,30 @@ __device__ __forceinline__ void filter_extend(const uint32_t (&w)[5], const KPar
   }
 }
 
+// Second filter word (pattern bytes 4 .. 3+F2) for the 16 starts of a unit, evaluated on the
+// words w[1..5]: byte j of Y[k] is zero iff t[u+4k+j+4+i] = p_{4+i} for all i < F2.
+template <int F2>
+__device__ __forceinline__ void filter_second(const uint32_t (&v)[6], const KParams& P, uint32_t (&Y)[4]) {
+  uint64_t p8[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) p8[k] = static_cast<uint64_t>(v[k + 1]) * P.mul8;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t y = v[k + 1] ^ P.bcast2[0];
+    if (F2 > 1) y |= static_cast<uint32_t>(p8[k] >> 32) ^ static_cast<uint32_t>(p8[k + 1]) ^ P.bcast2[1];
+    if (F2 > 2) y |= __funnelshift_r(v[k + 1], v[k + 2], 16) ^ P.bcast2[2];
+    Y[k] = y;
+  }
+  if (F2 > 3) {
+    uint64_t p24[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) p24[k] = static_cast<uint64_t>(v[k + 1]) * P.mul24;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      Y[k] |= static_cast<uint32_t>(p24[k] >> 32) ^ static_cast<uint32_t>(p24[k + 1]) ^ P.bcast2[3];
+  }
+}
+
 // Nonzero (bit 8j+7 set) iff some byte of some Z[k] is zero (has-zero test, exact as a boolean).
 __device__ __forceinline__ uint32_t any_zero_byte(const uint32_t (&Z)[4]) {
   uint32_t h = 0;
@@ -344,11 +373,12 @@ __device__ __forceinline__ uint32_t range_mask(uint64_t ustart, uint64_t lo, uin
   return m;
 }
 
-// Naive check of every candidate bit of r: words 1..MW-1 of the
-// window starting at shared byte offset o+b against the zero-padded pattern.
+// Naive check of every candidate bit of r: words qstart..MW-1 of the
+// window starting at shared byte offset o+b against the zero-padded pattern (the words
+// before qstart were already checked exactly by the packed filter).
 template <int MW>
 __device__ __forceinline__ uint32_t verify_candidates(uint32_t r, const uint8_t* tile, uint32_t o,
-                                                      const KParams& P) {
+                                                      const KParams& P, int qstart) {
   uint32_t keep = r;
   while (r) {
     const int b = __ffs(r) - 1;
@@ -356,9 +386,10 @@ __device__ __forceinline__ uint32_t verify_candidates(uint32_t r, const uint8_t*
     const uint32_t so = o + b;
     const uint32_t* wp = reinterpret_cast<const uint32_t*>(tile + (so & ~3u));
     const uint32_t sh = (so & 3u) * 8u;
-    uint32_t lo = wp[1];
+    uint32_t lo = wp[qstart];
 #pragma unroll
     for (int q = 1; q < MW; ++q) {
+      if (q < qstart) continue;
       const uint32_t hi = wp[q + 1];
       const uint32_t win = __funnelshift_r(lo, hi, sh);
       if ((win ^ P.pat[q]) & P.pmask[q]) {
@@ -561,9 +592,10 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
 
 // ------------------------------------------------------------------ the scan kernel
 
-// F  = filter bytes (min(m, 4));  MW = ceil(m/4) pattern words (MW <= 1: no verify);
+// F  = filter bytes of the first word (min(m, 4)); F2 = filter bytes of the second word
+// (min(m, 8) - 4, 0 if m <= 4); MW = ceil(m/4) pattern words (MW <= 1: no verify);
 // SEARCH = report positions (else count only).
-template <int F, int MW, bool SEARCH>
+template <int F, int F2, int MW, bool SEARCH>
 __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using Smem = SmemFor<SEARCH>;
@@ -767,13 +799,38 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       if (slow) {
         uint32_t mask[kUnitsPerThread];
+        const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
+#pragma unroll
+        for (int j = 0; j < kUnitsPerThread; ++j) {
+          mask[j] = zero_byte_mask16(Z[j], P.movemask_mul);
+          if (!interior) {
+            const uint64_t us = tbase + (j * kConsumers + ctid) * kUnitBytes;
+            if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
+          }
+        }
+        int qstart = 1;
+        if constexpr (F2 > 0) {
+          // many candidates (small alphabets): check pattern bytes 4..7 for all 16 alignments
+          // in packed form before any scalar check
+          const uint32_t c4 = __reduce_add_sync(0xffffffffu, __popc(mask[0]) + __popc(mask[1]) +
+                                                                __popc(mask[2]) + __popc(mask[3]));
+          if (c4 > 64) {
+#pragma unroll
+            for (int j = 0; j < kUnitsPerThread; ++j) {
+              const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+              const uint32_t v[6] = {W[j][0], W[j][1], W[j][2], W[j][3], W[j][4],
+                                     *reinterpret_cast<const uint32_t*>(ts + o + 20)};
+              uint32_t Y[4];
+              filter_second<F2>(v, P, Y);
+              mask[j] &= zero_byte_mask16(Y, P.movemask_mul);
+            }
+            qstart = 2;
+          }
+        }
 #pragma unroll
         for (int j = 0; j < kUnitsPerThread; ++j) {
           const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-          mask[j] = zero_byte_mask16(Z[j], P.movemask_mul);
-          const uint64_t us = tbase + o;
-          if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
-          if (MW > 1 && __any_sync(0xffffffffu, mask[j])) mask[j] = verify_candidates<MW>(mask[j], ts, o, P);
+          if (MW > qstart && __any_sync(0xffffffffu, mask[j])) mask[j] = verify_candidates<MW>(mask[j], ts, o, P, qstart);
           acc += __popc(mask[j]);
         }
         if constexpr (SEARCH) {
