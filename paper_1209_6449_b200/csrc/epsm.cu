@@ -106,8 +106,7 @@ static int ensure_workspace(epsm_plan_t* plan, uint64_t chunks, bool search, cud
   }
   if (!search) return EPSM_OK;
   // parked-mask scratch: 128 KiB per CTA of the grid this launch uses
-  const uint64_t max_ctas = static_cast<uint64_t>(plan->num_sms) * epsm::kCtasPerSm;
-  const uint64_t ctas = chunks < max_ctas ? chunks : max_ctas;
+  const uint64_t ctas = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
   if (ctas > plan->park_ctas) {
     if (plan->d_park) {
       cudaStreamSynchronize(s);
@@ -241,8 +240,7 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan->device, smem);
   if (rc) return rc;
-  const uint64_t max_grid = static_cast<uint64_t>(plan->num_sms) * epsm::kCtasPerSm;
-  const uint64_t grid = chunks < max_grid ? chunks : max_grid;
+  const uint64_t grid = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
   // programmatic dependent launch: the kernel's prologue (barrier setup, first chunk's TMA
   // loads and filtering) overlaps the previous grid's tail; it waits (griddepcontrol.wait)
   // before touching the workspace or any output

@@ -51,15 +51,14 @@
 namespace epsm {
 
 constexpr int kUnitBytes = 16;                                   // alpha
-constexpr int kTile = 16384;                                     // bytes per TMA stage
+constexpr int kTile = 32768;                                     // bytes per TMA stage
 constexpr int kHalo = 32;                                        // >= m-1, multiple of 16
 constexpr int kStageBytes = kTile + 64;                          // tile + halo + verify slack
 constexpr int kStagesSearch = 5;
 constexpr int kStagesCount = 6;
-constexpr int kChunkTiles = 8;                                   // 128 KiB look-back granularity
+constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
 constexpr int kChunkBytes = kChunkTiles * kTile;
-constexpr int kCtasPerSm = 2;                                    // two independent pipelines per SM
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = kConsumerWarps * 32;                  // 512
 constexpr int kThreads = kConsumers + 64;                        // + producer + look-back warps
 constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 2048
@@ -68,8 +67,8 @@ constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 4
 // (tile, j) step: unit = tile*2048 + j*512 + warp*32 + lane.  Text order of slices
 // is (tile, j, warp).
 constexpr int kSlices = kChunkTiles * kUnitsPerThread * kConsumerWarps;   // 256 per chunk
-constexpr int kParked = 4;                                       // chunks parked awaiting their prefix
-constexpr int kSlots = 8;                                        // look-back queue depth
+constexpr int kParked = 8;                                       // chunks parked awaiting their prefix
+constexpr int kSlots = 16;                                       // look-back queue depth
 constexpr int kWarpStage = 256;                                  // positions per warp round
 constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
 constexpr int kLookbackWindow = 256;                             // statuses per look-back round
@@ -77,8 +76,6 @@ constexpr int kLookbackWindow = 256;                             // statuses per
 constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
 static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking rotation");
 static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
-static_assert(kChunkTiles <= 8, "per-warp slow-tile bits of a chunk fit one byte");
-constexpr uint32_t kTileBitsMask = (1u << kChunkTiles) - 1u;
 static_assert(kSlices == 256 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
@@ -599,7 +596,7 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
 // (min(m, 8) - 4, 0 if m <= 4); MW = ceil(m/4) pattern words (MW <= 1: no verify);
 // SEARCH = report positions (else count only).
 template <int F, int F2, int MW, bool SEARCH>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) epsm_scan_kernel(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using Smem = SmemFor<SEARCH>;
   constexpr int kStages = Smem::kStages;
@@ -721,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) epsm_scan_kernel(const _
     uint32_t stage = 0, phase = 0;
     uint32_t seq = 0;                          // chunks this warp has started (same for all warps)
     uint32_t tpos = 0;                         // tile index inside the current chunk
-    uint32_t slowbits = 0;                     // bit kChunkTiles*b+t: masks parked for tile t of slot b
+    uint32_t slowbits = 0;                     // bit 4b+t: masks parked for tile t of slot b
     uint32_t acc = 0;                          // count mode: this thread's occurrences
     bool try_pair = true;                      // test the pair stage on its own (adaptive)
     uint32_t pair_streak = 0;                  // consecutive pair tests that found candidates
@@ -739,8 +736,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) epsm_scan_kernel(const _
     auto flush_chunk_seq = [&](uint32_t k) {
       const uint32_t b = k % kParked;
       wait_done(k);
-      flush_slices(P, S, scratch_cta, b, (slowbits >> (kChunkTiles * b)) & kTileBitsMask, cw, lane, keep_pol);
-      slowbits &= ~(kTileBitsMask << (kChunkTiles * b));
+      flush_slices(P, S, scratch_cta, b, (slowbits >> (4 * b)) & 0xFu, cw, lane, keep_pol);
+      slowbits &= ~(0xFu << (4 * b));
     };
 
     while (true) {
@@ -850,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) epsm_scan_kernel(const _
           sc.z = __reduce_add_sync(0xffffffffu, __popc(mask[2]));
           sc.w = __reduce_add_sync(0xffffffffu, __popc(mask[3]));
           if (lane == 0) *reinterpret_cast<uint4*>(&S.park[b].cnt[(cw * kChunkTiles + tpos) * kUnitsPerThread]) = sc;
-          slowbits |= 1u << (kChunkTiles * b + tpos);
+          slowbits |= 1u << (4 * b + tpos);
         }
       }
       __syncwarp();
@@ -870,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) epsm_scan_kernel(const _
       }
       const uint32_t chunk = tile / kChunkTiles;
       const uint32_t ntiles = tpos;
-      if (lane == 0) S.park[b].slow[cw] = static_cast<uint8_t>((slowbits >> (kChunkTiles * b)) & kTileBitsMask);
+      if (lane == 0) S.park[b].slow[cw] = static_cast<uint8_t>((slowbits >> (4 * b)) & 0xFu);
       __syncwarp();
       uint32_t prev = 0;
       if (lane == 0) {
