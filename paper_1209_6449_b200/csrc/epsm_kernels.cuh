@@ -628,30 +628,28 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // chunk ids: the first one is static (blockIdx.x: no atomic on the start-up path), the
     // rest come from a monotonic counter: gridDim.x + (atomicAdd(ctr) - ctr_base).  Every CTA
     // draws until it gets an id >= nchunks, so a launch advances the counter by nchunks.
-    unsigned long long next = blockIdx.x;
-    bool first = true;
-    auto fetch_next = [&]() {
-      if (first) griddep_wait();   // the counter belongs to the previous grid until it ends
-      first = false;
-      if (lane == 0) {
-        next = gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base);   // the next chunk id
-        if (next < P.nchunks) {
-          // pull the next chunk towards L2 now, so its TMA loads later hit L2: this deepens the
-          // pipeline beyond the shared-memory ring at no shared-memory cost
-          const uint64_t pb = next * static_cast<unsigned long long>(kChunkBytes);
-          const uint64_t pe_want = pb + kChunkBytes + kHalo;
-          const uint64_t pe = (pe_want < P.nbytes ? pe_want : P.nbytes) & ~15ull;
-          for (uint64_t a = pb; a < pe; a += kTile) {
-            const uint64_t e = a + kTile < pe ? a + kTile : pe;
-            bulk_prefetch_l2(P.text + a, static_cast<uint32_t>(e - a));
-          }
+    // chunk ids: the first one is static (blockIdx.x: no atomic on the start-up path), the
+    // rest come from a monotonic counter: gridDim.x + (atomicAdd(ctr) - ctr_base).  Every CTA
+    // draws until it gets an id >= nchunks, so a launch advances the counter by nchunks.
+    // Two ids are kept ahead: `after` (already known, pulled into L2 one chunk early) and a
+    // draw in flight whose result is only consumed when the current chunk has been issued,
+    // so the atomic's latency never stalls the TMA issue.
+    auto draw = [&]() -> unsigned long long { return gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base); };
+    auto prefetch_l2 = [&](unsigned long long c) {
+      if (lane == 0 && c < P.nchunks) {
+        const uint64_t pb = c * static_cast<unsigned long long>(kChunkBytes);
+        const uint64_t pe_want = pb + kChunkBytes + kHalo;
+        const uint64_t pe = (pe_want < P.nbytes ? pe_want : P.nbytes) & ~15ull;
+        for (uint64_t a = pb; a < pe; a += kTile) {
+          const uint64_t e = a + kTile < pe ? a + kTile : pe;
+          bulk_prefetch_l2(P.text + a, static_cast<uint32_t>(e - a));
         }
       }
-      next = __shfl_sync(0xffffffffu, next, 0);
     };
+    unsigned long long cur = blockIdx.x, after = 0, pend = 0;
+    bool first = true;
     while (true) {
-      const unsigned long long chunk = next;
-      if (chunk >= P.nchunks) {
+      if (cur >= P.nchunks) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
         if (lane == 0) {
           S.info[stage] = kInfoEnd;
@@ -659,13 +657,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
         break;
       }
-      const uint32_t t0 = static_cast<uint32_t>(chunk) * kChunkTiles;
+      const uint32_t t0 = static_cast<uint32_t>(cur) * kChunkTiles;
       const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
-      // the first chunk's loads are all issued before the (PDL) wait on the previous grid;
-      // afterwards the next id is fetched right after a chunk's first tile, one chunk ahead
-      const uint32_t fetch_after = first ? t1 - 1 : t0;
       for (uint32_t t = t0; t < t1; ++t) {
-        mbar_wait_sleep(&S.empty[stage], phase ^ 1u, 200);
+        mbar_wait(&S.empty[stage], phase ^ 1u);
         const uint64_t base = static_cast<uint64_t>(t) * kTile;
         const uint64_t want_end = base + kTile + kHalo;
         const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
@@ -681,13 +676,30 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           } else {
             mbar_arrive(&S.full[stage]);
           }
+          if (t == t0 && !first) pend = draw();   // consumed after this chunk
         }
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1u;
         }
-        if (t == fetch_after) fetch_next();
       }
+      if (first) {
+        // the first chunk's loads were issued before waiting on the previous grid (PDL)
+        griddep_wait();
+        if (lane == 0) {
+          after = draw();
+          pend = draw();
+        }
+        first = false;
+      }
+      unsigned long long nxt = 0;
+      if (lane == 0) {
+        nxt = after;
+        after = pend;
+      }
+      cur = __shfl_sync(0xffffffffu, nxt, 0);
+      after = __shfl_sync(0xffffffffu, after, 0);
+      prefetch_l2(after);
     }
   } else if (warp == 1) {
     // ================================================================ look-back
