@@ -258,9 +258,9 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   epsm_count_launch();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
-  // CTAs start on chunks [0, grid) and draw the rest from the counter until one draw is past
-  // the end: (chunks - grid) useful draws + grid final draws
-  plan->ctr_base += chunks;
+  // CTAs start on chunks [0, grid) and draw the rest from the counter, two draws ahead of the
+  // chunk they stream: (chunks - grid) useful draws + exactly 2 draws past the end per CTA
+  plan->ctr_base += chunks + grid;
   return EPSM_OK;
 }
 

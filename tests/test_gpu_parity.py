@@ -221,3 +221,26 @@ def test_launch_counter_moves(epsm, dev):
     before = epsm.launch_count()
     epsm.search(b"\x00\x00", td)
     assert epsm.launch_count() > before
+
+
+def test_plan_reuse_many_chunks(epsm, dev):
+    """One plan, many launches over a text of many chunks (> one CTA per SM): the chunk-id
+    counter bookkeeping and the status epochs must carry over launches exactly."""
+    rng = np.random.default_rng(77)
+    n = 300 * 128 * 1024 + 12345           # ~300 chunks of 128 KiB
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    p = t[5000:5006].tobytes()
+    want = oracle.search(p, t)
+    pl = epsm.plan(p)
+    out = torch.empty(want.size + 8, dtype=torch.int64, device=dev)
+    occ_d = torch.zeros(1, dtype=torch.int64, device=dev)
+    for i in range(5):
+        epsm.search_async(pl, td, out, occ_d)
+        epsm.count_async(pl, td, occ_d[0:1] if i % 2 else occ_d)
+    torch.cuda.synchronize()
+    assert int(occ_d.item()) == want.size
+    for _ in range(3):
+        pos, occ = epsm.search(pl, td, out=out)
+        assert occ == want.size and np.array_equal(pos.cpu().numpy().astype(np.uint64), want)
+        assert epsm.count(pl, td) == want.size
