@@ -270,24 +270,31 @@ def run_epsm(args, world, rank, local):
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
     clocks = clk.summary()
 
-    # per-(sigma, m) breakdown, outside the timed region (events between launches stop the
-    # launches from overlapping, so these per-search times are slightly pessimistic)
+    # per-(sigma, m) breakdown, outside the timed region: one event pair per group of searches
+    # of the same (sigma, m) (launches inside a group still overlap through PDL)
     breakdown = []
-    if args.breakdown:
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(jobs))]
-        one_step(ev)
-        torch.cuda.synchronize()
-        per = {}
+    if args.breakdown and world == 1:
+        groups = []                     # (key, first job, end job)
         for j, (ti, pl) in enumerate(jobs):
             key = (texts[ti][0], pl.m)
-            d = ev[2 * j].elapsed_time(ev[2 * j + 1])
-            a = per.setdefault(key, [0.0, 0, 0])
-            a[0] += d
-            a[1] += 1
-            a[2] += local_bytes[j] + 8 * min(int(occ[j]), cap)
-        for (s_, m), (d, c, b_) in sorted(per.items()):
+            if groups and groups[-1][0] == key:
+                groups[-1][2] = j + 1
+            else:
+                groups.append([key, j, j + 1])
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(groups))]
+        for gi, (key, j0, j1) in enumerate(groups):
+            ev[2 * gi].record(stream)
+            for j in range(j0, j1):
+                ti, pl = jobs[j]
+                epsm.search_async(pl, texts[ti][5], pos_buf, occ_buf[j:j + 1], stream=stream)
+            ev[2 * gi + 1].record(stream)
+        torch.cuda.synchronize()
+        for gi, ((s_, m), j0, j1) in enumerate(groups):
+            d = ev[2 * gi].elapsed_time(ev[2 * gi + 1])
+            c = j1 - j0
+            b_ = sum(local_bytes[j] + 8 * min(int(occ[j]), cap) for j in range(j0, j1))
             us = d / c * 1e3
-            breakdown.append([s_, m, round(us, 2), round(local_bytes[0] / (us * 1e-6) / 1e9, 1),
+            breakdown.append([s_, m, round(us, 2), round(local_bytes[j0] / (us * 1e-6) / 1e9, 1),
                               round(b_ / c / (us * 1e-6) / 1e9, 1)])
         if rank == 0:
             print("sigma m  us/search  text_GB/s  alg_GB/s", file=sys.stderr)

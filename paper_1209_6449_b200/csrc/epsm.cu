@@ -21,14 +21,42 @@ std::atomic<uint64_t> g_launches{0};
 
 using KernelFn = void (*)(epsm::KParams);
 
-template <int F, int F2, int MW>
+template <int F, int F2, int MW, int SK = 0, int SQ = 0>
 constexpr KernelFn pick(bool search) {
-  return search ? &epsm::epsm_scan_kernel<F, F2, MW, true> : &epsm::epsm_scan_kernel<F, F2, MW, false>;
+  return search ? &epsm::epsm_scan_kernel<F, F2, MW, SK, SQ, true>
+                : &epsm::epsm_scan_kernel<F, F2, MW, SK, SQ, false>;
 }
 
-// Kernel variant for a pattern of length m: F = min(m, 4) bytes in the first filter word,
-// F2 = min(m, 8) - 4 in the second (used where candidates are dense), MW = ceil(m/4) words.
+// Smallest m that takes the sampled (EPSMc-style) filter; EPSM_SAMPLE_MIN_M overrides
+// (A/B timing).  Below it the packed filter (EPSMa/b) runs.
+uint32_t sample_min_m() {
+  static const uint32_t v = [] {
+    const char* e = getenv("EPSM_SAMPLE_MIN_M");
+    return e && e[0] ? static_cast<uint32_t>(atoi(e)) : 9u;
+  }();
+  return v;
+}
+
+// Kernel variant for a pattern of length m (dispatch by m).
+//   packed:  F = min(m, 4) bytes in the first filter word, F2 = min(m, 8) - 4 in the second
+//            (used where candidates are dense), MW = ceil(m/4) words;
+//   sampled: one SQ-byte gram every SK bytes (SK + SQ <= m), MW words verified.
 KernelFn kernel_for(uint32_t m, bool search) {
+  if (m >= 8 && m >= sample_min_m()) {
+    switch (m) {
+      case 8: return pick<4, 4, 2, 4, 4>(search);
+      case 9: case 10: case 11: return pick<4, 4, 3, 4, 4>(search);
+      case 12: return pick<4, 4, 3, 8, 4>(search);
+      case 13: case 14: case 15: return pick<4, 4, 4, 8, 4>(search);
+      case 16: return pick<4, 4, 4, 8, 8>(search);
+      case 17: case 18: case 19: case 20: return pick<4, 4, 5, 8, 8>(search);
+      case 21: case 22: case 23: return pick<4, 4, 6, 8, 8>(search);
+      case 24: return pick<4, 4, 6, 8, 16>(search);
+      case 25: case 26: case 27: case 28: return pick<4, 4, 7, 8, 16>(search);
+      case 29: case 30: case 31: return pick<4, 4, 8, 8, 16>(search);
+      default: return pick<4, 4, 8, 16, 16>(search);
+    }
+  }
   switch (m) {
     case 1: return pick<1, 0, 1>(search);
     case 2: return pick<2, 0, 1>(search);

@@ -80,6 +80,14 @@ static_assert(kSlices == 256 && kUnitsPerThread == 4, "hand-off scan / mask pack
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 
+// Sampled (EPSMc-style) filter: fingerprint table of the pattern's q-grams.
+// Entry = candidate-offset mask (bits 0..15) | wildcard (bit 16) | 15-bit fingerprint (17..31).
+constexpr int kGramBits = 11;
+constexpr int kGramTab = 1 << kGramBits;                          // 2048 entries, 8 KiB
+__host__ __device__ constexpr uint32_t gram_mul(int r) {   // odd multipliers of the gram hash
+  return r == 0 ? 0x9E3779B1u : r == 1 ? 0x85EBCA77u : r == 2 ? 0xC2B2AE3Du : 0x27D4EB2Fu;
+}
+
 // Chunk status word: [63:40] epoch, [39:38] flag, [37:0] value.
 constexpr int kEpochShift = 40;
 constexpr unsigned long long kFlagAgg = 1ull << 38;
@@ -143,6 +151,7 @@ struct __align__(128) SmemLayoutT {
   uint64_t lb_full[kSlots];
   uint64_t lb_done[kSlots];
   ChunkSlot slot[kSlots];
+  uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
   uint32_t info[STAGES];        // tile index | (last-of-chunk << 31), or kInfoEnd
   uint32_t fin;                 // consumer warps that reached the end
 };
@@ -402,6 +411,106 @@ __device__ __forceinline__ uint32_t verify_candidates(uint32_t r, const uint8_t*
   return keep;
 }
 
+// ------------------------------------------------------------------ sampled filter (EPSMc)
+
+// EPSMc's fingerprint h (wscrc there, a multiply-add hash over the gram's
+// little-endian words here).  Bits [31:21] index the table, bits [20:6] are the fingerprint.
+template <int NW>
+__device__ __forceinline__ uint32_t gram_hash(const uint32_t (&w)[NW]) {
+  uint32_t h = w[0] * gram_mul(0);
+#pragma unroll
+  for (int r = 1; r < NW; ++r) h += w[r] * gram_mul(r);
+  return h;
+}
+
+// SQ bytes of text at a shared-memory address aligned to min(SK, SQ, 16).
+template <int SK, int SQ>
+__device__ __forceinline__ void load_sample(const uint8_t* p, uint32_t (&w)[SQ / 4]) {
+  if constexpr (SQ == 4) {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else if constexpr (SQ == 8) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    w[0] = v.x;
+    w[1] = v.y;
+  } else if constexpr (SK >= 16) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    w[0] = v.x;
+    w[1] = v.y;
+    w[2] = v.z;
+    w[3] = v.w;
+  } else {
+    const uint2 a = *reinterpret_cast<const uint2*>(p);
+    const uint2 b = *reinterpret_cast<const uint2*>(p + 8);
+    w[0] = a.x;
+    w[1] = a.y;
+    w[2] = b.x;
+    w[3] = b.y;
+  }
+}
+
+// EPSMc preprocessing (Fig. 1 lines 1-5): for every pattern offset
+// i = 1..SK the fingerprint of the gram p[i .. i+SQ-1] is entered in the table; the entry's
+// mask bit SK-i marks the start (sample offset - i) as a candidate.  Grams of different
+// fingerprints that share a bucket make it a wildcard (no fingerprint check).  One warp.
+template <int SK, int SQ>
+__device__ __forceinline__ void build_gram_table(const KParams& P, uint32_t* tab, uint32_t lane) {
+  const bool valid = lane < static_cast<uint32_t>(SK);
+  uint32_t h = 0, bit = 0;
+  if (valid) {
+    const uint32_t i = lane + 1;
+    uint32_t g[SQ / 4];
+#pragma unroll
+    for (int r = 0; r < SQ / 4; ++r)
+      g[r] = __funnelshift_r(P.pat[(i >> 2) + r], P.pat[(i >> 2) + r + 1], 8u * (i & 3u));
+    h = gram_hash<SQ / 4>(g);
+    bit = 1u << (SK - i);
+  }
+  uint32_t mask = 0, wild = 0;
+#pragma unroll
+  for (int l = 0; l < SK; ++l) {
+    const uint32_t hl = __shfl_sync(0xffffffffu, h, l);
+    const uint32_t bl = __shfl_sync(0xffffffffu, bit, l);
+    if (valid && (hl >> (32 - kGramBits)) == (h >> (32 - kGramBits))) {
+      mask |= bl;
+      if (((hl ^ h) << kGramBits) & 0xFFFE0000u) wild = 1u;
+    }
+  }
+  if (valid) tab[h >> (32 - kGramBits)] = mask | (wild << 16) | ((h << kGramBits) & 0xFFFE0000u);
+}
+
+// Naive check (Fig. 1 line 12) of every candidate bit of r against all MW
+// zero-padded pattern words (the sampled filter proves nothing about any single word).
+template <int MW>
+__device__ __forceinline__ uint32_t verify_full(uint32_t r, const uint8_t* tile, uint32_t o, const KParams& P) {
+  uint32_t keep = r;
+  while (r) {
+    const int b = __ffs(r) - 1;
+    r &= r - 1;
+    const uint32_t so = o + b;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(tile + (so & ~3u));
+    const uint32_t sh = (so & 3u) * 8u;
+    uint32_t lo = wp[0];
+#pragma unroll
+    for (int q = 0; q < MW; ++q) {
+      const uint32_t hi = wp[q + 1];
+      const uint32_t win = __funnelshift_r(lo, hi, sh);
+      if ((win ^ P.pat[q]) & P.pmask[q]) {
+        keep &= ~(1u << b);
+        break;
+      }
+      lo = hi;
+    }
+  }
+  return keep;
+}
+
+__device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_barrier_arrive(uint32_t id, uint32_t count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
@@ -594,8 +703,9 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
 
 // F  = filter bytes of the first word (min(m, 4)); F2 = filter bytes of the second word
 // (min(m, 8) - 4, 0 if m <= 4); MW = ceil(m/4) pattern words (MW <= 1: no verify);
-// SEARCH = report positions (else count only).
-template <int F, int F2, int MW, bool SEARCH>
+// SK, SQ = sampled filter (SK > 0: one SQ-byte gram every SK bytes, SK + SQ <= m; replaces
+// the packed filter); SEARCH = report positions (else count only).
+template <int F, int F2, int MW, int SK, int SQ, bool SEARCH>
 __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using Smem = SmemFor<SEARCH>;
@@ -605,6 +715,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   const uint32_t lane = tid & 31u;
   const uint32_t warp = tid >> 5;
 
+  if constexpr (SK > 0) {
+    for (uint32_t i = tid; i < kGramTab; i += kThreads) S.gram_tab[i] = 0u;
+  }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
@@ -703,6 +816,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ================================================================ look-back
+    if constexpr (SK > 0) {
+      build_gram_table<SK, SQ>(P, S.gram_tab, lane);
+      __threadfence_block();
+      named_barrier_arrive(1, kConsumers + 32);
+    }
     if constexpr (SEARCH) {
       griddep_wait();
       uint32_t q = 0, par = 0;
@@ -752,6 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       slowbits &= ~(0xFu << (4 * b));
     };
 
+    if constexpr (SK > 0) named_barrier_sync(1, kConsumers + 32);   // gram table built by warp 1
     while (true) {
       mbar_wait(&S.full[stage], phase);
       const uint32_t info = S.info[stage];
@@ -763,88 +882,133 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       const uint8_t* ts = S.ring[stage];
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
 
-      // filter all units first (independent chains), then one warp vote per stage.  The pair
-      // stage is tested on its own only while it pays off (large alphabets: almost never a
-      // candidate); otherwise the words are extended to F bytes straight away.  Both paths
-      // give the same Z, so the adaptation never changes the result.
-      uint32_t W[kUnitsPerThread][5];
-      uint32_t Z[kUnitsPerThread][4];
-#pragma unroll
-      for (int j = 0; j < kUnitsPerThread; ++j) {
-        const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-        const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
-        W[j][0] = v.x;
-        W[j][1] = v.y;
-        W[j][2] = v.z;
-        W[j][3] = v.w;
-        W[j][4] = *reinterpret_cast<const uint32_t*>(ts + o + 16);
-        filter_pair<F>(W[j], P, Z[j]);
-      }
+      uint32_t mask[kUnitsPerThread];
       bool slow;
-      if constexpr (F > 2) {
-        bool need_extend = true;
-        if (try_pair) {
-          uint32_t hz = 0;
-#pragma unroll
-          for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
-          need_extend = __any_sync(0xffffffffu, hz);
-          // hysteresis: stop testing the pair stage alone after two hits in a row (small
-          // alphabets), retry every 16th tile
-          pair_streak = need_extend ? pair_streak + 1 : 0u;
-        }
-        try_pair = pair_streak < 2 || ((++tiles_seen & 15u) == 0);
-        slow = false;
-        if (need_extend) {
-          uint32_t hz = 0;
-#pragma unroll
-          for (int j = 0; j < kUnitsPerThread; ++j) {
-            filter_extend<F>(W[j], P, Z[j]);
-            hz |= any_zero_byte(Z[j]);
-          }
-          slow = __any_sync(0xffffffffu, hz);
-        }
-      } else {
-        uint32_t hz = 0;
-#pragma unroll
-        for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
-        slow = __any_sync(0xffffffffu, hz);
-      }
-      if (slow) {
-        uint32_t mask[kUnitsPerThread];
-        const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
-#pragma unroll
-        for (int j = 0; j < kUnitsPerThread; ++j) {
-          mask[j] = zero_byte_mask16(Z[j], P.movemask_mul);
-          if (!interior) {
-            const uint64_t us = tbase + (j * kConsumers + ctid) * kUnitBytes;
-            if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
-          }
-        }
-        int qstart = 1;
-        if constexpr (F2 > 0) {
-          // many candidates (small alphabets): check pattern bytes 4..7 for all 16 alignments
-          // in packed form before any scalar check
-          const uint32_t c4 = __reduce_add_sync(0xffffffffu, __popc(mask[0]) + __popc(mask[1]) +
-                                                                __popc(mask[2]) + __popc(mask[3]));
-          if (c4 > 64) {
-#pragma unroll
-            for (int j = 0; j < kUnitsPerThread; ++j) {
-              const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-              const uint32_t v[6] = {W[j][0], W[j][1], W[j][2], W[j][3], W[j][4],
-                                     *reinterpret_cast<const uint32_t*>(ts + o + 20)};
-              uint32_t Y[4];
-              filter_second<F2>(v, P, Y);
-              mask[j] &= zero_byte_mask16(Y, P.movemask_mul);
-            }
-            qstart = 2;
-          }
-        }
+      if constexpr (SK > 0) {
+        // ---- sampled filter (EPSMc, Fig. 1 lines 7-12): the q-gram at unit
+        // offset SK*(g+1) is fingerprinted and looked up in the pattern's gram table, which
+        // yields the starts of group g whose window holds that gram at the right offset.
+        uint32_t anyc = 0;
 #pragma unroll
         for (int j = 0; j < kUnitsPerThread; ++j) {
           const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-          if (MW > qstart && __any_sync(0xffffffffu, mask[j])) mask[j] = verify_candidates<MW>(mask[j], ts, o, P, qstart);
-          acc += __popc(mask[j]);
+          uint32_t c = 0;
+#pragma unroll
+          for (int g = 0; g < 16 / SK; ++g) {
+            uint32_t sw[SQ / 4];
+            load_sample<SK, SQ>(ts + o + SK * (g + 1), sw);
+            const uint32_t H = gram_hash<SQ / 4>(sw);
+            const uint32_t e = S.gram_tab[H >> (32 - kGramBits)];
+            const bool ok = (((e ^ (H << kGramBits)) & 0xFFFE0000u) == 0u) || (e & 0x10000u);
+            c |= (ok ? (e & 0xFFFFu) : 0u) << (SK * g);
+          }
+          mask[j] = c;
+          anyc |= c;
         }
+        slow = __any_sync(0xffffffffu, anyc != 0u);
+        if (slow) {
+          const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
+          uint32_t left = 0;
+#pragma unroll
+          for (int j = 0; j < kUnitsPerThread; ++j) {
+            const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+            if (!interior) {
+              const uint64_t us = tbase + o;
+              if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
+            }
+            if (__any_sync(0xffffffffu, mask[j])) mask[j] = verify_full<MW>(mask[j], ts, o, P);
+            left |= mask[j];
+          }
+          slow = __any_sync(0xffffffffu, left != 0u);
+        }
+      } else {
+        // ---- packed filter (EPSMa/b): all units first (independent chains), then one warp
+        // vote per stage.  The pair stage is tested on its own only while it pays off (large
+        // alphabets: almost never a candidate); otherwise the words are extended to F bytes
+        // straight away.  Both paths give the same Z, so the adaptation never changes the result.
+        uint32_t W[kUnitsPerThread][5];
+        uint32_t Z[kUnitsPerThread][4];
+#pragma unroll
+        for (int j = 0; j < kUnitsPerThread; ++j) {
+          const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+          const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
+          W[j][0] = v.x;
+          W[j][1] = v.y;
+          W[j][2] = v.z;
+          W[j][3] = v.w;
+          W[j][4] = *reinterpret_cast<const uint32_t*>(ts + o + 16);
+          filter_pair<F>(W[j], P, Z[j]);
+        }
+        if constexpr (F > 2) {
+          bool need_extend = true;
+          if (try_pair) {
+            uint32_t hz = 0;
+#pragma unroll
+            for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
+            need_extend = __any_sync(0xffffffffu, hz);
+            // hysteresis: stop testing the pair stage alone after two hits in a row (small
+            // alphabets), retry every 16th tile
+            pair_streak = need_extend ? pair_streak + 1 : 0u;
+          }
+          try_pair = pair_streak < 2 || ((++tiles_seen & 15u) == 0);
+          slow = false;
+          if (need_extend) {
+            uint32_t hz = 0;
+#pragma unroll
+            for (int j = 0; j < kUnitsPerThread; ++j) {
+              filter_extend<F>(W[j], P, Z[j]);
+              hz |= any_zero_byte(Z[j]);
+            }
+            slow = __any_sync(0xffffffffu, hz);
+          }
+        } else {
+          uint32_t hz = 0;
+#pragma unroll
+          for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
+          slow = __any_sync(0xffffffffu, hz);
+        }
+        if (slow) {
+          const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
+#pragma unroll
+          for (int j = 0; j < kUnitsPerThread; ++j) {
+            mask[j] = zero_byte_mask16(Z[j], P.movemask_mul);
+            if (!interior) {
+              const uint64_t us = tbase + (j * kConsumers + ctid) * kUnitBytes;
+              if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
+            }
+          }
+          int qstart = 1;
+          if constexpr (F2 > 0) {
+            // many candidates (small alphabets): check pattern bytes 4..7 for all 16 alignments
+            // in packed form before any scalar check
+            const uint32_t c4 = __reduce_add_sync(0xffffffffu, __popc(mask[0]) + __popc(mask[1]) +
+                                                                  __popc(mask[2]) + __popc(mask[3]));
+            if (c4 > 64) {
+#pragma unroll
+              for (int j = 0; j < kUnitsPerThread; ++j) {
+                const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+                const uint32_t v[6] = {W[j][0], W[j][1], W[j][2], W[j][3], W[j][4],
+                                       *reinterpret_cast<const uint32_t*>(ts + o + 20)};
+                uint32_t Y[4];
+                filter_second<F2>(v, P, Y);
+                mask[j] &= zero_byte_mask16(Y, P.movemask_mul);
+              }
+              qstart = 2;
+            }
+          }
+          uint32_t left = 0;
+#pragma unroll
+          for (int j = 0; j < kUnitsPerThread; ++j) {
+            const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+            if (MW > qstart && __any_sync(0xffffffffu, mask[j])) mask[j] = verify_candidates<MW>(mask[j], ts, o, P, qstart);
+            left |= mask[j];
+          }
+          slow = __any_sync(0xffffffffu, left != 0u);
+        }
+      }
+      if (slow) {
+#pragma unroll
+        for (int j = 0; j < kUnitsPerThread; ++j) acc += __popc(mask[j]);
         if constexpr (SEARCH) {
           if (!waited) {                       // the scratch may still be read by the previous grid
             griddep_wait();

@@ -1,6 +1,7 @@
 // Microbenchmark: read bandwidth of (a) a persistent TMA bulk-copy ring with
 // consumers that only touch the data lightly, (b) a plain LDG.128 grid-stride read.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -71,12 +72,13 @@ void run_tma(const uint8_t* d, uint64_t n, uint32_t* o, int sms, int ctas_per_sm
          n * (double)R / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
-  const uint64_t n = 1ull << 30;
+int main(int argc, char** argv) {
+  const uint64_t n = argc > 1 ? strtoull(argv[1], 0, 0) : (1ull << 30);
   uint8_t* d; uint32_t* o;
   cudaMalloc(&d, n); cudaMalloc(&o, 64); cudaMemset(d, 1, n);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run_tma<32768, 4, 16>(d, n, o, sms, 1);
+  run_tma<32768, 5, 16>(d, n, o, sms, 1);
   run_tma<32768, 6, 16>(d, n, o, sms, 1);
   run_tma<16384, 8, 16>(d, n, o, sms, 1);
   run_tma<16384, 12, 16>(d, n, o, sms, 1);
