@@ -158,6 +158,17 @@ uint64_t epsm_launch_count(void);
 /* epsm_version -- ABI version (major * 10000 + minor * 100 + patch). */
 int epsm_version(void);
 
+/*
+ * epsm_debug_trace -- diagnostics only.  When the process was started with
+ * EPSM_TRACE=<slots>, every kernel launch records a per-CTA timeline of
+ * %globaltimer stamps (8 uint64 per CTA: start, first TMA issued, first tile
+ * ready, producer done, consumers done, drain done, CTA done, chunks) into slot
+ * (launch index mod slots) of a device buffer of 8192 words per slot.  Copies
+ * min(max_words, slots * 8192) words into the HOST buffer h_out (synchronises
+ * the device) and returns the count; 0 when tracing is off.
+ */
+int64_t epsm_debug_trace(uint64_t *h_out, uint64_t max_words);
+
 #ifdef __cplusplus
 }
 #endif

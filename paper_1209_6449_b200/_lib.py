@@ -63,12 +63,14 @@ _lib.epsm_launch_count.argtypes = []
 _lib.epsm_launch_count.restype = _u64
 _lib.epsm_version.argtypes = []
 _lib.epsm_version.restype = ctypes.c_int
+_lib.epsm_debug_trace.argtypes = [_vp, _u64]
+_lib.epsm_debug_trace.restype = _i64
 
 EXPORTED_SYMBOLS = (
     "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
     "epsm_search", "epsm_search_async", "epsm_search_host", "epsm_search_sharded",
     "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
-    "epsm_version",
+    "epsm_version", "epsm_debug_trace",
 )
 
 
@@ -90,6 +92,13 @@ def launch_count() -> int:
 
 def version() -> int:
     return int(_lib.epsm_version())
+
+
+def debug_trace() -> np.ndarray:
+    """Per-launch, per-CTA timeline (EPSM_TRACE=<slots> runs only): uint64 [slots, 1024, 8]."""
+    buf = np.zeros(1 << 22, dtype=np.uint64)
+    k = _check(int(_lib.epsm_debug_trace(buf.ctypes.data, buf.size)), "epsm_debug_trace")
+    return buf[:k].reshape(-1, 1024, 8)
 
 
 def _check(rc: int, where: str) -> int:

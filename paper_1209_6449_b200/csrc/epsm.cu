@@ -19,6 +19,32 @@ namespace {
 thread_local char g_last_error[512] = "";
 std::atomic<uint64_t> g_launches{0};
 
+// Diagnostics: EPSM_TRACE=<slots> makes every launch record a per-CTA timeline
+// (8 x u64 per CTA, slot = launch index mod slots); epsm_debug_trace copies it out.
+constexpr uint64_t kTraceWordsPerLaunch = 8 * 1024;
+unsigned long long* g_trace = nullptr;
+uint64_t g_trace_slots = 0;
+int g_trace_device = -1;
+
+unsigned long long* trace_slot(int device) {
+  static const uint64_t slots = [] {
+    const char* v = getenv("EPSM_TRACE");
+    return v && v[0] ? static_cast<uint64_t>(atoll(v)) : 0ull;
+  }();
+  if (slots == 0) return nullptr;
+  if (!g_trace) {
+    if (cudaMalloc(&g_trace, slots * kTraceWordsPerLaunch * sizeof(unsigned long long)) != cudaSuccess) {
+      g_trace = nullptr;
+      return nullptr;
+    }
+    cudaMemset(g_trace, 0, slots * kTraceWordsPerLaunch * sizeof(unsigned long long));
+    g_trace_slots = slots;
+    g_trace_device = device;
+  }
+  if (device != g_trace_device) return nullptr;
+  return g_trace + (g_launches.load() % g_trace_slots) * kTraceWordsPerLaunch;
+}
+
 using KernelFn = void (*)(epsm::KParams);
 
 template <int F, int F2, int MW, int SK = 0, int SQ = 0>
@@ -264,6 +290,7 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
     P.scratch = plan->d_park;
     P.tag = static_cast<unsigned long long>(plan->epoch) << epsm::kEpochShift;
   }
+  P.trace = trace_slot(plan->device);
   KernelFn fn = kernel_for(plan->m, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan->device, smem);
@@ -551,5 +578,16 @@ const char* epsm_last_error(void) { return g_last_error; }
 uint64_t epsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int epsm_version(void) { return 100; }
+
+int64_t epsm_debug_trace(uint64_t* h_out, uint64_t max_words) {
+  if (!g_trace) return 0;
+  const uint64_t words = g_trace_slots * kTraceWordsPerLaunch;
+  const uint64_t k = words < max_words ? words : max_words;
+  cudaSetDevice(g_trace_device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(h_out, g_trace, k * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_debug_trace");
+  return static_cast<int64_t>(k);
+}
 
 }  // extern "C"

@@ -63,20 +63,21 @@ constexpr int kConsumers = kConsumerWarps * 32;                  // 512
 constexpr int kThreads = kConsumers + 64;                        // + producer + look-back warps
 constexpr int kUnitsPerTile = kTile / kUnitBytes;                // 2048
 constexpr int kUnitsPerThread = kUnitsPerTile / kConsumers;      // 4
-// A slice = the 32 consecutive units (512 text bytes) one warp filters in one
-// (tile, j) step: unit = tile*2048 + j*512 + warp*32 + lane.  Text order of slices
-// is (tile, j, warp).
-constexpr int kSlices = kChunkTiles * kUnitsPerThread * kConsumerWarps;   // 256 per chunk
+constexpr int kSegBytes = kUnitsPerThread * kUnitBytes;          // 64 contiguous text bytes per lane
+constexpr int kWarpBytes = 32 * kSegBytes;                       // 2 KiB per consumer warp and tile
+// A slice = the 2 KiB of text (128 units, 64 starts per lane) one warp filters in one tile:
+// lane l of warp w covers tile bytes [w*2048 + l*64, +64).  Text order of slices is (tile, warp).
+constexpr int kSlices = kChunkTiles * kConsumerWarps;            // 64 per chunk
 constexpr int kParked = 8;                                       // chunks parked awaiting their prefix
 constexpr int kSlots = 16;                                       // look-back queue depth
 constexpr int kWarpStage = 256;                                  // positions per warp round
 constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
 constexpr int kLookbackWindow = 256;                             // statuses per look-back round
-// parked masks in global scratch: one u64 (4 units x 16 bits) per (chunk slot, tile, warp, lane)
+// parked masks in global scratch: one u64 (64 starts) per (chunk slot, tile, warp, lane)
 constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
 static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking rotation");
 static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
-static_assert(kSlices == 256 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
+static_assert(kSlices == 64 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 
@@ -119,7 +120,17 @@ struct KParams {
   uint32_t bcast2[4];           // B_{4+i}: the second filter word (pattern bytes 4..7)
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
   uint32_t pmask[9];            // per-word byte masks (partial last word)
+  unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
 };
+
+// %globaltimer stamps for the optional per-CTA timeline (EPSM_TRACE)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define EPSM_TRACE(P, i) \
+  do { if ((P).trace) (P).trace[blockIdx.x * 8 + (i)] = gtimer(); } while (0)
 
 struct ChunkSlot {              // consumers -> look-back warp
   uint32_t chunk;               // chunk id, or kInfoEnd
@@ -129,7 +140,7 @@ struct ChunkSlot {              // consumers -> look-back warp
 };
 
 struct __align__(16) ParkedChunk {   // per parking slot
-  uint32_t cnt[kSlices];        // per-slice counts, layout [warp][tile][j] (valid where slow)
+  uint32_t cnt[kSlices];        // per-slice counts, index tile*16 + warp (valid where slow)
   uint32_t off[kSlices];        // exclusive slice offsets inside the chunk, text order (hand-off)
   unsigned long long prefix;    // exclusive prefix (look-back warp)
   uint32_t chunk;               // chunk id
@@ -531,8 +542,11 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, uint32_t lan
 // returns the exclusive prefix of `chunk` and publishes its inclusive prefix (its
 // aggregate was published by the consumers).  Window: kLookbackWindow predecessors per round,
 // lane l / slot i reads predecessor pred - (32 i + l), nearest first.
+// With `fin` non-NULL the look-back gives up (returns kAborted, publishes nothing) once all
+// consumer warps of the CTA have finished: nobody needs this chunk's prefix any more.
+constexpr unsigned long long kAborted = ~0ull;
 __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_t chunk, uint32_t total,
-                                                       uint32_t lane) {
+                                                       uint32_t lane, const volatile uint32_t* fin) {
   const unsigned long long tag = P.tag;
   if (chunk == 0) {
     if (lane == 0) st_relaxed(P.status, tag | kFlagInc | total);
@@ -554,6 +568,7 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
         valid &= ((s[i] & kEpochMask) == tag) && (s[i] & kFlagMask);
       }
       if (__all_sync(0xffffffffu, valid)) break;
+      if (fin && *fin == static_cast<uint32_t>(kConsumerWarps)) return kAborted;
       __nanosleep(32);
       if (++spins > (1u << 24)) __trap();   // a predecessor never published: fail loudly, never hang
     }
@@ -575,43 +590,29 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
   return prefix;
 }
 
-// Stage the positions of one slice (lane: unit mask mk, c = popc(mk), off = exclusive
-// offset of the lane inside the slice, tg = slice total) in the warp's shared buffer and
-// store them coalesced at dst[0 .. min(tg, room)).  Positions of a unit are ub + bit.
-__device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint64_t room, uint32_t mk,
-                                            uint32_t c, uint32_t off, uint32_t tg, uint64_t ub,
-                                            uint32_t lane) {
+// Stage the positions of one slice in the warp's shared buffer and store them coalesced at
+// dst[0 .. min(tg, room)), kWarpStage per round.  Lane: 64-start mask M (bit k = start sb + k),
+// exclusive offset `off` inside the slice; tg = slice total.  Every lane walks its bits once
+// across the rounds, stopping at each round's end.
+__device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint64_t room, uint64_t M,
+                                            uint32_t off, uint32_t tg, uint64_t sb, uint32_t lane) {
+  uint32_t lo = static_cast<uint32_t>(M), hi = static_cast<uint32_t>(M >> 32);
+  uint32_t idx = off;
   for (uint32_t R = 0; R < tg; R += kWarpStage) {
-    if (tg <= kWarpStage) {
-      if (tg > 8 * 32) {
-        // dense slice: fixed 16-step loop, no divergence; rank of bit b = popc(mk below b)
-#pragma unroll
-        for (int bit = 0; bit < 16; ++bit) {
-          if ((mk >> bit) & 1u) {
-            const uint32_t i = off + __popc(mk & ((1u << bit) - 1u));
-            stage[i + (i >> 4)] = ub + static_cast<uint64_t>(bit);
-          }
-        }
-      } else {
-        uint32_t v = mk, i = off;
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          stage[i + (i >> 4)] = ub + static_cast<uint64_t>(bit);
-          ++i;
-        }
-      }
-    } else if (c && off < R + kWarpStage && off + c > R) {   // > 256 positions: two rounds
-      uint32_t v = mk, idx = off;
-      while (v) {
-        const int bit = __ffs(v) - 1;
-        v &= v - 1;
-        if (idx >= R && idx < R + kWarpStage) {
-          const uint32_t i = idx - R;
-          stage[i + (i >> 4)] = ub + static_cast<uint64_t>(bit);
-        }
-        ++idx;
-      }
+    const uint32_t lim = R + kWarpStage;
+    while (lo && idx < lim) {
+      const uint32_t bit = __ffs(lo) - 1;
+      lo &= lo - 1;
+      const uint32_t i = idx - R;
+      stage[i + (i >> 4)] = sb + bit;
+      ++idx;
+    }
+    while (hi && idx < lim) {
+      const uint32_t bit = __ffs(hi) + 31;
+      hi &= hi - 1;
+      const uint32_t i = idx - R;
+      stage[i + (i >> 4)] = sb + bit;
+      ++idx;
     }
     __syncwarp();
     uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
@@ -633,9 +634,14 @@ __device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint
   }
 }
 
+__device__ __forceinline__ uint32_t popc64(uint64_t v) {
+  return __popc(static_cast<uint32_t>(v)) + __popc(static_cast<uint32_t>(v >> 32));
+}
+
 // Write this warp's slices of the chunk parked in slot b (its masks in the global
 // scratch, the slice offsets computed at hand-off, the prefix from the look-back warp)
-// at pos[...].  `slow` bit t: this warp parked masks for tile t (else all zero).
+// at pos[...] -- the occurrences at i*alpha + {r} of PAPER.md:470 / Fig. 1 line 11, in
+// text order.  `slow` bit t: this warp parked masks for tile t (else all zero).
 template <class Smem>
 __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const uint64_t* scratch_cta,
                                              uint32_t b, uint32_t slow, uint32_t cw, uint32_t lane,
@@ -653,50 +659,57 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
     mk4[t] = (t < static_cast<int>(nt) && ((slow >> t) & 1u))
                  ? ld_keep_u64(scratch_cta + ((b * kChunkTiles + t) * kConsumerWarps + cw) * 32 + lane, keep_pol)
                  : 0ull;
+  const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int t = 0; t < kChunkTiles; ++t) {
     if (!((slow >> t) & 1u) || t >= static_cast<int>(nt)) continue;
-#pragma unroll 1
-    for (uint32_t j = 0; j < kUnitsPerThread; ++j) {
-      const uint32_t mk = static_cast<uint32_t>(mk4[t] >> (16 * j)) & 0xFFFFu;
-      const uint32_t c = __popc(mk);
-      const uint32_t any = __ballot_sync(0xffffffffu, c != 0);
-      if (any == 0) continue;
-      const uint64_t gidx = prefix + pk.off[(t * kUnitsPerThread + j) * kConsumerWarps + cw];
-      if (gidx >= P.cap) return;                              // later slices are even further out
-      const uint64_t room = P.cap - gidx;
-      const uint32_t unit = t * kUnitsPerTile + j * kConsumers + cw * 32 + lane;
-      const uint64_t ub = cbase + static_cast<uint64_t>(unit) * kUnitBytes;
-      const uint32_t lt = (1u << lane) - 1u;
-      if (__ballot_sync(0xffffffffu, c > 1) == 0) {
-        // sparse slice (<= 1 position per unit): lanes store straight to consecutive slots,
-        // which one warp store coalesces -- no staging, no scan
-        const uint32_t off = __popc(any & lt);
-        if (c && off < room) st_stream_u64(P.pos + gidx + off, ub + static_cast<uint64_t>(__ffs(mk) - 1));
-        continue;
-      }
-      // exclusive offsets from 5 bit-sliced ballots (c <= 16): independent ops, no shuffle chain
-      uint32_t off = 0, tg = 0;
-#pragma unroll
-      for (int bb = 0; bb < 5; ++bb) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, (c >> bb) & 1u);
-        off += __popc(bal & lt) << bb;
-        tg += __popc(bal) << bb;
-      }
-      if (tg <= 64) {
-        // moderately sparse: direct stores, lane by lane in bit order
-        uint32_t v = mk, i = off;
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          if (i < room) st_stream_u64(P.pos + gidx + i, ub + static_cast<uint64_t>(bit));
-          ++i;
-        }
-        continue;
-      }
-      write_slice(stage, P.pos + gidx, room, mk, c, off, tg, ub, lane);
+    const uint64_t M = mk4[t];
+    const uint32_t c = popc64(M);
+    const uint32_t any = __ballot_sync(0xffffffffu, c != 0);
+    if (any == 0) continue;
+    const uint64_t gidx = prefix + pk.off[t * kConsumerWarps + cw];
+    if (gidx >= P.cap) return;                                // later slices are even further out
+    const uint64_t room = P.cap - gidx;
+    const uint64_t sb = cbase + static_cast<uint64_t>(t) * kTile + cw * kWarpBytes + lane * kSegBytes;
+    if (__ballot_sync(0xffffffffu, c > 1) == 0) {
+      // sparse slice (<= 1 position per lane): lanes store straight to consecutive slots,
+      // which one warp store coalesces -- no staging, no scan
+      const uint32_t off = __popc(any & lt);
+      if (c && off < room) st_stream_u64(P.pos + gidx + off, sb + static_cast<uint64_t>(__ffsll(M) - 1));
+      continue;
     }
+    // exclusive offsets from 7 bit-sliced ballots (c <= 64): independent ops, no shuffle chain
+    uint32_t off = 0, tg = 0;
+#pragma unroll
+    for (int bb = 0; bb < 7; ++bb) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (c >> bb) & 1u);
+      off += __popc(bal & lt) << bb;
+      tg += __popc(bal) << bb;
+    }
+    if (tg <= 96) {
+      // moderately sparse: direct stores, lane by lane in bit order
+      uint64_t v = M;
+      uint32_t i = off;
+      while (v) {
+        const int bit = __ffsll(v) - 1;
+        v &= v - 1;
+        if (i < room) st_stream_u64(P.pos + gidx + i, sb + static_cast<uint64_t>(bit));
+        ++i;
+      }
+      continue;
+    }
+    write_slice(stage, P.pos + gidx, room, M, off, tg, sb, lane);
   }
+}
+
+// ------------------------------------------------------------------ lane segments
+
+// The lane's 64-byte segment (4 units) in rotated order: R[r] = unit (r + rot) & 3 with
+// rot = (lane >> 1) & 3, so the 8 lanes of every LDS.128 wavefront hit 8 different 16-byte
+// bank groups (a plain 64-byte lane stride would be 4-way conflicted).
+__device__ __forceinline__ void load_segment(const uint8_t* seg, uint32_t rot, uint4 (&R)[4]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) R[r] = *reinterpret_cast<const uint4*>(seg + 16u * ((r + rot) & 3u));
 }
 
 // ------------------------------------------------------------------ the scan kernel
@@ -715,21 +728,25 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   const uint32_t lane = tid & 31u;
   const uint32_t warp = tid >> 5;
 
+  if (tid == 0) EPSM_TRACE(P, 0);
   if constexpr (SK > 0) {
     for (uint32_t i = tid; i < kGramTab; i += kThreads) S.gram_tab[i] = 0u;
   }
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], kConsumerWarps);
-    }
-    for (int q = 0; q < kSlots; ++q) {
-      mbar_init(&S.lb_full[q], 1);
-      mbar_init(&S.lb_done[q], 1);
-    }
-    for (int b = 0; b < Smem::kPark; ++b) S.park[b].done = 0;
-    S.fin = 0;
+  // barrier set-up spread over the threads of warps 0-1 (one mbarrier init each: a serial
+  // init of all of them costs ~1 us on the start-up path)
+  if (tid < static_cast<uint32_t>(kStages)) {
+    mbar_init(&S.full[tid], 1);
+    mbar_init(&S.empty[tid], kConsumerWarps);
     fence_mbar_init();
+  } else if (tid >= 32 && tid < 32 + static_cast<uint32_t>(kSlots)) {
+    mbar_init(&S.lb_full[tid - 32], 1);
+    mbar_init(&S.lb_done[tid - 32], 1);
+    fence_mbar_init();
+  } else if (tid >= 64 && tid < 64 + static_cast<uint32_t>(Smem::kPark)) {
+    S.park[tid - 64].done = 0;
+  }
+  if (tid == 0) {
+    S.fin = 0;
     griddep_launch_dependents();   // the next grid may start its prologue as our CTAs retire
   }
   __syncthreads();
@@ -767,6 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         if (lane == 0) {
           S.info[stage] = kInfoEnd;
           mbar_arrive(&S.full[stage]);
+          EPSM_TRACE(P, 3);
         }
         break;
       }
@@ -789,6 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           } else {
             mbar_arrive(&S.full[stage]);
           }
+          if (first && t == t0) EPSM_TRACE(P, 1);
           if (t == t0 && !first) pend = draw();   // consumed after this chunk
         }
         if (++stage == kStages) {
@@ -825,13 +844,19 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       griddep_wait();
       uint32_t q = 0, par = 0;
       while (true) {
-        mbar_wait_sleep(&S.lb_full[q], par, 500);
+        mbar_wait_sleep(&S.lb_full[q], par, 200);
         const ChunkSlot sl = S.slot[q];
         if (sl.chunk == kInfoEnd) break;
-        const unsigned long long pre = lookback(P, sl.chunk, sl.total, lane);
+        // a chunk without occurrences needs no prefix of its own; its look-back only helps
+        // successors (an inclusive status shortens their walks), so it is dropped once every
+        // consumer warp of this CTA is done and the CTA could otherwise exit
+        const bool last = sl.chunk + 1 == P.nchunks;             // its prefix gives occ
+        const volatile uint32_t* fin = (sl.total == 0 && !last) ? &S.fin : nullptr;
+        const bool skip = fin && *fin == static_cast<uint32_t>(kConsumerWarps);
+        const unsigned long long pre = skip ? kAborted : lookback(P, sl.chunk, sl.total, lane, fin);
         if (lane == 0) {
-          S.park[sl.park].prefix = pre;
-          if (sl.chunk + 1 == P.nchunks) *P.occ = pre + sl.total;
+          if (pre != kAborted) S.park[sl.park].prefix = pre;
+          if (last) *P.occ = pre + sl.total;
           mbar_arrive(&S.lb_done[q]);
         }
         __syncwarp();
@@ -844,7 +869,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   } else {
     // ================================================================ consumers
     const uint32_t cw = warp - 2;
-    const uint32_t ctid = tid - 64;
+    const uint32_t seg_off = cw * kWarpBytes + lane * kSegBytes;   // this lane's 64 bytes in a tile
+    const uint32_t rot = (lane >> 1) & 3u;                           // load rotation (bank groups)
     uint32_t stage = 0, phase = 0;
     uint32_t seq = 0;                          // chunks this warp has started (same for all warps)
     uint32_t tpos = 0;                         // tile index inside the current chunk
@@ -863,26 +889,39 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       mbar_wait(&S.lb_done[k % kSlots], (k / kSlots) & 1u);
     };
     // write out chunk #k's slices (parked in slot k % kParked) once its prefix is known
+    // (a warp that parked no masks for the chunk has nothing to write and needs no prefix)
     auto flush_chunk_seq = [&](uint32_t k) {
       const uint32_t b = k % kParked;
-      wait_done(k);
-      flush_slices(P, S, scratch_cta, b, (slowbits >> (4 * b)) & 0xFu, cw, lane, keep_pol);
+      const uint32_t sb = (slowbits >> (4 * b)) & 0xFu;
+      if (sb) {
+        wait_done(k);
+        flush_slices(P, S, scratch_cta, b, sb, cw, lane, keep_pol);
+      }
       slowbits &= ~(0xFu << (4 * b));
     };
 
     if constexpr (SK > 0) named_barrier_sync(1, kConsumers + 32);   // gram table built by warp 1
+    bool first_tile = true;
     while (true) {
       mbar_wait(&S.full[stage], phase);
+      if (first_tile && cw == 0 && lane == 0) EPSM_TRACE(P, 2);
+      first_tile = false;
       const uint32_t info = S.info[stage];
-      if (info == kInfoEnd) break;
+      if (info == kInfoEnd) {
+        if (cw == 0 && lane == 0) EPSM_TRACE(P, 4);
+        break;
+      }
       const uint32_t tile = info & 0x7FFFFFFFu;
       const bool last_in_chunk = info >> 31;
       const uint32_t b = seq % kParked;
       if (SEARCH && tpos == 0 && seq >= kParked) flush_chunk_seq(seq - kParked);   // free slot b
       const uint8_t* ts = S.ring[stage];
+      const uint8_t* seg = ts + seg_off;
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
+      const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
 
-      uint32_t mask[kUnitsPerThread];
+      // slot r holds unit u = (r + rot) & 3 of the segment: text bytes [seg_off + 16u, +16)
+      uint32_t mask[4];                        // 16-bit match mask of the unit in slot r
       bool slow;
       if constexpr (SK > 0) {
         // ---- sampled filter (EPSMc, Fig. 1 lines 7-12): the q-gram at unit
@@ -890,34 +929,34 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // yields the starts of group g whose window holds that gram at the right offset.
         uint32_t anyc = 0;
 #pragma unroll
-        for (int j = 0; j < kUnitsPerThread; ++j) {
-          const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+        for (int r = 0; r < 4; ++r) {
+          const uint8_t* up = seg + 16u * ((r + rot) & 3u);
           uint32_t c = 0;
 #pragma unroll
           for (int g = 0; g < 16 / SK; ++g) {
-            uint32_t sw[SQ / 4];
-            load_sample<SK, SQ>(ts + o + SK * (g + 1), sw);
-            const uint32_t H = gram_hash<SQ / 4>(sw);
+            constexpr int kw = SQ / 4;
+            uint32_t sw[kw];
+            load_sample<SK, SQ>(up + SK * (g + 1), sw);
+            const uint32_t H = gram_hash<kw>(sw);
             const uint32_t e = S.gram_tab[H >> (32 - kGramBits)];
             const bool ok = (((e ^ (H << kGramBits)) & 0xFFFE0000u) == 0u) || (e & 0x10000u);
             c |= (ok ? (e & 0xFFFFu) : 0u) << (SK * g);
           }
-          mask[j] = c;
+          mask[r] = c;
           anyc |= c;
         }
         slow = __any_sync(0xffffffffu, anyc != 0u);
         if (slow) {
-          const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
           uint32_t left = 0;
 #pragma unroll
-          for (int j = 0; j < kUnitsPerThread; ++j) {
-            const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t o = seg_off + 16u * ((r + rot) & 3u);
             if (!interior) {
               const uint64_t us = tbase + o;
-              if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
+              if (us < P.s_lo || us + 16 > P.s_hi) mask[r] &= range_mask(us, P.s_lo, P.s_hi);
             }
-            if (__any_sync(0xffffffffu, mask[j])) mask[j] = verify_full<MW>(mask[j], ts, o, P);
-            left |= mask[j];
+            if (__any_sync(0xffffffffu, mask[r])) mask[r] = verify_full<MW>(mask[r], ts, o, P);
+            left |= mask[r];
           }
           slow = __any_sync(0xffffffffu, left != 0u);
         }
@@ -926,25 +965,25 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // vote per stage.  The pair stage is tested on its own only while it pays off (large
         // alphabets: almost never a candidate); otherwise the words are extended to F bytes
         // straight away.  Both paths give the same Z, so the adaptation never changes the result.
-        uint32_t W[kUnitsPerThread][5];
-        uint32_t Z[kUnitsPerThread][4];
+        uint4 R[4];
+        load_segment(seg, rot, R);
+        uint32_t W[4][5];
+        uint32_t Z[4][4];
 #pragma unroll
-        for (int j = 0; j < kUnitsPerThread; ++j) {
-          const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-          const uint4 v = *reinterpret_cast<const uint4*>(ts + o);
-          W[j][0] = v.x;
-          W[j][1] = v.y;
-          W[j][2] = v.z;
-          W[j][3] = v.w;
-          W[j][4] = *reinterpret_cast<const uint32_t*>(ts + o + 16);
-          filter_pair<F>(W[j], P, Z[j]);
+        for (int r = 0; r < 4; ++r) {
+          W[r][0] = R[r].x;
+          W[r][1] = R[r].y;
+          W[r][2] = R[r].z;
+          W[r][3] = R[r].w;
+          W[r][4] = *reinterpret_cast<const uint32_t*>(seg + 16u * ((r + rot) & 3u) + 16u);
+          filter_pair<F>(W[r], P, Z[r]);
         }
         if constexpr (F > 2) {
           bool need_extend = true;
           if (try_pair) {
             uint32_t hz = 0;
 #pragma unroll
-            for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
+            for (int r = 0; r < 4; ++r) hz |= any_zero_byte(Z[r]);
             need_extend = __any_sync(0xffffffffu, hz);
             // hysteresis: stop testing the pair stage alone after two hits in a row (small
             // alphabets), retry every 16th tile
@@ -955,26 +994,25 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           if (need_extend) {
             uint32_t hz = 0;
 #pragma unroll
-            for (int j = 0; j < kUnitsPerThread; ++j) {
-              filter_extend<F>(W[j], P, Z[j]);
-              hz |= any_zero_byte(Z[j]);
+            for (int r = 0; r < 4; ++r) {
+              filter_extend<F>(W[r], P, Z[r]);
+              hz |= any_zero_byte(Z[r]);
             }
             slow = __any_sync(0xffffffffu, hz);
           }
         } else {
           uint32_t hz = 0;
 #pragma unroll
-          for (int j = 0; j < kUnitsPerThread; ++j) hz |= any_zero_byte(Z[j]);
+          for (int r = 0; r < 4; ++r) hz |= any_zero_byte(Z[r]);
           slow = __any_sync(0xffffffffu, hz);
         }
         if (slow) {
-          const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
 #pragma unroll
-          for (int j = 0; j < kUnitsPerThread; ++j) {
-            mask[j] = zero_byte_mask16(Z[j], P.movemask_mul);
+          for (int r = 0; r < 4; ++r) {
+            mask[r] = zero_byte_mask16(Z[r], P.movemask_mul);
             if (!interior) {
-              const uint64_t us = tbase + (j * kConsumers + ctid) * kUnitBytes;
-              if (us < P.s_lo || us + 16 > P.s_hi) mask[j] &= range_mask(us, P.s_lo, P.s_hi);
+              const uint64_t us = tbase + seg_off + 16u * ((r + rot) & 3u);
+              if (us < P.s_lo || us + 16 > P.s_hi) mask[r] &= range_mask(us, P.s_lo, P.s_hi);
             }
           }
           int qstart = 1;
@@ -985,44 +1023,42 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
                                                                   __popc(mask[2]) + __popc(mask[3]));
             if (c4 > 64) {
 #pragma unroll
-              for (int j = 0; j < kUnitsPerThread; ++j) {
-                const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-                const uint32_t v[6] = {W[j][0], W[j][1], W[j][2], W[j][3], W[j][4],
+              for (int r = 0; r < 4; ++r) {
+                const uint32_t o = seg_off + 16u * ((r + rot) & 3u);
+                const uint32_t v[6] = {W[r][0], W[r][1], W[r][2], W[r][3], W[r][4],
                                        *reinterpret_cast<const uint32_t*>(ts + o + 20)};
                 uint32_t Y[4];
                 filter_second<F2>(v, P, Y);
-                mask[j] &= zero_byte_mask16(Y, P.movemask_mul);
+                mask[r] &= zero_byte_mask16(Y, P.movemask_mul);
               }
               qstart = 2;
             }
           }
           uint32_t left = 0;
 #pragma unroll
-          for (int j = 0; j < kUnitsPerThread; ++j) {
-            const uint32_t o = (j * kConsumers + ctid) * kUnitBytes;
-            if (MW > qstart && __any_sync(0xffffffffu, mask[j])) mask[j] = verify_candidates<MW>(mask[j], ts, o, P, qstart);
-            left |= mask[j];
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t o = seg_off + 16u * ((r + rot) & 3u);
+            if (MW > qstart && __any_sync(0xffffffffu, mask[r])) mask[r] = verify_candidates<MW>(mask[r], ts, o, P, qstart);
+            left |= mask[r];
           }
           slow = __any_sync(0xffffffffu, left != 0u);
         }
       }
       if (slow) {
+        // the lane's 64 starts as one mask: bit 16u + j = start seg_off + 16u + j
+        uint64_t M = 0;
 #pragma unroll
-        for (int j = 0; j < kUnitsPerThread; ++j) acc += __popc(mask[j]);
+        for (int r = 0; r < 4; ++r) M |= static_cast<uint64_t>(mask[r]) << (16u * ((r + rot) & 3u));
+        const uint32_t c = popc64(M);
+        acc += c;
         if constexpr (SEARCH) {
           if (!waited) {                       // the scratch may still be read by the previous grid
             griddep_wait();
             waited = true;
           }
-          const uint64_t packed = static_cast<uint64_t>(mask[0]) | (static_cast<uint64_t>(mask[1]) << 16) |
-                                  (static_cast<uint64_t>(mask[2]) << 32) | (static_cast<uint64_t>(mask[3]) << 48);
-          st_keep_u64(scratch_cta + ((b * kChunkTiles + tpos) * kConsumerWarps + cw) * 32 + lane, packed, keep_pol);
-          uint4 sc;
-          sc.x = __reduce_add_sync(0xffffffffu, __popc(mask[0]));
-          sc.y = __reduce_add_sync(0xffffffffu, __popc(mask[1]));
-          sc.z = __reduce_add_sync(0xffffffffu, __popc(mask[2]));
-          sc.w = __reduce_add_sync(0xffffffffu, __popc(mask[3]));
-          if (lane == 0) *reinterpret_cast<uint4*>(&S.park[b].cnt[(cw * kChunkTiles + tpos) * kUnitsPerThread]) = sc;
+          st_keep_u64(scratch_cta + ((b * kChunkTiles + tpos) * kConsumerWarps + cw) * 32 + lane, M, keep_pol);
+          const uint32_t sc = __reduce_add_sync(0xffffffffu, c);
+          if (lane == 0) S.park[b].cnt[tpos * kConsumerWarps + cw] = sc;
           slowbits |= 1u << (4 * b + tpos);
         }
       }
@@ -1053,26 +1089,20 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       prev = __shfl_sync(0xffffffffu, prev, 0);
       if (prev == kConsumerWarps - 1) {
         __threadfence_block();
-        // exclusive prefix over the 256 slice counts in text order (tile, j, warp); slices of
+        // exclusive prefix over the 64 slice counts in text order (tile, warp); slices of
         // warps that parked nothing for a tile count zero
-        uint32_t v[8], sum = 0;
+        uint32_t v[2], sum = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t s = lane * 8 + i;                      // text order
-          const uint32_t t = s / (kUnitsPerThread * kConsumerWarps);
-          const uint32_t j = (s / kConsumerWarps) % kUnitsPerThread;
-          const uint32_t w = s % kConsumerWarps;
-          v[i] = (t < ntiles && ((S.park[b].slow[w] >> t) & 1u))
-                     ? S.park[b].cnt[(w * kChunkTiles + t) * kUnitsPerThread + j] : 0u;
+        for (int i = 0; i < 2; ++i) {
+          const uint32_t sl = lane * 2 + i;                     // text order
+          const uint32_t t = sl / kConsumerWarps;
+          const uint32_t w = sl % kConsumerWarps;
+          v[i] = (t < ntiles && ((S.park[b].slow[w] >> t) & 1u)) ? S.park[b].cnt[sl] : 0u;
           sum += v[i];
         }
         const uint32_t incl = warp_inclusive_scan(sum, lane);
-        uint32_t run = incl - sum;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          S.park[b].off[lane * 8 + i] = run;
-          run += v[i];
-        }
+        S.park[b].off[lane * 2] = incl - sum;
+        S.park[b].off[lane * 2 + 1] = incl - sum + v[0];
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         if (seq >= kSlots) wait_done(seq - kSlots);          // slot seq % kSlots is free again
         if (lane == 0) {
@@ -1104,6 +1134,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         __threadfence();
         const uint32_t prev = atomicAdd(&S.fin, 1u);
         if (prev == kConsumerWarps - 1) {
+          EPSM_TRACE(P, 6);
           const unsigned long long ticket = atomicAdd(P.ctr + 2, 1ull);
           if (ticket == gridDim.x - 1) {
             __threadfence();
@@ -1115,10 +1146,18 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     } else {
       // ---- drain: write out the chunks still parked, then (last warp) stop the look-back warp
       for (uint32_t k = seq > kParked ? seq - kParked : 0; k < seq; ++k) flush_chunk_seq(k);
+      if (cw == 0 && lane == 0) {
+        EPSM_TRACE(P, 5);
+        if (P.trace) P.trace[blockIdx.x * 8 + 7] = seq;
+      }
       uint32_t prev = 0;
-      if (lane == 0) prev = atomicAdd(&S.fin, 1u);
+      if (lane == 0) {
+        __threadfence_block();
+        prev = atomicAdd(&S.fin, 1u);
+      }
       prev = __shfl_sync(0xffffffffu, prev, 0);
       if (prev == kConsumerWarps - 1 && lane == 0) {
+        EPSM_TRACE(P, 6);
         if (seq >= kSlots) mbar_wait(&S.lb_done[(seq - kSlots) % kSlots], ((seq - kSlots) / kSlots) & 1u);
         const uint32_t q = seq % kSlots;
         S.slot[q].chunk = kInfoEnd;
