@@ -70,8 +70,8 @@ constexpr int kWarpBytes = 32 * kSegBytes;                       // 2 KiB per co
 constexpr int kSlices = kChunkTiles * kConsumerWarps;            // 64 per chunk
 constexpr int kParked = 8;                                       // chunks parked awaiting their prefix
 constexpr int kSlots = 16;                                       // look-back queue depth
-constexpr int kWarpStage = 256;                                  // positions per warp round
-constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u64 every 16: 2-way banks
+constexpr int kWarpStage = 1024;                                 // positions per warp round
+constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u16 every 16 (bank spread)
 constexpr int kLookbackWindow = 256;                             // statuses per look-back round
 // parked masks in global scratch: one u64 (64 starts) per (chunk slot, tile, warp, lane)
 constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
@@ -155,7 +155,7 @@ struct __align__(128) SmemLayoutT {
   static constexpr int kStages = STAGES;
   static constexpr int kPark = SEARCH ? kParked : 1;
   uint8_t ring[STAGES][kStageBytes];
-  uint64_t wstage[SEARCH ? kConsumerWarps : 1][SEARCH ? kWarpStagePad : 1];
+  uint16_t wstage[SEARCH ? kConsumerWarps : 1][SEARCH ? kWarpStagePad : 2];   // slice-relative
   ParkedChunk park[kPark];
   alignas(8) uint64_t full[STAGES];
   uint64_t empty[STAGES];
@@ -591,12 +591,15 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
 }
 
 // Stage the positions of one slice in the warp's shared buffer and store them coalesced at
-// dst[0 .. min(tg, room)), kWarpStage per round.  Lane: 64-start mask M (bit k = start sb + k),
+// dst[0 .. min(tg, room)), kWarpStage per round.  Positions are staged as 16-bit offsets from
+// the slice base sbase (lane*64 + bit < 2048), so one round holds half a slice's 2048 starts
+// and the 64-bit adds happen only in the coalesced copy-out.  Lane: 64-start mask M,
 // exclusive offset `off` inside the slice; tg = slice total.  Every lane walks its bits once
 // across the rounds, stopping at each round's end.
-__device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint64_t room, uint64_t M,
-                                            uint32_t off, uint32_t tg, uint64_t sb, uint32_t lane) {
+__device__ __forceinline__ void write_slice(uint16_t* stage, uint64_t* dst, uint64_t room, uint64_t M,
+                                            uint32_t off, uint32_t tg, uint64_t sbase, uint32_t lane) {
   uint32_t lo = static_cast<uint32_t>(M), hi = static_cast<uint32_t>(M >> 32);
+  const uint32_t lbase = lane * kSegBytes;
   uint32_t idx = off;
   for (uint32_t R = 0; R < tg; R += kWarpStage) {
     const uint32_t lim = R + kWarpStage;
@@ -604,14 +607,14 @@ __device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint
       const uint32_t bit = __ffs(lo) - 1;
       lo &= lo - 1;
       const uint32_t i = idx - R;
-      stage[i + (i >> 4)] = sb + bit;
+      stage[i + (i >> 4)] = static_cast<uint16_t>(lbase + bit);
       ++idx;
     }
     while (hi && idx < lim) {
       const uint32_t bit = __ffs(hi) + 31;
       hi &= hi - 1;
       const uint32_t i = idx - R;
-      stage[i + (i >> 4)] = sb + bit;
+      stage[i + (i >> 4)] = static_cast<uint16_t>(lbase + bit);
       ++idx;
     }
     __syncwarp();
@@ -620,15 +623,16 @@ __device__ __forceinline__ void write_slice(uint64_t* stage, uint64_t* dst, uint
     else if (room - R < n) n = static_cast<uint32_t>(room - R);
     uint64_t* d = dst + R;
     if (n) {
-      // 16-byte stores: peel one entry if d is only 8-byte aligned
+      // 16-byte stores of entry pairs (e, e+1), e = lead + 2k: peel one entry if d is only
+      // 8-byte aligned (pairs then start odd and may straddle a pad: read them one by one)
       const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
-      if (lead && lane == 0) st_stream_u64(d, stage[0]);
+      if (lead && lane == 0) st_stream_u64(d, sbase + stage[0]);
       const uint32_t npairs = (n - lead) >> 1;
       for (uint32_t k = lane; k < npairs; k += 32) {
         const uint32_t e = lead + 2 * k;
-        st_stream_u64x2(d + e, stage[e + (e >> 4)], stage[(e + 1) + ((e + 1) >> 4)]);
+        st_stream_u64x2(d + e, sbase + stage[e + (e >> 4)], sbase + stage[(e + 1) + ((e + 1) >> 4)]);
       }
-      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, stage[(n - 1) + ((n - 1) >> 4)]);
+      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, sbase + stage[(n - 1) + ((n - 1) >> 4)]);
     }
     __syncwarp();
   }
@@ -651,7 +655,7 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
   const unsigned long long prefix = pk.prefix;
   if (prefix >= P.cap) return;
   const uint64_t cbase = static_cast<uint64_t>(pk.chunk) * kChunkBytes + P.pos_bias;
-  uint64_t* stage = S.wstage[cw];
+  uint16_t* stage = S.wstage[cw];
   const uint32_t nt = pk.ntiles;
   uint64_t mk4[kChunkTiles];
 #pragma unroll
@@ -698,7 +702,7 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
       }
       continue;
     }
-    write_slice(stage, P.pos + gidx, room, M, off, tg, sb, lane);
+    write_slice(stage, P.pos + gidx, room, M, off, tg, sb - lane * kSegBytes, lane);
   }
 }
 
