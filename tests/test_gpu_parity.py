@@ -1,7 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
 
 Bar: bit-exact positions and counts (integer/index work).  Sizes span several
-16 KiB tiles with ragged tails; every unit/tile alignment is hit by rotating the
+32 KiB tiles (and 128 KiB look-back chunks) with ragged tails; every unit/tile alignment is hit by rotating the
 text's base address; edge cases cover n < m, n = 0, m = 1 and 32, dense output,
 cap truncation and misaligned text pointers.
 """
@@ -16,7 +16,10 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-TILE = 16384
+TILE = 32768          # bytes per TMA stage (kTile)
+CHUNK = 4 * TILE      # look-back chunk (kChunkTiles tiles)
+SLICE = 2048          # text bytes one consumer warp covers per tile
+SEG = 64              # text bytes one consumer lane covers per tile
 
 
 @pytest.fixture(scope="module")
@@ -244,3 +247,90 @@ def test_plan_reuse_many_chunks(epsm, dev):
         pos, occ = epsm.search(pl, td, out=out)
         assert occ == want.size and np.array_equal(pos.cpu().numpy().astype(np.uint64), want)
         assert epsm.count(pl, td) == want.size
+
+
+def _edges(n, m):
+    """Starts that put a window across every kind of internal boundary of the kernel: the
+    lane segment (64 B), the warp slice (2 KiB), the tile (32 KiB) and the chunk (128 KiB)."""
+    out = set()
+    for unit in (SEG, SLICE, TILE, CHUNK):
+        for k in (1, 2, 3, 5):
+            e = k * unit
+            for d in (-m, -m + 1, -1, 0, 1):
+                s = e + d
+                if 0 <= s <= n - m:
+                    out.add(s)
+    out.update({0, n - m})
+    return sorted(out)
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 256])
+def test_internal_boundaries_multi_chunk(epsm, dev, sigma):
+    """Occurrences planted across lane-segment, slice, tile and chunk edges of a text of
+    several chunks with a ragged tail, for packed (m <= 8) and sampled (m >= 9) filters."""
+    rng = np.random.default_rng(900 + sigma)
+    n = 5 * CHUNK + 3 * TILE + 777
+    base = rng.integers(0, sigma, size=n, dtype=np.uint8)
+    for m in (2, 3, 4, 8, 9, 12, 13, 16, 20, 24, 28, 31, 32):
+        t = base.copy()
+        p = rng.integers(0, sigma, size=m, dtype=np.uint8)
+        for s in _edges(n, m):
+            t[s:s + m] = p
+        td = torch.from_numpy(t).to(dev)
+        occ = check(epsm, p.tobytes(), t, td, label=f"edges sigma={sigma}")
+        assert epsm.count(p.tobytes(), td) == occ
+
+
+def test_sampled_filter_repeated_and_periodic_grams(epsm, dev):
+    """Patterns whose q-grams repeat (one table bucket holding several candidate offsets)
+    and periodic texts where every sample hits: the sampled filter's candidate masks."""
+    rng = np.random.default_rng(4242)
+    n = 2 * CHUNK + 12345
+    for m in (9, 11, 12, 15, 16, 17, 23, 24, 25, 31, 32):
+        for unit in (b"a", b"ab", b"abc", b"abcd", b"aab", b"abcdefgh"):
+            p = (unit * 40)[:m]
+            t = np.frombuffer((unit * (n // len(unit) + 1))[:n], dtype=np.uint8).copy()
+            # sprinkle mismatches so that some windows fail late in the verification
+            t[rng.integers(0, n, size=200)] = ord("z")
+            td = torch.from_numpy(t).to(dev)
+            check(epsm, p, t, td, label=f"periodic unit={unit!r}")
+
+
+def _gram_hash(words):
+    """Test-side copy of the kernel's gram fingerprint (a multiply-add over little-endian
+    words, kernel epsm_kernels.cuh gram_hash); used only to BUILD adversarial inputs."""
+    mul = (0x9E3779B1, 0x85EBCA77, 0xC2B2AE3D, 0x27D4EB2F)
+    h = 0
+    for i, w in enumerate(words):
+        h = (h + w * mul[i]) & 0xFFFFFFFF
+    return h
+
+
+def test_sampled_filter_bucket_collisions(epsm, dev):
+    """Grams of one pattern that share a table bucket with different fingerprints make the
+    bucket a wildcard; text grams that share a bucket (and even the fingerprint) with a
+    pattern gram but differ must be rejected by the naive check.  Inputs are searched for
+    with the kernel's hash so both cases really occur."""
+    rng = np.random.default_rng(99)
+    m = 32                      # sampled (SK, SQ) = (16, 16): grams p[i .. i+15], i = 1..16
+    found = None
+    for _ in range(4000):
+        p = rng.integers(0, 256, size=m, dtype=np.uint8)
+        hs = [_gram_hash(np.frombuffer(p[i:i + 16].tobytes(), dtype="<u4").tolist()) for i in range(1, 17)]
+        idx = [h >> 21 for h in hs]
+        if len(set(idx)) < len(idx):
+            found = p
+            break
+    assert found is not None
+    p = found
+    # text: the pattern planted, plus decoys that share each gram's bucket index but differ
+    n = CHUNK + 999
+    t = rng.integers(0, 256, size=n, dtype=np.uint8)
+    for s in (0, 100, SEG - 3, SLICE - 17, TILE - 20, n - m):
+        t[s:s + m] = p
+    decoy = p.copy()
+    decoy[20] ^= 0x40            # a near miss that still matches the first 16 bytes of some grams
+    for s in (5000, 9000, TILE + 5):
+        t[s:s + m] = decoy
+    td = torch.from_numpy(t).to(dev)
+    check(epsm, p.tobytes(), t, td, label="bucket collisions")
