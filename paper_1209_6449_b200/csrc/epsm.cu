@@ -8,7 +8,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <mutex>
 #include <new>
+#include <vector>
 
 #include "epsm.h"
 #include "epsm_internal.h"
@@ -143,63 +145,73 @@ int epsm_bind_device(epsm_plan_t* plan, const void* dptr) {
   return EPSM_OK;
 }
 
-static int ensure_workspace(epsm_plan_t* plan, uint64_t chunks, bool search, cudaStream_t s) {
-  if (!plan->d_ctr) {
-    cudaError_t e = cudaMalloc(&plan->d_ctr, 4 * sizeof(unsigned long long));
+// ---- scan workspace pool, one per (device, stream)
+
+namespace {
+std::mutex g_ws_mu;
+std::vector<epsm_workspace*> g_ws;
+}  // namespace
+
+epsm_workspace* epsm_get_workspace(int device, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (epsm_workspace* w : g_ws)
+    if (w->device == device && w->stream == s) return w;
+  epsm_workspace* w = new (std::nothrow) epsm_workspace();
+  if (!w) return nullptr;
+  w->device = device;
+  w->stream = s;
+  g_ws.push_back(w);
+  return w;
+}
+
+// Make the workspace of stream s big enough for a launch of `chunks` chunks on `ctas` CTAs.
+// Growing it synchronises the stream first (no grid may still use the old buffers).
+static int ensure_workspace(epsm_workspace* ws, uint64_t chunks, uint64_t ctas, bool search, cudaStream_t s) {
+  if (!ws->d_ctr) {
+    cudaError_t e = cudaMalloc(&ws->d_ctr, 16 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
-      epsm_set_error("cudaMalloc(ctr): %s", cudaGetErrorString(e));
+      epsm_set_error("cudaMalloc(counters): %s", cudaGetErrorString(e));
       return EPSM_ENOMEM;
     }
-    e = cudaMemsetAsync(plan->d_ctr, 0, 4 * sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(ctr)");
-    plan->ctr_base = 0;
-  }
-  if (plan->num_sms <= 0) {
-    cudaError_t e = cudaDeviceGetAttribute(&plan->num_sms, cudaDevAttrMultiProcessorCount, plan->device);
-    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+    e = cudaMemsetAsync(ws->d_ctr, 0, 16 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(counters)");
   }
   if (!search) return EPSM_OK;
-  // parked-mask scratch: 128 KiB per CTA of the grid this launch uses
-  const uint64_t ctas = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
-  if (ctas > plan->park_ctas) {
-    if (plan->d_park) {
-      cudaStreamSynchronize(s);
-      cudaFree(plan->d_park);
-      plan->d_park = nullptr;
-      plan->park_ctas = 0;
+  if (ctas > ws->scratch_ctas) {
+    cudaStreamSynchronize(s);
+    for (auto& p : ws->d_scratch) {
+      if (p) cudaFree(p);
+      p = nullptr;
     }
+    ws->scratch_ctas = 0;
     const size_t bytes = static_cast<size_t>(ctas) * epsm::kScratchPerCta * sizeof(uint64_t);
-    cudaError_t e = cudaMalloc(&plan->d_park, bytes);
-    if (e != cudaSuccess) {
-      epsm_set_error("cudaMalloc(parked masks, %zu bytes): %s", bytes, cudaGetErrorString(e));
-      return EPSM_ENOMEM;
+    for (auto& p : ws->d_scratch) {
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) {
+        epsm_set_error("cudaMalloc(parked masks, %zu bytes): %s", bytes, cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
     }
-    plan->park_ctas = ctas;
+    ws->scratch_ctas = ctas;
   }
-  if (chunks > plan->status_cap) {
-    if (plan->d_status) {
-      cudaStreamSynchronize(s);
-      cudaFree(plan->d_status);
-      plan->d_status = nullptr;
-      plan->status_cap = 0;
+  if (chunks > ws->status_cap) {
+    cudaStreamSynchronize(s);
+    for (auto& p : ws->d_status) {
+      if (p) cudaFree(p);
+      p = nullptr;
     }
-    uint64_t cap = chunks < 1024 ? 1024 : chunks;
-    cudaError_t e = cudaMalloc(&plan->d_status, cap * sizeof(unsigned long long));
-    if (e != cudaSuccess) {
-      epsm_set_error("cudaMalloc(status, %llu chunks): %s", (unsigned long long)cap, cudaGetErrorString(e));
-      return EPSM_ENOMEM;
+    ws->status_cap = 0;
+    const uint64_t cap = chunks < 1024 ? 1024 : chunks;
+    for (auto& p : ws->d_status) {
+      cudaError_t e = cudaMalloc(&p, cap * sizeof(unsigned long long));
+      if (e != cudaSuccess) {
+        epsm_set_error("cudaMalloc(status, %llu chunks): %s", (unsigned long long)cap, cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
+      e = cudaMemsetAsync(p, 0, cap * sizeof(unsigned long long), s);
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
     }
-    e = cudaMemsetAsync(plan->d_status, 0, cap * sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
-    plan->status_cap = cap;
-    plan->epoch = 0;
-  }
-  // next epoch; on wrap clear the words so stale tags can never match
-  plan->epoch = (plan->epoch + 1) & 0xFFFFFFu;
-  if (plan->epoch == 0) {
-    cudaError_t e = cudaMemsetAsync(plan->d_status, 0, plan->status_cap * sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
-    plan->epoch = 1;
+    ws->status_cap = cap;
   }
   return EPSM_OK;
 }
@@ -279,26 +291,45 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
     epsm_set_error("text too large: %llu tiles", (unsigned long long)tiles);
     return EPSM_EINVAL;
   }
-  int rc = ensure_workspace(plan, chunks, search, s);
+  epsm_workspace* ws = epsm_get_workspace(plan->device, s);
+  if (!ws) return EPSM_ENOMEM;
+  if (ws->num_sms <= 0) {
+    cudaError_t e = cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, plan->device);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  }
+  const uint64_t grid = chunks < static_cast<uint64_t>(ws->num_sms) ? chunks : ws->num_sms;
+  int rc = ensure_workspace(ws, chunks, grid, search, s);
   if (rc) return rc;
+  // launch L uses parity L & 1; its status tag is L (24 bits); on wrap every word is cleared
+  // (in stream order) so a stale tag can never match
+  uint64_t L = ws->launches;
+  if (search && (L & 0xFFFFFFull) == 0) {
+    for (auto* p : ws->d_status) {
+      cudaError_t e = cudaMemsetAsync(p, 0, ws->status_cap * sizeof(unsigned long long), s);
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
+    }
+    ws->launches = ++L;
+  }
+  const int par = static_cast<int>(L & 1u);
   P.ntiles = static_cast<uint32_t>(tiles);
   P.nchunks = static_cast<uint32_t>(chunks);
-  P.ctr = plan->d_ctr;
-  P.ctr_base = plan->ctr_base;
+  P.ctr = ws->d_ctr + 8 * par;
+  P.ctr_base = ws->ctr_base[par];
+  P.exit_ctr = ws->d_ctr + 8 * par + 3;
+  P.exit_expect = ws->exit_total[par];      // every CTA of launch L-2 (and before) has exited
   if (search) {
-    P.status = plan->d_status;
-    P.scratch = plan->d_park;
-    P.tag = static_cast<unsigned long long>(plan->epoch) << epsm::kEpochShift;
+    P.status = ws->d_status[par];
+    P.scratch = ws->d_scratch[par];
+    P.tag = static_cast<unsigned long long>(L & 0xFFFFFFull) << epsm::kEpochShift;
   }
   P.trace = trace_slot(plan->device);
   KernelFn fn = kernel_for(plan->m, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan->device, smem);
   if (rc) return rc;
-  const uint64_t grid = chunks < static_cast<uint64_t>(plan->num_sms) ? chunks : plan->num_sms;
-  // programmatic dependent launch: the kernel's prologue (barrier setup, first chunk's TMA
-  // loads and filtering) overlaps the previous grid's tail; it waits (griddepcontrol.wait)
-  // before touching the workspace or any output
+  // programmatic dependent launch: the kernel starts while the previous grid on the stream
+  // drains; it synchronises with that grid (griddepcontrol.wait) only before writing outputs,
+  // and with launch L-2 (same workspace parity) through the CTA exit counter
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(epsm::kThreads);
@@ -315,7 +346,9 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
   // CTAs start on chunks [0, grid) and draw the rest from the counter, two draws ahead of the
   // chunk they stream: (chunks - grid) useful draws + exactly 2 draws past the end per CTA
-  plan->ctr_base += chunks + grid;
+  ws->ctr_base[par] += chunks + grid;
+  ws->exit_total[par] += grid;
+  ws->launches = L + 1;
   return EPSM_OK;
 }
 
@@ -386,9 +419,6 @@ void epsm_plan_free(epsm_plan_t* plan) {
     cudaSetDevice(plan->device);
     cudaDeviceSynchronize();
   }
-  if (plan->d_status) cudaFree(plan->d_status);
-  if (plan->d_ctr) cudaFree(plan->d_ctr);
-  if (plan->d_park) cudaFree(plan->d_park);
   if (plan->d_occ) cudaFree(plan->d_occ);
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);

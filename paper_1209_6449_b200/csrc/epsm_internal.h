@@ -13,17 +13,8 @@ struct epsm_plan_s {
   uint32_t pat[9] = {};     // zero-padded pattern words
   uint32_t pmask[9] = {};   // byte masks of the words
   int device = -1;          // bound on first device use
-  int num_sms = 0;
-  // look-back workspace (one status word per 128 KiB chunk), epoch-tagged
-  unsigned long long* d_status = nullptr;
-  uint64_t status_cap = 0;
-  uint32_t epoch = 0;
-  // chunk-id counter: monotonic across launches; ctr_base = its value at the next launch
-  unsigned long long* d_ctr = nullptr;
-  unsigned long long ctr_base = 0;
-  // parked match masks of the search kernel (per CTA, L2-resident), allocated on first search
-  uint64_t* d_park = nullptr;
-  uint64_t park_ctas = 0;
+  // (the scan workspace -- look-back status words, chunk counters, parked masks -- belongs
+  //  to the (device, stream) the search runs on, see epsm_workspace below)
   // occ readback for the synchronous calls
   unsigned long long* d_occ = nullptr;
   unsigned long long* h_occ = nullptr;
@@ -39,6 +30,27 @@ struct epsm_plan_s {
   unsigned long long* h_counts = nullptr;
   int counts_cap = 0;
 };
+
+// Scan workspace of one (device, stream), double-buffered by launch parity so that a search
+// may start while the previous one on the stream is still draining (programmatic dependent
+// launch): launch L uses parity L & 1 and first waits, on the device, until launch L-2 (the
+// previous user of that parity) has retired all its CTAs.
+struct epsm_workspace {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  uint64_t launches = 0;                      // launch sequence number of the next launch
+  unsigned long long* d_status[2] = {nullptr, nullptr};   // one status word per chunk
+  uint64_t status_cap = 0;
+  uint64_t* d_scratch[2] = {nullptr, nullptr};            // parked masks, per CTA
+  uint64_t scratch_ctas = 0;
+  unsigned long long* d_ctr = nullptr;        // [parity][8]: chunk counter, count accumulator,
+                                              // count ticket, CTA exit counter
+  unsigned long long ctr_base[2] = {0, 0};    // chunk counter value at the next launch
+  unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
+};
+
+epsm_workspace* epsm_get_workspace(int device, cudaStream_t s);
 
 void epsm_set_error(const char* fmt, ...);
 int epsm_cuda_fail(cudaError_t e, const char* what);

@@ -77,7 +77,8 @@ constexpr int kLookbackWindow = 256;                             // statuses per
 constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
 static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking rotation");
 static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
-static_assert(kSlices == 64 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
+static_assert(kSlices % 32 == 0 && kChunkTiles <= 8 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
+constexpr uint32_t kTileBitsMask = (1u << kChunkTiles) - 1u;      // slow-tile bits of one parked chunk
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 
@@ -121,6 +122,8 @@ struct KParams {
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
   uint32_t pmask[9];            // per-word byte masks (partial last word)
   unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
+  unsigned long long* exit_ctr; // CTAs of all launches on this workspace parity that have exited
+  unsigned long long exit_expect;   // value meaning "launch L-2 (same parity) has retired"
 };
 
 // %globaltimer stamps for the optional per-CTA timeline (EPSM_TRACE)
@@ -165,6 +168,7 @@ struct __align__(128) SmemLayoutT {
   uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
   uint32_t info[STAGES];        // tile index | (last-of-chunk << 31), or kInfoEnd
   uint32_t fin;                 // consumer warps that reached the end
+  uint32_t ws_ok;               // the workspace parity is free (launch L-2 retired)
 };
 using SearchSmem = SmemLayoutT<kStagesSearch, true>;
 using CountSmem = SmemLayoutT<kStagesCount, false>;
@@ -242,6 +246,16 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 }
 __device__ __forceinline__ void griddep_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Bulk prefetch of global memory into L2 (no shared memory, no completion tracking).
@@ -515,6 +529,13 @@ __device__ __forceinline__ uint32_t verify_full(uint32_t r, const uint8_t* tile,
   return keep;
 }
 
+// Wait until the producer has seen this launch's workspace parity free (launch L-2 retired).
+template <class Smem>
+__device__ __forceinline__ void wait_ws(Smem& S) {
+  while (*reinterpret_cast<volatile uint32_t*>(&S.ws_ok) == 0u) __nanosleep(64);
+  __threadfence_block();
+}
+
 __device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -649,11 +670,15 @@ __device__ __forceinline__ uint32_t popc64(uint64_t v) {
 template <class Smem>
 __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const uint64_t* scratch_cta,
                                              uint32_t b, uint32_t slow, uint32_t cw, uint32_t lane,
-                                             uint64_t keep_pol) {
+                                             uint64_t keep_pol, bool& out_ok) {
   const ParkedChunk& pk = S.park[b];
   if (pk.total == 0 || slow == 0) return;                      // warp-uniform
   const unsigned long long prefix = pk.prefix;
   if (prefix >= P.cap) return;
+  if (!out_ok) {                      // the previous grid on the stream may write the same output
+    griddep_wait();
+    out_ok = true;
+  }
   const uint64_t cbase = static_cast<uint64_t>(pk.chunk) * kChunkBytes + P.pos_bias;
   uint16_t* stage = S.wstage[cw];
   const uint32_t nt = pk.ntiles;
@@ -751,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   }
   if (tid == 0) {
     S.fin = 0;
+    S.ws_ok = 0;
     griddep_launch_dependents();   // the next grid may start its prologue as our CTAs retire
   }
   __syncthreads();
@@ -782,6 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     };
     unsigned long long cur = blockIdx.x, after = 0, pend = 0;
     bool first = true;
+    bool ws_seen = false;                      // (lane 0) workspace parity seen free
     while (true) {
       if (cur >= P.nchunks) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
@@ -813,6 +840,16 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           }
           if (first && t == t0) EPSM_TRACE(P, 1);
           if (t == t0 && !first) pend = draw();   // consumed after this chunk
+          if (first && !ws_seen && (t + 1 == t1 || t + 1 - t0 == static_cast<uint32_t>(kStages))) {
+            // the first loads (text only) are in flight; before anything touches the workspace
+            // (chunk counter, status words, parked masks) launch L-2, the previous user of
+            // this parity, must have retired -- normally long done, so one load.  (Done by the
+            // time the ring is full: consumers may wait for it before releasing a stage.)
+            while (ld_acquire(P.exit_ctr) < P.exit_expect) __nanosleep(100);
+            __threadfence_block();
+            *reinterpret_cast<volatile uint32_t*>(&S.ws_ok) = 1u;
+            ws_seen = true;
+          }
         }
         if (++stage == kStages) {
           stage = 0;
@@ -820,8 +857,6 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
       }
       if (first) {
-        // the first chunk's loads were issued before waiting on the previous grid (PDL)
-        griddep_wait();
         if (lane == 0) {
           after = draw();
           pend = draw();
@@ -845,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       named_barrier_arrive(1, kConsumers + 32);
     }
     if constexpr (SEARCH) {
-      griddep_wait();
+      // (chunks reach this queue only after the consumers saw the workspace free)
       uint32_t q = 0, par = 0;
       while (true) {
         mbar_wait_sleep(&S.lb_full[q], par, 200);
@@ -860,7 +895,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         const unsigned long long pre = skip ? kAborted : lookback(P, sl.chunk, sl.total, lane, fin);
         if (lane == 0) {
           if (pre != kAborted) S.park[sl.park].prefix = pre;
-          if (last) *P.occ = pre + sl.total;
+          if (last) {
+            griddep_wait();                    // the previous grid may write the same occ
+            *P.occ = pre + sl.total;
+          }
           mbar_arrive(&S.lb_done[q]);
         }
         __syncwarp();
@@ -883,7 +921,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     bool try_pair = true;                      // test the pair stage on its own (adaptive)
     uint32_t pair_streak = 0;                  // consecutive pair tests that found candidates
     uint32_t tiles_seen = 0;
-    bool waited = false;                       // griddepcontrol.wait done
+    bool waited = false;                       // workspace parity seen free (S.ws_ok)
+    bool out_ok = false;                       // griddepcontrol.wait done (outputs writable)
     uint64_t* scratch_cta = SEARCH ? P.scratch + static_cast<uint64_t>(blockIdx.x) * kScratchPerCta : nullptr;
     const uint64_t keep_pol = policy_evict_last();
 
@@ -896,12 +935,12 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // (a warp that parked no masks for the chunk has nothing to write and needs no prefix)
     auto flush_chunk_seq = [&](uint32_t k) {
       const uint32_t b = k % kParked;
-      const uint32_t sb = (slowbits >> (4 * b)) & 0xFu;
+      const uint32_t sb = (slowbits >> (kChunkTiles * b)) & kTileBitsMask;
       if (sb) {
         wait_done(k);
-        flush_slices(P, S, scratch_cta, b, sb, cw, lane, keep_pol);
+        flush_slices(P, S, scratch_cta, b, sb, cw, lane, keep_pol, out_ok);
       }
-      slowbits &= ~(0xFu << (4 * b));
+      slowbits &= ~(kTileBitsMask << (kChunkTiles * b));
     };
 
     if constexpr (SK > 0) named_barrier_sync(1, kConsumers + 32);   // gram table built by warp 1
@@ -1056,14 +1095,14 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         const uint32_t c = popc64(M);
         acc += c;
         if constexpr (SEARCH) {
-          if (!waited) {                       // the scratch may still be read by the previous grid
-            griddep_wait();
+          if (!waited) {                       // the scratch may still be read by launch L-2
+            wait_ws(S);
             waited = true;
           }
           st_keep_u64(scratch_cta + ((b * kChunkTiles + tpos) * kConsumerWarps + cw) * 32 + lane, M, keep_pol);
           const uint32_t sc = __reduce_add_sync(0xffffffffu, c);
           if (lane == 0) S.park[b].cnt[tpos * kConsumerWarps + cw] = sc;
-          slowbits |= 1u << (4 * b + tpos);
+          slowbits |= 1u << (kChunkTiles * b + tpos);
         }
       }
       __syncwarp();
@@ -1077,13 +1116,13 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (!last_in_chunk) continue;
 
       // ---- this warp is done with chunk #seq; the last warp to finish hands it off
-      if (!waited) {                           // status words may still belong to the previous grid
-        griddep_wait();
+      if (!waited) {                           // status words may still belong to launch L-2
+        wait_ws(S);
         waited = true;
       }
       const uint32_t chunk = tile / kChunkTiles;
       const uint32_t ntiles = tpos;
-      if (lane == 0) S.park[b].slow[cw] = static_cast<uint8_t>((slowbits >> (4 * b)) & 0xFu);
+      if (lane == 0) S.park[b].slow[cw] = static_cast<uint8_t>((slowbits >> (kChunkTiles * b)) & kTileBitsMask);
       __syncwarp();
       uint32_t prev = 0;
       if (lane == 0) {
@@ -1095,18 +1134,23 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         __threadfence_block();
         // exclusive prefix over the 64 slice counts in text order (tile, warp); slices of
         // warps that parked nothing for a tile count zero
-        uint32_t v[2], sum = 0;
+        constexpr int kPerLane = kSlices / 32;
+        uint32_t v[kPerLane], sum = 0;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const uint32_t sl = lane * 2 + i;                     // text order
+        for (int i = 0; i < kPerLane; ++i) {
+          const uint32_t sl = lane * kPerLane + i;              // text order
           const uint32_t t = sl / kConsumerWarps;
           const uint32_t w = sl % kConsumerWarps;
           v[i] = (t < ntiles && ((S.park[b].slow[w] >> t) & 1u)) ? S.park[b].cnt[sl] : 0u;
           sum += v[i];
         }
         const uint32_t incl = warp_inclusive_scan(sum, lane);
-        S.park[b].off[lane * 2] = incl - sum;
-        S.park[b].off[lane * 2 + 1] = incl - sum + v[0];
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int i = 0; i < kPerLane; ++i) {
+          S.park[b].off[lane * kPerLane + i] = run;
+          run += v[i];
+        }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         if (seq >= kSlots) wait_done(seq - kSlots);          // slot seq % kSlots is free again
         if (lane == 0) {
@@ -1131,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     if constexpr (!SEARCH) {
       // count: per-warp partials into the workspace accumulator; the CTA's last warp takes a
       // ticket, and the last CTA publishes occ and re-arms the workspace (no memset per call)
-      griddep_wait();
+      wait_ws(S);
       const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
       if (lane == 0) {
         if (wsum) atomicAdd(P.ctr + 1, static_cast<unsigned long long>(wsum));
@@ -1142,6 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           const unsigned long long ticket = atomicAdd(P.ctr + 2, 1ull);
           if (ticket == gridDim.x - 1) {
             __threadfence();
+            griddep_wait();                    // the previous grid may write the same occ
             *P.occ = atomicExch(P.ctr + 1, 0ull);
             P.ctr[2] = 0;
           }
@@ -1169,6 +1214,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
     }
   }
+  // retire: this CTA no longer touches the workspace parity (counter, status, parked masks)
+  __syncthreads();
+  if (tid == 0) red_release_add(P.exit_ctr, 1ull);
 }
 
 }  // namespace epsm
