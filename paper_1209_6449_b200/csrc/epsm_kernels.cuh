@@ -11,38 +11,40 @@
 //                          halo is the GPU analogue of EPSMb's wsblend, which only exists
 //                          to avoid unaligned loads: shared memory is
 //                          byte addressable, so every alignment is read directly.
-//   warps 2-17  consumers  16 candidate starts ("alpha = 16") per
-//                          thread and unit, 4 units per thread and tile.  The 16
-//                          consumer warps never wait for each other (no block
-//                          barrier): per-chunk bookkeeping is one shared-memory
-//                          atomic, and each warp writes out its own slices:
-//       filter   EPSMa's shift-AND (Fig. 1 lines 5-9), packed:
+//   warps 2-17  consumers  each lane owns 64 contiguous text bytes of a tile (4 units of
+//                          alpha = 16 candidate starts), a warp a 2 KiB
+//                          slice.  The 16 consumer warps never wait for each other (no block
+//                          barrier): per-chunk bookkeeping is one shared-memory atomic, and
+//                          each warp writes out its own slices:
+//       filter   m <= 8: EPSMa's shift-AND (Fig. 1 lines 5-9), packed:
 //                Z_k = OR_{i<F} ( S_i[k] XOR B_i ), S_i = the text shifted by i bytes,
 //                B_i = p_i * 0x01010101.  A zero byte j of Z_k
 //                <=> t[u+4k+j+i] = p_i for all i < F = min(m, 4).  Pair stage first,
 //                extended to F bytes only where the pair has candidates.
-//       verify   the "naive check" of each candidate for
-//                m > 4: word compares against the zero-padded pattern blocks P_i
-//                (PAPER.md:124-128), last partial word masked.
-//       count    popcount of the 16-bit match mask r.
-//       masks    tiles with candidates park their masks r (2 bytes per 16 text bytes)
-//                in a small per-CTA global scratch that stays in L2 (8 chunks, round
-//                robin), so the chunk's positions can be written once its global
-//                offset is known, without re-reading the text.
+//                m >= 9: EPSMc's block fingerprints: one gram every SK
+//                bytes, looked up in a shared-memory table of the pattern's grams.
+//       verify   the "naive check" of each candidate against the
+//                zero-padded pattern blocks P_i, last word masked.
+//       count    popcount of the 64-bit lane match mask.
+//       masks    tiles with matches park their lane masks (8 bytes per 64 text bytes) in a
+//                small per-CTA global scratch that stays in L2 (8 chunks, round robin), so
+//                a chunk's positions are written once its global offset is known, without
+//                re-reading the text.
 //   warp 1      look-back  per chunk: walk the predecessors' status words 256 at a time
 //                          until an inclusive prefix is found (decoupled look-back over
-//                          64-bit epoch-tagged words), publish the inclusive prefix.  It
+//                          64-bit launch-tagged words), publish the inclusive prefix.  It
 //                          runs concurrently with the consumers through a 16-deep slot
 //                          queue; the consumers published the chunk's aggregate already.
-//   report       eight chunks later each consumer warp turns ITS 16 slices (32 units
-//                each) of the parked chunk into positions chunk_base + unit*16 + {r}
-//                (Fig. 1 line 11), stages them in its own shared-
-//                memory buffer and stores them coalesced (16-byte stores) at
-//                pos[prefix + slice offset].
+//                          (Sampled variants: it first builds the gram table.)
+//   report       eight chunks later each consumer warp turns ITS 4 slices of the parked
+//                chunk into positions slice_base + lane*64 + {r} (PAPER.md:431-441,
+//                Fig. 1 line 11), directly or staged in its shared-memory buffer and
+//                stored coalesced (16-byte stores) at pos[prefix + slice offset].
 //
-// Launches use programmatic dependent launch: the prologue and the first chunk's loads
-// and filtering overlap the previous grid; griddepcontrol.wait precedes every access
-// to memory the previous grid may write (workspace, parked masks, outputs).
+// Launches use programmatic dependent launch: a grid starts scanning while the previous one
+// on the stream drains.  The workspace (counters, status words, parked masks) is double
+// buffered by launch parity: launch L waits, through a CTA exit counter, only for launch
+// L-2; griddepcontrol.wait precedes only the writes of outputs (positions, occ).
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -438,7 +440,7 @@ __device__ __forceinline__ uint32_t verify_candidates(uint32_t r, const uint8_t*
 
 // ------------------------------------------------------------------ sampled filter (EPSMc)
 
-// EPSMc's fingerprint h (PAPER.md:581-586; wscrc there, a multiply-add hash over the gram's
+// EPSMc's fingerprint h (PAPER.md:580-584; wscrc there, a multiply-add hash over the gram's
 // little-endian words here).  Bits [31:21] index the table, bits [20:6] are the fingerprint.
 template <int NW>
 __device__ __forceinline__ uint32_t gram_hash(const uint32_t (&w)[NW]) {
@@ -473,7 +475,7 @@ __device__ __forceinline__ void load_sample(const uint8_t* p, uint32_t (&w)[SQ /
   }
 }
 
-// EPSMc preprocessing (PAPER.md:588-594, Fig. 1 lines 1-5): for every pattern offset
+// EPSMc preprocessing (PAPER.md:590-594, Fig. 1 lines 1-5): for every pattern offset
 // i = 1..SK the fingerprint of the gram p[i .. i+SQ-1] is entered in the table; the entry's
 // mask bit SK-i marks the start (sample offset - i) as a candidate.  Grams of different
 // fingerprints that share a bucket make it a wildcard (no fingerprint check).  One warp.
