@@ -46,13 +46,14 @@ extern "C" {
 
 #define EPSM_OK       0
 #define EPSM_EINVAL  (-1)   /* NULL argument, m = 0, d_pos NULL with cap > 0, n too large */
-#define EPSM_EUNSUP  (-2)   /* m > 32 (long patterns, EPSMc territory: not built yet)    */
+#define EPSM_EUNSUP  (-2)   /* m > EPSM_MAX_M_LONG                                        */
 #define EPSM_EALIGN  (-3)   /* d_pos or d_occ not 8-byte aligned                          */
 #define EPSM_ECUDA   (-4)   /* a CUDA runtime call or kernel launch failed                */
 #define EPSM_ENCCL   (-5)   /* NCCL missing or an NCCL call failed (sharded search)       */
 #define EPSM_ENOMEM  (-6)   /* device or pinned-host allocation failed                    */
 
-#define EPSM_MAX_M   32u
+#define EPSM_MAX_M   32u     /* short patterns: the packed / sampled filters of Sec. 3.2-3.4   */
+#define EPSM_MAX_M_LONG 4096u /* long patterns (EPSMc block fingerprints)  */
 
 typedef struct epsm_plan_s epsm_plan_t;   /* opaque, host-owned */
 typedef void *epsm_stream_t;              /* a cudaStream_t     */
@@ -60,10 +61,14 @@ typedef void *epsm_stream_t;              /* a cudaStream_t     */
 /*
  * epsm_plan -- preprocessing (Sec. 3.2: B[i] = (p_i)^alpha for
  * i < m' = min(m, 4); Sec. 3.3: the filter prefix p'; dispatch by m,
- * PAPER.md:150-152).  Copies pattern[0..m-1] (1 <= m <= 32) into a new plan,
- * builds the broadcast words and selects the kernel variant for m.  No device
- * work.  *out receives the plan (caller frees with epsm_plan_free).
- * Returns EPSM_OK, EPSM_EINVAL (NULL pattern/out, m = 0) or EPSM_EUNSUP (m > 32).
+ * PAPER.md:150-152).  Copies pattern[0..m-1] (1 <= m <= EPSM_MAX_M_LONG) into a
+ * new plan, builds the broadcast words and selects the kernel variant for m
+ * (m > 32: EPSMc's sampled block fingerprints with the naive check of each
+ * candidate against the pattern in device memory; the plan
+ * uploads the pattern on its first search).  No device work.  *out receives the
+ * plan (caller frees with epsm_plan_free).
+ * Returns EPSM_OK, EPSM_EINVAL (NULL pattern/out, m = 0) or EPSM_EUNSUP
+ * (m > EPSM_MAX_M_LONG).
  */
 int epsm_plan(const uint8_t *pattern, uint32_t m, epsm_plan_t **out);
 

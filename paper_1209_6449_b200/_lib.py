@@ -23,7 +23,8 @@ EPSM_EALIGN = -3
 EPSM_ECUDA = -4
 EPSM_ENCCL = -5
 EPSM_ENOMEM = -6
-MAX_M = 32
+MAX_M = 32          # short patterns (packed / sampled filters in shared memory)
+MAX_M_LONG = 4096   # long patterns (sampled filter, naive check against device memory)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -70,6 +70,7 @@ uint32_t sample_min_m() {
 //            (used where candidates are dense), MW = ceil(m/4) words;
 //   sampled: one SQ-byte gram every SK bytes (SK + SQ <= m), MW words verified.
 KernelFn kernel_for(uint32_t m, bool search) {
+  if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
   if (m >= 8 && m >= sample_min_m()) {
     switch (m) {
       case 8: return pick<4, 4, 2, 4, 4>(search);
@@ -285,6 +286,21 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   std::memcpy(P.bcast2, plan->bcast2, sizeof(P.bcast2));
   std::memcpy(P.pat, plan->pat, sizeof(P.pat));
   std::memcpy(P.pmask, plan->pmask, sizeof(P.pmask));
+  P.m = plan->m;
+  if (plan->m > EPSM_MAX_M) {
+    if (!plan->d_pat) {   // first long search: upload the zero-padded pattern words
+      const size_t bytes = ((plan->m + 3) / 4 + 1) * sizeof(uint32_t);
+      cudaError_t e = cudaMalloc(&plan->d_pat, bytes);
+      if (e != cudaSuccess) {
+        plan->d_pat = nullptr;
+        epsm_set_error("cudaMalloc(pattern, %zu bytes): %s", bytes, cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
+      e = cudaMemcpyAsync(plan->d_pat, plan->pattern, bytes, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(pattern)");
+    }
+    P.dpat = plan->d_pat;
+  }
   const uint64_t tiles = (P.s_hi + epsm::kTile - 1) / epsm::kTile;
   const uint64_t chunks = (tiles + epsm::kChunkTiles - 1) / epsm::kChunkTiles;
   if (tiles > 0x7FFFFFFFull) {
@@ -384,8 +400,8 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
     epsm_set_error("pattern must be non-NULL with m >= 1");
     return EPSM_EINVAL;
   }
-  if (m > EPSM_MAX_M) {
-    epsm_set_error("m = %u > %u is not supported (long-pattern filter not built)", m, EPSM_MAX_M);
+  if (m > EPSM_MAX_M_LONG) {
+    epsm_set_error("m = %u > %u is not supported", m, EPSM_MAX_M_LONG);
     return EPSM_EUNSUP;
   }
   epsm_plan_t* p = new (std::nothrow) epsm_plan_t();
@@ -420,6 +436,7 @@ void epsm_plan_free(epsm_plan_t* plan) {
     cudaDeviceSynchronize();
   }
   if (plan->d_occ) cudaFree(plan->d_occ);
+  if (plan->d_pat) cudaFree(plan->d_pat);
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);
   if (plan->d_pos_buf) cudaFree(plan->d_pos_buf);
@@ -594,7 +611,7 @@ const char* epsm_strerror(int64_t code) {
   switch (code) {
     case EPSM_OK: return "EPSM_OK: success";
     case EPSM_EINVAL: return "EPSM_EINVAL: invalid argument";
-    case EPSM_EUNSUP: return "EPSM_EUNSUP: unsupported pattern length (m > 32)";
+    case EPSM_EUNSUP: return "EPSM_EUNSUP: unsupported pattern length (m > 4096)";
     case EPSM_EALIGN: return "EPSM_EALIGN: misaligned output pointer (needs 8-byte alignment)";
     case EPSM_ECUDA: return "EPSM_ECUDA: CUDA error";
     case EPSM_ENCCL: return "EPSM_ENCCL: NCCL error";

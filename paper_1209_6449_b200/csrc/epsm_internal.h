@@ -7,7 +7,8 @@
 
 struct epsm_plan_s {
   uint32_t m = 0;
-  uint8_t pattern[EPSM_MAX_M] = {};
+  uint8_t pattern[EPSM_MAX_M_LONG] = {};
+  uint32_t* d_pat = nullptr;  // m > 32: zero-padded pattern words in device memory
   uint32_t bcast[4] = {};   // B_i = p_i * 0x01010101
   uint32_t bcast2[4] = {};  // B_{4+i}: second filter word
   uint32_t pat[9] = {};     // zero-padded pattern words

@@ -124,6 +124,8 @@ struct KParams {
   uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
   uint32_t pmask[9];            // per-word byte masks (partial last word)
   unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
+  const uint32_t* dpat;         // m > 32: zero-padded pattern words in device memory
+  uint32_t m;                   // pattern length
   unsigned long long* exit_ctr; // CTAs of all launches on this workspace parity that have exited
   unsigned long long exit_expect;   // value meaning "launch L-2 (same parity) has retired"
 };
@@ -538,6 +540,38 @@ __device__ __forceinline__ void wait_ws(Smem& S) {
   __threadfence_block();
 }
 
+// Naive check for long patterns (m > 32, MW = 0 variants): the window runs past the tile
+// halo, so it is compared against the text in global memory (L2: the tile was just
+// streamed) and the pattern words in device memory.  Reads stay inside the words that hold
+// text bytes (the last one lies in the 16-byte block of the text's last byte).
+__device__ __forceinline__ uint32_t verify_long(uint32_t r, uint64_t us, const KParams& P) {
+  const uint32_t* t32 = reinterpret_cast<const uint32_t*>(P.text);
+  const uint64_t last_word = (P.nbytes - 1) >> 2;
+  const uint32_t nw = (P.m + 3) >> 2;
+  const uint32_t tail_mask = (P.m & 3u) ? (0xFFFFFFFFu >> (8u * (4u - (P.m & 3u)))) : 0xFFFFFFFFu;
+  uint32_t keep = r;
+  while (r) {
+    const int b = __ffs(r) - 1;
+    r &= r - 1;
+    const uint64_t st = us + b;
+    const uint64_t w0 = st >> 2;
+    const uint32_t sh = static_cast<uint32_t>(st & 3u) * 8u;
+    uint32_t lo = __ldg(t32 + w0);
+    for (uint32_t q = 0; q < nw; ++q) {
+      const uint64_t wi = w0 + q + 1;
+      const uint32_t hi = wi <= last_word ? __ldg(t32 + wi) : 0u;
+      const uint32_t win = __funnelshift_r(lo, hi, sh);
+      const uint32_t pm = q + 1 == nw ? tail_mask : 0xFFFFFFFFu;
+      if ((win ^ __ldg(P.dpat + q)) & pm) {
+        keep &= ~(1u << b);
+        break;
+      }
+      lo = hi;
+    }
+  }
+  return keep;
+}
+
 __device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -746,7 +780,8 @@ __device__ __forceinline__ void load_segment(const uint8_t* seg, uint32_t rot, u
 // ------------------------------------------------------------------ the scan kernel
 
 // F  = filter bytes of the first word (min(m, 4)); F2 = filter bytes of the second word
-// (min(m, 8) - 4, 0 if m <= 4); MW = ceil(m/4) pattern words (MW <= 1: no verify);
+// (min(m, 8) - 4, 0 if m <= 4); MW = ceil(m/4) pattern words (MW <= 1: no verify; MW = 0:
+// long pattern, m > 32, verified against device memory);
 // SK, SQ = sampled filter (SK > 0: one SQ-byte gram every SK bytes, SK + SQ <= m; replaces
 // the packed filter); SEARCH = report positions (else count only).
 template <int F, int F2, int MW, int SK, int SQ, bool SEARCH>
@@ -1000,7 +1035,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
               const uint64_t us = tbase + o;
               if (us < P.s_lo || us + 16 > P.s_hi) mask[r] &= range_mask(us, P.s_lo, P.s_hi);
             }
-            if (__any_sync(0xffffffffu, mask[r])) mask[r] = verify_full<MW>(mask[r], ts, o, P);
+            if (__any_sync(0xffffffffu, mask[r])) {
+              if constexpr (MW == 0) mask[r] = verify_long(mask[r], tbase + o, P);
+              else mask[r] = verify_full<MW>(mask[r], ts, o, P);
+            }
             left |= mask[r];
           }
           slow = __any_sync(0xffffffffu, left != 0u);

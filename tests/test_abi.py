@@ -49,9 +49,9 @@ def test_plan_argument_errors():
         epsm.plan(b"")
     assert e.value.code == epsm.EPSM_EINVAL
     with pytest.raises(epsm.EpsmError) as e:
-        epsm.plan(b"x" * 33)
+        epsm.plan(b"x" * (epsm.MAX_M_LONG + 1))
     assert e.value.code == epsm.EPSM_EUNSUP
-    for m in (1, 2, 4, 5, 16, 32):
+    for m in (1, 2, 4, 5, 16, 32, 33, 100, epsm.MAX_M_LONG):
         p = epsm.plan(b"q" * m)
         assert p.m == m
         p.close()

@@ -156,7 +156,7 @@ def test_edge_cases(epsm, dev):
     with pytest.raises(epsm.EpsmError):
         epsm.plan(b"")
     with pytest.raises(epsm.EpsmError) as ei:
-        epsm.plan(b"x" * 33)
+        epsm.plan(b"x" * (epsm.MAX_M_LONG + 1))
     assert ei.value.code == epsm.EPSM_EUNSUP
 
 
@@ -334,3 +334,40 @@ def test_sampled_filter_bucket_collisions(epsm, dev):
         t[s:s + m] = decoy
     td = torch.from_numpy(t).to(dev)
     check(epsm, p.tobytes(), t, td, label="bucket collisions")
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 256])
+def test_long_patterns(epsm, dev, sigma):
+    """m > 32 (EPSMc's block fingerprints, checked against device memory):
+    planted occurrences across internal boundaries and at the text end, ragged sizes."""
+    rng = np.random.default_rng(5000 + sigma)
+    for n in (100, 5000, 2 * CHUNK + 4321):
+        base = rng.integers(0, sigma, size=n, dtype=np.uint8)
+        for m in (33, 34, 35, 40, 47, 48, 63, 64, 65, 100, 257, 1000, 4096):
+            if m > n:
+                continue
+            t = base.copy()
+            p = rng.integers(0, sigma, size=m, dtype=np.uint8)
+            for s in _edges(n, m)[::3]:
+                t[s:s + m] = p
+            td = torch.from_numpy(t).to(dev)
+            occ = check(epsm, p.tobytes(), t, td, label=f"long sigma={sigma} n={n}")
+            assert epsm.count(p.tobytes(), td) == occ
+
+
+def test_long_patterns_dense_and_misaligned(epsm, dev):
+    """'a'^m in 'a'^n for m > 32 (every start verifies the whole window) and a misaligned
+    text whose last byte ends a match (reads stay inside the last 16-byte block)."""
+    n = CHUNK + 77
+    td = torch.full((n,), ord("a"), dtype=torch.uint8, device=dev)
+    for m in (33, 64, 300):
+        pos, occ = epsm.search(b"a" * m, td)
+        assert occ == n - m + 1
+        assert torch.equal(pos, torch.arange(n - m + 1, device=dev, dtype=torch.int64))
+    rng = np.random.default_rng(8)
+    full = rng.integers(0, 256, size=TILE + 200, dtype=np.uint8)
+    fd = torch.from_numpy(full).to(dev)
+    for off in (1, 5, 11):
+        t = full[off:off + TILE + 101]
+        p = t[-70:].tobytes()
+        check(epsm, p, t, fd[off:off + TILE + 101], label=f"long misaligned off={off}")
