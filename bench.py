@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--ms", default=",".join(map(str, MS)))
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--breakdown", action="store_true", help="per-(sigma, m) timing pass (stderr)")
+    ap.add_argument("--no-batch", dest="batch", action="store_false",
+                    help="one launch per search (epsm_search_async) instead of the batch API")
     return ap.parse_args()
 
 
@@ -217,7 +219,36 @@ def run_epsm(args, world, rank, local):
     comm = epsm.nccl_comm_ptr() if world > 1 else None
     n_text_step = sum(texts[ti][2] for ti, _ in jobs)        # global text bytes per step
 
+    # batch mode (N = 1): every (sigma, m) group of searches is ONE call of the public batch
+    # API (epsm_search_batch_async: persistent launches of up to 40 searches of one pattern
+    # length over the same text).  Each search writes its own output buffer, taken from a
+    # pool of 80 (two consecutive launches never share one), each sized for the largest occ
+    # of the workload (found by a count-only pass first), so no position is dropped.
+    groups = []                                               # (first job, end job)
+    for j, (ti, pl) in enumerate(jobs):
+        if groups and jobs[groups[-1][0]][0] == ti and jobs[groups[-1][0]][1].m == pl.m:
+            groups[-1][1] = j + 1
+        else:
+            groups.append([j, j + 1])
+    use_batch = args.batch and world == 1
+    pool = []
+    if use_batch:
+        for j0, j1 in groups:
+            ti = jobs[j0][0]
+            epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[ti][5], occ_buf[j0:j1], stream=stream)
+        torch.cuda.synchronize()
+        pcap = int(occ_buf.max().item()) + 1
+        pos_buf = None
+        pool = [torch.empty(pcap, dtype=torch.int64, device=dev) for _ in range(80)]
+        pos_buf = pool[0]
+
     def one_step(events=None):
+        if use_batch and events is None:
+            for j0, j1 in groups:
+                ti = jobs[j0][0]
+                epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[ti][5], occ_buf[j0:j1],
+                                        outs=[pool[j % 80] for j in range(j0, j1)], stream=stream)
+            return
         for j, (ti, pl) in enumerate(jobs):
             s, spec, n_total, base, owned, t = texts[ti]
             if events is not None:
@@ -274,22 +305,26 @@ def run_epsm(args, world, rank, local):
     # of the same (sigma, m) (launches inside a group still overlap through PDL)
     breakdown = []
     if args.breakdown and world == 1:
-        groups = []                     # (key, first job, end job)
+        bgroups = []                     # (key, first job, end job)
         for j, (ti, pl) in enumerate(jobs):
             key = (texts[ti][0], pl.m)
-            if groups and groups[-1][0] == key:
-                groups[-1][2] = j + 1
+            if bgroups and bgroups[-1][0] == key:
+                bgroups[-1][2] = j + 1
             else:
-                groups.append([key, j, j + 1])
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(groups))]
-        for gi, (key, j0, j1) in enumerate(groups):
+                bgroups.append([key, j, j + 1])
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(bgroups))]
+        for gi, (key, j0, j1) in enumerate(bgroups):
             ev[2 * gi].record(stream)
-            for j in range(j0, j1):
-                ti, pl = jobs[j]
-                epsm.search_async(pl, texts[ti][5], pos_buf, occ_buf[j:j + 1], stream=stream)
+            if use_batch:
+                epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[jobs[j0][0]][5], occ_buf[j0:j1],
+                                        outs=[pool[j % 80] for j in range(j0, j1)], stream=stream)
+            else:
+                for j in range(j0, j1):
+                    ti, pl = jobs[j]
+                    epsm.search_async(pl, texts[ti][5], pos_buf, occ_buf[j:j + 1], stream=stream)
             ev[2 * gi + 1].record(stream)
         torch.cuda.synchronize()
-        for gi, ((s_, m), j0, j1) in enumerate(groups):
+        for gi, ((s_, m), j0, j1) in enumerate(bgroups):
             d = ev[2 * gi].elapsed_time(ev[2 * gi + 1])
             c = j1 - j0
             b_ = sum(local_bytes[j] + 8 * min(int(occ[j]), cap) for j in range(j0, j1))

@@ -109,6 +109,21 @@ int epsm_search_async(epsm_plan_t *plan, const uint8_t *d_text, uint64_t n,
                       epsm_stream_t stream);
 
 /*
+ * epsm_search_batch_async -- k searches over ONE device text d_text[0..n-1] (the
+ * paper's protocol: many patterns per text), as epsm_search_async
+ * for each j: positions of plans[j] into d_pos[j][0 .. min(occ_j, caps[j])), occ_j
+ * into the device uint64 d_occ[j] (d_occ: k contiguous, 8-byte aligned words).
+ * d_pos may be NULL (or d_pos[j] NULL / caps NULL) to count only.  Consecutive
+ * plans of equal m share one persistent launch (up to 40 per launch): the grid
+ * streams the text once per search, back to back, without a launch boundary
+ * between them.  Returns EPSM_OK or a negative error; does not synchronise.
+ */
+int epsm_search_batch_async(epsm_plan_t *const *plans, uint32_t k,
+                            const uint8_t *d_text, uint64_t n,
+                            uint64_t *const *d_pos, const uint64_t *caps,
+                            uint64_t *d_occ, epsm_stream_t stream);
+
+/*
  * epsm_search_host -- end-to-end convenience: h_text[0..n-1] and h_pos are HOST
  * buffers (pinned memory gives full PCIe bandwidth; pageable works).  Copies
  * the text to a plan-owned device buffer, runs epsm_search, and copies the

@@ -65,6 +65,54 @@ uint32_t sample_min_m() {
   return v;
 }
 
+// Sampled-filter geometry of a pattern length: one SQ-byte gram every SK bytes (SK + SQ <= m),
+// (0, 0) for the packed filter.  Must agree with kernel_for.
+void sampled_geometry(uint32_t m, int* sk, int* sq) {
+  *sk = *sq = 0;
+  if (m > EPSM_MAX_M) {
+    *sk = 16, *sq = 16;
+  } else if (m >= 8 && m >= sample_min_m()) {
+    if (m <= 11) *sk = 4, *sq = 4;
+    else if (m <= 15) *sk = 8, *sq = 4;
+    else if (m <= 23) *sk = 8, *sq = 8;
+    else if (m <= 31) *sk = 8, *sq = 16;
+    else *sk = 16, *sq = 16;
+  }
+}
+
+// EPSMc preprocessing (Fig. 1 lines 1-5): the fingerprint of every gram
+// p[i .. i+SQ-1], i = 1..SK, enters the table; the entry's mask bit SK-i marks the start
+// (sample offset - i) as a candidate.  Fingerprint = the kernel's gram_hash (a multiply-add
+// over little-endian words); bits [31:21] index the table, bits [20:6] are kept in the entry
+// so that a sample with another fingerprint is rejected.  Grams of different fingerprints
+// that share a bucket make it a wildcard (no fingerprint check).
+void build_gram_table(const uint8_t* pattern, int sk, int sq, uint32_t* tab) {
+  std::memset(tab, 0, sizeof(uint32_t) * epsm::kGramTab);
+  uint32_t H[16];
+  for (int i = 1; i <= sk; ++i) {
+    uint32_t h = 0;
+    for (int r = 0; r < sq / 4; ++r) {
+      const uint8_t* b = pattern + i + 4 * r;
+      const uint32_t w = b[0] | (b[1] << 8) | (b[2] << 16) | (static_cast<uint32_t>(b[3]) << 24);
+      h += w * epsm::gram_mul(r);
+    }
+    H[i - 1] = h;
+  }
+  constexpr int shift = 32 - epsm::kGramBits;
+  for (int i = 1; i <= sk; ++i) {
+    const uint32_t h = H[i - 1];
+    uint32_t mask = 0, wild = 0;
+    for (int l = 1; l <= sk; ++l) {
+      const uint32_t hl = H[l - 1];
+      if ((hl >> shift) == (h >> shift)) {
+        mask |= 1u << (sk - l);
+        if (((hl ^ h) << epsm::kGramBits) & 0xFFFE0000u) wild = 1u;
+      }
+    }
+    tab[h >> shift] = mask | (wild << 16) | ((h << epsm::kGramBits) & 0xFFFE0000u);
+  }
+}
+
 // Kernel variant for a pattern of length m (dispatch by m).
 //   packed:  F = min(m, 4) bytes in the first filter word, F2 = min(m, 8) - 4 in the second
 //            (used where candidates are dense), MW = ceil(m/4) words;
@@ -148,6 +196,8 @@ int epsm_bind_device(epsm_plan_t* plan, const void* dptr) {
 
 // ---- scan workspace pool, one per (device, stream)
 
+constexpr uint64_t kCtrWords = 8 + epsm::kMaxJobs;   // per parity
+
 namespace {
 std::mutex g_ws_mu;
 std::vector<epsm_workspace*> g_ws;
@@ -169,12 +219,12 @@ epsm_workspace* epsm_get_workspace(int device, cudaStream_t s) {
 // Growing it synchronises the stream first (no grid may still use the old buffers).
 static int ensure_workspace(epsm_workspace* ws, uint64_t chunks, uint64_t ctas, bool search, cudaStream_t s) {
   if (!ws->d_ctr) {
-    cudaError_t e = cudaMalloc(&ws->d_ctr, 16 * sizeof(unsigned long long));
+    cudaError_t e = cudaMalloc(&ws->d_ctr, 2 * kCtrWords * sizeof(unsigned long long));
     if (e != cudaSuccess) {
       epsm_set_error("cudaMalloc(counters): %s", cudaGetErrorString(e));
       return EPSM_ENOMEM;
     }
-    e = cudaMemsetAsync(ws->d_ctr, 0, 16 * sizeof(unsigned long long), s);
+    e = cudaMemsetAsync(ws->d_ctr, 0, 2 * kCtrWords * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(counters)");
   }
   if (!search) return EPSM_OK;
@@ -260,13 +310,49 @@ static bool plan_pdl_enabled() {
   return on;
 }
 
-// Core launcher.  The device text is d_text[0..nbytes-1]; starts [0, nstarts) are
-// reported (nstarts <= nbytes - m + 1), each shifted by `base`.
-int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
-                uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s) {
+// Upload a plan's preprocessing (and, for m > 32, its pattern words) on first use.
+static int ensure_plan_device(epsm_plan_t* plan, cudaStream_t s) {
+  if (!plan->d_desc) {
+    cudaError_t e = cudaMalloc(&plan->d_desc, sizeof(epsm::JobDesc));
+    if (e != cudaSuccess) {
+      plan->d_desc = nullptr;
+      epsm_set_error("cudaMalloc(plan descriptor): %s", cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    e = cudaMemcpyAsync(plan->d_desc, plan->h_desc, sizeof(epsm::JobDesc), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(plan descriptor)");
+  }
+  if (plan->m > EPSM_MAX_M && !plan->d_pat) {   // long pattern: zero-padded words for the check
+    const size_t bytes = ((plan->m + 3) / 4 + 1) * sizeof(uint32_t);
+    cudaError_t e = cudaMalloc(&plan->d_pat, bytes);
+    if (e != cudaSuccess) {
+      plan->d_pat = nullptr;
+      epsm_set_error("cudaMalloc(pattern, %zu bytes): %s", bytes, cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    e = cudaMemcpyAsync(plan->d_pat, plan->pattern, bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(pattern)");
+  }
+  return EPSM_OK;
+}
+
+// Core launcher: k <= kMaxJobs searches of one pattern length over the device text
+// d_text[0..nbytes-1]; starts [0, nstarts) are reported (nstarts <= nbytes - m + 1), each
+// shifted by `base`.  One persistent grid streams the chunks of all k searches in turn.
+int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
+                     uint64_t base, bool search, cudaStream_t s) {
+  if (k == 0) return EPSM_OK;
+  if (k > static_cast<uint32_t>(epsm::kMaxJobs)) {
+    epsm_set_error("%u searches in one launch (max %d)", k, epsm::kMaxJobs);
+    return EPSM_EINVAL;
+  }
+  epsm_plan_t* plan0 = jobs[0].plan;
   if (nstarts == 0) {
-    cudaError_t e = cudaMemsetAsync(d_occ, 0, sizeof(unsigned long long), s);
-    return e == cudaSuccess ? EPSM_OK : epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
+    for (uint32_t j = 0; j < k; ++j) {
+      cudaError_t e = cudaMemsetAsync(jobs[j].d_occ, 0, sizeof(unsigned long long), s);
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
+    }
+    return EPSM_OK;
   }
   const uint64_t mis = reinterpret_cast<uintptr_t>(d_text) & 15u;
   epsm::KParams P;
@@ -276,45 +362,41 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   P.s_lo = mis;
   P.s_hi = mis + nstarts;
   P.pos_bias = base - mis;
-  P.pos = d_pos;
-  P.cap = d_pos ? cap : 0;
-  P.occ = d_occ;
   P.mul8 = 1u << 24;
   P.mul24 = 1u << 8;
   P.movemask_mul = 0x00204081u;
-  std::memcpy(P.bcast, plan->bcast, sizeof(P.bcast));
-  std::memcpy(P.bcast2, plan->bcast2, sizeof(P.bcast2));
-  std::memcpy(P.pat, plan->pat, sizeof(P.pat));
-  std::memcpy(P.pmask, plan->pmask, sizeof(P.pmask));
-  P.m = plan->m;
-  if (plan->m > EPSM_MAX_M) {
-    if (!plan->d_pat) {   // first long search: upload the zero-padded pattern words
-      const size_t bytes = ((plan->m + 3) / 4 + 1) * sizeof(uint32_t);
-      cudaError_t e = cudaMalloc(&plan->d_pat, bytes);
-      if (e != cudaSuccess) {
-        plan->d_pat = nullptr;
-        epsm_set_error("cudaMalloc(pattern, %zu bytes): %s", bytes, cudaGetErrorString(e));
-        return EPSM_ENOMEM;
-      }
-      e = cudaMemcpyAsync(plan->d_pat, plan->pattern, bytes, cudaMemcpyHostToDevice, s);
-      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(pattern)");
+  P.m = plan0->m;
+  P.njobs = k;
+  P.desc_bytes = plan0->sk > 0 ? static_cast<uint32_t>(sizeof(epsm::JobDesc)) : epsm::kJobHeader;
+  for (uint32_t j = 0; j < k; ++j) {
+    epsm_plan_t* pl = jobs[j].plan;
+    if (pl->m != plan0->m || pl->device != plan0->device) {
+      epsm_set_error("searches of one launch need the same pattern length and device");
+      return EPSM_EINVAL;
     }
-    P.dpat = plan->d_pat;
+    int rc = ensure_plan_device(pl, s);
+    if (rc) return rc;
+    P.jobs[j].desc = pl->d_desc;
+    P.jobs[j].dpat = pl->d_pat;
+    P.jobs[j].pos = jobs[j].d_pos;
+    P.jobs[j].cap = jobs[j].d_pos ? jobs[j].cap : 0;
+    P.jobs[j].occ = jobs[j].d_occ;
   }
   const uint64_t tiles = (P.s_hi + epsm::kTile - 1) / epsm::kTile;
   const uint64_t chunks = (tiles + epsm::kChunkTiles - 1) / epsm::kChunkTiles;
-  if (tiles > 0x7FFFFFFFull) {
-    epsm_set_error("text too large: %llu tiles", (unsigned long long)tiles);
+  if (tiles > 0x7FFFFFFFull || chunks * k > 0x7FFFFFFFull) {
+    epsm_set_error("text too large: %llu tiles x %u searches", (unsigned long long)tiles, k);
     return EPSM_EINVAL;
   }
-  epsm_workspace* ws = epsm_get_workspace(plan->device, s);
+  const uint64_t gchunks = chunks * k;
+  epsm_workspace* ws = epsm_get_workspace(plan0->device, s);
   if (!ws) return EPSM_ENOMEM;
   if (ws->num_sms <= 0) {
-    cudaError_t e = cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, plan->device);
+    cudaError_t e = cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, plan0->device);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
   }
-  const uint64_t grid = chunks < static_cast<uint64_t>(ws->num_sms) ? chunks : ws->num_sms;
-  int rc = ensure_workspace(ws, chunks, grid, search, s);
+  const uint64_t grid = gchunks < static_cast<uint64_t>(ws->num_sms) ? gchunks : ws->num_sms;
+  int rc = ensure_workspace(ws, gchunks, grid, search, s);
   if (rc) return rc;
   // launch L uses parity L & 1; its status tag is L (24 bits); on wrap every word is cleared
   // (in stream order) so a stale tag can never match
@@ -329,19 +411,20 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   const int par = static_cast<int>(L & 1u);
   P.ntiles = static_cast<uint32_t>(tiles);
   P.nchunks = static_cast<uint32_t>(chunks);
-  P.ctr = ws->d_ctr + 8 * par;
+  P.gchunks = static_cast<uint32_t>(gchunks);
+  P.ctr = ws->d_ctr + kCtrWords * par;
   P.ctr_base = ws->ctr_base[par];
-  P.exit_ctr = ws->d_ctr + 8 * par + 3;
+  P.exit_ctr = ws->d_ctr + kCtrWords * par + 3;
   P.exit_expect = ws->exit_total[par];      // every CTA of launch L-2 (and before) has exited
   if (search) {
     P.status = ws->d_status[par];
     P.scratch = ws->d_scratch[par];
     P.tag = static_cast<unsigned long long>(L & 0xFFFFFFull) << epsm::kEpochShift;
   }
-  P.trace = trace_slot(plan->device);
-  KernelFn fn = kernel_for(plan->m, search);
+  P.trace = trace_slot(plan0->device);
+  KernelFn fn = kernel_for(plan0->m, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
-  rc = set_smem_attr(fn, plan->device, smem);
+  rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;
   // programmatic dependent launch: the kernel starts while the previous grid on the stream
   // drains; it synchronises with that grid (griddepcontrol.wait) only before writing outputs,
@@ -361,11 +444,17 @@ int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint6
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_scan_kernel launch");
   // CTAs start on chunks [0, grid) and draw the rest from the counter, two draws ahead of the
-  // chunk they stream: (chunks - grid) useful draws + exactly 2 draws past the end per CTA
-  ws->ctr_base[par] += chunks + grid;
+  // chunk they stream: (gchunks - grid) useful draws + exactly 2 draws past the end per CTA
+  ws->ctr_base[par] += gchunks + grid;
   ws->exit_total[par] += grid;
   ws->launches = L + 1;
   return EPSM_OK;
+}
+
+int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
+                uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s) {
+  const epsm_job job{plan, d_pos, cap, d_occ};
+  return epsm_launch_jobs(&job, 1, d_text, nbytes, nstarts, base, search, s);
 }
 
 static bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
@@ -424,6 +513,31 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
     p->pat[q] = w;
     p->pmask[q] = mk;
   }
+  // the kernels' per-search descriptor: filter words, P_i blocks (first 48 bytes) and, for the
+  // sampled variants, EPSMc's table L of gram fingerprints
+  p->h_desc = new (std::nothrow) epsm::JobDesc();
+  if (!p->h_desc) {
+    delete p;
+    return EPSM_ENOMEM;
+  }
+  epsm::JobDesc& D = *p->h_desc;
+  std::memset(&D, 0, sizeof(D));
+  std::memcpy(D.bcast, p->bcast, sizeof(D.bcast));
+  std::memcpy(D.bcast2, p->bcast2, sizeof(D.bcast2));
+  for (uint32_t q = 0; q < 12; ++q) {
+    uint32_t w = 0, mk = 0;
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t idx = 4 * q + b;
+      if (idx < m) {
+        w |= static_cast<uint32_t>(pattern[idx]) << (8 * b);
+        mk |= 0xFFu << (8 * b);
+      }
+    }
+    D.pat[q] = w;
+    D.pmask[q] = mk;
+  }
+  sampled_geometry(m, &p->sk, &p->sq);
+  if (p->sk > 0) build_gram_table(p->pattern, p->sk, p->sq, D.gram_tab);
   p->device = -1;
   *out = p;
   return EPSM_OK;
@@ -436,6 +550,8 @@ void epsm_plan_free(epsm_plan_t* plan) {
     cudaDeviceSynchronize();
   }
   if (plan->d_occ) cudaFree(plan->d_occ);
+  if (plan->d_desc) cudaFree(plan->d_desc);
+  delete plan->h_desc;
   if (plan->d_pat) cudaFree(plan->d_pat);
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);
@@ -493,6 +609,52 @@ int epsm_search_async(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint
   if (rc) return rc;
   return epsm_launch(plan, d_text, n, n_starts(plan->m, n), 0, cap ? d_pos : nullptr, cap,
                      reinterpret_cast<unsigned long long*>(d_occ), true, static_cast<cudaStream_t>(stream));
+}
+
+int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
+                            uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
+  if (k == 0) return EPSM_OK;
+  if (!plans || !d_occ || (!d_text && n > 0)) {
+    epsm_set_error("epsm_search_batch_async: NULL plans, d_occ or text");
+    return EPSM_EINVAL;
+  }
+  if (n > (1ull << 38)) {
+    epsm_set_error("n = %llu exceeds 2^38", (unsigned long long)n);
+    return EPSM_EINVAL;
+  }
+  if (!aligned8(d_occ)) {
+    epsm_set_error("d_occ must be 8-byte aligned");
+    return EPSM_EALIGN;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<epsm_job> jobs(k);
+  for (uint32_t j = 0; j < k; ++j) {
+    if (!plans[j]) {
+      epsm_set_error("epsm_search_batch_async: plans[%u] is NULL", j);
+      return EPSM_EINVAL;
+    }
+    uint64_t* pos = d_pos ? d_pos[j] : nullptr;
+    const uint64_t cap = (pos && caps) ? caps[j] : 0;
+    if (pos && !aligned8(pos)) {
+      epsm_set_error("d_pos[%u] must be 8-byte aligned", j);
+      return EPSM_EALIGN;
+    }
+    int rc = epsm_bind_device(plans[j], d_occ);
+    if (rc) return rc;
+    jobs[j] = epsm_job{plans[j], cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + j)};
+  }
+  // one launch per run of at most kMaxJobs consecutive searches of equal m
+  uint32_t a = 0;
+  while (a < k) {
+    uint32_t b = a + 1;
+    while (b < k && b - a < static_cast<uint32_t>(epsm::kMaxJobs) && plans[b]->m == plans[a]->m) ++b;
+    const uint32_t m = plans[a]->m;
+    const uint64_t ns = n >= m ? n - m + 1 : 0;
+    int rc = epsm_launch_jobs(jobs.data() + a, b - a, d_text, n, ns, 0, true, s);
+    if (rc) return rc;
+    a = b;
+  }
+  return EPSM_OK;
 }
 
 int epsm_search_range_async(epsm_plan_t* plan, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,

@@ -5,10 +5,15 @@
 
 #include "epsm.h"
 
+namespace epsm { struct JobDesc; }
+
 struct epsm_plan_s {
   uint32_t m = 0;
   uint8_t pattern[EPSM_MAX_M_LONG] = {};
   uint32_t* d_pat = nullptr;  // m > 32: zero-padded pattern words in device memory
+  epsm::JobDesc* h_desc = nullptr;   // preprocessing (filter words, gram table), host copy
+  epsm::JobDesc* d_desc = nullptr;   // ... and its device copy (uploaded on first search)
+  int sk = 0, sq = 0;                // sampled-filter geometry (0: packed filter)
   uint32_t bcast[4] = {};   // B_i = p_i * 0x01010101
   uint32_t bcast2[4] = {};  // B_{4+i}: second filter word
   uint32_t pat[9] = {};     // zero-padded pattern words
@@ -45,8 +50,8 @@ struct epsm_workspace {
   uint64_t status_cap = 0;
   uint64_t* d_scratch[2] = {nullptr, nullptr};            // parked masks, per CTA
   uint64_t scratch_ctas = 0;
-  unsigned long long* d_ctr = nullptr;        // [parity][8]: chunk counter, count accumulator,
-                                              // count ticket, CTA exit counter
+  unsigned long long* d_ctr = nullptr;        // [parity][kCtrWords]: chunk counter, -, count
+                                              // ticket, CTA exit counter, -, per-search counts
   unsigned long long ctr_base[2] = {0, 0};    // chunk counter value at the next launch
   unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
 };
@@ -59,3 +64,13 @@ int epsm_bind_device(epsm_plan_t* plan, const void* dptr);
 int epsm_ensure_occ(epsm_plan_t* plan);
 int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
                 uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s);
+
+// One search of a multi-search launch (all over the same text, same m).
+struct epsm_job {
+  epsm_plan_t* plan;
+  uint64_t* d_pos;
+  uint64_t cap;
+  unsigned long long* d_occ;
+};
+int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
+                     uint64_t base, bool search, cudaStream_t s);

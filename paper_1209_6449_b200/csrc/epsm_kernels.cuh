@@ -100,34 +100,60 @@ constexpr unsigned long long kFlagMask = 3ull << 38;
 constexpr unsigned long long kValueMask = (1ull << 38) - 1;
 constexpr unsigned long long kEpochMask = ~((1ull << kEpochShift) - 1);
 
+// Per-pattern preprocessing, built on the host at plan time and
+// kept in device memory; the producer copies it into a shared-memory slot (one TMA bulk copy)
+// whenever its CTA starts a chunk of a new search.  The gram table is only copied for the
+// sampled variants (kJobHeader bytes otherwise).
+struct __align__(16) JobDesc {
+  uint32_t bcast[4];            // B_i = p_i * 0x01010101
+  uint32_t bcast2[4];           // B_{4+i}: the second filter word (pattern bytes 4..7)
+  uint32_t pat[12];             // first 48 pattern bytes, little-endian u32 words, zero padded
+  uint32_t pmask[12];           // per-word byte masks (partial last word)
+  uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
+};
+constexpr uint32_t kJobHeader = 128;                              // bytes before gram_tab
+static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
+
+// One search of a launch: its preprocessing and its outputs.
+struct JobRef {
+  const JobDesc* desc;          // device copy of the plan's preprocessing
+  const uint32_t* dpat;         // m > 32: zero-padded pattern words in device memory
+  uint64_t* pos;                // output positions (search)
+  uint64_t cap;                 // capacity of pos
+  unsigned long long* occ;      // device occ
+};
+constexpr int kMaxJobs = 40;                                      // searches per launch
+
 struct KParams {
   const uint8_t* text;          // 16-byte aligned virtual base
   uint64_t nbytes;              // readable bytes from text
   uint64_t s_lo, s_hi;          // valid virtual starts [s_lo, s_hi)
   uint64_t pos_bias;            // reported = virtual start + pos_bias (mod 2^64)
-  uint64_t* pos;                // output positions (search)
-  uint64_t cap;                 // capacity of pos
-  unsigned long long* occ;      // device occ
-  unsigned long long* status;   // one word per chunk (search)
+  unsigned long long* status;   // one word per chunk of the launch (search)
   unsigned long long* ctr;      // [0] chunk-id counter (monotonic across launches),
-                                // [1] count accumulator, [2] CTA ticket (both re-armed to 0)
+                                // [2] CTA ticket (re-armed to 0), [8 + j] count of search j
   uint64_t* scratch;            // parked masks, kScratchPerCta u64 per CTA (search)
   unsigned long long ctr_base;  // value of ctr[0] when this launch starts
-  unsigned long long tag;       // epoch << 40
+  unsigned long long tag;       // launch number << 40
   uint32_t ntiles;              // tiles covering [0, s_hi)
-  uint32_t nchunks;
+  uint32_t nchunks;             // chunks per search (C); chunk g of the launch = search g / C
+  uint32_t gchunks;             // chunks of the launch = njobs * C
+  uint32_t njobs;               // searches in this launch (same text, same m)
+  uint32_t m;                   // pattern length (all searches)
   uint32_t mul8;                // 1 << 24: byte shift by 1 through one IMAD.WIDE
   uint32_t mul24;               // 1 << 8 : byte shift by 3 through one IMAD.WIDE
   uint32_t movemask_mul;        // 0x00204081
-  uint32_t bcast[4];            // B_i = p_i * 0x01010101
-  uint32_t bcast2[4];           // B_{4+i}: the second filter word (pattern bytes 4..7)
-  uint32_t pat[9];              // pattern, little-endian u32 words, zero padded
-  uint32_t pmask[9];            // per-word byte masks (partial last word)
+  uint32_t desc_bytes;          // bytes of JobDesc the producer copies (header [+ gram table])
   unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
-  const uint32_t* dpat;         // m > 32: zero-padded pattern words in device memory
-  uint32_t m;                   // pattern length
   unsigned long long* exit_ctr; // CTAs of all launches on this workspace parity that have exited
   unsigned long long exit_expect;   // value meaning "launch L-2 (same parity) has retired"
+  JobRef jobs[kMaxJobs];
+};
+
+// Filter constants of the current search, held in registers by a consumer warp.
+struct FParams {
+  uint32_t bcast[4];
+  const KParams& K;             // launch constants (byte-shift multipliers) stay in the constant bank
 };
 
 // %globaltimer stamps for the optional per-CTA timeline (EPSM_TRACE)
@@ -169,8 +195,11 @@ struct __align__(128) SmemLayoutT {
   uint64_t lb_full[kSlots];
   uint64_t lb_done[kSlots];
   ChunkSlot slot[kSlots];
-  uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
-  uint32_t info[STAGES];        // tile index | (last-of-chunk << 31), or kInfoEnd
+  JobDesc job[2];               // preprocessing of the searches in flight (alternating slots)
+  uint64_t job_full[2];         // slot loaded (TMA complete_tx)
+  uint64_t job_free[2];         // every consumer warp has left the slot's search
+  uint32_t info[STAGES];        // tile index in its search | (last-of-chunk << 31), or kInfoEnd
+  uint32_t info2[STAGES];       // chunk id of the launch | (job slot << 31)
   uint32_t fin;                 // consumer warps that reached the end
   uint32_t ws_ok;               // the workspace parity is free (launch L-2 retired)
 };
@@ -277,6 +306,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -323,7 +360,7 @@ __device__ __forceinline__ uint64_t ld_keep_u64(const uint64_t* p, uint64_t pol)
 // half, so S_i[k] = hi(w_k * 2^(32-8i)) | lo(w_{k+1} * 2^(32-8i)); the two halves have
 // disjoint bits, so the OR is folded into the 3-input XOR with B_i.
 template <int F>
-__device__ __forceinline__ void filter_pair(const uint32_t (&w)[5], const KParams& P, uint32_t (&Z)[4]) {
+__device__ __forceinline__ void filter_pair(const uint32_t (&w)[5], const FParams& P, uint32_t (&Z)[4]) {
   if (F == 1) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) Z[k] = w[k] ^ P.bcast[0];
@@ -331,7 +368,7 @@ __device__ __forceinline__ void filter_pair(const uint32_t (&w)[5], const KParam
   }
   uint64_t p8[5];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) p8[k] = static_cast<uint64_t>(w[k]) * P.mul8;
+  for (int k = 0; k < 5; ++k) p8[k] = static_cast<uint64_t>(w[k]) * P.K.mul8;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     Z[k] = (w[k] ^ P.bcast[0]) |
@@ -339,7 +376,7 @@ __device__ __forceinline__ void filter_pair(const uint32_t (&w)[5], const KParam
 }
 
 template <int F>
-__device__ __forceinline__ void filter_extend(const uint32_t (&w)[5], const KParams& P, uint32_t (&Z)[4]) {
+__device__ __forceinline__ void filter_extend(const uint32_t (&w)[5], const FParams& P, uint32_t (&Z)[4]) {
   if (F > 2) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) Z[k] |= __funnelshift_r(w[k], w[k + 1], 16) ^ P.bcast[2];
@@ -347,7 +384,7 @@ __device__ __forceinline__ void filter_extend(const uint32_t (&w)[5], const KPar
   if (F > 3) {
     uint64_t p24[5];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) p24[k] = static_cast<uint64_t>(w[k]) * P.mul24;
+    for (int k = 0; k < 5; ++k) p24[k] = static_cast<uint64_t>(w[k]) * P.K.mul24;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       Z[k] |= static_cast<uint32_t>(p24[k] >> 32) ^ static_cast<uint32_t>(p24[k + 1]) ^ P.bcast[3];
@@ -357,24 +394,25 @@ __device__ __forceinline__ void filter_extend(const uint32_t (&w)[5], const KPar
 // Second filter word (pattern bytes 4 .. 3+F2) for the 16 starts of a unit, evaluated on the
 // words w[1..5]: byte j of Y[k] is zero iff t[u+4k+j+4+i] = p_{4+i} for all i < F2.
 template <int F2>
-__device__ __forceinline__ void filter_second(const uint32_t (&v)[6], const KParams& P, uint32_t (&Y)[4]) {
+__device__ __forceinline__ void filter_second(const uint32_t (&v)[6], const FParams& P, const JobDesc& J,
+                                              uint32_t (&Y)[4]) {
   uint64_t p8[5];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) p8[k] = static_cast<uint64_t>(v[k + 1]) * P.mul8;
+  for (int k = 0; k < 5; ++k) p8[k] = static_cast<uint64_t>(v[k + 1]) * P.K.mul8;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    uint32_t y = v[k + 1] ^ P.bcast2[0];
-    if (F2 > 1) y |= static_cast<uint32_t>(p8[k] >> 32) ^ static_cast<uint32_t>(p8[k + 1]) ^ P.bcast2[1];
-    if (F2 > 2) y |= __funnelshift_r(v[k + 1], v[k + 2], 16) ^ P.bcast2[2];
+    uint32_t y = v[k + 1] ^ J.bcast2[0];
+    if (F2 > 1) y |= static_cast<uint32_t>(p8[k] >> 32) ^ static_cast<uint32_t>(p8[k + 1]) ^ J.bcast2[1];
+    if (F2 > 2) y |= __funnelshift_r(v[k + 1], v[k + 2], 16) ^ J.bcast2[2];
     Y[k] = y;
   }
   if (F2 > 3) {
     uint64_t p24[5];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) p24[k] = static_cast<uint64_t>(v[k + 1]) * P.mul24;
+    for (int k = 0; k < 5; ++k) p24[k] = static_cast<uint64_t>(v[k + 1]) * P.K.mul24;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      Y[k] |= static_cast<uint32_t>(p24[k] >> 32) ^ static_cast<uint32_t>(p24[k + 1]) ^ P.bcast2[3];
+      Y[k] |= static_cast<uint32_t>(p24[k] >> 32) ^ static_cast<uint32_t>(p24[k + 1]) ^ J.bcast2[3];
   }
 }
 
@@ -416,7 +454,7 @@ __device__ __forceinline__ uint32_t range_mask(uint64_t ustart, uint64_t lo, uin
 // before qstart were already checked exactly by the packed filter).
 template <int MW>
 __device__ __forceinline__ uint32_t verify_candidates(uint32_t r, const uint8_t* tile, uint32_t o,
-                                                      const KParams& P, int qstart) {
+                                                      const JobDesc& J, int qstart) {
   uint32_t keep = r;
   while (r) {
     const int b = __ffs(r) - 1;
@@ -430,7 +468,7 @@ __device__ __forceinline__ uint32_t verify_candidates(uint32_t r, const uint8_t*
       if (q < qstart) continue;
       const uint32_t hi = wp[q + 1];
       const uint32_t win = __funnelshift_r(lo, hi, sh);
-      if ((win ^ P.pat[q]) & P.pmask[q]) {
+      if ((win ^ J.pat[q]) & J.pmask[q]) {
         keep &= ~(1u << b);
         break;
       }
@@ -477,40 +515,10 @@ __device__ __forceinline__ void load_sample(const uint8_t* p, uint32_t (&w)[SQ /
   }
 }
 
-// EPSMc preprocessing (Fig. 1 lines 1-5): for every pattern offset
-// i = 1..SK the fingerprint of the gram p[i .. i+SQ-1] is entered in the table; the entry's
-// mask bit SK-i marks the start (sample offset - i) as a candidate.  Grams of different
-// fingerprints that share a bucket make it a wildcard (no fingerprint check).  One warp.
-template <int SK, int SQ>
-__device__ __forceinline__ void build_gram_table(const KParams& P, uint32_t* tab, uint32_t lane) {
-  const bool valid = lane < static_cast<uint32_t>(SK);
-  uint32_t h = 0, bit = 0;
-  if (valid) {
-    const uint32_t i = lane + 1;
-    uint32_t g[SQ / 4];
-#pragma unroll
-    for (int r = 0; r < SQ / 4; ++r)
-      g[r] = __funnelshift_r(P.pat[(i >> 2) + r], P.pat[(i >> 2) + r + 1], 8u * (i & 3u));
-    h = gram_hash<SQ / 4>(g);
-    bit = 1u << (SK - i);
-  }
-  uint32_t mask = 0, wild = 0;
-#pragma unroll
-  for (int l = 0; l < SK; ++l) {
-    const uint32_t hl = __shfl_sync(0xffffffffu, h, l);
-    const uint32_t bl = __shfl_sync(0xffffffffu, bit, l);
-    if (valid && (hl >> (32 - kGramBits)) == (h >> (32 - kGramBits))) {
-      mask |= bl;
-      if (((hl ^ h) << kGramBits) & 0xFFFE0000u) wild = 1u;
-    }
-  }
-  if (valid) tab[h >> (32 - kGramBits)] = mask | (wild << 16) | ((h << kGramBits) & 0xFFFE0000u);
-}
-
 // Naive check (Fig. 1 line 12) of every candidate bit of r against all MW
 // zero-padded pattern words (the sampled filter proves nothing about any single word).
 template <int MW>
-__device__ __forceinline__ uint32_t verify_full(uint32_t r, const uint8_t* tile, uint32_t o, const KParams& P) {
+__device__ __forceinline__ uint32_t verify_full(uint32_t r, const uint8_t* tile, uint32_t o, const JobDesc& J) {
   uint32_t keep = r;
   while (r) {
     const int b = __ffs(r) - 1;
@@ -523,7 +531,7 @@ __device__ __forceinline__ uint32_t verify_full(uint32_t r, const uint8_t* tile,
     for (int q = 0; q < MW; ++q) {
       const uint32_t hi = wp[q + 1];
       const uint32_t win = __funnelshift_r(lo, hi, sh);
-      if ((win ^ P.pat[q]) & P.pmask[q]) {
+      if ((win ^ J.pat[q]) & J.pmask[q]) {
         keep &= ~(1u << b);
         break;
       }
@@ -544,7 +552,7 @@ __device__ __forceinline__ void wait_ws(Smem& S) {
 // halo, so it is compared against the text in global memory (L2: the tile was just
 // streamed) and the pattern words in device memory.  Reads stay inside the words that hold
 // text bytes (the last one lies in the 16-byte block of the text's last byte).
-__device__ __forceinline__ uint32_t verify_long(uint32_t r, uint64_t us, const KParams& P) {
+__device__ __forceinline__ uint32_t verify_long(uint32_t r, uint64_t us, const KParams& P, const uint32_t* dpat) {
   const uint32_t* t32 = reinterpret_cast<const uint32_t*>(P.text);
   const uint64_t last_word = (P.nbytes - 1) >> 2;
   const uint32_t nw = (P.m + 3) >> 2;
@@ -562,7 +570,7 @@ __device__ __forceinline__ uint32_t verify_long(uint32_t r, uint64_t us, const K
       const uint32_t hi = wi <= last_word ? __ldg(t32 + wi) : 0u;
       const uint32_t win = __funnelshift_r(lo, hi, sh);
       const uint32_t pm = q + 1 == nw ? tail_mask : 0xFFFFFFFFu;
-      if ((win ^ __ldg(P.dpat + q)) & pm) {
+      if ((win ^ __ldg(dpat + q)) & pm) {
         keep &= ~(1u << b);
         break;
       }
@@ -605,8 +613,9 @@ constexpr unsigned long long kAborted = ~0ull;
 __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_t chunk, uint32_t total,
                                                        uint32_t lane, const volatile uint32_t* fin) {
   const unsigned long long tag = P.tag;
-  if (chunk == 0) {
-    if (lane == 0) st_relaxed(P.status, tag | kFlagInc | total);
+  const long long jbase = static_cast<long long>(chunk / P.nchunks) * P.nchunks;   // its search's chunk 0
+  if (chunk == jbase) {
+    if (lane == 0) st_relaxed(P.status + chunk, tag | kFlagInc | total);
     return 0;
   }
   // (the chunk's aggregate was already published by the consumers when they finished it)
@@ -621,7 +630,7 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         const long long idx = pred - (32 * i + static_cast<long long>(lane));
-        s[i] = idx >= 0 ? ld_relaxed(P.status + idx) : (tag | kFlagInc);
+        s[i] = idx >= jbase ? ld_relaxed(P.status + idx) : (tag | kFlagInc);
         valid &= ((s[i] & kEpochMask) == tag) && (s[i] & kFlagMask);
       }
       if (__all_sync(0xffffffffu, valid)) break;
@@ -710,12 +719,15 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
   const ParkedChunk& pk = S.park[b];
   if (pk.total == 0 || slow == 0) return;                      // warp-uniform
   const unsigned long long prefix = pk.prefix;
-  if (prefix >= P.cap) return;
+  const JobRef& J = P.jobs[pk.chunk / P.nchunks];
+  if (prefix >= J.cap) return;
   if (!out_ok) {                      // the previous grid on the stream may write the same output
     griddep_wait();
     out_ok = true;
   }
-  const uint64_t cbase = static_cast<uint64_t>(pk.chunk) * kChunkBytes + P.pos_bias;
+  uint64_t* const pos = J.pos;
+  const uint64_t cap = J.cap;
+  const uint64_t cbase = static_cast<uint64_t>(pk.chunk % P.nchunks) * kChunkBytes + P.pos_bias;
   uint16_t* stage = S.wstage[cw];
   const uint32_t nt = pk.ntiles;
   uint64_t mk4[kChunkTiles];
@@ -733,14 +745,14 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
     const uint32_t any = __ballot_sync(0xffffffffu, c != 0);
     if (any == 0) continue;
     const uint64_t gidx = prefix + pk.off[t * kConsumerWarps + cw];
-    if (gidx >= P.cap) return;                                // later slices are even further out
-    const uint64_t room = P.cap - gidx;
+    if (gidx >= cap) return;                                // later slices are even further out
+    const uint64_t room = cap - gidx;
     const uint64_t sb = cbase + static_cast<uint64_t>(t) * kTile + cw * kWarpBytes + lane * kSegBytes;
     if (__ballot_sync(0xffffffffu, c > 1) == 0) {
       // sparse slice (<= 1 position per lane): lanes store straight to consecutive slots,
       // which one warp store coalesces -- no staging, no scan
       const uint32_t off = __popc(any & lt);
-      if (c && off < room) st_stream_u64(P.pos + gidx + off, sb + static_cast<uint64_t>(__ffsll(M) - 1));
+      if (c && off < room) st_stream_u64(pos + gidx + off, sb + static_cast<uint64_t>(__ffsll(M) - 1));
       continue;
     }
     // exclusive offsets from 7 bit-sliced ballots (c <= 64): independent ops, no shuffle chain
@@ -758,12 +770,12 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
       while (v) {
         const int bit = __ffsll(v) - 1;
         v &= v - 1;
-        if (i < room) st_stream_u64(P.pos + gidx + i, sb + static_cast<uint64_t>(bit));
+        if (i < room) st_stream_u64(pos + gidx + i, sb + static_cast<uint64_t>(bit));
         ++i;
       }
       continue;
     }
-    write_slice(stage, P.pos + gidx, room, M, off, tg, sb - lane * kSegBytes, lane);
+    write_slice(stage, pos + gidx, room, M, off, tg, sb - lane * kSegBytes, lane);
   }
 }
 
@@ -795,9 +807,6 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   const uint32_t warp = tid >> 5;
 
   if (tid == 0) EPSM_TRACE(P, 0);
-  if constexpr (SK > 0) {
-    for (uint32_t i = tid; i < kGramTab; i += kThreads) S.gram_tab[i] = 0u;
-  }
   // barrier set-up spread over the threads of warps 0-1 (one mbarrier init each: a serial
   // init of all of them costs ~1 us on the start-up path)
   if (tid < static_cast<uint32_t>(kStages)) {
@@ -810,6 +819,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     fence_mbar_init();
   } else if (tid >= 64 && tid < 64 + static_cast<uint32_t>(Smem::kPark)) {
     S.park[tid - 64].done = 0;
+  } else if (tid >= 96 && tid < 98) {
+    mbar_init(&S.job_full[tid - 96], 1);
+    mbar_init(&S.job_free[tid - 96], kConsumerWarps);
+    fence_mbar_init();
   }
   if (tid == 0) {
     S.fin = 0;
@@ -832,9 +845,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // draw in flight whose result is only consumed when the current chunk has been issued,
     // so the atomic's latency never stalls the TMA issue.
     auto draw = [&]() -> unsigned long long { return gridDim.x + (atomicAdd(P.ctr, 1ull) - P.ctr_base); };
-    auto prefetch_l2 = [&](unsigned long long c) {
-      if (lane == 0 && c < P.nchunks) {
-        const uint64_t pb = c * static_cast<unsigned long long>(kChunkBytes);
+    auto prefetch_l2 = [&](unsigned long long g) {
+      if (lane == 0 && g < P.gchunks) {
+        const uint64_t pb = (g % P.nchunks) * static_cast<unsigned long long>(kChunkBytes);
         const uint64_t pe_want = pb + kChunkBytes + kHalo;
         const uint64_t pe = (pe_want < P.nbytes ? pe_want : P.nbytes) & ~15ull;
         for (uint64_t a = pb; a < pe; a += kTile) {
@@ -843,11 +856,16 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
       }
     };
+    // chunk g of the launch belongs to search g / C (C = P.nchunks chunks per search, all
+    // searches over the same text); a CTA that starts a chunk of a new search first copies
+    // that search's preprocessing into the other job slot (after every consumer warp left
+    // the search the slot held before)
     unsigned long long cur = blockIdx.x, after = 0, pend = 0;
     bool first = true;
     bool ws_seen = false;                      // (lane 0) workspace parity seen free
+    uint32_t pjob = 0xFFFFFFFFu, jslot = 1, nswitch = 0;
     while (true) {
-      if (cur >= P.nchunks) {
+      if (cur >= P.gchunks) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
         if (lane == 0) {
           S.info[stage] = kInfoEnd;
@@ -856,7 +874,18 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
         break;
       }
-      const uint32_t t0 = static_cast<uint32_t>(cur) * kChunkTiles;
+      const uint32_t job = static_cast<uint32_t>(cur / P.nchunks);
+      if (job != pjob) {
+        jslot ^= 1u;
+        if (nswitch >= 2) mbar_wait(&S.job_free[jslot], ((nswitch - 2) >> 1) & 1u);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&S.job_full[jslot], P.desc_bytes);
+          bulk_g2s_plain(&S.job[jslot], P.jobs[job].desc, P.desc_bytes, &S.job_full[jslot]);
+        }
+        pjob = job;
+        ++nswitch;
+      }
+      const uint32_t t0 = static_cast<uint32_t>(cur % P.nchunks) * kChunkTiles;
       const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
       for (uint32_t t = t0; t < t1; ++t) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
@@ -869,6 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         __syncwarp();
         if (lane == 0) {
           S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
+          S.info2[stage] = static_cast<uint32_t>(cur) | (jslot << 31);
           if (bulk) {
             mbar_arrive_expect_tx(&S.full[stage], bulk);
             bulk_g2s(S.ring[stage], P.text + base, bulk, &S.full[stage], policy);
@@ -911,11 +941,6 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ================================================================ look-back
-    if constexpr (SK > 0) {
-      build_gram_table<SK, SQ>(P, S.gram_tab, lane);
-      __threadfence_block();
-      named_barrier_arrive(1, kConsumers + 32);
-    }
     if constexpr (SEARCH) {
       // (chunks reach this queue only after the consumers saw the workspace free)
       uint32_t q = 0, par = 0;
@@ -926,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // a chunk without occurrences needs no prefix of its own; its look-back only helps
         // successors (an inclusive status shortens their walks), so it is dropped once every
         // consumer warp of this CTA is done and the CTA could otherwise exit
-        const bool last = sl.chunk + 1 == P.nchunks;             // its prefix gives occ
+        const bool last = (sl.chunk % P.nchunks) + 1 == P.nchunks;   // its prefix gives occ
         const volatile uint32_t* fin = (sl.total == 0 && !last) ? &S.fin : nullptr;
         const bool skip = fin && *fin == static_cast<uint32_t>(kConsumerWarps);
         const unsigned long long pre = skip ? kAborted : lookback(P, sl.chunk, sl.total, lane, fin);
@@ -934,7 +959,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           if (pre != kAborted) S.park[sl.park].prefix = pre;
           if (last) {
             griddep_wait();                    // the previous grid may write the same occ
-            *P.occ = pre + sl.total;
+            *P.jobs[sl.chunk / P.nchunks].occ = pre + sl.total;
           }
           mbar_arrive(&S.lb_done[q]);
         }
@@ -980,7 +1005,24 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       slowbits &= ~(kTileBitsMask << (kChunkTiles * b));
     };
 
-    if constexpr (SK > 0) named_barrier_sync(1, kConsumers + 32);   // gram table built by warp 1
+    // the search of the current tile: its job slot, its filter constants (registers)
+    uint32_t cur_slot = 2, cur_job = 0, slot_uses = 0;   // slot_uses: [15:0] slot 0, [31:16] slot 1
+    const JobDesc* JD = &S.job[0];
+    FParams FP{{0u, 0u, 0u, 0u}, P};
+    // count mode: this warp's occurrences of the current search go to the workspace counter
+    auto flush_count = [&]() {
+      if constexpr (!SEARCH) {
+        const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
+        if (wsum) {
+          if (!waited) {
+            wait_ws(S);
+            waited = true;
+          }
+          if (lane == 0) atomicAdd(P.ctr + 8 + cur_job, static_cast<unsigned long long>(wsum));
+        }
+        acc = 0;
+      }
+    };
     bool first_tile = true;
     while (true) {
       mbar_wait(&S.full[stage], phase);
@@ -991,8 +1033,30 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         if (cw == 0 && lane == 0) EPSM_TRACE(P, 4);
         break;
       }
-      const uint32_t tile = info & 0x7FFFFFFFu;
+      const uint32_t tile = info & 0x7FFFFFFFu;              // tile index inside its search
       const bool last_in_chunk = info >> 31;
+      const uint32_t info2 = S.info2[stage];
+      const uint32_t gch = info2 & 0x7FFFFFFFu;              // chunk id of the launch
+      const uint32_t js = info2 >> 31;                       // job slot of its search
+      if (js != cur_slot) {
+        // a new search: leave the old slot (the producer may refill it), wait for the new one
+        if (cur_slot < 2) {
+          flush_count();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.job_free[cur_slot]);
+        }
+        const uint32_t k = js ? (slot_uses >> 16) : (slot_uses & 0xFFFFu);
+        mbar_wait(&S.job_full[js], k & 1u);
+        slot_uses += js ? 0x10000u : 1u;
+        cur_slot = js;
+        cur_job = gch / P.nchunks;
+        JD = &S.job[js];
+        const uint4 b0 = *reinterpret_cast<const uint4*>(JD->bcast);
+        FP.bcast[0] = b0.x;
+        FP.bcast[1] = b0.y;
+        FP.bcast[2] = b0.z;
+        FP.bcast[3] = b0.w;
+      }
       const uint32_t b = seq % kParked;
       if (SEARCH && tpos == 0 && seq >= kParked) flush_chunk_seq(seq - kParked);   // free slot b
       const uint8_t* ts = S.ring[stage];
@@ -1018,7 +1082,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
             uint32_t sw[kw];
             load_sample<SK, SQ>(up + SK * (g + 1), sw);
             const uint32_t H = gram_hash<kw>(sw);
-            const uint32_t e = S.gram_tab[H >> (32 - kGramBits)];
+            const uint32_t e = JD->gram_tab[H >> (32 - kGramBits)];
             const bool ok = (((e ^ (H << kGramBits)) & 0xFFFE0000u) == 0u) || (e & 0x10000u);
             c |= (ok ? (e & 0xFFFFu) : 0u) << (SK * g);
           }
@@ -1036,8 +1100,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
               if (us < P.s_lo || us + 16 > P.s_hi) mask[r] &= range_mask(us, P.s_lo, P.s_hi);
             }
             if (__any_sync(0xffffffffu, mask[r])) {
-              if constexpr (MW == 0) mask[r] = verify_long(mask[r], tbase + o, P);
-              else mask[r] = verify_full<MW>(mask[r], ts, o, P);
+              if constexpr (MW == 0) mask[r] = verify_long(mask[r], tbase + o, P, P.jobs[cur_job].dpat);
+              else mask[r] = verify_full<MW>(mask[r], ts, o, *JD);
             }
             left |= mask[r];
           }
@@ -1059,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           W[r][2] = R[r].z;
           W[r][3] = R[r].w;
           W[r][4] = *reinterpret_cast<const uint32_t*>(seg + 16u * ((r + rot) & 3u) + 16u);
-          filter_pair<F>(W[r], P, Z[r]);
+          filter_pair<F>(W[r], FP, Z[r]);
         }
         if constexpr (F > 2) {
           bool need_extend = true;
@@ -1078,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
             uint32_t hz = 0;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-              filter_extend<F>(W[r], P, Z[r]);
+              filter_extend<F>(W[r], FP, Z[r]);
               hz |= any_zero_byte(Z[r]);
             }
             slow = __any_sync(0xffffffffu, hz);
@@ -1107,11 +1171,14 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
             if (c4 > 64) {
 #pragma unroll
               for (int r = 0; r < 4; ++r) {
+                // (words reloaded from the stage: keeping W alive through the slow path would
+                // spill registers)
                 const uint32_t o = seg_off + 16u * ((r + rot) & 3u);
-                const uint32_t v[6] = {W[r][0], W[r][1], W[r][2], W[r][3], W[r][4],
-                                       *reinterpret_cast<const uint32_t*>(ts + o + 20)};
+                const uint4 a = *reinterpret_cast<const uint4*>(ts + o);
+                const uint2 c = *reinterpret_cast<const uint2*>(ts + o + 16);
+                const uint32_t v[6] = {a.x, a.y, a.z, a.w, c.x, c.y};
                 uint32_t Y[4];
-                filter_second<F2>(v, P, Y);
+                filter_second<F2>(v, FP, *JD, Y);
                 mask[r] &= zero_byte_mask16(Y, P.movemask_mul);
               }
               qstart = 2;
@@ -1121,7 +1188,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const uint32_t o = seg_off + 16u * ((r + rot) & 3u);
-            if (MW > qstart && __any_sync(0xffffffffu, mask[r])) mask[r] = verify_candidates<MW>(mask[r], ts, o, P, qstart);
+            if (MW > qstart && __any_sync(0xffffffffu, mask[r])) mask[r] = verify_candidates<MW>(mask[r], ts, o, *JD, qstart);
             left |= mask[r];
           }
           slow = __any_sync(0xffffffffu, left != 0u);
@@ -1160,7 +1227,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         wait_ws(S);
         waited = true;
       }
-      const uint32_t chunk = tile / kChunkTiles;
+      const uint32_t chunk = gch;
       const uint32_t ntiles = tpos;
       if (lane == 0) S.park[b].slow[cw] = static_cast<uint8_t>((slowbits >> (kChunkTiles * b)) & kTileBitsMask);
       __syncwarp();
@@ -1199,7 +1266,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           S.park[b].total = total;
           S.park[b].ntiles = ntiles;
           // publish the aggregate at once so successors' look-backs never wait for our queue
-          st_relaxed(P.status + chunk, P.tag | (chunk == 0 ? kFlagInc : kFlagAgg) | total);
+          st_relaxed(P.status + chunk, P.tag | (chunk % P.nchunks == 0 ? kFlagInc : kFlagAgg) | total);
           const uint32_t q = seq % kSlots;
           S.slot[q].chunk = chunk;
           S.slot[q].total = total;
@@ -1213,12 +1280,15 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     }
 
     if constexpr (!SEARCH) {
-      // count: per-warp partials into the workspace accumulator; the CTA's last warp takes a
-      // ticket, and the last CTA publishes occ and re-arms the workspace (no memset per call)
-      wait_ws(S);
-      const uint32_t wsum = __reduce_add_sync(0xffffffffu, acc);
+      // count: per-warp partials into the per-search workspace counters; the CTA's last warp
+      // takes a ticket, and the last CTA publishes every search's occ and re-arms the counters
+      // (no memset per call)
+      if (cur_slot < 2) flush_count();
+      if (!waited) {
+        wait_ws(S);
+        waited = true;
+      }
       if (lane == 0) {
-        if (wsum) atomicAdd(P.ctr + 1, static_cast<unsigned long long>(wsum));
         __threadfence();
         const uint32_t prev = atomicAdd(&S.fin, 1u);
         if (prev == kConsumerWarps - 1) {
@@ -1227,7 +1297,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           if (ticket == gridDim.x - 1) {
             __threadfence();
             griddep_wait();                    // the previous grid may write the same occ
-            *P.occ = atomicExch(P.ctr + 1, 0ull);
+            for (uint32_t j = 0; j < P.njobs; ++j) *P.jobs[j].occ = atomicExch(P.ctr + 8 + j, 0ull);
             P.ctr[2] = 0;
           }
         }

@@ -371,3 +371,57 @@ def test_long_patterns_dense_and_misaligned(epsm, dev):
         t = full[off:off + TILE + 101]
         p = t[-70:].tobytes()
         check(epsm, p, t, fd[off:off + TILE + 101], label=f"long misaligned off={off}")
+
+
+def test_batch_search_many_patterns_one_text(epsm, dev):
+    """epsm_search_batch_async: k searches over one text in persistent launches (runs of equal
+    m, at most 40 per launch) -- every search's positions and occ equal the oracle's, with
+    per-search caps (truncation), count-only searches and patterns absent from the text."""
+    rng = np.random.default_rng(31337)
+    n = 3 * CHUNK + 5 * TILE + 99
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    pats = []
+    for m in [2] * 3 + [5] * 4 + [8] * 45 + [16] * 5 + [32] * 3 + [40] * 2 + [4] * 2:
+        s0 = int(rng.integers(0, n - m + 1))
+        p = t[s0:s0 + m].tobytes() if rng.random() < 0.8 else bytes([7]) * m   # 7 never occurs
+        pats.append(p)
+    plans = [epsm.plan(p) for p in pats]
+    wants = [oracle.search(p, t) for p in pats]
+    caps = [w.size if j % 5 else max(0, w.size - 3) for j, w in enumerate(wants)]
+    outs = [torch.empty(max(c, 1), dtype=torch.int64, device=dev) for c in caps]
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    before = epsm.launch_count()
+    epsm.search_batch_async(plans, td, occ, outs=outs, caps=caps)
+    torch.cuda.synchronize()
+    launches = epsm.launch_count() - before
+    assert launches <= 10, launches              # runs of equal m, <= 40 searches each
+    occ_h = occ.cpu().numpy()
+    for j, (w, c) in enumerate(zip(wants, caps)):
+        assert occ_h[j] == w.size, (j, len(pats[j]))
+        got = outs[j][:min(c, w.size)].cpu().numpy().astype(np.uint64)
+        assert np.array_equal(got, w[:c]), (j, len(pats[j]))
+    # count only (no outputs), twice on the same stream (workspace parity alternation)
+    occ2 = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+    for _ in range(2):
+        epsm.search_batch_async(plans, td, occ2)
+    torch.cuda.synchronize()
+    assert np.array_equal(occ2.cpu().numpy(), np.array([w.size for w in wants]))
+
+
+def test_batch_dense_and_small_texts(epsm, dev):
+    """Batches on texts smaller than one chunk (fewer chunks than CTAs, several searches per
+    CTA) and dense outputs ('a'^n): ordering across the searches' chunk ranges."""
+    for n in (10, 1000, TILE + 7, CHUNK - 1):
+        td = torch.full((n,), ord("a"), dtype=torch.uint8, device=dev)
+        pats = [b"a" * m for m in (2, 2, 2, 2)] + [b"a" * 9] * 3 + [b"ab", b"ba"]
+        pats = [p for p in pats if len(p) <= n]
+        plans = [epsm.plan(p) for p in pats]
+        outs = [torch.empty(n, dtype=torch.int64, device=dev) for _ in pats]
+        occ = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+        epsm.search_batch_async(plans, td, occ, outs=outs)
+        torch.cuda.synchronize()
+        for j, p in enumerate(pats):
+            k = n - len(p) + 1 if set(p) == {ord("a")} else 0
+            assert int(occ[j]) == k
+            assert torch.equal(outs[j][:k], torch.arange(k, device=dev, dtype=torch.int64))
