@@ -425,3 +425,42 @@ def test_batch_dense_and_small_texts(epsm, dev):
             k = n - len(p) + 1 if set(p) == {ord("a")} else 0
             assert int(occ[j]) == k
             assert torch.equal(outs[j][:k], torch.arange(k, device=dev, dtype=torch.int64))
+
+
+def test_concurrent_streams_have_separate_workspaces(epsm, dev):
+    """Searches enqueued on two streams at once (each stream owns a scan workspace) and
+    interleaved single/batch/count launches on one stream (workspace parity alternation)."""
+    rng = np.random.default_rng(2024)
+    n = 2 * CHUNK + 333
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    pats = [t[s:s + m].tobytes() for s, m in ((100, 3), (5000, 8), (70000, 16), (123, 33))]
+    wants = [oracle.search(p, t) for p in pats]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    results = []
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for si, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                for j, p in enumerate(pats):
+                    pl = epsm.plan(p)
+                    out = torch.empty(wants[j].size + 4, dtype=torch.int64, device=dev)
+                    occ = torch.zeros(1, dtype=torch.int64, device=dev)
+                    if (rep + si + j) % 3 == 0:
+                        epsm.search_batch_async([pl], td, occ, outs=[out], stream=st)
+                    else:
+                        epsm.search_async(pl, td, out, occ, stream=st)
+                    occ2 = torch.zeros(1, dtype=torch.int64, device=dev)
+                    epsm.count_async(pl, td, occ2, stream=st)
+                    results.append((j, out, occ, occ2, pl))
+    torch.cuda.synchronize()
+    for j, out, occ, occ2, _ in results:
+        assert int(occ.item()) == wants[j].size and int(occ2.item()) == wants[j].size
+        assert np.array_equal(out[: wants[j].size].cpu().numpy().astype(np.uint64), wants[j])
+
+
+def test_debug_trace_is_off_by_default(epsm, dev):
+    td = torch.zeros(1000, dtype=torch.uint8, device=dev)
+    epsm.search(b"\x00\x01", td)
+    tr = epsm.debug_trace()
+    assert tr.size == 0 or tr.shape[1:] == (1024, 8)
