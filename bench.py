@@ -13,8 +13,13 @@ count kernel on the first step).  Each text (256 MiB) is larger than the
 126 MB L2, so no L2 flush is inserted between searches.
 
 N > 1 (torchrun): weak scaling -- each rank holds a 256 MiB shard (+31-byte
-halo) of an N x 256 MiB text per sigma and every search is the full collective
-epsm_search_sharded (local scan + NCCL all-gather of counts and positions).
+halo) of an N x 256 MiB text per sigma.  Default (batch API): per (sigma, m) group
+every rank runs epsm_search_range_batch_async over its owned starts (global
+positions into its own buffers) and ONE NCCL all-gather of the group's counts gives
+every search's global occ and each rank's output offset -- the positions stay
+distributed, ordered by rank (SURVEY 8e / NEXT-3's "keep results sharded").
+--no-batch: every search is the full collective epsm_search_sharded (local scan +
+NCCL all-gather of counts and positions).
 
 --impl reference: the CPU oracle (brute force, oracle/) timed on this box's host
 cores over a bounded sample of the same workload (rank 0 only).
@@ -216,7 +221,7 @@ def run_epsm(args, world, rank, local):
     pos_buf = torch.empty(cap, dtype=torch.int64, device=dev)
     occ_buf = torch.zeros(len(jobs), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    comm = epsm.nccl_comm_ptr() if world > 1 else None
+    comm = epsm.nccl_comm_ptr() if (world > 1 and not args.batch) else None
     n_text_step = sum(texts[ti][2] for ti, _ in jobs)        # global text bytes per step
 
     # batch mode (N = 1): every (sigma, m) group of searches is ONE call of the public batch
@@ -230,14 +235,32 @@ def run_epsm(args, world, rank, local):
             groups[-1][1] = j + 1
         else:
             groups.append([j, j + 1])
-    use_batch = args.batch and world == 1
+    use_batch = args.batch
     pool = []
+    occ_loc = occ_buf                                         # N > 1: this rank's counts
+    if use_batch and world > 1:
+        from paper_1209_6449_b200 import sharding
+        occ_loc = torch.zeros(len(jobs), dtype=torch.int64, device=dev)
+
+    def batch_call(j0, j1, outs):
+        ti = jobs[j0][0]
+        s_, spec_, n_total_, base_, owned_, t_ = texts[ti]
+        plans_ = [pl for _, pl in jobs[j0:j1]]
+        if world == 1:
+            epsm.search_batch_async(plans_, t_, occ_buf[j0:j1], outs=outs, stream=stream)
+        else:
+            # sharded batch: local scan of the owned starts (global positions), then ONE
+            # all-gather of the group's counts -> global occ and this rank's output offsets;
+            # positions stay on the rank that found them (a distributed, ordered result)
+            epsm.search_range_batch_async(plans_, t_, owned_, base_, occ_loc[j0:j1], outs=outs, stream=stream)
+            occ_g, _off = sharding.exchange_batch_counts(occ_loc[j0:j1])
+            occ_buf[j0:j1].copy_(occ_g)
+
     if use_batch:
         for j0, j1 in groups:
-            ti = jobs[j0][0]
-            epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[ti][5], occ_buf[j0:j1], stream=stream)
+            batch_call(j0, j1, None)
         torch.cuda.synchronize()
-        pcap = int(occ_buf.max().item()) + 1
+        pcap = int(occ_loc.max().item()) + 1
         pos_buf = None
         pool = [torch.empty(pcap, dtype=torch.int64, device=dev) for _ in range(80)]
         pos_buf = pool[0]
@@ -245,9 +268,7 @@ def run_epsm(args, world, rank, local):
     def one_step(events=None):
         if use_batch and events is None:
             for j0, j1 in groups:
-                ti = jobs[j0][0]
-                epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[ti][5], occ_buf[j0:j1],
-                                        outs=[pool[j % 80] for j in range(j0, j1)], stream=stream)
+                batch_call(j0, j1, [pool[j % 80] for j in range(j0, j1)])
             return
         for j, (ti, pl) in enumerate(jobs):
             s, spec, n_total, base, owned, t = texts[ti]
@@ -293,7 +314,7 @@ def run_epsm(args, world, rank, local):
 
     # roofline of the scan kernel (the only kernel in the region): algorithmic bytes =
     # n + 8 * min(occ, cap) per launch; average launch duration = region time / launches
-    occ = occ_buf.cpu().numpy().astype(np.int64)
+    occ = occ_loc.cpu().numpy().astype(np.int64)             # this rank's positions written
     local_bytes = [texts[ti][5].numel() for ti, _ in jobs]
     alg_bytes = sum(nb + 8 * min(int(o), cap) for nb, o in zip(local_bytes, occ)) * args.steps
     kernel_ms = ms_total
@@ -346,7 +367,11 @@ def run_epsm(args, world, rank, local):
                    "sigmas": sigmas, "ms": ms, "patterns_per_sigma_m": args.patterns,
                    "searches_per_step": len(jobs), "text_bytes_per_step": n_text_step,
                    "l2": "no flush: every text (256 MiB) is larger than the 126 MB L2",
-                   "parallelism": f"dp{world} over text shards" if world > 1 else "single GPU"},
+                   "parallelism": f"dp{world} over text shards" if world > 1 else "single GPU",
+                   "api": ("epsm_search_batch_async per (sigma, m) group" if world == 1 else
+                           "epsm_search_range_batch_async + NCCL all-gather of counts per group; "
+                           "positions kept sharded at their global offsets") if args.batch
+                   else "epsm_search_async per search" if world == 1 else "epsm_search_sharded per search"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, copy read+write)",

@@ -124,6 +124,19 @@ int epsm_search_batch_async(epsm_plan_t *const *plans, uint32_t k,
                             uint64_t *d_occ, epsm_stream_t stream);
 
 /*
+ * epsm_search_range_batch_async -- the local step of a sharded batch: as
+ * epsm_search_batch_async over the shard d_text[0..n-1], reporting only starts
+ * s < owned_len, each as s + base (the rank's global offset).  With the per-rank
+ * counts exchanged (every rank learns each search's global occ and its own
+ * offset), the union of the ranks' outputs is each search's Occ, in rank order.
+ */
+int epsm_search_range_batch_async(epsm_plan_t *const *plans, uint32_t k,
+                                  const uint8_t *d_text, uint64_t n,
+                                  uint64_t owned_len, uint64_t base,
+                                  uint64_t *const *d_pos, const uint64_t *caps,
+                                  uint64_t *d_occ, epsm_stream_t stream);
+
+/*
  * epsm_search_host -- end-to-end convenience: h_text[0..n-1] and h_pos are HOST
  * buffers (pinned memory gives full PCIe bandwidth; pageable works).  Copies
  * the text to a plan-owned device buffer, runs epsm_search, and copies the

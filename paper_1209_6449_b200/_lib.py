@@ -52,6 +52,8 @@ _lib.epsm_search_async.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp, _vp]
 _lib.epsm_search_async.restype = ctypes.c_int
 _lib.epsm_search_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_search_batch_async.restype = ctypes.c_int
+_lib.epsm_search_range_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_search_range_batch_async.restype = ctypes.c_int
 _lib.epsm_search_host.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
 _lib.epsm_search_host.restype = _i64
 _lib.epsm_search_sharded.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _u64, _vp, _vp]
@@ -71,7 +73,8 @@ _lib.epsm_debug_trace.restype = _i64
 
 EXPORTED_SYMBOLS = (
     "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
-    "epsm_search", "epsm_search_async", "epsm_search_batch_async", "epsm_search_host", "epsm_search_sharded",
+    "epsm_search", "epsm_search_async", "epsm_search_batch_async", "epsm_search_range_batch_async",
+    "epsm_search_host", "epsm_search_sharded",
     "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
     "epsm_version", "epsm_debug_trace",
 )
@@ -250,18 +253,9 @@ def search_async(p: Plan, text: torch.Tensor, out: torch.Tensor | None, occ_out:
            "epsm_search_async")
 
 
-def search_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, outs=None, caps=None,
-                       stream=None) -> None:
-    """Enqueue len(plans) searches over one text (one persistent launch per run of equal m).
-
-    occ_out: CUDA int64 tensor with >= len(plans) elements (occ of search j -> occ_out[j]).
-    outs: None (count only) or a sequence of CUDA int64 tensors / None, one per plan;
-    caps: optional sequence of capacities (default: each out's numel).
-    """
+def _batch_args(plans, text, occ_out, outs, caps):
     plans = [p if isinstance(p, Plan) else Plan(p) for p in plans]
     k = len(plans)
-    if k == 0:
-        return
     _check_text(text)
     _check_out(occ_out, "occ_out")
     if occ_out.numel() < k:
@@ -277,9 +271,35 @@ def search_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, outs=No
             cs.append(c)
         pos_arr = (ctypes.c_void_p * k)(*ptrs)
         caps_arr = (ctypes.c_uint64 * k)(*cs)
+    return plans, k, hp, pos_arr, caps_arr
+
+
+def search_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, outs=None, caps=None,
+                       stream=None) -> None:
+    """Enqueue len(plans) searches over one text (one persistent launch per run of equal m).
+
+    occ_out: CUDA int64 tensor with >= len(plans) elements (occ of search j -> occ_out[j]).
+    outs: None (count only) or a sequence of CUDA int64 tensors / None, one per plan;
+    caps: optional sequence of capacities (default: each out's numel).
+    """
+    if len(plans) == 0:
+        return
+    plans, k, hp, pos_arr, caps_arr = _batch_args(plans, text, occ_out, outs, caps)
     _check(_lib.epsm_search_batch_async(hp, k, text.data_ptr(), text.numel(), pos_arr, caps_arr,
                                         occ_out.data_ptr(), _stream_handle(stream, text.device)),
            "epsm_search_batch_async")
+
+
+def search_range_batch_async(plans, shard: torch.Tensor, owned_len: int, base: int, occ_out: torch.Tensor,
+                             outs=None, caps=None, stream=None) -> None:
+    """Local step of a sharded batch: starts s < owned_len of ``shard``, reported as s + base."""
+    if len(plans) == 0:
+        return
+    plans, k, hp, pos_arr, caps_arr = _batch_args(plans, shard, occ_out, outs, caps)
+    _check(_lib.epsm_search_range_batch_async(hp, k, shard.data_ptr(), shard.numel(), int(owned_len), int(base),
+                                              pos_arr, caps_arr, occ_out.data_ptr(),
+                                              _stream_handle(stream, shard.device)),
+           "epsm_search_range_batch_async")
 
 
 def search_range_async(p: Plan, shard: torch.Tensor, owned_len: int, base: int,

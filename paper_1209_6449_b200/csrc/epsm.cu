@@ -611,11 +611,12 @@ int epsm_search_async(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint
                      reinterpret_cast<unsigned long long*>(d_occ), true, static_cast<cudaStream_t>(stream));
 }
 
-int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
-                            uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
+int epsm_search_range_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
+                                  uint64_t owned_len, uint64_t base, uint64_t* const* d_pos, const uint64_t* caps,
+                                  uint64_t* d_occ, epsm_stream_t stream) {
   if (k == 0) return EPSM_OK;
   if (!plans || !d_occ || (!d_text && n > 0)) {
-    epsm_set_error("epsm_search_batch_async: NULL plans, d_occ or text");
+    epsm_set_error("epsm_search_(range_)batch_async: NULL plans, d_occ or text");
     return EPSM_EINVAL;
   }
   if (n > (1ull << 38)) {
@@ -649,12 +650,18 @@ int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t
     uint32_t b = a + 1;
     while (b < k && b - a < static_cast<uint32_t>(epsm::kMaxJobs) && plans[b]->m == plans[a]->m) ++b;
     const uint32_t m = plans[a]->m;
-    const uint64_t ns = n >= m ? n - m + 1 : 0;
-    int rc = epsm_launch_jobs(jobs.data() + a, b - a, d_text, n, ns, 0, true, s);
+    uint64_t ns = n >= m ? n - m + 1 : 0;
+    if (owned_len < ns) ns = owned_len;
+    int rc = epsm_launch_jobs(jobs.data() + a, b - a, d_text, n, ns, base, true, s);
     if (rc) return rc;
     a = b;
   }
   return EPSM_OK;
+}
+
+int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
+                            uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
+  return epsm_search_range_batch_async(plans, k, d_text, n, n, 0, d_pos, caps, d_occ, stream);
 }
 
 int epsm_search_range_async(epsm_plan_t* plan, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,

@@ -76,6 +76,23 @@ def exchange_positions(local_pos: torch.Tensor, local_occ: int, group=None, cap:
     return out, occ
 
 
+def exchange_batch_counts(local_occ: torch.Tensor, group=None):
+    """Counts exchange of a sharded batch of k searches (one all-gather of k int64 per rank).
+
+    ``local_occ[j]`` = occurrences of search j among this rank's owned starts.  Returns
+    (occ, offset): occ[j] = the global count, offset[j] = this rank's exclusive prefix (its
+    positions of search j are the global positions [offset[j], offset[j] + local_occ[j]) of
+    Occ in ascending order).  Stays on the device (no host synchronisation)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    k = local_occ.numel()
+    allc = torch.empty(world * k, dtype=torch.int64, device=local_occ.device)
+    dist.all_gather_into_tensor(allc, local_occ.reshape(-1).to(torch.int64).contiguous(), group=group)
+    allc = allc.view(world, k)
+    offset = allc.cumsum(0) - allc
+    return allc.sum(0), offset[rank]
+
+
 def search_sharded_torch(shard: torch.Tensor, base: int, owned_len: int, n_total: int, local_search,
                          group=None, cap: int | None = None):
     """Sharded search with the exchange done by torch.distributed.

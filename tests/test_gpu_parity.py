@@ -464,3 +464,36 @@ def test_debug_trace_is_off_by_default(epsm, dev):
     epsm.search(b"\x00\x01", td)
     tr = epsm.debug_trace()
     assert tr.size == 0 or tr.shape[1:] == (1024, 8)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_shards_batch_compose(epsm, dev, world):
+    """Sharded batch (bench N > 1 path) emulated on one GPU: each shard's
+    epsm_search_range_batch_async output, placed at the exclusive prefix of the per-shard
+    counts, is every search's Occ."""
+    from paper_1209_6449_b200 import sharding
+    rng = np.random.default_rng(77 + world)
+    n = 5 * CHUNK + 4567
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    pats = []
+    for m in (2, 4, 8, 9, 16, 24, 32):
+        p = t[1000 * m:1000 * m + m].copy()
+        for r in range(1, world):
+            b = sharding.shard_base(n, world, r)
+            t[b - m // 2:b - m // 2 + m] = p
+        pats.append(p.tobytes())
+    td = torch.from_numpy(t).to(dev)
+    plans = [epsm.plan(p) for p in pats]
+    wants = [oracle.search(p, t) for p in pats]
+    parts = [[] for _ in pats]
+    for r in range(world):
+        base, owned, slen = sharding.shard_layout(n, world, r)
+        occ = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+        outs = [torch.empty(w.size + 1, dtype=torch.int64, device=dev) for w in wants]
+        epsm.search_range_batch_async(plans, td[base:base + slen], owned, base, occ, outs=outs)
+        torch.cuda.synchronize()
+        for j in range(len(pats)):
+            k = int(occ[j])
+            parts[j].append(outs[j][:k].cpu().numpy().astype(np.uint64))
+    for j, w in enumerate(wants):
+        assert np.array_equal(np.concatenate(parts[j]), w), len(pats[j])

@@ -91,3 +91,60 @@ def test_gloo_sharded_search_equals_unsharded(world):
             pos, occ = got[r][i]
             assert occ == want.size
             assert np.array_equal(pos.astype(np.uint64), want[:cap] if cap else want)
+
+
+def _batch_worker(rank, world, port, text, patterns, q):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = text.size
+        base, owned, slen = sharding.shard_layout(n, world, rank)
+        shard = text[base:base + slen]
+        local_pos, local_occ = [], []
+        for p in patterns:
+            pos = oracle.search(p, shard)
+            pos = pos[pos < owned].astype(np.int64) + base
+            local_pos.append(pos)
+            local_occ.append(pos.size)
+        occ, off = sharding.exchange_batch_counts(torch.tensor(local_occ, dtype=torch.int64))
+        q.put((rank, occ.numpy().copy(), off.numpy().copy(), local_pos))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_counts_exchange_gives_global_layout(world):
+    """A sharded batch: every rank learns each search's global occ and its own offset, and the
+    ranks' positions placed at those offsets are exactly Occ (oracle over the whole text)."""
+    import oracle
+    rng = np.random.default_rng(world + 40)
+    n = 50_000
+    text = rng.integers(0, 3, size=n, dtype=np.uint8)
+    patterns = [text[s:s + m].tobytes() for s, m in ((7, 2), (1000, 5), (20_000, 9), (30_001, 17))]
+    patterns.append(b"\x07\x07")                             # absent
+    for r in range(1, world):                               # straddle every cut
+        b = sharding.shard_base(n, world, r)
+        text[b - 3:b - 3 + 9] = np.frombuffer(patterns[2], dtype=np.uint8)
+    patterns = [text[s:s + m].tobytes() if i < 4 else p
+                for i, (p, (s, m)) in enumerate(zip(patterns, ((7, 2), (1000, 5), (20_000, 9), (30_001, 17), (0, 2))))]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, text, patterns, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict((r, (o, f, lp)) for r, o, f, lp in (q.get(timeout=120) for _ in range(world)))
+    for pr in procs:
+        pr.join(timeout=60)
+    for j, p in enumerate(patterns):
+        want = oracle.search(p, text)
+        out = np.full(want.size, -1, dtype=np.int64)
+        for r in range(world):
+            occ, off, lp = res[r]
+            assert occ[j] == want.size
+            out[off[j]: off[j] + lp[j].size] = lp[j]
+        assert np.array_equal(out.astype(np.uint64), want)
