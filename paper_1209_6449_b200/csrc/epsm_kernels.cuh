@@ -73,7 +73,7 @@ constexpr int kSlices = kChunkTiles * kConsumerWarps;            // 64 per chunk
 constexpr int kParked = 8;                                       // chunks parked awaiting their prefix
 constexpr int kSlots = 16;                                       // look-back queue depth
 constexpr int kWarpStage = 1024;                                 // positions per warp round
-constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16;      // +1 u16 every 16 (bank spread)
+constexpr int kWarpStagePad = kWarpStage + kWarpStage / 16 + 4;  // slots + 2 pad per 32 + lead
 constexpr int kLookbackWindow = 256;                             // statuses per look-back round
 // parked masks in global scratch: one u64 (64 starts) per (chunk slot, tile, warp, lane)
 constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
@@ -262,6 +262,22 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Blocking wait for an idle warp: try_wait with a suspend-time hint parks the warp in hardware
+// until the phase completes (no issue slots spent polling).
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITS:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONES;\n"
+      "bra LAB_WAITS;\n"
+      "DONES:\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
   while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
@@ -326,6 +342,10 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
 
 __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_stream_u32x4(uint64_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
 __device__ __forceinline__ void st_stream_u64x2(uint64_t* p, uint64_t a, uint64_t b) {   // 16-byte aligned p
@@ -661,44 +681,79 @@ __device__ __forceinline__ unsigned long long lookback(const KParams& P, uint32_
 // the slice base sbase (lane*64 + bit < 2048), so one round holds half a slice's 2048 starts
 // and the 64-bit adds happen only in the coalesced copy-out.  Lane: 64-start mask M,
 // exclusive offset `off` inside the slice; tg = slice total.  Every lane walks its bits once
-// across the rounds, stopping at each round's end.
+// across the rounds (two per step), stopping at each round's end.
+// Stage slot of round entry i is i + lead (lead = 8-byte misalignment of the round's output),
+// so slots (2k, 2k+1) are one 16-byte output pair; slot s lives at u16 index s + 2*(s >> 5)
+// (a pad every 32 spreads the lanes' scattered writes over the banks and keeps each pair in
+// one aligned 32-bit word).
+__device__ __forceinline__ uint32_t stage_idx(uint32_t s) { return s + 2u * (s >> 5); }
+
 __device__ __forceinline__ void write_slice(uint16_t* stage, uint64_t* dst, uint64_t room, uint64_t M,
                                             uint32_t off, uint32_t tg, uint64_t sbase, uint32_t lane) {
   uint32_t lo = static_cast<uint32_t>(M), hi = static_cast<uint32_t>(M >> 32);
   const uint32_t lbase = lane * kSegBytes;
+  const uint32_t base_lo = static_cast<uint32_t>(sbase), base_hi = static_cast<uint32_t>(sbase >> 32);
+  const bool no_carry = base_lo <= 0xFFFFFFFFu - 2048u;         // warp-uniform; 32-bit adds suffice
   uint32_t idx = off;
   for (uint32_t R = 0; R < tg; R += kWarpStage) {
     const uint32_t lim = R + kWarpStage;
-    while (lo && idx < lim) {
-      const uint32_t bit = __ffs(lo) - 1;
+    uint64_t* d = dst + R;
+    const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
+    const uint32_t sh = lead - R;                                  // slot = idx + sh
+    while (idx + 1 < lim && (lo & (lo - 1u))) {                    // two bits of lo per step
+      const uint32_t b0 = __ffs(lo) - 1;
       lo &= lo - 1;
-      const uint32_t i = idx - R;
-      stage[i + (i >> 4)] = static_cast<uint16_t>(lbase + bit);
+      const uint32_t b1 = __ffs(lo) - 1;
+      lo &= lo - 1;
+      const uint32_t s0 = idx + sh;
+      stage[stage_idx(s0)] = static_cast<uint16_t>(lbase + b0);
+      stage[stage_idx(s0 + 1)] = static_cast<uint16_t>(lbase + b1);
+      idx += 2;
+    }
+    if (lo && idx < lim) {
+      const uint32_t b0 = __ffs(lo) - 1;
+      lo &= lo - 1;
+      stage[stage_idx(idx + sh)] = static_cast<uint16_t>(lbase + b0);
       ++idx;
     }
-    while (hi && idx < lim) {
-      const uint32_t bit = __ffs(hi) + 31;
+    while (idx + 1 < lim && (hi & (hi - 1u))) {
+      const uint32_t b0 = __ffs(hi) + 31;
       hi &= hi - 1;
-      const uint32_t i = idx - R;
-      stage[i + (i >> 4)] = static_cast<uint16_t>(lbase + bit);
+      const uint32_t b1 = __ffs(hi) + 31;
+      hi &= hi - 1;
+      const uint32_t s0 = idx + sh;
+      stage[stage_idx(s0)] = static_cast<uint16_t>(lbase + b0);
+      stage[stage_idx(s0 + 1)] = static_cast<uint16_t>(lbase + b1);
+      idx += 2;
+    }
+    if (hi && idx < lim) {
+      const uint32_t b0 = __ffs(hi) + 31;
+      hi &= hi - 1;
+      stage[stage_idx(idx + sh)] = static_cast<uint16_t>(lbase + b0);
       ++idx;
     }
     __syncwarp();
     uint32_t n = tg - R < kWarpStage ? tg - R : kWarpStage;
     if (room <= R) n = 0;
     else if (room - R < n) n = static_cast<uint32_t>(room - R);
-    uint64_t* d = dst + R;
     if (n) {
-      // 16-byte stores of entry pairs (e, e+1), e = lead + 2k: peel one entry if d is only
-      // 8-byte aligned (pairs then start odd and may straddle a pad: read them one by one)
-      const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
-      if (lead && lane == 0) st_stream_u64(d, sbase + stage[0]);
-      const uint32_t npairs = (n - lead) >> 1;
+      uint64_t* dp = d - lead;                                     // 16-byte aligned
+      const uint32_t nslots = n + lead;
+      const uint32_t npairs = nslots >> 1;
       for (uint32_t k = lane; k < npairs; k += 32) {
-        const uint32_t e = lead + 2 * k;
-        st_stream_u64x2(d + e, sbase + stage[e + (e >> 4)], sbase + stage[(e + 1) + ((e + 1) >> 4)]);
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(stage + stage_idx(2 * k));
+        if (k == 0 && lead) {
+          st_stream_u64(dp + 1, sbase + (v >> 16));
+        } else if (no_carry) {
+          st_stream_u32x4(dp + 2 * k, base_lo + (v & 0xFFFFu), base_hi, base_lo + (v >> 16), base_hi);
+        } else {
+          st_stream_u64x2(dp + 2 * k, sbase + (v & 0xFFFFu), sbase + (v >> 16));
+        }
       }
-      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, sbase + stage[(n - 1) + ((n - 1) >> 4)]);
+      if ((nslots & 1u) && lane == 0) {
+        const uint32_t sl = nslots - 1;
+        st_stream_u64(dp + sl, sbase + stage[stage_idx(sl)]);
+      }
     }
     __syncwarp();
   }
@@ -945,7 +1000,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       // (chunks reach this queue only after the consumers saw the workspace free)
       uint32_t q = 0, par = 0;
       while (true) {
-        mbar_wait_sleep(&S.lb_full[q], par, 200);
+        mbar_wait_suspend(&S.lb_full[q], par);
         const ChunkSlot sl = S.slot[q];
         if (sl.chunk == kInfoEnd) break;
         // a chunk without occurrences needs no prefix of its own; its look-back only helps
