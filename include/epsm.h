@@ -123,6 +123,13 @@ int epsm_search_batch_async(epsm_plan_t *const *plans, uint32_t k,
                             uint64_t *const *d_pos, const uint64_t *caps,
                             uint64_t *d_occ, epsm_stream_t stream);
 
+/* epsm_count_batch_async -- as epsm_search_batch_async with no positions: the count
+ * kernel (popcounts only) for k patterns over one text; occ_j
+ * into d_occ[j].  Does not synchronise. */
+int epsm_count_batch_async(epsm_plan_t *const *plans, uint32_t k,
+                           const uint8_t *d_text, uint64_t n, uint64_t *d_occ,
+                           epsm_stream_t stream);
+
 /*
  * epsm_search_range_batch_async -- the local step of a sharded batch: as
  * epsm_search_batch_async over the shard d_text[0..n-1], reporting only starts

@@ -52,6 +52,8 @@ _lib.epsm_search_async.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp, _vp]
 _lib.epsm_search_async.restype = ctypes.c_int
 _lib.epsm_search_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_search_batch_async.restype = ctypes.c_int
+_lib.epsm_count_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _vp]
+_lib.epsm_count_batch_async.restype = ctypes.c_int
 _lib.epsm_search_range_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_search_range_batch_async.restype = ctypes.c_int
 _lib.epsm_search_host.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
@@ -73,7 +75,7 @@ _lib.epsm_debug_trace.restype = _i64
 
 EXPORTED_SYMBOLS = (
     "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
-    "epsm_search", "epsm_search_async", "epsm_search_batch_async", "epsm_search_range_batch_async",
+    "epsm_search", "epsm_search_async", "epsm_search_batch_async", "epsm_search_range_batch_async", "epsm_count_batch_async",
     "epsm_search_host", "epsm_search_sharded",
     "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
     "epsm_version", "epsm_debug_trace",
@@ -288,6 +290,16 @@ def search_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, outs=No
     _check(_lib.epsm_search_batch_async(hp, k, text.data_ptr(), text.numel(), pos_arr, caps_arr,
                                         occ_out.data_ptr(), _stream_handle(stream, text.device)),
            "epsm_search_batch_async")
+
+
+def count_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, stream=None) -> None:
+    """Enqueue len(plans) counts over one text (count kernel; occ of pattern j -> occ_out[j])."""
+    if len(plans) == 0:
+        return
+    plans, k, hp, _, _ = _batch_args(plans, text, occ_out, None, None)
+    _check(_lib.epsm_count_batch_async(hp, k, text.data_ptr(), text.numel(), occ_out.data_ptr(),
+                                       _stream_handle(stream, text.device)),
+           "epsm_count_batch_async")
 
 
 def search_range_batch_async(plans, shard: torch.Tensor, owned_len: int, base: int, occ_out: torch.Tensor,

@@ -611,9 +611,9 @@ int epsm_search_async(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint
                      reinterpret_cast<unsigned long long*>(d_occ), true, static_cast<cudaStream_t>(stream));
 }
 
-int epsm_search_range_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
-                                  uint64_t owned_len, uint64_t base, uint64_t* const* d_pos, const uint64_t* caps,
-                                  uint64_t* d_occ, epsm_stream_t stream) {
+static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n, uint64_t owned_len,
+                        uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
+                        epsm_stream_t stream) {
   if (k == 0) return EPSM_OK;
   if (!plans || !d_occ || (!d_text && n > 0)) {
     epsm_set_error("epsm_search_(range_)batch_async: NULL plans, d_occ or text");
@@ -652,16 +652,27 @@ int epsm_search_range_batch_async(epsm_plan_t* const* plans, uint32_t k, const u
     const uint32_t m = plans[a]->m;
     uint64_t ns = n >= m ? n - m + 1 : 0;
     if (owned_len < ns) ns = owned_len;
-    int rc = epsm_launch_jobs(jobs.data() + a, b - a, d_text, n, ns, base, true, s);
+    int rc = epsm_launch_jobs(jobs.data() + a, b - a, d_text, n, ns, base, search, s);
     if (rc) return rc;
     a = b;
   }
   return EPSM_OK;
 }
 
+int epsm_search_range_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
+                                  uint64_t owned_len, uint64_t base, uint64_t* const* d_pos, const uint64_t* caps,
+                                  uint64_t* d_occ, epsm_stream_t stream) {
+  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, true, stream);
+}
+
 int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
                             uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
-  return epsm_search_range_batch_async(plans, k, d_text, n, n, 0, d_pos, caps, d_occ, stream);
+  return batch_common(plans, k, d_text, n, n, 0, d_pos, caps, d_occ, true, stream);
+}
+
+int epsm_count_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
+                           uint64_t* d_occ, epsm_stream_t stream) {
+  return batch_common(plans, k, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream);
 }
 
 int epsm_search_range_async(epsm_plan_t* plan, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,

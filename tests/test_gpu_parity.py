@@ -407,6 +407,12 @@ def test_batch_search_many_patterns_one_text(epsm, dev):
         epsm.search_batch_async(plans, td, occ2)
     torch.cuda.synchronize()
     assert np.array_equal(occ2.cpu().numpy(), np.array([w.size for w in wants]))
+    # the count kernel, batched (per-search counters in the workspace, published by the last CTA)
+    occ3 = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    for _ in range(2):
+        epsm.count_batch_async(plans, td, occ3)
+    torch.cuda.synchronize()
+    assert np.array_equal(occ3.cpu().numpy(), np.array([w.size for w in wants]))
 
 
 def test_batch_dense_and_small_texts(epsm, dev):
