@@ -376,8 +376,11 @@ def run_epsm(args, world, rank, local):
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, copy read+write)",
                      "kernel": "epsm_scan_kernel (search), the only kernel in the timed region",
-                     "per_launch_ms": round(kernel_ms / (args.steps * len(jobs)), 5),
-                     "alg_bytes_per_launch": int(alg_bytes / (args.steps * len(jobs))),
+                     "traffic_unit": "DRAM bytes per search (ncu, one search per launch)",
+                     "per_search_ms": round(kernel_ms / (args.steps * len(jobs)), 5),
+                     "alg_bytes_per_search": int(alg_bytes / (args.steps * len(jobs))),
+                     "per_launch_ms": round(kernel_ms / max(1, launches), 5),
+                     "searches_per_launch": round(args.steps * len(jobs) / max(1, launches), 2),
                      "kernel_share_of_step": 1.0},
         "clocks": clocks,
         "gpu_launches": int(launches),
