@@ -150,9 +150,14 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: EPSM_BENCH_EMULATE=1 runs every rank on cuda:0 over gloo (a host-side check of
+    # the N > 1 logic on a one-GPU box; no kernel waits on another rank, only gloo does)
+    emulate = os.environ.get("EPSM_BENCH_EMULATE") == "1"
+    if emulate:
+        local = 0
     if world > 1:
         import torch.distributed as dist
-        if args.impl == "epsm":
+        if args.impl == "epsm" and not emulate:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -170,7 +175,7 @@ def max_over_ranks(x: float, world: int, dev) -> float:
     if world == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -86,8 +86,16 @@ def exchange_batch_counts(local_occ: torch.Tensor, group=None):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     k = local_occ.numel()
-    allc = torch.empty(world * k, dtype=torch.int64, device=local_occ.device)
-    dist.all_gather_into_tensor(allc, local_occ.reshape(-1).to(torch.int64).contiguous(), group=group)
+    dev = local_occ.device
+    # gloo has no device all-gather: stage through the host (CPU tests, one-GPU emulation)
+    via_host = dev.type == "cuda" and dist.get_backend(group) == "gloo"
+    src = local_occ.reshape(-1).to(torch.int64)
+    if via_host:
+        src = src.cpu()
+    allc = torch.empty(world * k, dtype=torch.int64, device=src.device)
+    dist.all_gather_into_tensor(allc, src.contiguous(), group=group)
+    if via_host:
+        allc = allc.to(dev)
     allc = allc.view(world, k)
     offset = allc.cumsum(0) - allc
     return allc.sum(0), offset[rank]
