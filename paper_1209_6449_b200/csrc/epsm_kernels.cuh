@@ -79,7 +79,7 @@ constexpr int kLookbackWindow = 256;                             // statuses per
 constexpr int kScratchPerCta = kParked * kChunkTiles * kConsumerWarps * 32;   // u64 words
 static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking rotation");
 static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
-static_assert(kSlices % 32 == 0 && kChunkTiles <= 8 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
+static_assert(kSlices <= 128 && kChunkTiles <= 8 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
 constexpr uint32_t kTileBitsMask = (1u << kChunkTiles) - 1u;      // slow-tile bits of one parked chunk
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
@@ -1314,21 +1314,22 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         __threadfence_block();
         // exclusive prefix over the 64 slice counts in text order (tile, warp); slices of
         // warps that parked nothing for a tile count zero
-        constexpr int kPerLane = kSlices / 32;
+        constexpr int kPerLane = (kSlices + 31) / 32;
         uint32_t v[kPerLane], sum = 0;
 #pragma unroll
         for (int i = 0; i < kPerLane; ++i) {
-          const uint32_t sl = lane * kPerLane + i;              // text order
+          const uint32_t sl = lane * kPerLane + i;              // text order (>= kSlices: none)
           const uint32_t t = sl / kConsumerWarps;
           const uint32_t w = sl % kConsumerWarps;
-          v[i] = (t < ntiles && ((S.park[b].slow[w] >> t) & 1u)) ? S.park[b].cnt[sl] : 0u;
+          v[i] = (sl < static_cast<uint32_t>(kSlices) && t < ntiles && ((S.park[b].slow[w] >> t) & 1u))
+                     ? S.park[b].cnt[sl] : 0u;
           sum += v[i];
         }
         const uint32_t incl = warp_inclusive_scan(sum, lane);
         uint32_t run = incl - sum;
 #pragma unroll
         for (int i = 0; i < kPerLane; ++i) {
-          S.park[b].off[lane * kPerLane + i] = run;
+          if (lane * kPerLane + i < static_cast<uint32_t>(kSlices)) S.park[b].off[lane * kPerLane + i] = run;
           run += v[i];
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
