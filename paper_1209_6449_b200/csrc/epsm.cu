@@ -422,6 +422,11 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     P.tag = static_cast<unsigned long long>(L & 0xFFFFFFull) << epsm::kEpochShift;
   }
   P.trace = trace_slot(plan0->device);
+  static const uint32_t env_flags = [] {
+    const char* v = getenv("EPSM_FLAGS");
+    return v && v[0] ? static_cast<uint32_t>(strtoul(v, nullptr, 0)) : 0u;
+  }();
+  P.flags = env_flags;
   KernelFn fn = kernel_for(plan0->m, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);

@@ -6,8 +6,8 @@
 //                          first one is static, the rest come from a global counter) and
 //                          streams every tile plus a 32-byte halo (>= m-1 for m <= 32)
 //                          into a shared-memory ring with ONE TMA bulk copy per tile
-//                          (cp.async.bulk ... mbarrier::complete_tx), and pulls the next
-//                          chunk into L2 ahead of time (cp.async.bulk.prefetch.L2).  The
+//                          (cp.async.bulk ... mbarrier::complete_tx); the chunk ids are
+//                          drawn two ahead so the atomic never stalls the issue.  The
 //                          halo is the GPU analogue of EPSMb's wsblend, which only exists
 //                          to avoid unaligned loads: shared memory is
 //                          byte addressable, so every alignment is read directly.
@@ -144,6 +144,9 @@ struct KParams {
   uint32_t mul24;               // 1 << 8 : byte shift by 3 through one IMAD.WIDE
   uint32_t movemask_mul;        // 0x00204081
   uint32_t desc_bytes;          // bytes of JobDesc the producer copies (header [+ gram table])
+  uint32_t flags;               // EPSM_FLAGS (A/B timing): bit 1 = L2 prefetch of the next chunk
+                                // (off by default: measured no gain, and under dense position
+                                // writes the prefetched lines are evicted and read twice)
   unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
   unsigned long long* exit_ctr; // CTAs of all launches on this workspace parity that have exited
   unsigned long long exit_expect;   // value meaning "launch L-2 (same parity) has retired"
@@ -1010,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       cur = __shfl_sync(0xffffffffu, nxt, 0);
       after = __shfl_sync(0xffffffffu, after, 0);
-      prefetch_l2(after);
+      if (P.flags & 2u) prefetch_l2(after);
     }
   } else if (warp == 1) {
     // ================================================================ look-back
