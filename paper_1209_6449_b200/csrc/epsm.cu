@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <new>
@@ -65,13 +66,29 @@ uint32_t sample_min_m() {
   return v;
 }
 
-// Sampled-filter geometry of a pattern length: one SQ-byte gram every SK bytes (SK + SQ <= m),
-// (0, 0) for the packed filter.  Must agree with kernel_for.
-void sampled_geometry(uint32_t m, int* sk, int* sq) {
+// Sampled-filter geometry of a pattern: one SQ-byte gram every SK bytes (SK + SQ <= m), (0, 0)
+// for the packed filter.  Must agree with kernel_for.  m = 8 sits at the crossover: the packed
+// 8-byte filter wins on binary texts and on large alphabets, the sampled 4-byte grams on
+// 4..8-letter alphabets (B200: sigma=4 107 -> 91 us, sigma=8 74 -> 64 us per 256 MiB), so the
+// choice follows the pattern's number of distinct bytes d (an extracted pattern's d tracks
+// the text's alphabet): sampled for 3 <= d <= 5.  Speed only: both filters are exact.
+void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
   *sk = *sq = 0;
+  bool take8 = false;
+  if (m == 8) {
+    uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d = 0;
+    for (uint32_t i = 0; i < 8; ++i) {
+      const uint32_t b = pattern[i];
+      if (!((seen[b >> 5] >> (b & 31)) & 1u)) {
+        seen[b >> 5] |= 1u << (b & 31);
+        ++d;
+      }
+    }
+    take8 = d >= 3 && d <= 5;
+  }
   if (m > EPSM_MAX_M) {
     *sk = 16, *sq = 16;
-  } else if (m >= 8 && m >= sample_min_m()) {
+  } else if (m >= 8 && (m >= sample_min_m() || take8)) {
     if (m <= 11) *sk = 4, *sq = 4;
     else if (m <= 15) *sk = 8, *sq = 4;
     else if (m <= 23) *sk = 8, *sq = 8;
@@ -117,9 +134,9 @@ void build_gram_table(const uint8_t* pattern, int sk, int sq, uint32_t* tab) {
 //   packed:  F = min(m, 4) bytes in the first filter word, F2 = min(m, 8) - 4 in the second
 //            (used where candidates are dense), MW = ceil(m/4) words;
 //   sampled: one SQ-byte gram every SK bytes (SK + SQ <= m), MW words verified.
-KernelFn kernel_for(uint32_t m, bool search) {
+KernelFn kernel_for(uint32_t m, int sk, bool search) {
   if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
-  if (m >= 8 && m >= sample_min_m()) {
+  if (sk > 0) {
     switch (m) {
       case 8: return pick<4, 4, 2, 4, 4>(search);
       case 9: case 10: case 11: return pick<4, 4, 3, 4, 4>(search);
@@ -370,8 +387,8 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   P.desc_bytes = plan0->sk > 0 ? static_cast<uint32_t>(sizeof(epsm::JobDesc)) : epsm::kJobHeader;
   for (uint32_t j = 0; j < k; ++j) {
     epsm_plan_t* pl = jobs[j].plan;
-    if (pl->m != plan0->m || pl->device != plan0->device) {
-      epsm_set_error("searches of one launch need the same pattern length and device");
+    if (pl->m != plan0->m || pl->sk != plan0->sk || pl->device != plan0->device) {
+      epsm_set_error("searches of one launch need the same pattern length, filter and device");
       return EPSM_EINVAL;
     }
     int rc = ensure_plan_device(pl, s);
@@ -427,7 +444,7 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     return v && v[0] ? static_cast<uint32_t>(strtoul(v, nullptr, 0)) : 0u;
   }();
   P.flags = env_flags;
-  KernelFn fn = kernel_for(plan0->m, search);
+  KernelFn fn = kernel_for(plan0->m, plan0->sk, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;
@@ -541,7 +558,7 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
     D.pat[q] = w;
     D.pmask[q] = mk;
   }
-  sampled_geometry(m, &p->sk, &p->sq);
+  sampled_geometry(m, p->pattern, &p->sk, &p->sq);
   if (p->sk > 0) build_gram_table(p->pattern, p->sk, p->sq, D.gram_tab);
   p->device = -1;
   *out = p;
@@ -649,15 +666,28 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
     if (rc) return rc;
     jobs[j] = epsm_job{plans[j], cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + j)};
   }
-  // one launch per run of at most kMaxJobs consecutive searches of equal m
+  // searches are independent: group them by kernel variant (m, filter), keeping their order
+  // within a group, and launch each group in runs of at most kMaxJobs
+  std::vector<uint32_t> order(k);
+  for (uint32_t j = 0; j < k; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+    if (plans[x]->m != plans[y]->m) return plans[x]->m < plans[y]->m;
+    return plans[x]->sk < plans[y]->sk;
+  });
+  std::vector<epsm_job> run;
   uint32_t a = 0;
   while (a < k) {
     uint32_t b = a + 1;
-    while (b < k && b - a < static_cast<uint32_t>(epsm::kMaxJobs) && plans[b]->m == plans[a]->m) ++b;
-    const uint32_t m = plans[a]->m;
+    const epsm_plan_t* pa = plans[order[a]];
+    while (b < k && b - a < static_cast<uint32_t>(epsm::kMaxJobs) && plans[order[b]]->m == pa->m &&
+           plans[order[b]]->sk == pa->sk)
+      ++b;
+    run.clear();
+    for (uint32_t i = a; i < b; ++i) run.push_back(jobs[order[i]]);
+    const uint32_t m = pa->m;
     uint64_t ns = n >= m ? n - m + 1 : 0;
     if (owned_len < ns) ns = owned_len;
-    int rc = epsm_launch_jobs(jobs.data() + a, b - a, d_text, n, ns, base, search, s);
+    int rc = epsm_launch_jobs(run.data(), b - a, d_text, n, ns, base, search, s);
     if (rc) return rc;
     a = b;
   }
