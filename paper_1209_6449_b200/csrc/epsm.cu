@@ -94,6 +94,20 @@ void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
     else if (m <= 23) *sk = 8, *sq = 8;
     else if (m <= 31) *sk = 8, *sq = 16;
     else *sk = 16, *sq = 16;
+    // small alphabets (few distinct bytes): longer grams at a 4-byte stride -- four lookups
+    // per unit, but far fewer candidates to check (genome-like m = 12: 300 -> ~240 us/GiB)
+    if (m >= 12 && m <= 23) {
+      uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d = 0;
+      for (uint32_t i = 0; i < m; ++i) {
+        const uint32_t b = pattern[i];
+        if (!((seen[b >> 5] >> (b & 31)) & 1u)) {
+          seen[b >> 5] |= 1u << (b & 31);
+          ++d;
+        }
+      }
+      if (m <= 15 && d <= 5) *sk = 4, *sq = 8;
+      else if (m >= 16 && d <= 2) *sk = 4, *sq = 12;
+    }
   }
 }
 
@@ -134,8 +148,14 @@ void build_gram_table(const uint8_t* pattern, int sk, int sq, uint32_t* tab) {
 //   packed:  F = min(m, 4) bytes in the first filter word, F2 = min(m, 8) - 4 in the second
 //            (used where candidates are dense), MW = ceil(m/4) words;
 //   sampled: one SQ-byte gram every SK bytes (SK + SQ <= m), MW words verified.
-KernelFn kernel_for(uint32_t m, int sk, bool search) {
+KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
+  if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
+  if (sk == 4 && sq == 12) {
+    if (m == 16) return pick<4, 4, 4, 4, 12>(search);
+    if (m <= 20) return pick<4, 4, 5, 4, 12>(search);
+    return pick<4, 4, 6, 4, 12>(search);
+  }
   if (sk > 0) {
     switch (m) {
       case 8: return pick<4, 4, 2, 4, 4>(search);
@@ -444,7 +464,7 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     return v && v[0] ? static_cast<uint32_t>(strtoul(v, nullptr, 0)) : 0u;
   }();
   P.flags = env_flags;
-  KernelFn fn = kernel_for(plan0->m, plan0->sk, search);
+  KernelFn fn = kernel_for(plan0->m, plan0->sk, plan0->sq, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;

@@ -518,25 +518,23 @@ __device__ __forceinline__ uint32_t gram_hash(const uint32_t (&w)[NW]) {
 // SQ bytes of text at a shared-memory address aligned to min(SK, SQ, 16).
 template <int SK, int SQ>
 __device__ __forceinline__ void load_sample(const uint8_t* p, uint32_t (&w)[SQ / 4]) {
-  if constexpr (SQ == 4) {
-    w[0] = *reinterpret_cast<const uint32_t*>(p);
-  } else if constexpr (SQ == 8) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
-    w[0] = v.x;
-    w[1] = v.y;
-  } else if constexpr (SK >= 16) {
+  // the sample address is aligned to min(SK, 16) bytes: widest loads that alignment allows
+  if constexpr (SK >= 16 && SQ == 16) {
     const uint4 v = *reinterpret_cast<const uint4*>(p);
     w[0] = v.x;
     w[1] = v.y;
     w[2] = v.z;
     w[3] = v.w;
+  } else if constexpr (SK >= 8 && SQ % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < SQ / 8; ++i) {
+      const uint2 v = *reinterpret_cast<const uint2*>(p + 8 * i);
+      w[2 * i] = v.x;
+      w[2 * i + 1] = v.y;
+    }
   } else {
-    const uint2 a = *reinterpret_cast<const uint2*>(p);
-    const uint2 b = *reinterpret_cast<const uint2*>(p + 8);
-    w[0] = a.x;
-    w[1] = a.y;
-    w[2] = b.x;
-    w[3] = b.y;
+#pragma unroll
+    for (int i = 0; i < SQ / 4; ++i) w[i] = *reinterpret_cast<const uint32_t*>(p + 4 * i);
   }
 }
 
