@@ -67,28 +67,29 @@ uint32_t sample_min_m() {
 }
 
 // Sampled-filter geometry of a pattern: one SQ-byte gram every SK bytes (SK + SQ <= m), (0, 0)
-// for the packed filter.  Must agree with kernel_for.  m = 8 sits at the crossover: the packed
-// 8-byte filter wins on binary texts and on large alphabets, the sampled 4-byte grams on
-// 4..8-letter alphabets (B200: sigma=4 107 -> 91 us, sigma=8 74 -> 64 us per 256 MiB), so the
-// choice follows the pattern's number of distinct bytes d (an extracted pattern's d tracks
-// the text's alphabet): sampled for 3 <= d <= 5.  Speed only: both filters are exact.
+// for the packed filter.  Must agree with kernel_for.  m = 8..11 sits at the crossover: the
+// packed filter wins on binary texts and on large alphabets, the sampled 4-byte grams on
+// 4..8-letter alphabets (B200, m = 8: sigma=4 107 -> 89 us, sigma=8 74 -> 68 us per 256 MiB;
+// m = 10: sigma=4 108 -> 88 us, sigma=256 58 -> 47 us packed), so the choice follows the
+// pattern's number of distinct bytes d (an extracted pattern's d tracks the text's
+// alphabet): sampled for 3 <= d <= 5.  EPSM_SAMPLE_MIN_M <= 8 forces the sampled filter.
+// Speed only: both filters are exact.
 void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
   *sk = *sq = 0;
-  bool take8 = false;
-  if (m == 8) {
-    uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d = 0;
-    for (uint32_t i = 0; i < 8; ++i) {
-      const uint32_t b = pattern[i];
-      if (!((seen[b >> 5] >> (b & 31)) & 1u)) {
-        seen[b >> 5] |= 1u << (b & 31);
-        ++d;
-      }
+  uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d = 0;   // distinct bytes of the pattern
+  for (uint32_t i = 0; i < m && i < EPSM_MAX_M; ++i) {
+    const uint32_t b = pattern[i];
+    if (!((seen[b >> 5] >> (b & 31)) & 1u)) {
+      seen[b >> 5] |= 1u << (b & 31);
+      ++d;
     }
-    take8 = d >= 3 && d <= 5;
   }
+  // m = 8..11: (4,4) grams on 4..8-letter alphabets, the packed filter otherwise
+  const bool mid = m >= 8 && m <= 11;
+  const bool take_mid = mid && d >= 3 && d <= 5;
   if (m > EPSM_MAX_M) {
     *sk = 16, *sq = 16;
-  } else if (m >= 8 && (m >= sample_min_m() || take8)) {
+  } else if (m >= 8 && (mid ? (take_mid || sample_min_m() <= 8) : m >= sample_min_m())) {
     if (m <= 11) *sk = 4, *sq = 4;
     else if (m <= 15) *sk = 8, *sq = 4;
     else if (m <= 23) *sk = 8, *sq = 8;
@@ -96,18 +97,8 @@ void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
     else *sk = 16, *sq = 16;
     // small alphabets (few distinct bytes): longer grams at a 4-byte stride -- four lookups
     // per unit, but far fewer candidates to check (genome-like m = 12: 300 -> ~240 us/GiB)
-    if (m >= 12 && m <= 23) {
-      uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d = 0;
-      for (uint32_t i = 0; i < m; ++i) {
-        const uint32_t b = pattern[i];
-        if (!((seen[b >> 5] >> (b & 31)) & 1u)) {
-          seen[b >> 5] |= 1u << (b & 31);
-          ++d;
-        }
-      }
-      if (m <= 15 && d <= 5) *sk = 4, *sq = 8;
-      else if (m >= 16 && d <= 2) *sk = 4, *sq = 12;
-    }
+    if (m >= 12 && m <= 15 && d <= 5) *sk = 4, *sq = 8;
+    else if (m >= 16 && m <= 23 && d <= 2) *sk = 4, *sq = 12;
   }
 }
 
