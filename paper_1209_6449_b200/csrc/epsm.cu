@@ -66,6 +66,15 @@ uint32_t sample_min_m() {
   return v;
 }
 
+// EPSM_NO_EQ=1 disables the equality-mask variant (A/B timing).
+static bool eq_disabled() {
+  static const bool off = [] {
+    const char* v = getenv("EPSM_NO_EQ");
+    return v && v[0] && v[0] != '0';
+  }();
+  return off;
+}
+
 // Sampled-filter geometry of a pattern: one SQ-byte gram every SK bytes (SK + SQ <= m), (0, 0)
 // for the packed filter.  Must agree with kernel_for.  m = 8..11 sits at the crossover: the
 // packed filter wins on binary texts and on large alphabets, the sampled 4-byte grams on
@@ -89,6 +98,8 @@ void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
   const bool take_mid = mid && d >= 3 && d <= 5;
   if (m > EPSM_MAX_M) {
     *sk = 16, *sq = 16;
+  } else if (m >= 5 && m <= 11 && d <= 2 && !eq_disabled()) {
+    *sk = epsm::kEqMode;                 // EPSMa's equality masks + shift-AND (binary alphabets)
   } else if (m >= 8 && (mid ? (take_mid || sample_min_m() <= 8) : m >= sample_min_m())) {
     if (m <= 11) *sk = 4, *sq = 4;
     else if (m <= 15) *sk = 8, *sq = 4;
@@ -141,6 +152,7 @@ void build_gram_table(const uint8_t* pattern, int sk, int sq, uint32_t* tab) {
 //   sampled: one SQ-byte gram every SK bytes (SK + SQ <= m), MW words verified.
 KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
+  if (sk == epsm::kEqMode) return pick<4, 4, 1, epsm::kEqMode, 0>(search);   // EPSMa, <= 2 values
   if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
   if (sk == 4 && sq == 12) {
     if (m == 16) return pick<4, 4, 4, 4, 12>(search);
@@ -568,6 +580,28 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
     }
     D.pat[q] = w;
     D.pmask[q] = mk;
+  }
+  // EPSMa's equality masks: the pattern's distinct bytes (if at most 2)
+  // and the positions holding each
+  {
+    uint32_t d = 0;
+    uint8_t vals[2] = {0, 0};
+    for (uint32_t i = 0; i < m && i < 12 && d <= 2; ++i) {
+      uint32_t v = 0;
+      while (v < d && vals[v] != pattern[i]) ++v;
+      if (v == d) {
+        if (d < 2) vals[d] = pattern[i];
+        ++d;
+      }
+      if (v < 2) D.eqsel[v] |= 1u << i;
+    }
+    if (d <= 2 && m <= 11) {
+      D.eqd = d;
+      for (uint32_t v = 0; v < d; ++v) D.eqv[v] = 0x01010101u * vals[v];
+    } else {
+      D.eqd = 0;
+      D.eqsel[0] = D.eqsel[1] = 0;
+    }
   }
   sampled_geometry(m, p->pattern, &p->sk, &p->sq);
   if (p->sk > 0) build_gram_table(p->pattern, p->sk, p->sq, D.gram_tab);

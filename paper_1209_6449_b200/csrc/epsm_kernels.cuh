@@ -109,9 +109,16 @@ struct __align__(16) JobDesc {
   uint32_t bcast2[4];           // B_{4+i}: the second filter word (pattern bytes 4..7)
   uint32_t pat[12];             // first 48 pattern bytes, little-endian u32 words, zero padded
   uint32_t pmask[12];           // per-word byte masks (partial last word)
+  // EPSMa's shift-AND over exact equality masks, the variant for patterns of
+  // 5 <= m <= 11 with at most 2 distinct bytes: value v broadcast, pattern positions holding it
+  uint32_t eqv[2];              // value_v * 0x01010101
+  uint32_t eqsel[2];            // bit i: p_i == value_v
+  uint32_t eqd;                 // number of distinct bytes (1 or 2)
+  uint32_t eqpad[3];
   uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
 };
-constexpr uint32_t kJobHeader = 128;                              // bytes before gram_tab
+constexpr uint32_t kJobHeader = 160;                              // bytes before gram_tab
+constexpr int kEqMode = -1;                                       // SK value of the equality variant
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
 // One search of a launch: its preprocessing and its outputs.
@@ -1140,8 +1147,62 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 
       // slot r holds unit u = (r + rot) & 3 of the segment: text bytes [seg_off + 16u, +16)
       uint32_t mask[4];                        // 16-bit match mask of the unit in slot r
+      uint64_t Meq = 0;                        // equality variant: the lane mask directly
       bool slow;
-      if constexpr (SK > 0) {
+      if constexpr (SK == kEqMode) {
+        // ---- EPSMa (Fig. 1 lines 5-9) for a pattern with <= 2 distinct
+        // bytes: exact equality masks E_v of the lane's 64 bytes (+ the next 16, the halo of
+        // windows crossing the segment), then r = AND_i (E_{v(p_i)} >> i) -- the shift-AND
+        // gives the exact match mask of all 64 starts, no candidates, no check
+        uint4 R[4];
+        load_segment(seg, rot, R);
+        const uint32_t r0 = (4u - rot) & 3u;                // slot holding unit 0
+        uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;       // result, starts 0-31 / 32-63
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          if (v == 1 && JD->eqd < 2) break;                  // warp-uniform
+          const uint32_t vb = JD->eqv[v];
+          uint32_t e16[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t Zv[4] = {R[r].x ^ vb, R[r].y ^ vb, R[r].z ^ vb, R[r].w ^ vb};
+            e16[r] = zero_byte_mask16(Zv, P.movemask_mul);
+          }
+          uint32_t lo = 0, hi = 0;                          // E_v of starts 0-31, 32-63
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t u = (r + rot) & 3u;
+            const uint32_t sh = (u & 1u) * 16u;
+            if (u < 2) lo |= e16[r] << sh;
+            else hi |= e16[r] << sh;
+          }
+          // positions 64..79: the next lane's unit 0 (lane 31: the next slice / the halo)
+          const uint32_t own0 = r0 == 0 ? e16[0] : r0 == 1 ? e16[1] : r0 == 2 ? e16[2] : e16[3];
+          uint32_t halo = __shfl_down_sync(0xffffffffu, own0, 1);
+          if (lane == 31) {
+            const uint4 h = *reinterpret_cast<const uint4*>(seg + kSegBytes);
+            const uint32_t Zh[4] = {h.x ^ vb, h.y ^ vb, h.z ^ vb, h.w ^ vb};
+            halo = zero_byte_mask16(Zh, P.movemask_mul);
+          }
+          const uint32_t sel = JD->eqsel[v];
+#pragma unroll
+          for (int i = 0; i < 12; ++i) {
+            if ((sel >> i) & 1u) {                           // p_i == value_v: AND E_v >> i
+              rl &= __funnelshift_r(lo, hi, i);
+              rh &= __funnelshift_r(hi, halo, i);
+            }
+          }
+        }
+        Meq = (static_cast<uint64_t>(rh) << 32) | rl;
+        if (!interior) {
+          uint64_t rm = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            rm |= static_cast<uint64_t>(range_mask(tbase + seg_off + 16u * u, P.s_lo, P.s_hi)) << (16 * u);
+          Meq &= rm;
+        }
+        slow = __any_sync(0xffffffffu, Meq != 0ull);
+      } else if constexpr (SK > 0) {
         // ---- sampled filter (EPSMc, Fig. 1 lines 7-12): the q-gram at unit
         // offset SK*(g+1) is fingerprinted and looked up in the pattern's gram table, which
         // yields the starts of group g whose window holds that gram at the right offset.
@@ -1271,8 +1332,12 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (slow) {
         // the lane's 64 starts as one mask: bit 16u + j = start seg_off + 16u + j
         uint64_t M = 0;
+        if constexpr (SK == kEqMode) {
+          M = Meq;
+        } else {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) M |= static_cast<uint64_t>(mask[r]) << (16u * ((r + rot) & 3u));
+          for (int r = 0; r < 4; ++r) M |= static_cast<uint64_t>(mask[r]) << (16u * ((r + rot) & 3u));
+        }
         const uint32_t c = popc64(M);
         acc += c;
         if constexpr (SEARCH) {

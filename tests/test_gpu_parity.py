@@ -395,7 +395,8 @@ def test_batch_search_many_patterns_one_text(epsm, dev):
     epsm.search_batch_async(plans, td, occ, outs=outs, caps=caps)
     torch.cuda.synchronize()
     launches = epsm.launch_count() - before
-    assert launches <= 10, launches              # runs of equal m, <= 40 searches each
+    # one launch per run of <= 40 searches of one kernel variant (m and filter)
+    assert launches <= 3 * len({len(p) for p in pats}), launches
     occ_h = occ.cpu().numpy()
     for j, (w, c) in enumerate(zip(wants, caps)):
         assert occ_h[j] == w.size, (j, len(pats[j]))
