@@ -813,22 +813,6 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
     if (gidx >= cap) return;                                // later slices are even further out
     const uint64_t room = cap - gidx;
     const uint64_t sb = cbase + static_cast<uint64_t>(t) * kTile + cw * kWarpBytes + lane * kSegBytes;
-    if (__all_sync(0xffffffffu, M == ~0ull)) {
-      // every start of the slice matches (periodic texts, e.g. 'a'^n): the positions are
-      // slice_base + 0..2047, written arithmetically with 16-byte stores
-      const uint64_t sbase = sb - lane * kSegBytes;
-      uint64_t* d = pos + gidx;
-      const uint32_t n = room < static_cast<uint64_t>(kWarpBytes) ? static_cast<uint32_t>(room) : kWarpBytes;
-      const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
-      if (lead && lane == 0) st_stream_u64(d, sbase);
-      const uint32_t npairs = (n - lead) >> 1;
-      for (uint32_t k = lane; k < npairs; k += 32) {
-        const uint32_t e = lead + 2 * k;
-        st_stream_u64x2(d + e, sbase + e, sbase + e + 1);
-      }
-      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, sbase + n - 1);
-      continue;
-    }
     if (__ballot_sync(0xffffffffu, c > 1) == 0) {
       // sparse slice (<= 1 position per lane): lanes store straight to consecutive slots,
       // which one warp store coalesces -- no staging, no scan
@@ -854,6 +838,22 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
         if (i < room) st_stream_u64(pos + gidx + i, sb + static_cast<uint64_t>(bit));
         ++i;
       }
+      continue;
+    }
+    if (tg == static_cast<uint32_t>(kWarpBytes)) {
+      // every start of the slice matches (periodic texts, e.g. 'a'^n): the positions are
+      // slice_base + 0..2047, written arithmetically with 16-byte stores
+      const uint64_t sbase = sb - lane * kSegBytes;
+      uint64_t* d = pos + gidx;
+      const uint32_t n = room < static_cast<uint64_t>(kWarpBytes) ? static_cast<uint32_t>(room) : kWarpBytes;
+      const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
+      if (lead && lane == 0) st_stream_u64(d, sbase);
+      const uint32_t npairs = (n - lead) >> 1;
+      for (uint32_t k = lane; k < npairs; k += 32) {
+        const uint32_t e = lead + 2 * k;
+        st_stream_u64x2(d + e, sbase + e, sbase + e + 1);
+      }
+      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, sbase + n - 1);
       continue;
     }
     write_slice(stage, pos + gidx, room, M, off, tg, sb - lane * kSegBytes, lane);
