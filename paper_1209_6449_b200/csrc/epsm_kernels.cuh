@@ -769,6 +769,21 @@ __device__ __forceinline__ void write_slice(uint16_t* stage, uint64_t* dst, uint
   }
 }
 
+// A slice where every start matches (e.g. 'a'^n): positions sbase + 0..2047, written
+// arithmetically with 16-byte stores.  Out of line: inlined into the flush loop it costs the
+// common sparse flushes registers and ~10%.
+__device__ __noinline__ void write_full_slice(uint64_t* d, uint64_t room, uint64_t sbase, uint32_t lane) {
+  const uint32_t n = room < static_cast<uint64_t>(kWarpBytes) ? static_cast<uint32_t>(room) : kWarpBytes;
+  const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
+  if (lead && lane == 0) st_stream_u64(d, sbase);
+  const uint32_t npairs = (n - lead) >> 1;
+  for (uint32_t k = lane; k < npairs; k += 32) {
+    const uint32_t e = lead + 2 * k;
+    st_stream_u64x2(d + e, sbase + e, sbase + e + 1);
+  }
+  if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, sbase + n - 1);
+}
+
 __device__ __forceinline__ uint32_t popc64(uint64_t v) {
   return __popc(static_cast<uint32_t>(v)) + __popc(static_cast<uint32_t>(v >> 32));
 }
@@ -840,20 +855,8 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
       }
       continue;
     }
-    if (tg == static_cast<uint32_t>(kWarpBytes)) {
-      // every start of the slice matches (periodic texts, e.g. 'a'^n): the positions are
-      // slice_base + 0..2047, written arithmetically with 16-byte stores
-      const uint64_t sbase = sb - lane * kSegBytes;
-      uint64_t* d = pos + gidx;
-      const uint32_t n = room < static_cast<uint64_t>(kWarpBytes) ? static_cast<uint32_t>(room) : kWarpBytes;
-      const uint32_t lead = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(d) >> 3) & 1u);
-      if (lead && lane == 0) st_stream_u64(d, sbase);
-      const uint32_t npairs = (n - lead) >> 1;
-      for (uint32_t k = lane; k < npairs; k += 32) {
-        const uint32_t e = lead + 2 * k;
-        st_stream_u64x2(d + e, sbase + e, sbase + e + 1);
-      }
-      if (((n - lead) & 1u) && lane == 0) st_stream_u64(d + n - 1, sbase + n - 1);
+    if (tg == static_cast<uint32_t>(kWarpBytes)) {   // every start matches (periodic texts)
+      write_full_slice(pos + gidx, room, sb - lane * kSegBytes, lane);
       continue;
     }
     write_slice(stage, pos + gidx, room, M, off, tg, sb - lane * kSegBytes, lane);
