@@ -29,10 +29,16 @@
  *  - stream is a cudaStream_t (NULL = the legacy default stream).  All device
  *    work is enqueued on it.  The *_async calls return without synchronising;
  *    the others end with one cudaStreamSynchronize(stream).
- *  - A plan owns a small device workspace (look-back status words, 8 bytes per
- *    16 KiB tile of text, and scratch).  One plan must not be used by two
- *    searches that may run concurrently (e.g. on two streams); use one plan
- *    per stream.  Plans are bound to the device of their first search.
+ *  - A plan holds the preprocessed pattern (a ~8 KiB device descriptor, uploaded
+ *    on its first search) and an 8-byte occ slot for the synchronous calls.  The
+ *    scan workspace (look-back status words, 8 bytes per 128 KiB chunk of text,
+ *    and parked match masks, 128 KiB per SM) belongs to the (device, stream) a
+ *    search is enqueued on, double-buffered by launch so that consecutive
+ *    searches on a stream overlap; it is allocated on first use and grows (with a
+ *    stream synchronisation) when a larger text needs it.  Calls on one stream
+ *    must come from one host thread at a time; the synchronous calls of one plan
+ *    must not run concurrently.  Plans are bound to the device of their first
+ *    search.
  *  - Maximum n: 2^38 bytes (256 GiB) per call.
  */
 #ifndef EPSM_H

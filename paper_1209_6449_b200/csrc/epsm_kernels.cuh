@@ -35,7 +35,6 @@
 //                          64-bit launch-tagged words), publish the inclusive prefix.  It
 //                          runs concurrently with the consumers through a 16-deep slot
 //                          queue; the consumers published the chunk's aggregate already.
-//                          (Sampled variants: it first builds the gram table.)
 //   report       eight chunks later each consumer warp turns ITS 4 slices of the parked
 //                chunk into positions slice_base + lane*64 + {r} (PAPER.md:431-441,
 //                Fig. 1 line 11), directly or staged in its shared-memory buffer and
@@ -257,23 +256,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Same, for waiters off the critical path (idle look-back warp, producer with a full ring):
-// back off with nanosleep between probes, so the waiting warp does not steal issue slots
-// from the consumer warps.
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_addr(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 // Blocking wait for an idle warp: try_wait with a suspend-time hint parks the warp in hardware
 // until the phase completes (no issue slots spent polling).
 __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
@@ -288,10 +270,6 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity
       "}\n" ::"r"(smem_addr(bar)),
       "r"(parity), "r"(1000000u)
       : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -610,12 +588,6 @@ __device__ __forceinline__ uint32_t verify_long(uint32_t r, uint64_t us, const K
   return keep;
 }
 
-__device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void named_barrier_arrive(uint32_t id, uint32_t count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
