@@ -10,7 +10,7 @@
  * EPSM's procedures (EPSMa/b, Sec. 3.2-3.3) filter with a packed
  * compare of alpha = 16 alignments per 128-bit word and then "naively check"
  * candidates; every entry point here returns exactly Occ(p, t).
- * Readings where the paper is silent are listed in DESIGN.md (R1-R13).
+ * Readings where the paper is silent are listed in DESIGN.md (R1-R16).
  *
  * Conventions shared by every call
  * --------------------------------
@@ -78,7 +78,7 @@ typedef void *epsm_stream_t;              /* a cudaStream_t     */
  */
 int epsm_plan(const uint8_t *pattern, uint32_t m, epsm_plan_t **out);
 
-/* epsm_plan_free -- release a plan and its device workspace.  NULL-safe.
+/* epsm_plan_free -- release a plan and its device memory.  NULL-safe.
  * Synchronises the plan's device before freeing device memory. */
 void epsm_plan_free(epsm_plan_t *plan);
 
@@ -119,10 +119,11 @@ int epsm_search_async(epsm_plan_t *plan, const uint8_t *d_text, uint64_t n,
  * paper's protocol: many patterns per text), as epsm_search_async
  * for each j: positions of plans[j] into d_pos[j][0 .. min(occ_j, caps[j])), occ_j
  * into the device uint64 d_occ[j] (d_occ: k contiguous, 8-byte aligned words).
- * d_pos may be NULL (or d_pos[j] NULL / caps NULL) to count only.  Consecutive
- * plans of equal m share one persistent launch (up to 40 per launch): the grid
- * streams the text once per search, back to back, without a launch boundary
- * between them.  Returns EPSM_OK or a negative error; does not synchronise.
+ * d_pos may be NULL (or d_pos[j] NULL / caps NULL) to count only.  The searches
+ * are grouped by kernel variant (pattern length and filter) and each group runs
+ * as persistent launches of up to 40 searches: the grid streams the text once
+ * per search, back to back, without a launch boundary between them.  Returns
+ * EPSM_OK or a negative error; does not synchronise.
  */
 int epsm_search_batch_async(epsm_plan_t *const *plans, uint32_t k,
                             const uint8_t *d_text, uint64_t n,
