@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--ms", default=",".join(map(str, MS)))
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--breakdown", action="store_true", help="per-(sigma, m) timing pass (stderr)")
+    ap.add_argument("--no-index", dest="index", action="store_false",
+                    help="no equality-mask index (every search scans the text)")
     ap.add_argument("--no-batch", dest="batch", action="store_false",
                     help="one launch per search (epsm_search_async) instead of the batch API")
     return ap.parse_args()
@@ -241,6 +243,17 @@ def run_epsm(args, world, rank, local):
         else:
             groups.append([j, j + 1])
     use_batch = args.batch
+    # equality-mask index (N = 1, batch mode): per text, the planes of the byte values its
+    # qualifying searches need, rebuilt inside every step right before that text's groups
+    # (its cost is part of the step); those searches stream their planes instead of the text
+    idx_vals, ixs = {}, {}
+    if use_batch and world == 1 and args.index:
+        for ti in range(len(texts)):
+            v = epsm.index_values([pl for tj, pl in jobs if tj == ti])
+            if v:
+                idx_vals[ti] = v
+                ixs[ti] = epsm.EqIndex()
+    uses_ix = [ti in ixs and len(pl.index_values()) > 0 for ti, pl in jobs]
     pool = []
     occ_loc = occ_buf                                         # N > 1: this rank's counts
     if use_batch and world > 1:
@@ -252,7 +265,7 @@ def run_epsm(args, world, rank, local):
         s_, spec_, n_total_, base_, owned_, t_ = texts[ti]
         plans_ = [pl for _, pl in jobs[j0:j1]]
         if world == 1:
-            epsm.search_batch_async(plans_, t_, occ_buf[j0:j1], outs=outs, stream=stream)
+            epsm.search_batch_async(plans_, t_, occ_buf[j0:j1], outs=outs, stream=stream, index=ixs.get(ti))
         else:
             # sharded batch: local scan of the owned starts (global positions), then ONE
             # all-gather of the group's counts -> global occ and this rank's output offsets;
@@ -261,9 +274,20 @@ def run_epsm(args, world, rank, local):
             occ_g, _off = sharding.exchange_batch_counts(occ_loc[j0:j1])
             occ_buf[j0:j1].copy_(occ_g)
 
-    if use_batch:
+    def build_index(ti):
+        ixs[ti].build_async(texts[ti][5], idx_vals[ti], stream=stream)
+
+    def run_groups(outs_of):
+        last = None
         for j0, j1 in groups:
-            batch_call(j0, j1, None)
+            ti = jobs[j0][0]
+            if ti != last and ti in ixs:
+                build_index(ti)
+            last = ti
+            batch_call(j0, j1, outs_of(j0, j1))
+
+    if use_batch:
+        run_groups(lambda j0, j1: None)
         torch.cuda.synchronize()
         pcap = int(occ_loc.max().item()) + 1
         pos_buf = None
@@ -272,8 +296,7 @@ def run_epsm(args, world, rank, local):
 
     def one_step(events=None):
         if use_batch and events is None:
-            for j0, j1 in groups:
-                batch_call(j0, j1, [pool[j % 80] for j in range(j0, j1)])
+            run_groups(lambda j0, j1: [pool[j % 80] for j in range(j0, j1)])
             return
         for j, (ti, pl) in enumerate(jobs):
             s, spec, n_total, base, owned, t = texts[ti]
@@ -317,11 +340,16 @@ def run_epsm(args, world, rank, local):
     ms_step = ms_total / args.steps
     value = n_text_step * args.steps / (ms_total * 1e-3) / 1e9
 
-    # roofline of the scan kernel (the only kernel in the region): algorithmic bytes =
-    # n + 8 * min(occ, cap) per launch; average launch duration = region time / launches
+    # roofline over the kernels of the region: algorithmic bytes = per text-path search
+    # n + 8 * min(occ, cap); per index-path search d * n / 8 (its planes) + 8 * min(occ, cap);
+    # per index build n + nv * n / 8 (text in, planes out); average launch duration = region
+    # time / launches
     occ = occ_loc.cpu().numpy().astype(np.int64)             # this rank's positions written
     local_bytes = [texts[ti][5].numel() for ti, _ in jobs]
-    alg_bytes = sum(nb + 8 * min(int(o), cap) for nb, o in zip(local_bytes, occ)) * args.steps
+    read_bytes = [nb * len(pl.index_values()) // 8 if ix else nb
+                  for nb, ix, (_, pl) in zip(local_bytes, uses_ix, jobs)]
+    build_bytes = sum(texts[ti][5].numel() * (1 + len(v) / 8) for ti, v in idx_vals.items())
+    alg_bytes = (sum(rb + 8 * min(int(o), cap) for rb, o in zip(read_bytes, occ)) + build_bytes) * args.steps
     kernel_ms = ms_total
     hbm_peak, peak_src = peaks()
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
@@ -339,21 +367,35 @@ def run_epsm(args, world, rank, local):
             else:
                 bgroups.append([key, j, j + 1])
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(bgroups))]
+        ib = {}
+        for ti in ixs:                   # index builds, timed on their own (m = 0 rows)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            build_index(ti)
+            e1.record(stream)
+            ib[ti] = (e0, e1)
         for gi, (key, j0, j1) in enumerate(bgroups):
             ev[2 * gi].record(stream)
             if use_batch:
-                epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[jobs[j0][0]][5], occ_buf[j0:j1],
-                                        outs=[pool[j % 80] for j in range(j0, j1)], stream=stream)
+                ti_ = jobs[j0][0]
+                epsm.search_batch_async([pl for _, pl in jobs[j0:j1]], texts[ti_][5], occ_buf[j0:j1],
+                                        outs=[pool[j % 80] for j in range(j0, j1)], stream=stream,
+                                        index=ixs.get(ti_))
             else:
                 for j in range(j0, j1):
                     ti, pl = jobs[j]
                     epsm.search_async(pl, texts[ti][5], pos_buf, occ_buf[j:j + 1], stream=stream)
             ev[2 * gi + 1].record(stream)
         torch.cuda.synchronize()
+        for ti, (e0, e1) in ib.items():
+            us = e0.elapsed_time(e1) * 1e3
+            nb = texts[ti][5].numel()
+            breakdown.append([texts[ti][0], 0, round(us, 2), round(nb / (us * 1e-6) / 1e9, 1),
+                              round(nb * (1 + len(idx_vals[ti]) / 8) / (us * 1e-6) / 1e9, 1)])
         for gi, ((s_, m), j0, j1) in enumerate(bgroups):
             d = ev[2 * gi].elapsed_time(ev[2 * gi + 1])
             c = j1 - j0
-            b_ = sum(local_bytes[j] + 8 * min(int(occ[j]), cap) for j in range(j0, j1))
+            b_ = sum(read_bytes[j] + 8 * min(int(occ[j]), cap) for j in range(j0, j1))
             us = d / c * 1e3
             breakdown.append([s_, m, round(us, 2), round(local_bytes[j0] / (us * 1e-6) / 1e9, 1),
                               round(b_ / c / (us * 1e-6) / 1e9, 1)])
@@ -373,14 +415,21 @@ def run_epsm(args, world, rank, local):
                    "searches_per_step": len(jobs), "text_bytes_per_step": n_text_step,
                    "l2": "no flush: every text (256 MiB) is larger than the 126 MB L2",
                    "parallelism": f"dp{world} over text shards" if world > 1 else "single GPU",
-                   "api": ("epsm_search_batch_async per (sigma, m) group" if world == 1 else
+                   "api": ("epsm_search_batch_async per (sigma, m) group"
+                           + (" + epsm_eqidx_build_async per text (equality-mask index, built inside "
+                              "every step)" if ixs else "") if world == 1 else
                            "epsm_search_range_batch_async + NCCL all-gather of counts per group; "
                            "positions kept sharded at their global offsets") if args.batch
                    else "epsm_search_async per search" if world == 1 else "epsm_search_sharded per search"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs, copy read+write)",
-                     "kernel": "epsm_scan_kernel (search), the only kernel in the timed region",
+                     "kernel": "epsm_scan_kernel (search: text and index variants)"
+                               + (" + epsm_eqidx_kernel (index builds)" if ixs else "")
+                               + ": the kernels of the timed region",
+                     "index": {"searches_per_step": int(sum(uses_ix)),
+                               "values_per_text": {str(texts[ti][0]): len(v) for ti, v in idx_vals.items()},
+                               "alg_bytes": "index search: d*n/8 planes + 8*occ; build: n + nv*n/8"},
                      "traffic_unit": "DRAM bytes per search (ncu, one search per launch)",
                      "per_search_ms": round(kernel_ms / (args.steps * len(jobs)), 5),
                      "alg_bytes_per_search": int(alg_bytes / (args.steps * len(jobs))),
@@ -394,7 +443,7 @@ def run_epsm(args, world, rank, local):
                       if breakdown else None),
     }
     if not args.no_e2e:
-        res["e2e"] = run_e2e(args, epsm, texts, pats, jobs, world, dev)
+        res["e2e"] = run_e2e(args, epsm, texts, pats, jobs, world, dev, idx_vals)
     if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_sample(args, texts, pats, ms)
     for _, pl in jobs:
@@ -402,7 +451,7 @@ def run_epsm(args, world, rank, local):
     return res
 
 
-def run_e2e(args, epsm, texts, pats, jobs, world, dev):
+def run_e2e(args, epsm, texts, pats, jobs, world, dev, idx_vals=None):
     """Same sweep through the public API with HOST buffers: every step, each text is copied
     host->device from pinned memory, every search's occ is read back and ALL its positions
     are copied device->host into pinned memory.  The searches run through the batch API in
@@ -431,6 +480,8 @@ def run_e2e(args, epsm, texts, pats, jobs, world, dev):
     host_pos = [torch.empty(cap, dtype=torch.int64).pin_memory() for _ in range(2)]
     occ_dev = [torch.zeros(SUB, dtype=torch.int64, device=dev) for _ in range(2)]
     occ_host = [torch.zeros(SUB, dtype=torch.int64).pin_memory() for _ in range(2)]
+    idx_vals = idx_vals or {}
+    e_ix = [epsm.EqIndex() for _ in range(2)] if idx_vals else None   # one per device text buffer
 
     def step():
         h2d = d2h = 0
@@ -442,13 +493,16 @@ def run_e2e(args, epsm, texts, pats, jobs, world, dev):
             dt = dev_texts[i % 2][: ht.numel()]
             dt.copy_(ht, non_blocking=True)           # H2D on the compute stream
             h2d += ht.numel()
+            ix = None
+            if ti in idx_vals:                        # the text's equality-mask index, on device
+                ix = e_ix[i % 2].build_async(dt, idx_vals[ti], stream=comp)
             for a in range(0, len(plans), SUB):
                 group = plans[a:a + SUB]
                 bs = sb % 2
                 if freed[bs] is not None:
                     comp.wait_event(freed[bs])        # its previous positions are copied out
                 epsm.search_batch_async(group, dt, occ_dev[bs][: len(group)], outs=outs[bs][: len(group)],
-                                        stream=comp)
+                                        stream=comp, index=ix)
                 occ_host[bs][: len(group)].copy_(occ_dev[bs][: len(group)], non_blocking=True)
                 done = torch.cuda.Event()
                 done.record(comp)
@@ -491,7 +545,8 @@ def run_e2e(args, epsm, texts, pats, jobs, world, dev):
     n_step = sum(texts[ti][2] for ti, _ in jobs)
     return {"value": round(n_step / dt_s / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt_s * 1e3, 2), "steps": args.e2e_steps,
-            "note": "public API (epsm_search_batch_async, sub-batches of 20) with pinned host text in and "
+            "note": "public API (epsm_eqidx_build_async per text, epsm_search_batch_async in sub-batches "
+                    "of 20) with pinned host text in and "
                     "every position copied out over PCIe on two copy streams, overlapped with compute"}
 
 

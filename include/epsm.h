@@ -62,6 +62,9 @@ extern "C" {
 #define EPSM_MAX_M_LONG 4096u /* long patterns (EPSMc block fingerprints)  */
 
 typedef struct epsm_plan_s epsm_plan_t;   /* opaque, host-owned */
+typedef struct epsm_eqidx_s epsm_eqidx_t; /* opaque, host-owned (equality-mask index) */
+#define EPSM_MAX_PLANES 32u  /* byte values one equality-mask index holds                  */
+#define EPSM_INDEX_MAX_D 8u  /* distinct pattern bytes a search over an index may have     */
 typedef void *epsm_stream_t;              /* a cudaStream_t     */
 
 /*
@@ -136,6 +139,58 @@ int epsm_search_batch_async(epsm_plan_t *const *plans, uint32_t k,
 int epsm_count_batch_async(epsm_plan_t *const *plans, uint32_t k,
                            const uint8_t *d_text, uint64_t n, uint64_t *d_occ,
                            epsm_stream_t stream);
+
+/*
+ * Equality-mask index of a text (EPSMa).  EPSMa compares a text
+ * block with the broadcast pattern bytes (wscmp) and combines the masks by
+ * shift-AND.  For a batch of searches over ONE text (the paper's protocol,
+ * PAPER.md:630-632) the masks depend only on (text, byte value), so the index
+ * computes them once: plane v holds bit i of word w = [t[64w + i] == v] (bits
+ * past n zero), nv planes of (ceil(n / 32768) * 512 + 2) uint64 words in device
+ * memory owned by the index.  A search whose distinct pattern bytes are all in
+ * the index and that qualifies (epsm_plan_index_values > 0) then streams only
+ * its d planes (d/8 bytes per text byte) and runs the shift-AND on them;
+ * results are identical to the text path.
+ *
+ * epsm_eqidx_create -- an empty index (no device memory yet).  Returns EPSM_OK,
+ *   EPSM_EINVAL (NULL out) or EPSM_ENOMEM.
+ * epsm_eqidx_free -- release the index and its planes (synchronises the device
+ *   first).  NULL-safe.
+ * epsm_eqidx_build_async -- (re)build the planes of d_text[0..n-1] for the
+ *   distinct byte values values[0..nv-1] (1 <= nv <= EPSM_MAX_PLANES) on stream
+ *   (ordered before later work on that stream).  d_text must be 16-byte aligned
+ *   (EPSM_EALIGN otherwise).  The index remembers (d_text, n): searches name the
+ *   same text.  Growing the planes re-allocates (synchronises the stream).
+ *   Returns EPSM_OK or EPSM_EINVAL (NULL, nv out of range, duplicate values,
+ *   n > 2^38), EPSM_EALIGN, EPSM_ENOMEM, EPSM_ECUDA.
+ * epsm_eqidx_values -- the values the index holds: writes up to 32 bytes into
+ *   out_values and returns nv (0 before the first build).
+ */
+int epsm_eqidx_create(epsm_eqidx_t **out);
+void epsm_eqidx_free(epsm_eqidx_t *index);
+int epsm_eqidx_build_async(epsm_eqidx_t *index, const uint8_t *d_text, uint64_t n,
+                           const uint8_t *values, uint32_t nv, epsm_stream_t stream);
+int epsm_eqidx_values(const epsm_eqidx_t *index, uint8_t *out_values);
+
+/* epsm_plan_index_values -- the byte values a search with this plan would read
+ * from an index: writes its d <= EPSM_INDEX_MAX_D distinct pattern bytes (in order
+ * of first occurrence) into out_values and returns d, or returns 0 if the plan
+ * never runs over an index (m > 16, more than 4 distinct bytes at 9 <= m <= 16,
+ * or more than EPSM_INDEX_MAX_D; there the text kernels are faster). */
+int epsm_plan_index_values(const epsm_plan_t *plan, uint8_t *out_values);
+
+/*
+ * epsm_search_batch_index_async -- as epsm_search_batch_async over d_text[0..n-1]
+ * (which must be the text `index` was last built over: same pointer and n,
+ * EPSM_EINVAL otherwise), with every search that qualifies (see above) run over
+ * the index's planes; the others take the text kernels.  index may be NULL
+ * (then identical to epsm_search_batch_async).  Does not synchronise.
+ */
+int epsm_search_batch_index_async(epsm_plan_t *const *plans, uint32_t k,
+                                  const epsm_eqidx_t *index,
+                                  const uint8_t *d_text, uint64_t n,
+                                  uint64_t *const *d_pos, const uint64_t *caps,
+                                  uint64_t *d_occ, epsm_stream_t stream);
 
 /*
  * epsm_search_range_batch_async -- the local step of a sharded batch: as

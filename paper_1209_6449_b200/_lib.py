@@ -72,6 +72,18 @@ _lib.epsm_version.argtypes = []
 _lib.epsm_version.restype = ctypes.c_int
 _lib.epsm_debug_trace.argtypes = [_vp, _u64]
 _lib.epsm_debug_trace.restype = _i64
+_lib.epsm_eqidx_create.argtypes = [ctypes.POINTER(_vp)]
+_lib.epsm_eqidx_create.restype = ctypes.c_int
+_lib.epsm_eqidx_free.argtypes = [_vp]
+_lib.epsm_eqidx_free.restype = None
+_lib.epsm_eqidx_build_async.argtypes = [_vp, _vp, _u64, _vp, ctypes.c_uint32, _vp]
+_lib.epsm_eqidx_build_async.restype = ctypes.c_int
+_lib.epsm_eqidx_values.argtypes = [_vp, _vp]
+_lib.epsm_eqidx_values.restype = ctypes.c_int
+_lib.epsm_plan_index_values.argtypes = [_vp, _vp]
+_lib.epsm_plan_index_values.restype = ctypes.c_int
+_lib.epsm_search_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_search_batch_index_async.restype = ctypes.c_int
 
 EXPORTED_SYMBOLS = (
     "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
@@ -79,7 +91,11 @@ EXPORTED_SYMBOLS = (
     "epsm_search_host", "epsm_search_sharded",
     "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
     "epsm_version", "epsm_debug_trace",
+    "epsm_eqidx_create", "epsm_eqidx_free", "epsm_eqidx_build_async", "epsm_eqidx_values",
+    "epsm_search_batch_index_async", "epsm_plan_index_values",
 )
+MAX_PLANES = 32
+INDEX_MAX_D = 8
 
 
 class EpsmError(RuntimeError):
@@ -138,6 +154,12 @@ class Plan:
     @property
     def m(self) -> int:
         return len(self.pattern)
+
+    def index_values(self) -> bytes:
+        """epsm_plan_index_values: the bytes this search reads from an index (b"" if it never
+        runs over one)."""
+        buf = ctypes.create_string_buffer(8)
+        return buf.raw[:_lib.epsm_plan_index_values(self.handle, buf)]
 
     @property
     def handle(self):
@@ -276,17 +298,94 @@ def _batch_args(plans, text, occ_out, outs, caps):
     return plans, k, hp, pos_arr, caps_arr
 
 
+class EqIndex:
+    """epsm_eqidx_*: the equality-mask planes of one text for a set of byte values
+    (EPSMa's wscmp masks, computed once and shared by a batch)."""
+
+    def __init__(self):
+        h = _vp()
+        _check(_lib.epsm_eqidx_create(ctypes.byref(h)), "epsm_eqidx_create")
+        self._h = h
+        self._text = None
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("index is closed")
+        return self._h
+
+    def build_async(self, text: torch.Tensor, values, stream=None) -> "EqIndex":
+        """(Re)build the planes of `text` for the distinct byte values `values` on stream."""
+        _check_text(text)
+        vals = bytes(_pattern_bytes(values))
+        buf = ctypes.create_string_buffer(vals, max(len(vals), 1))
+        _check(_lib.epsm_eqidx_build_async(self.handle, text.data_ptr(), text.numel(), buf, len(vals),
+                                           _stream_handle(stream, text.device)), "epsm_eqidx_build_async")
+        self._text = text            # keep the text alive while the index refers to it
+        return self
+
+    @property
+    def values(self) -> bytes:
+        out = ctypes.create_string_buffer(MAX_PLANES)
+        k = _lib.epsm_eqidx_values(self.handle, out)
+        return out.raw[:k]
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.epsm_eqidx_free(self._h)
+            self._h = None
+        self._text = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def eq_index(text: torch.Tensor, values, stream=None) -> EqIndex:
+    """An EqIndex of `text` for `values` (built asynchronously on stream)."""
+    return EqIndex().build_async(text, values, stream=stream)
+
+
+def index_values(patterns, limit: int = MAX_PLANES) -> bytes:
+    """Byte values an index needs for the searches among `patterns` that would run over one
+    (epsm_plan_index_values), in first-seen order; empty if more than `limit` values."""
+    seen = []
+    buf = ctypes.create_string_buffer(INDEX_MAX_D)
+    for p in patterns:
+        pl = p if isinstance(p, Plan) else Plan(p)
+        d = _lib.epsm_plan_index_values(pl.handle, buf)
+        for v in buf.raw[:d]:
+            if v not in seen:
+                seen.append(v)
+    return bytes(seen) if len(seen) <= limit else b""
+
+
 def search_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, outs=None, caps=None,
-                       stream=None) -> None:
+                       stream=None, index: EqIndex | None = None) -> None:
     """Enqueue len(plans) searches over one text (one persistent launch per run of equal m).
 
     occ_out: CUDA int64 tensor with >= len(plans) elements (occ of search j -> occ_out[j]).
     outs: None (count only) or a sequence of CUDA int64 tensors / None, one per plan;
     caps: optional sequence of capacities (default: each out's numel).
+    index: an EqIndex built over this text: qualifying searches stream its planes.
     """
     if len(plans) == 0:
         return
     plans, k, hp, pos_arr, caps_arr = _batch_args(plans, text, occ_out, outs, caps)
+    if index is not None:
+        _check(_lib.epsm_search_batch_index_async(hp, k, index.handle, text.data_ptr(), text.numel(), pos_arr,
+                                                  caps_arr, occ_out.data_ptr(),
+                                                  _stream_handle(stream, text.device)),
+               "epsm_search_batch_index_async")
+        return
     _check(_lib.epsm_search_batch_async(hp, k, text.data_ptr(), text.numel(), pos_arr, caps_arr,
                                         occ_out.data_ptr(), _stream_handle(stream, text.device)),
            "epsm_search_batch_async")

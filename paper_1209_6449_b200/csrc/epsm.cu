@@ -153,6 +153,7 @@ void build_gram_table(const uint8_t* pattern, int sk, int sq, uint32_t* tab) {
 KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
   if (sk == epsm::kEqMode) return pick<4, 4, 1, epsm::kEqMode, 0>(search);   // EPSMa, <= 2 values
+  if (sk == epsm::kPlaneMode) return pick<4, 4, 1, epsm::kPlaneMode, 0>(search);   // EPSMa, index
   if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
   if (sk == 4 && sq == 12) {
     if (m == 16) return pick<4, 4, 4, 4, 12>(search);
@@ -380,7 +381,7 @@ static int ensure_plan_device(epsm_plan_t* plan, cudaStream_t s) {
 // d_text[0..nbytes-1]; starts [0, nstarts) are reported (nstarts <= nbytes - m + 1), each
 // shifted by `base`.  One persistent grid streams the chunks of all k searches in turn.
 int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
-                     uint64_t base, bool search, cudaStream_t s) {
+                     uint64_t base, bool search, cudaStream_t s, const epsm_eqidx_t* index) {
   if (k == 0) return EPSM_OK;
   if (k > static_cast<uint32_t>(epsm::kMaxJobs)) {
     epsm_set_error("%u searches in one launch (max %d)", k, epsm::kMaxJobs);
@@ -407,12 +408,36 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   P.movemask_mul = 0x00204081u;
   P.m = plan0->m;
   P.njobs = k;
-  P.desc_bytes = plan0->sk > 0 ? static_cast<uint32_t>(sizeof(epsm::JobDesc)) : epsm::kJobHeader;
+  P.desc_bytes = (plan0->sk > 0 && !index) ? static_cast<uint32_t>(sizeof(epsm::JobDesc)) : epsm::kJobHeader;
+  if (index) {
+    if (mis != 0 || base != 0 || index->text != d_text || index->n != nbytes) {
+      epsm_set_error("index searches need the aligned text the index was built over");
+      return EPSM_EINVAL;
+    }
+    P.planes = index->d_planes;
+    P.pstride = index->pstride;
+  }
   for (uint32_t j = 0; j < k; ++j) {
     epsm_plan_t* pl = jobs[j].plan;
-    if (pl->m != plan0->m || pl->sk != plan0->sk || pl->device != plan0->device) {
+    if (pl->m != plan0->m || (!index && pl->sk != plan0->sk) || pl->device != plan0->device) {
       epsm_set_error("searches of one launch need the same pattern length, filter and device");
       return EPSM_EINVAL;
+    }
+    if (index) {
+      const epsm::JobDesc& D = *pl->h_desc;
+      if (D.np == 0 || pl->m > EPSM_MAX_M) {
+        epsm_set_error("pattern does not qualify for the index (m <= 32, <= 8 distinct bytes)");
+        return EPSM_EINVAL;
+      }
+      P.jobs[j].np = D.np;
+      for (uint32_t q = 0; q < D.np; ++q) {
+        const int pid = index->plane_of[D.pval[q]];
+        if (pid < 0) {
+          epsm_set_error("byte %u of the pattern is not in the index", static_cast<unsigned>(D.pval[q]));
+          return EPSM_EINVAL;
+        }
+        P.jobs[j].pid[q] = static_cast<uint8_t>(pid);
+      }
     }
     int rc = ensure_plan_device(pl, s);
     if (rc) return rc;
@@ -467,7 +492,8 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     return v && v[0] ? static_cast<uint32_t>(strtoul(v, nullptr, 0)) : 0u;
   }();
   P.flags = env_flags;
-  KernelFn fn = kernel_for(plan0->m, plan0->sk, plan0->sq, search);
+  KernelFn fn = index ? kernel_for(plan0->m, epsm::kPlaneMode, 0, search)
+                     : kernel_for(plan0->m, plan0->sk, plan0->sq, search);
   const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;
@@ -603,6 +629,43 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
       D.eqsel[0] = D.eqsel[1] = 0;
     }
   }
+  // the same shift-AND over an equality-mask index: up to kMaxPlaneSlots distinct bytes in
+  // order of first occurrence, and the positions holding each (m <= 32) as packed shift lists
+  if (m <= EPSM_MAX_M) {
+    constexpr uint32_t kSlots = static_cast<uint32_t>(epsm::kMaxPlaneSlots);
+    uint32_t d = 0, sel[kSlots] = {};
+    for (uint32_t i = 0; i < m && d <= kSlots; ++i) {
+      uint32_t v = 0;
+      while (v < d && D.pval[v] != pattern[i]) ++v;
+      if (v == d) {
+        if (d < kSlots) D.pval[d] = pattern[i];
+        ++d;
+      }
+      if (v < kSlots) sel[v] |= 1u << i;
+    }
+    if (d <= kSlots) {
+      D.np = d;
+      uint32_t w = 0;
+      for (uint32_t v = 0; v < d; ++v) {
+        uint8_t list[32 + 3];
+        uint32_t c = 0;
+        for (uint32_t i = 0; i < m; ++i)
+          if ((sel[v] >> i) & 1u) list[c++] = static_cast<uint8_t>(i);
+        while (c % 4) list[c] = list[0], ++c;            // pad: repeat the first position
+        D.pw0[v] = static_cast<uint8_t>(w);
+        D.pwn[v] = static_cast<uint8_t>(c / 4);
+        for (uint32_t q = 0; q < c / 4; ++q, ++w)
+          D.plist[w] = list[4 * q] | (list[4 * q + 1] << 8) | (list[4 * q + 2] << 16) |
+                       (static_cast<uint32_t>(list[4 * q + 3]) << 24);
+      }
+    }
+  }
+  if (D.np == 0) {
+    std::memset(D.plist, 0, sizeof(D.plist));
+    std::memset(D.pw0, 0, sizeof(D.pw0));
+    std::memset(D.pwn, 0, sizeof(D.pwn));
+    std::memset(D.pval, 0, sizeof(D.pval));
+  }
   sampled_geometry(m, p->pattern, &p->sk, &p->sq);
   if (p->sk > 0) build_gram_table(p->pattern, p->sk, p->sq, D.gram_tab);
   p->device = -1;
@@ -678,10 +741,51 @@ int epsm_search_async(epsm_plan_t* plan, const uint8_t* d_text, uint64_t n, uint
                      reinterpret_cast<unsigned long long*>(d_occ), true, static_cast<cudaStream_t>(stream));
 }
 
+// Largest number of distinct pattern bytes a search runs over an index with (EPSM_INDEX_MAX_D
+// overrides, 0 disables; A/B timing).  Speed only: both paths are exact.
+static uint32_t index_max_d() {
+  static const uint32_t v = [] {
+    const char* e = getenv("EPSM_INDEX_MAX_D");
+    return e && e[0] ? static_cast<uint32_t>(strtoul(e, nullptr, 0)) : static_cast<uint32_t>(EPSM_INDEX_MAX_D);
+  }();
+  return v;
+}
+
+// Does plans' search run over the index?  Its distinct bytes must all be in the index.  Speed
+// rule (B200, 256 MiB texts, us per search text -> index): the shift-AND over planes wins for
+// m <= 8 at every alphabet the index covers (sigma=2 m=8 137 -> 80, sigma=16 m=4 63 -> 52,
+// sigma=32 m=8 61 -> 56) and for m <= 16 with <= 4 distinct bytes (sigma=2 m=16 68 -> 52);
+// beyond that the text kernels are at the HBM roofline already (m=32: 38 us) and the
+// per-position shifts cost more than the sampled filter.
+static bool index_worthwhile(const epsm_plan_t* pl) {
+  const epsm::JobDesc& D = *pl->h_desc;
+  if (pl->m > EPSM_MAX_M || D.np == 0 || D.np > index_max_d()) return false;
+  return pl->m <= 8 || (pl->m <= 16 && D.np <= 4);
+}
+
+static bool use_index(const epsm_plan_t* pl, const epsm_eqidx_t* ix) {
+  if (!ix || !index_worthwhile(pl) || (pl->device >= 0 && pl->device != ix->device)) return false;
+  const epsm::JobDesc& D = *pl->h_desc;
+  for (uint32_t q = 0; q < D.np; ++q)
+    if (ix->plane_of[D.pval[q]] < 0) return false;
+  return true;
+}
+
+int epsm_plan_index_values(const epsm_plan_t* plan, uint8_t* out_values) {
+  if (!plan || !index_worthwhile(plan)) return 0;
+  const epsm::JobDesc& D = *plan->h_desc;
+  if (out_values) std::memcpy(out_values, D.pval, D.np);
+  return static_cast<int>(D.np);
+}
+
 static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n, uint64_t owned_len,
                         uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
-                        epsm_stream_t stream) {
+                        epsm_stream_t stream, const epsm_eqidx_t* index = nullptr) {
   if (k == 0) return EPSM_OK;
+  if (index && (index->text != d_text || index->n != n)) {
+    epsm_set_error("the index was built over another text (pointer or length differ)");
+    return EPSM_EINVAL;
+  }
   if (!plans || !d_occ || (!d_text && n > 0)) {
     epsm_set_error("epsm_search_(range_)batch_async: NULL plans, d_occ or text");
     return EPSM_EINVAL;
@@ -711,28 +815,32 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
     if (rc) return rc;
     jobs[j] = epsm_job{plans[j], cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + j)};
   }
-  // searches are independent: group them by kernel variant (m, filter), keeping their order
-  // within a group, and launch each group in runs of at most kMaxJobs
+  // searches are independent: group them by kernel variant (m, filter or index), keeping
+  // their order within a group, and launch each group in runs of at most kMaxJobs
+  std::vector<int> variant(k);
+  for (uint32_t j = 0; j < k; ++j) variant[j] = use_index(plans[j], index) ? epsm::kPlaneMode : plans[j]->sk;
   std::vector<uint32_t> order(k);
   for (uint32_t j = 0; j < k; ++j) order[j] = j;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
     if (plans[x]->m != plans[y]->m) return plans[x]->m < plans[y]->m;
-    return plans[x]->sk < plans[y]->sk;
+    return variant[x] < variant[y];
   });
   std::vector<epsm_job> run;
   uint32_t a = 0;
   while (a < k) {
     uint32_t b = a + 1;
     const epsm_plan_t* pa = plans[order[a]];
+    const int va = variant[order[a]];
     while (b < k && b - a < static_cast<uint32_t>(epsm::kMaxJobs) && plans[order[b]]->m == pa->m &&
-           plans[order[b]]->sk == pa->sk)
+           variant[order[b]] == va)
       ++b;
     run.clear();
     for (uint32_t i = a; i < b; ++i) run.push_back(jobs[order[i]]);
     const uint32_t m = pa->m;
     uint64_t ns = n >= m ? n - m + 1 : 0;
     if (owned_len < ns) ns = owned_len;
-    int rc = epsm_launch_jobs(run.data(), b - a, d_text, n, ns, base, search, s);
+    int rc = epsm_launch_jobs(run.data(), b - a, d_text, n, ns, base, search, s,
+                              va == epsm::kPlaneMode ? index : nullptr);
     if (rc) return rc;
     a = b;
   }
@@ -753,6 +861,130 @@ int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t
 int epsm_count_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
                            uint64_t* d_occ, epsm_stream_t stream) {
   return batch_common(plans, k, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream);
+}
+
+int epsm_search_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,
+                                  const uint8_t* d_text, uint64_t n, uint64_t* const* d_pos, const uint64_t* caps,
+                                  uint64_t* d_occ, epsm_stream_t stream) {
+  return batch_common(plans, k, d_text, n, n, 0, d_pos, caps, d_occ, true, stream, index);
+}
+
+// ---- equality-mask index (EPSMa's wscmp masks of a whole text)
+
+int epsm_eqidx_create(epsm_eqidx_t** out) {
+  if (!out) {
+    epsm_set_error("epsm_eqidx_create: NULL out");
+    return EPSM_EINVAL;
+  }
+  epsm_eqidx_t* ix = new (std::nothrow) epsm_eqidx_t();
+  if (!ix) return EPSM_ENOMEM;
+  for (int v = 0; v < 256; ++v) ix->plane_of[v] = -1;
+  *out = ix;
+  return EPSM_OK;
+}
+
+void epsm_eqidx_free(epsm_eqidx_t* ix) {
+  if (!ix) return;
+  if (ix->d_planes) {
+    cudaSetDevice(ix->device);
+    cudaDeviceSynchronize();
+    cudaFree(ix->d_planes);
+  }
+  delete ix;
+}
+
+int epsm_eqidx_values(const epsm_eqidx_t* ix, uint8_t* out_values) {
+  if (!ix) return 0;
+  if (out_values) std::memcpy(out_values, ix->vals, ix->nv);
+  return static_cast<int>(ix->nv);
+}
+
+int epsm_eqidx_build_async(epsm_eqidx_t* ix, const uint8_t* d_text, uint64_t n, const uint8_t* values, uint32_t nv,
+                           epsm_stream_t stream) {
+  if (!ix || !values || (!d_text && n > 0) || nv == 0 || nv > EPSM_MAX_PLANES) {
+    epsm_set_error("epsm_eqidx_build_async: NULL argument or nv = %u not in [1, %u]", nv, EPSM_MAX_PLANES);
+    return EPSM_EINVAL;
+  }
+  if (n > (1ull << 38)) {
+    epsm_set_error("n = %llu exceeds 2^38", (unsigned long long)n);
+    return EPSM_EINVAL;
+  }
+  if (reinterpret_cast<uintptr_t>(d_text) & 15u) {
+    epsm_set_error("epsm_eqidx_build_async: d_text must be 16-byte aligned");
+    return EPSM_EALIGN;
+  }
+  bool seen[256] = {};
+  for (uint32_t q = 0; q < nv; ++q) {
+    if (seen[values[q]]) {
+      epsm_set_error("epsm_eqidx_build_async: value %u listed twice", static_cast<unsigned>(values[q]));
+      return EPSM_EINVAL;
+    }
+    seen[values[q]] = true;
+  }
+  int dev = -1;
+  cudaPointerAttributes attr;
+  cudaError_t e = d_text ? cudaPointerGetAttributes(&attr, d_text) : cudaErrorInvalidValue;
+  if (e == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+    dev = attr.device;
+  } else {
+    cudaGetLastError();
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaGetDevice");
+  }
+  e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaSetDevice");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t tiles = (n + epsm::kTile - 1) / epsm::kTile;
+  const uint64_t pstride = tiles * epsm::kPlaneWordsPerTile + 2;   // + the last tile's halo word
+  const uint64_t words = pstride * nv;
+  if (ix->d_planes && (ix->device != dev || words > ix->cap_words)) {
+    cudaStreamSynchronize(s);
+    cudaSetDevice(ix->device);
+    cudaDeviceSynchronize();
+    cudaFree(ix->d_planes);
+    cudaSetDevice(dev);
+    ix->d_planes = nullptr;
+    ix->cap_words = 0;
+  }
+  if (!ix->d_planes) {
+    e = cudaMalloc(&ix->d_planes, words * sizeof(uint64_t));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ix->d_planes = nullptr;
+      epsm_set_error("cudaMalloc(%llu bytes) for the index planes failed", (unsigned long long)(words * 8));
+      return EPSM_ENOMEM;
+    }
+    ix->cap_words = words;
+  }
+  ix->device = dev;
+  ix->text = d_text;
+  ix->n = n;
+  ix->nv = nv;
+  ix->pstride = pstride;
+  for (int v = 0; v < 256; ++v) ix->plane_of[v] = -1;
+  epsm::IdxParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.text = d_text;
+  P.n = n;
+  P.planes = ix->d_planes;
+  P.pstride = pstride;
+  P.nv = nv;
+  for (uint32_t q = 0; q < nv; ++q) {
+    ix->vals[q] = values[q];
+    ix->plane_of[values[q]] = static_cast<int16_t>(q);
+    P.vb[q] = 0x01010101u * values[q];
+  }
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  const uint64_t want = (pstride + 255) / 256;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+  const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+  epsm::epsm_eqidx_kernel<<<grid, 256, 0, s>>>(P);
+  epsm_count_launch();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_eqidx_kernel launch");
+  return EPSM_OK;
 }
 
 int epsm_search_range_async(epsm_plan_t* plan, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,

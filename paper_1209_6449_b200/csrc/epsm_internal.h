@@ -72,5 +72,19 @@ struct epsm_job {
   uint64_t cap;
   unsigned long long* d_occ;
 };
+// index: run the searches over its equality-mask planes (every plan qualifies), else the text
 int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
-                     uint64_t base, bool search, cudaStream_t s);
+                     uint64_t base, bool search, cudaStream_t s, const epsm_eqidx_t* index = nullptr);
+
+// Equality-mask index of one text (epsm_eqidx_build_async).
+struct epsm_eqidx_s {
+  int device = -1;
+  const uint8_t* text = nullptr;     // the text the planes were built over
+  uint64_t n = 0;
+  uint32_t nv = 0;
+  uint8_t vals[EPSM_MAX_PLANES] = {};
+  int16_t plane_of[256] = {};        // plane of a byte value, -1 if absent
+  uint64_t* d_planes = nullptr;      // nv planes of pstride words
+  uint64_t pstride = 0;
+  uint64_t cap_words = 0;            // allocated words
+};

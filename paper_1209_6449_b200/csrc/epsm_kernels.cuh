@@ -54,7 +54,14 @@ namespace epsm {
 constexpr int kUnitBytes = 16;                                   // alpha
 constexpr int kTile = 32768;                                     // bytes per TMA stage
 constexpr int kHalo = 32;                                        // >= m-1, multiple of 16
-constexpr int kStageBytes = kTile + 64;                          // tile + halo + verify slack
+constexpr int kStageBytes = kTile + 128;                         // tile + halo + verify slack
+// Equality-mask index (planes): plane v of a text holds bit i of word w = [t[64w + i] == v].
+// A stage then holds, per plane of the search, the tile's 512 words + the next word (the halo
+// of windows crossing the tile), copied as 4112 bytes (16-byte multiple).
+constexpr int kPlaneWordsPerTile = kTile / 64;                   // 512
+constexpr int kPlaneStride = kTile / 8 + 16;                     // bytes per plane in a stage
+constexpr int kMaxPlaneSlots = 8;                                // planes per search (distinct bytes)
+static_assert(kMaxPlaneSlots * kPlaneStride <= kStageBytes, "planes of a stage");
 constexpr int kStagesSearch = 5;
 constexpr int kStagesCount = 6;
 constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
@@ -114,10 +121,22 @@ struct __align__(16) JobDesc {
   uint32_t eqsel[2];            // bit i: p_i == value_v
   uint32_t eqd;                 // number of distinct bytes (1 or 2)
   uint32_t eqpad[3];
+  // the same shift-AND over a text's equality-mask index (planes built once per text, shared
+  // by every search of a batch): the pattern's distinct bytes (m <= 32, at most 8) in order
+  // of first occurrence, and for each the positions i holding it as shift amounts, four per
+  // word (byte b of plist[pw0[k] + q]), each plane's list padded to a multiple of four by
+  // repeating its first position (AND is idempotent)
+  uint32_t plist[16];
+  uint8_t pw0[kMaxPlaneSlots];  // first word of plane k's list
+  uint8_t pwn[kMaxPlaneSlots];  // words of plane k's list
+  uint8_t pval[kMaxPlaneSlots]; // the byte value of plane k
+  uint32_t np;                  // distinct bytes (0: more than kMaxPlaneSlots or m > 32)
+  uint32_t ppad[5];
   uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
 };
-constexpr uint32_t kJobHeader = 160;                              // bytes before gram_tab
+constexpr uint32_t kJobHeader = 272;                              // bytes before gram_tab
 constexpr int kEqMode = -1;                                       // SK value of the equality variant
+constexpr int kPlaneMode = -2;                                    // SK value of the index variant
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
 // One search of a launch: its preprocessing and its outputs.
@@ -127,6 +146,9 @@ struct JobRef {
   uint64_t* pos;                // output positions (search)
   uint64_t cap;                 // capacity of pos
   unsigned long long* occ;      // device occ
+  uint8_t pid[kMaxPlaneSlots];  // index variant: plane of the search's k-th distinct byte
+  uint32_t np;                  // index variant: planes streamed per tile
+  uint32_t pad;
 };
 constexpr int kMaxJobs = 40;                                      // searches per launch
 
@@ -156,6 +178,8 @@ struct KParams {
   unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
   unsigned long long* exit_ctr; // CTAs of all launches on this workspace parity that have exited
   unsigned long long exit_expect;   // value meaning "launch L-2 (same parity) has retired"
+  const uint64_t* planes;       // index variant: plane v at planes + v * pstride (u64 words)
+  uint64_t pstride;
   JobRef jobs[kMaxJobs];
 };
 
@@ -950,12 +974,23 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
         const uint32_t bulk = static_cast<uint32_t>((end & ~15ull) - base);
         const uint32_t tail = static_cast<uint32_t>(end - base) - bulk;   // < 16 bytes
-        if (lane < tail) S.ring[stage][bulk + lane] = P.text[base + bulk + lane];
+        if constexpr (SK != kPlaneMode) {
+          if (lane < tail) S.ring[stage][bulk + lane] = P.text[base + bulk + lane];
+        }
         __syncwarp();
         if (lane == 0) {
           S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
           S.info2[stage] = static_cast<uint32_t>(cur) | (jslot << 31);
-          if (bulk) {
+          if constexpr (SK == kPlaneMode) {
+            // the tile's words of the search's planes (padded: always whole)
+            const JobRef& J = P.jobs[job];
+            mbar_arrive_expect_tx(&S.full[stage], J.np * kPlaneStride);
+            // (no evict-first hint: the next searches of the batch read the same planes)
+            for (uint32_t k = 0; k < J.np; ++k)
+              bulk_g2s_plain(S.ring[stage] + k * kPlaneStride,
+                             P.planes + J.pid[k] * P.pstride + static_cast<uint64_t>(t) * kPlaneWordsPerTile,
+                             kPlaneStride, &S.full[stage]);
+          } else if (bulk) {
             mbar_arrive_expect_tx(&S.full[stage], bulk);
             bulk_g2s(S.ring[stage], P.text + base, bulk, &S.full[stage], policy);
           } else {
@@ -993,7 +1028,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       cur = __shfl_sync(0xffffffffu, nxt, 0);
       after = __shfl_sync(0xffffffffu, after, 0);
-      if (P.flags & 2u) prefetch_l2(after);
+      if (SK != kPlaneMode && (P.flags & 2u)) prefetch_l2(after);
     }
   } else if (warp == 1) {
     // ================================================================ look-back
@@ -1177,6 +1212,43 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           Meq &= rm;
         }
         slow = __any_sync(0xffffffffu, Meq != 0ull);
+      } else if constexpr (SK == kPlaneMode) {
+        // ---- EPSMa's shift-AND over the text's equality-mask index: the
+        // masks E_v of the lane's 64 starts (+ the next 64) are read, not computed --
+        // r = AND_i (E_{p_i} >> i), exact, no candidates, no check
+        const uint32_t wi = cw * 32u + lane;                 // the lane's word in each plane tile
+        uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;
+        const uint32_t np = JD->np;
+#pragma unroll
+        for (int k = 0; k < kMaxPlaneSlots; ++k) {
+          if (k >= static_cast<int>(np)) break;              // warp-uniform
+          const uint2* pl = reinterpret_cast<const uint2*>(ts + k * kPlaneStride);
+          const uint2 e = pl[wi], h = pl[wi + 1];            // starts 0..63, 64..127
+          const uint32_t w0 = JD->pw0[k], wn = JD->pwn[k];
+          bool live = true;
+          for (uint32_t q = 0; q < wn; ++q) {
+            // four positions i with p_i == value of plane k (shift amounts: the funnel shift
+            // uses the low 5 bits, so the packed word is shifted, not masked; no bit scans)
+            const uint32_t sw = JD->plist[w0 + q];
+            rl &= __funnelshift_r(e.x, e.y, sw) & __funnelshift_r(e.x, e.y, sw >> 8) &
+                  __funnelshift_r(e.x, e.y, sw >> 16) & __funnelshift_r(e.x, e.y, sw >> 24);
+            rh &= __funnelshift_r(e.y, h.x, sw) & __funnelshift_r(e.y, h.x, sw >> 8) &
+                  __funnelshift_r(e.y, h.x, sw >> 16) & __funnelshift_r(e.y, h.x, sw >> 24);
+            // no start of the warp's slice survives: the rest of the AND cannot revive one
+            live = __any_sync(0xffffffffu, (rl | rh) != 0u);
+            if (!live) break;
+          }
+          if (!live) break;
+        }
+        Meq = (static_cast<uint64_t>(rh) << 32) | rl;
+        if (!interior) {
+          uint64_t rm = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            rm |= static_cast<uint64_t>(range_mask(tbase + seg_off + 16u * u, P.s_lo, P.s_hi)) << (16 * u);
+          Meq &= rm;
+        }
+        slow = __any_sync(0xffffffffu, Meq != 0ull);
       } else if constexpr (SK > 0) {
         // ---- sampled filter (EPSMc, Fig. 1 lines 7-12): the q-gram at unit
         // offset SK*(g+1) is fingerprinted and looked up in the pattern's gram table, which
@@ -1307,7 +1379,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (slow) {
         // the lane's 64 starts as one mask: bit 16u + j = start seg_off + 16u + j
         uint64_t M = 0;
-        if constexpr (SK == kEqMode) {
+        if constexpr (SK == kEqMode || SK == kPlaneMode) {
           M = Meq;
         } else {
 #pragma unroll
@@ -1442,6 +1514,57 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
   // retire: this CTA no longer touches the workspace parity (counter, status, parked masks)
   __syncthreads();
   if (tid == 0) red_release_add(P.exit_ctr, 1ull);
+}
+
+// ------------------------------------------------------------------ equality-mask index
+
+// EPSMa's equality masks (wscmp of a text block against a broadcast pattern
+// byte) computed once per text for a set of byte values and kept in HBM, so that every search
+// of a batch over that text reads the masks of its own distinct bytes instead of recomputing
+// them from the text: plane k, word w, bit i = [t[64w + i] == vals[k]]; zero past n and in the
+// padding words up to pstride (the search kernel streams whole tiles + one halo word).
+constexpr int kMaxPlanes = 32;
+struct IdxParams {
+  const uint8_t* text;          // 16-byte aligned
+  uint64_t n;
+  uint64_t* planes;             // nv planes of pstride words
+  uint64_t pstride;
+  uint32_t nv;
+  uint32_t vb[kMaxPlanes];      // vals[k] * 0x01010101
+};
+
+__global__ void __launch_bounds__(256) epsm_eqidx_kernel(const __grid_constant__ IdxParams P) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < P.pstride; w += stride) {
+    const uint64_t b0 = w * 64;
+    uint4 R[4];
+    uint64_t valid = ~0ull;
+    if (b0 + 64 <= P.n) {
+      const uint4* src = reinterpret_cast<const uint4*>(P.text + b0);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) R[r] = __ldg(src + r);
+    } else {
+      // the text's last partial word (or padding): bytes past n read as 0 and masked out
+      uint32_t wd[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) wd[q] = 0;
+      const uint32_t have = b0 < P.n ? static_cast<uint32_t>(P.n - b0) : 0u;
+      for (uint32_t i = 0; i < have; ++i) wd[i >> 2] |= static_cast<uint32_t>(P.text[b0 + i]) << (8 * (i & 3));
+#pragma unroll
+      for (int r = 0; r < 4; ++r) R[r] = make_uint4(wd[4 * r], wd[4 * r + 1], wd[4 * r + 2], wd[4 * r + 3]);
+      valid = have ? (1ull << have) - 1ull : 0ull;
+    }
+    for (uint32_t k = 0; k < P.nv; ++k) {
+      const uint32_t vb = P.vb[k];
+      uint64_t M = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t Z[4] = {R[r].x ^ vb, R[r].y ^ vb, R[r].z ^ vb, R[r].w ^ vb};
+        M |= static_cast<uint64_t>(zero_byte_mask16(Z, 0x00204081u)) << (16 * r);
+      }
+      P.planes[k * P.pstride + w] = M & valid;
+    }
+  }
 }
 
 }  // namespace epsm

@@ -16,6 +16,7 @@ ap.add_argument("--n", type=int, default=256 * synth.MiB)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--count", action="store_true")
 ap.add_argument("--batch", type=int, default=0, help="searches per batch launch (0: single launches)")
+ap.add_argument("--index", action="store_true", help="batch over an equality-mask index of the text")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 t = synth.text_torch(synth.raw_sigma_spec(a.sigma, (2, a.sigma)), 0, a.n, device=dev)
@@ -33,13 +34,14 @@ if a.batch:
     # warm-up batch, then timed batches of a.batch searches each (one launch per batch)
     occb = torch.zeros(a.batch, dtype=torch.int64, device=dev)
     outs = [torch.empty(a.n // 2, dtype=torch.int64, device=dev) for _ in range(2)]
+    ix = epsm.eq_index(t, epsm.index_values(plans)) if a.index else None
     groups = [plans[i:i + a.batch] for i in range(0, len(plans) - a.batch + 1, a.batch)]
-    epsm.search_batch_async(groups[0], t, occb, outs=[outs[i % 2] for i in range(a.batch)])
+    epsm.search_batch_async(groups[0], t, occb, outs=[outs[i % 2] for i in range(a.batch)], index=ix)
     torch.cuda.synchronize()
     for g in groups:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        epsm.search_batch_async(g, t, occb, outs=[outs[i % 2] for i in range(a.batch)])
+        epsm.search_batch_async(g, t, occb, outs=[outs[i % 2] for i in range(a.batch)], index=ix)
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / a.batch
