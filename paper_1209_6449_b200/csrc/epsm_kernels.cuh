@@ -831,22 +831,31 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
       if (c && off < room) st_stream_u64(pos + gidx + off, sb + static_cast<uint64_t>(__ffsll(M) - 1));
       continue;
     }
-    // exclusive offsets from 7 bit-sliced ballots (c <= 64): independent ops, no shuffle chain
+    // exclusive offsets from bit-sliced ballots (c <= 64): independent ops, no shuffle chain;
+    // as many as the largest lane count has bits (2 for the common sparse slices, not 7)
+    const uint32_t nbits = 32u - __clz(__reduce_max_sync(0xffffffffu, c));
     uint32_t off = 0, tg = 0;
 #pragma unroll
     for (int bb = 0; bb < 7; ++bb) {
+      if (bb >= static_cast<int>(nbits)) break;              // warp-uniform
       const uint32_t bal = __ballot_sync(0xffffffffu, (c >> bb) & 1u);
       off += __popc(bal & lt) << bb;
       tg += __popc(bal) << bb;
     }
     if (tg <= 96) {
       // moderately sparse: direct stores, lane by lane in bit order
-      uint64_t v = M;
+      uint32_t lo = static_cast<uint32_t>(M), hi = static_cast<uint32_t>(M >> 32);
       uint32_t i = off;
-      while (v) {
-        const int bit = __ffsll(v) - 1;
-        v &= v - 1;
-        if (i < room) st_stream_u64(pos + gidx + i, sb + static_cast<uint64_t>(bit));
+      while (lo) {
+        const uint32_t bit = __ffs(lo) - 1;
+        lo &= lo - 1;
+        if (i < room) st_stream_u64(pos + gidx + i, sb + bit);
+        ++i;
+      }
+      while (hi) {
+        const uint32_t bit = __ffs(hi) + 31;
+        hi &= hi - 1;
+        if (i < room) st_stream_u64(pos + gidx + i, sb + bit);
         ++i;
       }
       continue;
