@@ -154,6 +154,7 @@ KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
   if (sk == epsm::kEqMode) return pick<4, 4, 1, epsm::kEqMode, 0>(search);   // EPSMa, <= 2 values
   if (sk == epsm::kPlaneMode) return pick<4, 4, 1, epsm::kPlaneMode, 0>(search);   // EPSMa, index
+  if (sk == epsm::kPlaneMode4) return pick<4, 4, 1, epsm::kPlaneMode4, 0>(search);
   if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
   if (sk == 4 && sq == 12) {
     if (m == 16) return pick<4, 4, 4, 4, 12>(search);
@@ -325,7 +326,7 @@ int epsm_ensure_occ(epsm_plan_t* plan) {
 
 // One-time per (device, kernel variant): opt in to > 48 KiB of dynamic shared memory.
 static int set_smem_attr(KernelFn fn, int device, int smem) {
-  static std::atomic<KernelFn> done[16][32];
+  static std::atomic<KernelFn> done[16][64];
   if (device < 0 || device >= 16) device = 15;
   for (auto& slot : done[device]) {
     KernelFn f = slot.load(std::memory_order_acquire);
@@ -492,9 +493,19 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     return v && v[0] ? static_cast<uint32_t>(strtoul(v, nullptr, 0)) : 0u;
   }();
   P.flags = env_flags;
-  KernelFn fn = index ? kernel_for(plan0->m, epsm::kPlaneMode, 0, search)
+  // index searches of at most 4 planes each take the variant with twice the (half-size) stages
+  uint32_t max_np = 0;
+  for (uint32_t j = 0; j < k && index; ++j) max_np = std::max(max_np, P.jobs[j].np);
+  static const bool index4_on = [] {
+    const char* v = getenv("EPSM_INDEX4");
+    return !(v && v[0] == '0');
+  }();
+  const bool index4 = index && search && index4_on && max_np <= 4;
+  KernelFn fn = index ? kernel_for(plan0->m, index4 ? epsm::kPlaneMode4 : epsm::kPlaneMode, 0, search)
                      : kernel_for(plan0->m, plan0->sk, plan0->sq, search);
-  const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
+  const int smem = index4   ? static_cast<int>(sizeof(epsm::Index4Smem))
+                   : search ? static_cast<int>(sizeof(epsm::SearchSmem))
+                            : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;
   // programmatic dependent launch: the kernel starts while the previous grid on the stream
@@ -818,7 +829,9 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
   // searches are independent: group them by kernel variant (m, filter or index), keeping
   // their order within a group, and launch each group in runs of at most kMaxJobs
   std::vector<int> variant(k);
-  for (uint32_t j = 0; j < k; ++j) variant[j] = use_index(plans[j], index) ? epsm::kPlaneMode : plans[j]->sk;
+  for (uint32_t j = 0; j < k; ++j)
+    variant[j] = !use_index(plans[j], index) ? plans[j]->sk
+                 : plans[j]->h_desc->np <= 4 ? epsm::kPlaneMode4 : epsm::kPlaneMode;
   std::vector<uint32_t> order(k);
   for (uint32_t j = 0; j < k; ++j) order[j] = j;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
@@ -840,7 +853,7 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
     uint64_t ns = n >= m ? n - m + 1 : 0;
     if (owned_len < ns) ns = owned_len;
     int rc = epsm_launch_jobs(run.data(), b - a, d_text, n, ns, base, search, s,
-                              va == epsm::kPlaneMode ? index : nullptr);
+                              epsm::is_plane(va) ? index : nullptr);
     if (rc) return rc;
     a = b;
   }

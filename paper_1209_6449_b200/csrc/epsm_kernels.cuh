@@ -136,7 +136,9 @@ struct __align__(16) JobDesc {
 };
 constexpr uint32_t kJobHeader = 272;                              // bytes before gram_tab
 constexpr int kEqMode = -1;                                       // SK value of the equality variant
-constexpr int kPlaneMode = -2;                                    // SK value of the index variant
+constexpr int kPlaneMode = -2;                                    // SK of the index variant (<= 8 planes)
+constexpr int kPlaneMode4 = -3;                                   // ... <= 4 planes: twice the stages
+__host__ __device__ constexpr bool is_plane(int sk) { return sk == kPlaneMode || sk == kPlaneMode4; }
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
 // One search of a launch: its preprocessing and its outputs.
@@ -216,11 +218,11 @@ struct __align__(16) ParkedChunk {   // per parking slot
   uint8_t slow[kConsumerWarps]; // bit t: the warp parked masks for tile t (else all zero)
 };
 
-template <int STAGES, bool SEARCH>
+template <int STAGES, bool SEARCH, int STAGE_BYTES = kStageBytes>
 struct __align__(128) SmemLayoutT {
   static constexpr int kStages = STAGES;
   static constexpr int kPark = SEARCH ? kParked : 1;
-  uint8_t ring[STAGES][kStageBytes];
+  uint8_t ring[STAGES][STAGE_BYTES];
   uint16_t wstage[SEARCH ? kConsumerWarps : 1][SEARCH ? kWarpStagePad : 2];   // slice-relative
   ParkedChunk park[kPark];
   alignas(8) uint64_t full[STAGES];
@@ -240,6 +242,14 @@ using SearchSmem = SmemLayoutT<kStagesSearch, true>;
 using CountSmem = SmemLayoutT<kStagesCount, false>;
 template <bool SEARCH>
 using SmemFor = typename std::conditional<SEARCH, SearchSmem, CountSmem>::type;
+// index variant with <= 4 planes per search: stages of 4 planes, twice as many (the consumers
+// get through a stage of planes far faster than through a text tile, so the ring must cover
+// more of the copy latency)
+constexpr int kStagesIndex4 = 2 * kStagesSearch;
+using Index4Smem = SmemLayoutT<kStagesIndex4, true, 4 * kPlaneStride>;
+static_assert(sizeof(Index4Smem) <= 232448, "index layout fits 227 KB of shared memory");
+template <bool SEARCH, int SK>
+using SmemForK = typename std::conditional<SEARCH && SK == kPlaneMode4, Index4Smem, SmemFor<SEARCH>>::type;
 
 // ------------------------------------------------------------------ PTX helpers
 
@@ -888,7 +898,7 @@ __device__ __forceinline__ void load_segment(const uint8_t* seg, uint32_t rot, u
 template <int F, int F2, int MW, int SK, int SQ, bool SEARCH>
 __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using Smem = SmemFor<SEARCH>;
+  using Smem = SmemForK<SEARCH, SK>;
   constexpr int kStages = Smem::kStages;
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
@@ -983,14 +993,14 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
         const uint32_t bulk = static_cast<uint32_t>((end & ~15ull) - base);
         const uint32_t tail = static_cast<uint32_t>(end - base) - bulk;   // < 16 bytes
-        if constexpr (SK != kPlaneMode) {
+        if constexpr (!is_plane(SK)) {
           if (lane < tail) S.ring[stage][bulk + lane] = P.text[base + bulk + lane];
         }
         __syncwarp();
         if (lane == 0) {
           S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
           S.info2[stage] = static_cast<uint32_t>(cur) | (jslot << 31);
-          if constexpr (SK == kPlaneMode) {
+          if constexpr (is_plane(SK)) {
             // the tile's words of the search's planes (padded: always whole)
             const JobRef& J = P.jobs[job];
             mbar_arrive_expect_tx(&S.full[stage], J.np * kPlaneStride);
@@ -1037,7 +1047,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       cur = __shfl_sync(0xffffffffu, nxt, 0);
       after = __shfl_sync(0xffffffffu, after, 0);
-      if (SK != kPlaneMode && (P.flags & 2u)) prefetch_l2(after);
+      if (!is_plane(SK) && (P.flags & 2u)) prefetch_l2(after);
     }
   } else if (warp == 1) {
     // ================================================================ look-back
@@ -1221,7 +1231,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           Meq &= rm;
         }
         slow = __any_sync(0xffffffffu, Meq != 0ull);
-      } else if constexpr (SK == kPlaneMode) {
+      } else if constexpr (is_plane(SK)) {
         // ---- EPSMa's shift-AND over the text's equality-mask index: the
         // masks E_v of the lane's 64 starts (+ the next 64) are read, not computed --
         // r = AND_i (E_{p_i} >> i), exact, no candidates, no check
@@ -1388,7 +1398,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       if (slow) {
         // the lane's 64 starts as one mask: bit 16u + j = start seg_off + 16u + j
         uint64_t M = 0;
-        if constexpr (SK == kEqMode || SK == kPlaneMode) {
+        if constexpr (SK == kEqMode || is_plane(SK)) {
           M = Meq;
         } else {
 #pragma unroll
