@@ -403,6 +403,8 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   P.nbytes = nbytes + mis;
   P.s_lo = mis;
   P.s_hi = mis + nstarts;
+  P.it_lo = mis ? 1u : 0u;                                   // tile 0 holds starts < mis
+  P.it_hi = static_cast<uint32_t>(P.s_hi / epsm::kTile);     // tiles wholly below s_hi
   P.pos_bias = base - mis;
   P.mul8 = 1u << 24;
   P.mul24 = 1u << 8;
@@ -663,6 +665,8 @@ int epsm_plan(const uint8_t* pattern, uint32_t m, epsm_plan_t** out) {
         for (uint32_t i = 0; i < m; ++i)
           if ((sel[v] >> i) & 1u) list[c++] = static_cast<uint8_t>(i);
         while (c % 4) list[c] = list[0], ++c;            // pad: repeat the first position
+        for (uint32_t i = 0; i < m; ++i)
+          if ((sel[v] >> i) & 1u) D.pslot[i] = static_cast<uint8_t>(v);
         D.pw0[v] = static_cast<uint8_t>(w);
         D.pwn[v] = static_cast<uint8_t>(c / 4);
         for (uint32_t q = 0; q < c / 4; ++q, ++w)

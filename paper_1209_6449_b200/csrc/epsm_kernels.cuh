@@ -132,9 +132,10 @@ struct __align__(16) JobDesc {
   uint8_t pval[kMaxPlaneSlots]; // the byte value of plane k
   uint32_t np;                  // distinct bytes (0: more than kMaxPlaneSlots or m > 32)
   uint32_t ppad[5];
+  uint8_t pslot[32];            // plane of p_i (short patterns read the planes position by position)
   uint32_t gram_tab[kGramTab];  // sampled filter: q-gram fingerprints -> candidate offsets
 };
-constexpr uint32_t kJobHeader = 272;                              // bytes before gram_tab
+constexpr uint32_t kJobHeader = 304;                              // bytes before gram_tab
 constexpr int kEqMode = -1;                                       // SK value of the equality variant
 constexpr int kPlaneMode = -2;                                    // SK of the index variant (<= 8 planes)
 constexpr int kPlaneMode4 = -3;                                   // ... <= 4 planes: twice the stages
@@ -166,6 +167,7 @@ struct KParams {
   unsigned long long ctr_base;  // value of ctr[0] when this launch starts
   unsigned long long tag;       // launch number << 40
   uint32_t ntiles;              // tiles covering [0, s_hi)
+  uint32_t it_lo, it_hi;        // interior tiles [it_lo, it_hi): every start in [s_lo, s_hi)
   uint32_t nchunks;             // chunks per search (C); chunk g of the launch = search g / C
   uint32_t gchunks;             // chunks of the launch = njobs * C
   uint32_t njobs;               // searches in this launch (same text, same m)
@@ -1172,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       const uint8_t* ts = S.ring[stage];
       const uint8_t* seg = ts + seg_off;
       const uint64_t tbase = static_cast<uint64_t>(tile) * kTile;
-      const bool interior = tbase >= P.s_lo && tbase + kTile <= P.s_hi;   // warp-uniform
+      const bool interior = tile >= P.it_lo && tile < P.it_hi;          // warp-uniform
 
       // slot r holds unit u = (r + rot) & 3 of the segment: text bytes [seg_off + 16u, +16)
       uint32_t mask[4];                        // 16-bit match mask of the unit in slot r
@@ -1237,7 +1239,25 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // r = AND_i (E_{p_i} >> i), exact, no candidates, no check
         const uint32_t wi = cw * 32u + lane;                 // the lane's word in each plane tile
         uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;
-        const uint32_t np = JD->np;
+        const uint32_t np = P.m <= 8 ? 0u : JD->np;          // (warp-uniform)
+        if (P.m <= 8) {
+          // short patterns: position by position, each reading the words of its own plane
+          // (compile-time shifts, no list)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i >= static_cast<int>(P.m)) break;
+            const uint2* pl = reinterpret_cast<const uint2*>(ts + JD->pslot[i] * kPlaneStride);
+            const uint2 e = pl[wi];
+            if (i == 0) {
+              rl &= e.x;
+              rh &= e.y;
+            } else {
+              const uint32_t h = pl[wi + 1].x;
+              rl &= __funnelshift_r(e.x, e.y, i);
+              rh &= __funnelshift_r(e.y, h, i);
+            }
+          }
+        }
 #pragma unroll
         for (int k = 0; k < kMaxPlaneSlots; ++k) {
           if (k >= static_cast<int>(np)) break;              // warp-uniform
