@@ -94,7 +94,7 @@ EXPORTED_SYMBOLS = (
     "epsm_eqidx_create", "epsm_eqidx_free", "epsm_eqidx_build_async", "epsm_eqidx_values",
     "epsm_search_batch_index_async", "epsm_plan_index_values",
 )
-MAX_PLANES = 32
+MAX_PLANES = 64
 INDEX_MAX_D = 8
 
 

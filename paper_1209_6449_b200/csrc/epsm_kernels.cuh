@@ -1562,7 +1562,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 // of a batch over that text reads the masks of its own distinct bytes instead of recomputing
 // them from the text: plane k, word w, bit i = [t[64w + i] == vals[k]]; zero past n and in the
 // padding words up to pstride (the search kernel streams whole tiles + one halo word).
-constexpr int kMaxPlanes = 32;
+constexpr int kMaxPlanes = 64;
 struct IdxParams {
   const uint8_t* text;          // 16-byte aligned
   uint64_t n;

@@ -157,8 +157,28 @@ def test_index_build_errors(epsm, dev):
             ix.build_async(buf, b"\x00\x00")            # duplicate value
         assert e.value.code == epsm.EPSM_EINVAL
         with pytest.raises(epsm.EpsmError):
-            ix.build_async(buf, bytes(range(33)))       # more than 32 planes
+            ix.build_async(buf, bytes(range(65)))       # more than 64 planes
         with pytest.raises(epsm.EpsmError):
             ix.build_async(buf, b"")
     finally:
         ix.close()
+
+
+def test_index_many_values(epsm, dev):
+    """64 planes (the maximum): a 64-letter text, short patterns over it, plane ids above 32;
+    and an index over values that do not occur (their planes are all zero)."""
+    rng = np.random.default_rng(64)
+    n = CHUNK + 5 * TILE + 3
+    t = rng.integers(0, 64, size=n, dtype=np.uint8)
+    pats = [t[s:s + m].tobytes() for m in (1, 2, 3, 4, 6, 8, 12, 16) for s in rng.integers(0, n - m, 4)]
+    pats += [bytes([63, 62]), bytes([200, 201]), bytes([0, 63, 0])]
+    t = planted_text(rng, n, 64, pats)
+    td = torch.from_numpy(t).to(dev)
+    vals = bytes(range(63, -1, -1))                # reversed: plane id != value
+    with epsm.eq_index(td, vals) as ix:
+        assert ix.values == vals
+        res = run_batch(epsm, pats, td, ix)
+    assert_parity(pats, res, t, "64 planes")
+    with epsm.eq_index(td, bytes(range(100, 164))) as ix:   # none of these bytes occur
+        res = run_batch(epsm, [bytes([100, 101]), bytes([100]) * 5], td, ix)
+    assert all(k == 0 for k, _ in res)
