@@ -82,6 +82,8 @@ _lib.epsm_eqidx_values.argtypes = [_vp, _vp]
 _lib.epsm_eqidx_values.restype = ctypes.c_int
 _lib.epsm_plan_index_values.argtypes = [_vp, _vp]
 _lib.epsm_plan_index_values.restype = ctypes.c_int
+_lib.epsm_count_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp]
+_lib.epsm_count_batch_index_async.restype = ctypes.c_int
 _lib.epsm_search_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_search_batch_index_async.restype = ctypes.c_int
 
@@ -92,7 +94,7 @@ EXPORTED_SYMBOLS = (
     "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
     "epsm_version", "epsm_debug_trace",
     "epsm_eqidx_create", "epsm_eqidx_free", "epsm_eqidx_build_async", "epsm_eqidx_values",
-    "epsm_search_batch_index_async", "epsm_plan_index_values",
+    "epsm_search_batch_index_async", "epsm_count_batch_index_async", "epsm_plan_index_values",
 )
 MAX_PLANES = 64
 INDEX_MAX_D = 8
@@ -391,14 +393,20 @@ def search_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, outs=No
            "epsm_search_batch_async")
 
 
-def count_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, stream=None) -> None:
-    """Enqueue len(plans) counts over one text (count kernel; occ of pattern j -> occ_out[j])."""
+def count_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, stream=None,
+                      index: "EqIndex | None" = None) -> None:
+    """Enqueue len(plans) counts over one text (count kernel; occ of pattern j -> occ_out[j]);
+    with an EqIndex of the text, qualifying searches count over its planes."""
     if len(plans) == 0:
         return
     plans, k, hp, _, _ = _batch_args(plans, text, occ_out, None, None)
+    if index is not None:
+        _check(_lib.epsm_count_batch_index_async(hp, k, index.handle, text.data_ptr(), text.numel(),
+                                                 occ_out.data_ptr(), _stream_handle(stream, text.device)),
+               "epsm_count_batch_index_async")
+        return
     _check(_lib.epsm_count_batch_async(hp, k, text.data_ptr(), text.numel(), occ_out.data_ptr(),
-                                       _stream_handle(stream, text.device)),
-           "epsm_count_batch_async")
+                                       _stream_handle(stream, text.device)), "epsm_count_batch_async")
 
 
 def search_range_batch_async(plans, shard: torch.Tensor, owned_len: int, base: int, occ_out: torch.Tensor,

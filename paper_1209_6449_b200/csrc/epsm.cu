@@ -880,6 +880,11 @@ int epsm_count_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t*
   return batch_common(plans, k, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream);
 }
 
+int epsm_count_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,
+                                 const uint8_t* d_text, uint64_t n, uint64_t* d_occ, epsm_stream_t stream) {
+  return batch_common(plans, k, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream, index);
+}
+
 int epsm_search_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,
                                   const uint8_t* d_text, uint64_t n, uint64_t* const* d_pos, const uint64_t* caps,
                                   uint64_t* d_occ, epsm_stream_t stream) {

@@ -89,6 +89,13 @@ def test_index_batch_matches_oracle(epsm, dev, sigma):
     with epsm.eq_index(td, vals) as ix:
         assert set(ix.values) == set(vals)
         res = run_batch(epsm, pats, td, ix)
+        # the count kernel over the same index
+        plans = [epsm.plan(p) for p in pats]
+        occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+        for _ in range(2):
+            epsm.count_batch_async(plans, td, occ, index=ix)
+        torch.cuda.synchronize()
+        assert occ.cpu().tolist() == [k for k, _ in res]
     assert_parity(pats, res, t, f"sigma={sigma}")
 
 

@@ -22,4 +22,6 @@ for s, m in [(4, 2), (2, 4), (16, 2), (32, 2), (2, 8)]:
     a = tm(lambda: epsm.search_batch_async(plans, t, occ, outs=outs, index=ix))
     b = tm(lambda: epsm.search_batch_async(plans, t, occ, index=ix))
     c = tm(lambda: epsm.search_batch_async(plans, t, occ, outs=outs, caps=[1] * 16, index=ix))
-    print(f"sigma={s} m={m}: positions {a:.1f} us, no outputs {b:.1f} us, cap 1 {c:.1f} us, occ {int(occ[0])}")
+    d = tm(lambda: epsm.count_batch_async(plans, t, occ, index=ix))
+    print(f"sigma={s} m={m}: positions {a:.1f} us, no outputs {b:.1f} us, cap 1 {c:.1f} us, "
+          f"count kernel {d:.1f} us, occ {int(occ[0])}")
