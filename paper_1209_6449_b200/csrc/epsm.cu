@@ -155,6 +155,7 @@ KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (sk == epsm::kEqMode) return pick<4, 4, 1, epsm::kEqMode, 0>(search);   // EPSMa, <= 2 values
   if (sk == epsm::kPlaneMode) return pick<4, 4, 1, epsm::kPlaneMode, 0>(search);   // EPSMa, index
   if (sk == epsm::kPlaneMode4) return pick<4, 4, 1, epsm::kPlaneMode4, 0>(search);
+  if (sk == epsm::kPlaneModeC) return pick<4, 4, 1, epsm::kPlaneModeC, 0>(search);
   if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
   if (sk == 4 && sq == 12) {
     if (m == 16) return pick<4, 4, 4, 4, 12>(search);
@@ -502,8 +503,14 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     const char* v = getenv("EPSM_INDEX4");
     return !(v && v[0] == '0');
   }();
-  const bool index4 = index && search && index4_on && max_np <= 4;
-  KernelFn fn = index ? kernel_for(plan0->m, index4 ? epsm::kPlaneMode4 : epsm::kPlaneMode, 0, search)
+  static const bool indexc_on = [] {
+    const char* v = getenv("EPSM_INDEXC");
+    return !(v && v[0] == '0');
+  }();
+  const bool indexc = index && indexc_on && max_np <= 2;
+  const bool index4 = index && !indexc && search && index4_on && max_np <= 4;
+  KernelFn fn = index ? kernel_for(plan0->m, indexc ? epsm::kPlaneModeC : index4 ? epsm::kPlaneMode4 : epsm::kPlaneMode,
+                                   0, search)
                      : kernel_for(plan0->m, plan0->sk, plan0->sq, search);
   const int smem = index4   ? static_cast<int>(sizeof(epsm::Index4Smem))
                    : search ? static_cast<int>(sizeof(epsm::SearchSmem))
@@ -835,6 +842,7 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
   std::vector<int> variant(k);
   for (uint32_t j = 0; j < k; ++j)
     variant[j] = !use_index(plans[j], index) ? plans[j]->sk
+                 : plans[j]->h_desc->np <= 2 ? epsm::kPlaneModeC
                  : plans[j]->h_desc->np <= 4 ? epsm::kPlaneMode4 : epsm::kPlaneMode;
   std::vector<uint32_t> order(k);
   for (uint32_t j = 0; j < k; ++j) order[j] = j;

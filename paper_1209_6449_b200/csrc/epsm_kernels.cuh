@@ -62,6 +62,10 @@ constexpr int kPlaneWordsPerTile = kTile / 64;                   // 512
 constexpr int kPlaneStride = kTile / 8 + 16;                     // bytes per plane in a stage
 constexpr int kMaxPlaneSlots = 8;                                // planes per search (distinct bytes)
 static_assert(kMaxPlaneSlots * kPlaneStride <= kStageBytes, "planes of a stage");
+// searches of at most 2 planes: one stage holds a whole chunk (4 tiles) of both planes, so the
+// ring's round trip (copy, consumers, release) is paid once per 4 tiles
+constexpr int kChunkPlaneStride = 4 * (kTile / 8) + 16;            // 16400 (kChunkTiles = 4 tiles)
+static_assert(2 * kChunkPlaneStride <= kStageBytes, "a chunk of 2 planes per stage");
 constexpr int kStagesSearch = 5;
 constexpr int kStagesCount = 6;
 constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
@@ -87,6 +91,7 @@ static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking ro
 static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
 static_assert(kSlices <= 128 && kChunkTiles <= 8 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
 constexpr uint32_t kTileBitsMask = (1u << kChunkTiles) - 1u;      // slow-tile bits of one parked chunk
+static_assert(kChunkPlaneStride == kChunkTiles * (kTile / 8) + 16, "chunk-per-stage plane layout");
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 
@@ -139,7 +144,10 @@ constexpr uint32_t kJobHeader = 304;                              // bytes befor
 constexpr int kEqMode = -1;                                       // SK value of the equality variant
 constexpr int kPlaneMode = -2;                                    // SK of the index variant (<= 8 planes)
 constexpr int kPlaneMode4 = -3;                                   // ... <= 4 planes: twice the stages
-__host__ __device__ constexpr bool is_plane(int sk) { return sk == kPlaneMode || sk == kPlaneMode4; }
+constexpr int kPlaneModeC = -4;                                   // ... <= 2 planes: a chunk per stage
+__host__ __device__ constexpr bool is_plane(int sk) {
+  return sk == kPlaneMode || sk == kPlaneMode4 || sk == kPlaneModeC;
+}
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
 // One search of a launch: its preprocessing and its outputs.
@@ -988,7 +996,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       const uint32_t t0 = static_cast<uint32_t>(cur % P.nchunks) * kChunkTiles;
       const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
-      for (uint32_t t = t0; t < t1; ++t) {
+      constexpr uint32_t tstep = SK == kPlaneModeC ? kChunkTiles : 1u;   // tiles per stage
+      for (uint32_t t = t0; t < t1; t += tstep) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
         const uint64_t base = static_cast<uint64_t>(t) * kTile;
         const uint64_t want_end = base + kTile + kHalo;
@@ -1000,9 +1009,23 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
         __syncwarp();
         if (lane == 0) {
-          S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
+          if constexpr (SK == kPlaneModeC) {
+            // the whole chunk: first tile, tile count - 1 in [30:29], last-of-chunk
+            S.info[stage] = t | ((t1 - t - 1) << 29) | 0x80000000u;
+          } else {
+            S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
+          }
           S.info2[stage] = static_cast<uint32_t>(cur) | (jslot << 31);
-          if constexpr (is_plane(SK)) {
+          if constexpr (SK == kPlaneModeC) {
+            // the chunk's words of the search's (<= 2) planes + the halo word, per plane
+            const JobRef& J = P.jobs[job];
+            const uint32_t bytes = (t1 - t) * (kTile / 8) + 16;
+            mbar_arrive_expect_tx(&S.full[stage], J.np * bytes);
+            for (uint32_t k = 0; k < J.np; ++k)
+              bulk_g2s_plain(S.ring[stage] + k * kChunkPlaneStride,
+                             P.planes + J.pid[k] * P.pstride + static_cast<uint64_t>(t) * kPlaneWordsPerTile,
+                             bytes, &S.full[stage]);
+          } else if constexpr (is_plane(SK)) {
             // the tile's words of the search's planes (padded: always whole)
             const JobRef& J = P.jobs[job];
             mbar_arrive_expect_tx(&S.full[stage], J.np * kPlaneStride);
@@ -1019,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           }
           if (first && t == t0) EPSM_TRACE(P, 1);
           if (t == t0 && !first) pend = draw();   // consumed after this chunk
-          if (first && !ws_seen && (t + 1 == t1 || t + 1 - t0 == static_cast<uint32_t>(kStages))) {
+          if (first && !ws_seen && (t + tstep >= t1 || t + 1 - t0 == static_cast<uint32_t>(kStages))) {
             // the first loads (text only) are in flight; before anything touches the workspace
             // (chunk counter, status words, parked masks) launch L-2, the previous user of
             // this parity, must have retired -- normally long done, so one load.  (Done by the
@@ -1136,7 +1159,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
     };
     bool first_tile = true;
+    // chunk-per-stage index variant: sub-tile of the stage's chunk, its first tile and size
+    uint32_t sub = 0, c_t0 = 0, c_ntc = 1, gch = 0;
+    bool c_last = false;
     while (true) {
+      if (SK != kPlaneModeC || sub == 0) {
       mbar_wait(&S.full[stage], phase);
       if (first_tile && cw == 0 && lane == 0) EPSM_TRACE(P, 2);
       first_tile = false;
@@ -1145,10 +1172,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         if (cw == 0 && lane == 0) EPSM_TRACE(P, 4);
         break;
       }
-      const uint32_t tile = info & 0x7FFFFFFFu;              // tile index inside its search
-      const bool last_in_chunk = info >> 31;
+      c_t0 = info & (SK == kPlaneModeC ? 0x1FFFFFFFu : 0x7FFFFFFFu);   // (first) tile in its search
+      c_ntc = SK == kPlaneModeC ? ((info >> 29) & 3u) + 1u : 1u;
+      c_last = info >> 31;
       const uint32_t info2 = S.info2[stage];
-      const uint32_t gch = info2 & 0x7FFFFFFFu;              // chunk id of the launch
+      gch = info2 & 0x7FFFFFFFu;                             // chunk id of the launch
       const uint32_t js = info2 >> 31;                       // job slot of its search
       if (js != cur_slot) {
         // a new search: leave the old slot (the producer may refill it), wait for the new one
@@ -1169,6 +1197,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         FP.bcast[2] = b0.z;
         FP.bcast[3] = b0.w;
       }
+      }
+      const uint32_t tile = c_t0 + sub;
+      const bool last_in_chunk = SK == kPlaneModeC ? sub + 1 == c_ntc : c_last;
       const uint32_t b = seq % kParked;
       if (SEARCH && tpos == 0 && seq >= kParked) flush_chunk_seq(seq - kParked);   // free slot b
       const uint8_t* ts = S.ring[stage];
@@ -1238,6 +1269,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // masks E_v of the lane's 64 starts (+ the next 64) are read, not computed --
         // r = AND_i (E_{p_i} >> i), exact, no candidates, no check
         const uint32_t wi = cw * 32u + lane;                 // the lane's word in each plane tile
+        constexpr uint32_t kPS = SK == kPlaneModeC ? kChunkPlaneStride : kPlaneStride;
+        const uint8_t* pb = ts + (SK == kPlaneModeC ? sub * (kTile / 8) : 0u);   // this tile's words
         uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;
         const uint32_t np = P.m <= 8 ? 0u : JD->np;          // (warp-uniform)
         if (P.m <= 8) {
@@ -1246,7 +1279,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (i >= static_cast<int>(P.m)) break;
-            const uint2* pl = reinterpret_cast<const uint2*>(ts + JD->pslot[i] * kPlaneStride);
+            const uint2* pl = reinterpret_cast<const uint2*>(pb + JD->pslot[i] * kPS);
             const uint2 e = pl[wi];
             if (i == 0) {
               rl &= e.x;
@@ -1261,7 +1294,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 #pragma unroll
         for (int k = 0; k < kMaxPlaneSlots; ++k) {
           if (k >= static_cast<int>(np)) break;              // warp-uniform
-          const uint2* pl = reinterpret_cast<const uint2*>(ts + k * kPlaneStride);
+          const uint2* pl = reinterpret_cast<const uint2*>(pb + k * kPS);
           const uint2 e = pl[wi], h = pl[wi + 1];            // starts 0..63, 64..127
           const uint32_t w0 = JD->pw0[k], wn = JD->pwn[k];
           bool live = true;
@@ -1438,10 +1471,15 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[stage]);   // the text of this stage is no longer needed
-      if (++stage == kStages) {
-        stage = 0;
-        phase ^= 1u;
+      if (SK != kPlaneModeC || last_in_chunk) {
+        if (lane == 0) mbar_arrive(&S.empty[stage]);   // the text of this stage is no longer needed
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+        sub = 0;
+      } else {
+        ++sub;                                         // the next tile of the stage's chunk
       }
       if constexpr (!SEARCH) continue;
       ++tpos;
