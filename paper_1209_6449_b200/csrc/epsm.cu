@@ -154,8 +154,8 @@ KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (m > EPSM_MAX_M) return pick<4, 4, 0, 16, 16>(search);     // long: EPSMc + device-memory check
   if (sk == epsm::kEqMode) return pick<4, 4, 1, epsm::kEqMode, 0>(search);   // EPSMa, <= 2 values
   if (sk == epsm::kPlaneMode) return pick<4, 4, 1, epsm::kPlaneMode, 0>(search);   // EPSMa, index
-  if (sk == epsm::kPlaneMode4) return pick<4, 4, 1, epsm::kPlaneMode4, 0>(search);
   if (sk == epsm::kPlaneModeC) return pick<4, 4, 1, epsm::kPlaneModeC, 0>(search);
+  if (sk == epsm::kPlaneModeC2) return pick<4, 4, 1, epsm::kPlaneModeC2, 0>(search);
   if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
   if (sk == 4 && sq == 12) {
     if (m == 16) return pick<4, 4, 4, 4, 12>(search);
@@ -496,25 +496,18 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     return v && v[0] ? static_cast<uint32_t>(strtoul(v, nullptr, 0)) : 0u;
   }();
   P.flags = env_flags;
-  // index searches of at most 4 planes each take the variant with twice the (half-size) stages
+  // index searches of at most 2 (4) planes each take the variant with 4 (2) tiles per stage
   uint32_t max_np = 0;
   for (uint32_t j = 0; j < k && index; ++j) max_np = std::max(max_np, P.jobs[j].np);
-  static const bool index4_on = [] {
-    const char* v = getenv("EPSM_INDEX4");
-    return !(v && v[0] == '0');
-  }();
-  static const bool indexc_on = [] {
+  static const bool multi_tile = [] {
     const char* v = getenv("EPSM_INDEXC");
     return !(v && v[0] == '0');
   }();
-  const bool indexc = index && indexc_on && max_np <= 2;
-  const bool index4 = index && !indexc && search && index4_on && max_np <= 4;
-  KernelFn fn = index ? kernel_for(plan0->m, indexc ? epsm::kPlaneModeC : index4 ? epsm::kPlaneMode4 : epsm::kPlaneMode,
-                                   0, search)
-                     : kernel_for(plan0->m, plan0->sk, plan0->sq, search);
-  const int smem = index4   ? static_cast<int>(sizeof(epsm::Index4Smem))
-                   : search ? static_cast<int>(sizeof(epsm::SearchSmem))
-                            : static_cast<int>(sizeof(epsm::CountSmem));
+  const int pmode = !multi_tile ? epsm::kPlaneMode
+                    : max_np <= 2 ? epsm::kPlaneModeC
+                    : max_np <= 4 ? epsm::kPlaneModeC2 : epsm::kPlaneMode;
+  KernelFn fn = index ? kernel_for(plan0->m, pmode, 0, search) : kernel_for(plan0->m, plan0->sk, plan0->sq, search);
+  const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;
   // programmatic dependent launch: the kernel starts while the previous grid on the stream
@@ -843,7 +836,7 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
   for (uint32_t j = 0; j < k; ++j)
     variant[j] = !use_index(plans[j], index) ? plans[j]->sk
                  : plans[j]->h_desc->np <= 2 ? epsm::kPlaneModeC
-                 : plans[j]->h_desc->np <= 4 ? epsm::kPlaneMode4 : epsm::kPlaneMode;
+                 : plans[j]->h_desc->np <= 4 ? epsm::kPlaneModeC2 : epsm::kPlaneMode;
   std::vector<uint32_t> order(k);
   for (uint32_t j = 0; j < k; ++j) order[j] = j;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {

@@ -62,10 +62,11 @@ constexpr int kPlaneWordsPerTile = kTile / 64;                   // 512
 constexpr int kPlaneStride = kTile / 8 + 16;                     // bytes per plane in a stage
 constexpr int kMaxPlaneSlots = 8;                                // planes per search (distinct bytes)
 static_assert(kMaxPlaneSlots * kPlaneStride <= kStageBytes, "planes of a stage");
-// searches of at most 2 planes: one stage holds a whole chunk (4 tiles) of both planes, so the
-// ring's round trip (copy, consumers, release) is paid once per 4 tiles
-constexpr int kChunkPlaneStride = 4 * (kTile / 8) + 16;            // 16400 (kChunkTiles = 4 tiles)
-static_assert(2 * kChunkPlaneStride <= kStageBytes, "a chunk of 2 planes per stage");
+// searches of few planes: one stage holds several tiles of every plane (a whole chunk of 4
+// tiles for <= 2 planes, 2 tiles for <= 4), so the ring's round trip (copy, consumers,
+// release) is paid once per 4 or 2 tiles
+static_assert(2 * (4 * (kTile / 8) + 16) <= kStageBytes, "a chunk of 2 planes per stage");
+static_assert(4 * (2 * (kTile / 8) + 16) <= kStageBytes, "2 tiles of 4 planes per stage");
 constexpr int kStagesSearch = 5;
 constexpr int kStagesCount = 6;
 constexpr int kChunkTiles = 4;                                   // 128 KiB look-back granularity
@@ -91,7 +92,7 @@ static_assert(kSlots % kParked == 0 && kSlots >= 2 * kParked, "slot / parking ro
 static_assert(kParked * kChunkTiles <= 32, "slow-tile bits of all parked chunks fit one u32");
 static_assert(kSlices <= 128 && kChunkTiles <= 8 && kUnitsPerThread == 4, "hand-off scan / mask packing layout");
 constexpr uint32_t kTileBitsMask = (1u << kChunkTiles) - 1u;      // slow-tile bits of one parked chunk
-static_assert(kChunkPlaneStride == kChunkTiles * (kTile / 8) + 16, "chunk-per-stage plane layout");
+static_assert(kChunkTiles == 4, "tiles-per-stage index variants (4 = a chunk, 2 = half)");
 
 constexpr uint32_t kInfoEnd = 0xFFFFFFFFu;
 
@@ -143,11 +144,16 @@ struct __align__(16) JobDesc {
 constexpr uint32_t kJobHeader = 304;                              // bytes before gram_tab
 constexpr int kEqMode = -1;                                       // SK value of the equality variant
 constexpr int kPlaneMode = -2;                                    // SK of the index variant (<= 8 planes)
-constexpr int kPlaneMode4 = -3;                                   // ... <= 4 planes: twice the stages
 constexpr int kPlaneModeC = -4;                                   // ... <= 2 planes: a chunk per stage
+constexpr int kPlaneModeC2 = -5;                                  // ... <= 4 planes: 2 tiles per stage
 __host__ __device__ constexpr bool is_plane(int sk) {
-  return sk == kPlaneMode || sk == kPlaneMode4 || sk == kPlaneModeC;
+  return sk == kPlaneMode || sk == kPlaneModeC || sk == kPlaneModeC2;
 }
+// tiles per ring stage and bytes per plane in a stage (tiles' words + the halo word)
+__host__ __device__ constexpr uint32_t plane_tps(int sk) {
+  return sk == kPlaneModeC ? 4u : sk == kPlaneModeC2 ? 2u : 1u;
+}
+__host__ __device__ constexpr uint32_t plane_stride(int sk) { return plane_tps(sk) * (kTile / 8) + 16; }
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
 // One search of a launch: its preprocessing and its outputs.
@@ -252,14 +258,6 @@ using SearchSmem = SmemLayoutT<kStagesSearch, true>;
 using CountSmem = SmemLayoutT<kStagesCount, false>;
 template <bool SEARCH>
 using SmemFor = typename std::conditional<SEARCH, SearchSmem, CountSmem>::type;
-// index variant with <= 4 planes per search: stages of 4 planes, twice as many (the consumers
-// get through a stage of planes far faster than through a text tile, so the ring must cover
-// more of the copy latency)
-constexpr int kStagesIndex4 = 2 * kStagesSearch;
-using Index4Smem = SmemLayoutT<kStagesIndex4, true, 4 * kPlaneStride>;
-static_assert(sizeof(Index4Smem) <= 232448, "index layout fits 227 KB of shared memory");
-template <bool SEARCH, int SK>
-using SmemForK = typename std::conditional<SEARCH && SK == kPlaneMode4, Index4Smem, SmemFor<SEARCH>>::type;
 
 // ------------------------------------------------------------------ PTX helpers
 
@@ -908,7 +906,7 @@ __device__ __forceinline__ void load_segment(const uint8_t* seg, uint32_t rot, u
 template <int F, int F2, int MW, int SK, int SQ, bool SEARCH>
 __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using Smem = SmemForK<SEARCH, SK>;
+  using Smem = SmemFor<SEARCH>;
   constexpr int kStages = Smem::kStages;
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
@@ -996,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       const uint32_t t0 = static_cast<uint32_t>(cur % P.nchunks) * kChunkTiles;
       const uint32_t t1 = min(t0 + kChunkTiles, P.ntiles);
-      constexpr uint32_t tstep = SK == kPlaneModeC ? kChunkTiles : 1u;   // tiles per stage
+      constexpr uint32_t tstep = plane_tps(SK);                          // tiles per stage
       for (uint32_t t = t0; t < t1; t += tstep) {
         mbar_wait(&S.empty[stage], phase ^ 1u);
         const uint64_t base = static_cast<uint64_t>(t) * kTile;
@@ -1009,20 +1007,21 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
         __syncwarp();
         if (lane == 0) {
-          if constexpr (SK == kPlaneModeC) {
-            // the whole chunk: first tile, tile count - 1 in [30:29], last-of-chunk
-            S.info[stage] = t | ((t1 - t - 1) << 29) | 0x80000000u;
+          if constexpr (tstep > 1) {
+            // first tile, tile count - 1 in [30:29], last-of-chunk
+            const uint32_t ntc = min(tstep, t1 - t);
+            S.info[stage] = t | ((ntc - 1) << 29) | (t + ntc == t1 ? 0x80000000u : 0u);
           } else {
             S.info[stage] = t | ((t + 1 == t1) ? 0x80000000u : 0u);
           }
           S.info2[stage] = static_cast<uint32_t>(cur) | (jslot << 31);
-          if constexpr (SK == kPlaneModeC) {
-            // the chunk's words of the search's (<= 2) planes + the halo word, per plane
+          if constexpr (tstep > 1) {
+            // the stage's tiles of the search's planes + the halo word, per plane
             const JobRef& J = P.jobs[job];
-            const uint32_t bytes = (t1 - t) * (kTile / 8) + 16;
+            const uint32_t bytes = min(tstep, t1 - t) * (kTile / 8) + 16;
             mbar_arrive_expect_tx(&S.full[stage], J.np * bytes);
             for (uint32_t k = 0; k < J.np; ++k)
-              bulk_g2s_plain(S.ring[stage] + k * kChunkPlaneStride,
+              bulk_g2s_plain(S.ring[stage] + k * plane_stride(SK),
                              P.planes + J.pid[k] * P.pstride + static_cast<uint64_t>(t) * kPlaneWordsPerTile,
                              bytes, &S.full[stage]);
           } else if constexpr (is_plane(SK)) {
@@ -1163,7 +1162,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     uint32_t sub = 0, c_t0 = 0, c_ntc = 1, gch = 0;
     bool c_last = false;
     while (true) {
-      if (SK != kPlaneModeC || sub == 0) {
+      if (plane_tps(SK) == 1 || sub == 0) {
       mbar_wait(&S.full[stage], phase);
       if (first_tile && cw == 0 && lane == 0) EPSM_TRACE(P, 2);
       first_tile = false;
@@ -1172,8 +1171,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         if (cw == 0 && lane == 0) EPSM_TRACE(P, 4);
         break;
       }
-      c_t0 = info & (SK == kPlaneModeC ? 0x1FFFFFFFu : 0x7FFFFFFFu);   // (first) tile in its search
-      c_ntc = SK == kPlaneModeC ? ((info >> 29) & 3u) + 1u : 1u;
+      c_t0 = info & (plane_tps(SK) > 1 ? 0x1FFFFFFFu : 0x7FFFFFFFu);   // (first) tile in its search
+      c_ntc = plane_tps(SK) > 1 ? ((info >> 29) & 3u) + 1u : 1u;
       c_last = info >> 31;
       const uint32_t info2 = S.info2[stage];
       gch = info2 & 0x7FFFFFFFu;                             // chunk id of the launch
@@ -1199,7 +1198,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       }
       const uint32_t tile = c_t0 + sub;
-      const bool last_in_chunk = SK == kPlaneModeC ? sub + 1 == c_ntc : c_last;
+      const bool last_in_chunk = plane_tps(SK) > 1 ? (sub + 1 == c_ntc && c_last) : c_last;
       const uint32_t b = seq % kParked;
       if (SEARCH && tpos == 0 && seq >= kParked) flush_chunk_seq(seq - kParked);   // free slot b
       const uint8_t* ts = S.ring[stage];
@@ -1269,8 +1268,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // masks E_v of the lane's 64 starts (+ the next 64) are read, not computed --
         // r = AND_i (E_{p_i} >> i), exact, no candidates, no check
         const uint32_t wi = cw * 32u + lane;                 // the lane's word in each plane tile
-        constexpr uint32_t kPS = SK == kPlaneModeC ? kChunkPlaneStride : kPlaneStride;
-        const uint8_t* pb = ts + (SK == kPlaneModeC ? sub * (kTile / 8) : 0u);   // this tile's words
+        constexpr uint32_t kPS = plane_stride(SK);
+        const uint8_t* pb = ts + sub * (kTile / 8);         // this tile's words (sub = 0: one tile)
         uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;
         const uint32_t np = P.m <= 8 ? 0u : JD->np;          // (warp-uniform)
         if (P.m <= 8) {
@@ -1471,7 +1470,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         }
       }
       __syncwarp();
-      if (SK != kPlaneModeC || last_in_chunk) {
+      if (plane_tps(SK) == 1 || sub + 1 == c_ntc) {
         if (lane == 0) mbar_arrive(&S.empty[stage]);   // the text of this stage is no longer needed
         if (++stage == kStages) {
           stage = 0;
