@@ -247,7 +247,7 @@ def run_epsm(args, world, rank, local):
     # qualifying searches need, rebuilt inside every step right before that text's groups
     # (its cost is part of the step); those searches stream their planes instead of the text
     idx_vals, ixs = {}, {}
-    if use_batch and world == 1 and args.index:
+    if use_batch and args.index:
         for ti in range(len(texts)):
             v = epsm.index_values([pl for tj, pl in jobs if tj == ti])
             if v:
@@ -270,7 +270,8 @@ def run_epsm(args, world, rank, local):
             # sharded batch: local scan of the owned starts (global positions), then ONE
             # all-gather of the group's counts -> global occ and this rank's output offsets;
             # positions stay on the rank that found them (a distributed, ordered result)
-            epsm.search_range_batch_async(plans_, t_, owned_, base_, occ_loc[j0:j1], outs=outs, stream=stream)
+            epsm.search_range_batch_async(plans_, t_, owned_, base_, occ_loc[j0:j1], outs=outs, stream=stream,
+                                          index=ixs.get(ti))
             occ_g, _off = sharding.exchange_batch_counts(occ_loc[j0:j1])
             occ_buf[j0:j1].copy_(occ_g)
 
@@ -418,7 +419,8 @@ def run_epsm(args, world, rank, local):
                    "api": ("epsm_search_batch_async per (sigma, m) group"
                            + (" + epsm_eqidx_build_async per text (equality-mask index, built inside "
                               "every step)" if ixs else "") if world == 1 else
-                           "epsm_search_range_batch_async + NCCL all-gather of counts per group; "
+                           "epsm_search_range_batch_async (over a per-shard equality-mask index where "
+                           "it qualifies) + NCCL all-gather of counts per group; "
                            "positions kept sharded at their global offsets") if args.batch
                    else "epsm_search_async per search" if world == 1 else "epsm_search_sharded per search"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",

@@ -192,6 +192,16 @@ int epsm_search_batch_index_async(epsm_plan_t *const *plans, uint32_t k,
                                   uint64_t *const *d_pos, const uint64_t *caps,
                                   uint64_t *d_occ, epsm_stream_t stream);
 
+/* epsm_search_range_batch_index_async -- the local step of a sharded batch
+ * (epsm_search_range_batch_async) with the qualifying searches run over `index`,
+ * built over this rank's shard d_text[0..n-1] (same pointer and n). */
+int epsm_search_range_batch_index_async(epsm_plan_t *const *plans, uint32_t k,
+                                        const epsm_eqidx_t *index,
+                                        const uint8_t *d_text, uint64_t n,
+                                        uint64_t owned_len, uint64_t base,
+                                        uint64_t *const *d_pos, const uint64_t *caps,
+                                        uint64_t *d_occ, epsm_stream_t stream);
+
 /* epsm_count_batch_index_async -- as epsm_count_batch_async (counts only, the
  * count kernel) with the qualifying searches run over the index's planes. */
 int epsm_count_batch_index_async(epsm_plan_t *const *plans, uint32_t k,

@@ -82,6 +82,9 @@ _lib.epsm_eqidx_values.argtypes = [_vp, _vp]
 _lib.epsm_eqidx_values.restype = ctypes.c_int
 _lib.epsm_plan_index_values.argtypes = [_vp, _vp]
 _lib.epsm_plan_index_values.restype = ctypes.c_int
+_lib.epsm_search_range_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _u64, _u64, _vp, _vp,
+                                                     _vp, _vp]
+_lib.epsm_search_range_batch_index_async.restype = ctypes.c_int
 _lib.epsm_count_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp]
 _lib.epsm_count_batch_index_async.restype = ctypes.c_int
 _lib.epsm_search_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp, _vp, _vp]
@@ -95,6 +98,7 @@ EXPORTED_SYMBOLS = (
     "epsm_version", "epsm_debug_trace",
     "epsm_eqidx_create", "epsm_eqidx_free", "epsm_eqidx_build_async", "epsm_eqidx_values",
     "epsm_search_batch_index_async", "epsm_count_batch_index_async", "epsm_plan_index_values",
+    "epsm_search_range_batch_index_async",
 )
 MAX_PLANES = 64
 INDEX_MAX_D = 8
@@ -410,11 +414,18 @@ def count_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, stream=N
 
 
 def search_range_batch_async(plans, shard: torch.Tensor, owned_len: int, base: int, occ_out: torch.Tensor,
-                             outs=None, caps=None, stream=None) -> None:
-    """Local step of a sharded batch: starts s < owned_len of ``shard``, reported as s + base."""
+                             outs=None, caps=None, stream=None, index: "EqIndex | None" = None) -> None:
+    """Local step of a sharded batch: starts s < owned_len of ``shard``, reported as s + base
+    (with an EqIndex built over ``shard``, qualifying searches stream its planes)."""
     if len(plans) == 0:
         return
     plans, k, hp, pos_arr, caps_arr = _batch_args(plans, shard, occ_out, outs, caps)
+    if index is not None:
+        _check(_lib.epsm_search_range_batch_index_async(hp, k, index.handle, shard.data_ptr(), shard.numel(),
+                                                        int(owned_len), int(base), pos_arr, caps_arr,
+                                                        occ_out.data_ptr(), _stream_handle(stream, shard.device)),
+               "epsm_search_range_batch_index_async")
+        return
     _check(_lib.epsm_search_range_batch_async(hp, k, shard.data_ptr(), shard.numel(), int(owned_len), int(base),
                                               pos_arr, caps_arr, occ_out.data_ptr(),
                                               _stream_handle(stream, shard.device)),

@@ -414,7 +414,7 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   P.njobs = k;
   P.desc_bytes = (plan0->sk > 0 && !index) ? static_cast<uint32_t>(sizeof(epsm::JobDesc)) : epsm::kJobHeader;
   if (index) {
-    if (mis != 0 || base != 0 || index->text != d_text || index->n != nbytes) {
+    if (mis != 0 || index->text != d_text || index->n != nbytes) {
       epsm_set_error("index searches need the aligned text the index was built over");
       return EPSM_EINVAL;
     }
@@ -879,6 +879,13 @@ int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t
 int epsm_count_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
                            uint64_t* d_occ, epsm_stream_t stream) {
   return batch_common(plans, k, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream);
+}
+
+int epsm_search_range_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,
+                                        const uint8_t* d_text, uint64_t n, uint64_t owned_len, uint64_t base,
+                                        uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ,
+                                        epsm_stream_t stream) {
+  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, true, stream, index);
 }
 
 int epsm_count_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,

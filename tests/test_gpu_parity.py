@@ -493,14 +493,19 @@ def test_emulated_shards_batch_compose(epsm, dev, world):
     plans = [epsm.plan(p) for p in pats]
     wants = [oracle.search(p, t) for p in pats]
     parts = [[] for _ in pats]
-    for r in range(world):
-        base, owned, slen = sharding.shard_layout(n, world, r)
-        occ = torch.zeros(len(pats), dtype=torch.int64, device=dev)
-        outs = [torch.empty(w.size + 1, dtype=torch.int64, device=dev) for w in wants]
-        epsm.search_range_batch_async(plans, td[base:base + slen], owned, base, occ, outs=outs)
-        torch.cuda.synchronize()
-        for j in range(len(pats)):
-            k = int(occ[j])
-            parts[j].append(outs[j][:k].cpu().numpy().astype(np.uint64))
-    for j, w in enumerate(wants):
-        assert np.array_equal(np.concatenate(parts[j]), w), len(pats[j])
+    for use_index in (False, True):
+        parts = [[] for _ in pats]
+        for r in range(world):
+            base, owned, slen = sharding.shard_layout(n, world, r)
+            occ = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+            outs = [torch.empty(w.size + 1, dtype=torch.int64, device=dev) for w in wants]
+            # each rank's shard in its own (aligned) buffer, as make_texts builds it
+            shard = td[base:base + slen].clone()
+            ix = epsm.eq_index(shard, epsm.index_values(plans)) if use_index else None
+            epsm.search_range_batch_async(plans, shard, owned, base, occ, outs=outs, index=ix)
+            torch.cuda.synchronize()
+            for j in range(len(pats)):
+                k = int(occ[j])
+                parts[j].append(outs[j][:k].cpu().numpy().astype(np.uint64))
+        for j, w in enumerate(wants):
+            assert np.array_equal(np.concatenate(parts[j]), w), (use_index, len(pats[j]))
