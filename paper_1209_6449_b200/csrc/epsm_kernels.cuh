@@ -1198,7 +1198,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       }
       }
       const uint32_t tile = c_t0 + sub;
-      const bool last_in_chunk = plane_tps(SK) > 1 ? (sub + 1 == c_ntc && c_last) : c_last;
+      const bool last_in_chunk = c_last;   // (the index variants take a stage's tiles at once)
       const uint32_t b = seq % kParked;
       if (SEARCH && tpos == 0 && seq >= kParked) flush_chunk_seq(seq - kParked);   // free slot b
       const uint8_t* ts = S.ring[stage];
@@ -1269,55 +1269,106 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // r = AND_i (E_{p_i} >> i), exact, no candidates, no check
         const uint32_t wi = cw * 32u + lane;                 // the lane's word in each plane tile
         constexpr uint32_t kPS = plane_stride(SK);
-        const uint8_t* pb = ts + sub * (kTile / 8);         // this tile's words (sub = 0: one tile)
-        uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;
-        const uint32_t np = P.m <= 8 ? 0u : JD->np;          // (warp-uniform)
+        constexpr uint32_t kTPS = plane_tps(SK);             // tiles of this stage (<= c_ntc used)
+        uint64_t Mu[kTPS];
         if (P.m <= 8) {
           // short patterns: position by position, each reading the words of its own plane
-          // (compile-time shifts, no list)
+          // (compile-time shifts, no list); the stage's tiles side by side (independent chains)
+          uint32_t rl[kTPS], rh[kTPS];
+#pragma unroll
+          for (uint32_t u = 0; u < kTPS; ++u) rl[u] = rh[u] = 0xFFFFFFFFu;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (i >= static_cast<int>(P.m)) break;
-            const uint2* pl = reinterpret_cast<const uint2*>(pb + JD->pslot[i] * kPS);
-            const uint2 e = pl[wi];
-            if (i == 0) {
-              rl &= e.x;
-              rh &= e.y;
-            } else {
-              const uint32_t h = pl[wi + 1].x;
-              rl &= __funnelshift_r(e.x, e.y, i);
-              rh &= __funnelshift_r(e.y, h, i);
+            const uint8_t* pp = ts + JD->pslot[i] * kPS;
+#pragma unroll
+            for (uint32_t u = 0; u < kTPS; ++u) {
+              const uint2* pl = reinterpret_cast<const uint2*>(pp + u * (kTile / 8));
+              const uint2 e = pl[wi];
+              if (i == 0) {
+                rl[u] &= e.x;
+                rh[u] &= e.y;
+              } else {
+                const uint32_t h = pl[wi + 1].x;
+                rl[u] &= __funnelshift_r(e.x, e.y, i);
+                rh[u] &= __funnelshift_r(e.y, h, i);
+              }
             }
           }
-        }
 #pragma unroll
-        for (int k = 0; k < kMaxPlaneSlots; ++k) {
-          if (k >= static_cast<int>(np)) break;              // warp-uniform
-          const uint2* pl = reinterpret_cast<const uint2*>(pb + k * kPS);
-          const uint2 e = pl[wi], h = pl[wi + 1];            // starts 0..63, 64..127
-          const uint32_t w0 = JD->pw0[k], wn = JD->pwn[k];
-          bool live = true;
-          for (uint32_t q = 0; q < wn; ++q) {
-            // four positions i with p_i == value of plane k (shift amounts: the funnel shift
-            // uses the low 5 bits, so the packed word is shifted, not masked; no bit scans)
-            const uint32_t sw = JD->plist[w0 + q];
-            rl &= __funnelshift_r(e.x, e.y, sw) & __funnelshift_r(e.x, e.y, sw >> 8) &
-                  __funnelshift_r(e.x, e.y, sw >> 16) & __funnelshift_r(e.x, e.y, sw >> 24);
-            rh &= __funnelshift_r(e.y, h.x, sw) & __funnelshift_r(e.y, h.x, sw >> 8) &
-                  __funnelshift_r(e.y, h.x, sw >> 16) & __funnelshift_r(e.y, h.x, sw >> 24);
-            // no start of the warp's slice survives: the rest of the AND cannot revive one
-            live = __any_sync(0xffffffffu, (rl | rh) != 0u);
-            if (!live) break;
+          for (uint32_t u = 0; u < kTPS; ++u) Mu[u] = (static_cast<uint64_t>(rh[u]) << 32) | rl[u];
+        } else {
+#pragma unroll
+          for (uint32_t u = 0; u < kTPS; ++u) {
+            if (u >= c_ntc) {
+              Mu[u] = 0;
+              continue;
+            }
+            const uint8_t* pb = ts + u * (kTile / 8);
+            uint32_t rl = 0xFFFFFFFFu, rh = 0xFFFFFFFFu;
+            const uint32_t np = JD->np;
+#pragma unroll
+            for (int k = 0; k < kMaxPlaneSlots; ++k) {
+              if (k >= static_cast<int>(np)) break;              // warp-uniform
+              const uint2* pl = reinterpret_cast<const uint2*>(pb + k * kPS);
+              const uint2 e = pl[wi], h = pl[wi + 1];            // starts 0..63, 64..127
+              const uint32_t w0 = JD->pw0[k], wn = JD->pwn[k];
+              bool live = true;
+              for (uint32_t q = 0; q < wn; ++q) {
+                // four positions i with p_i == value of plane k (shift amounts: the funnel
+                // shift uses the low 5 bits, so the packed word is shifted, not masked)
+                const uint32_t sw = JD->plist[w0 + q];
+                rl &= __funnelshift_r(e.x, e.y, sw) & __funnelshift_r(e.x, e.y, sw >> 8) &
+                      __funnelshift_r(e.x, e.y, sw >> 16) & __funnelshift_r(e.x, e.y, sw >> 24);
+                rh &= __funnelshift_r(e.y, h.x, sw) & __funnelshift_r(e.y, h.x, sw >> 8) &
+                      __funnelshift_r(e.y, h.x, sw >> 16) & __funnelshift_r(e.y, h.x, sw >> 24);
+                // no start of the warp's slice survives: the rest of the AND cannot revive one
+                live = __any_sync(0xffffffffu, (rl | rh) != 0u);
+                if (!live) break;
+              }
+              if (!live) break;
+            }
+            Mu[u] = (static_cast<uint64_t>(rh) << 32) | rl;
           }
-          if (!live) break;
         }
-        Meq = (static_cast<uint64_t>(rh) << 32) | rl;
-        if (!interior) {
-          uint64_t rm = 0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            rm |= static_cast<uint64_t>(range_mask(tbase + seg_off + 16u * u, P.s_lo, P.s_hi)) << (16 * u);
-          Meq &= rm;
+        for (uint32_t u = 0; u < kTPS; ++u) {
+          const uint32_t tl = c_t0 + u;
+          if (!(tl >= P.it_lo && tl < P.it_hi)) {              // (warp-uniform) a tile at an end
+            const uint64_t tb = static_cast<uint64_t>(tl) * kTile;
+            uint64_t rm = 0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              rm |= static_cast<uint64_t>(range_mask(tb + seg_off + 16u * v, P.s_lo, P.s_hi)) << (16 * v);
+            Mu[u] &= rm;
+          }
+        }
+        if constexpr (kTPS > 1) {
+          // all but the stage's last tile are parked here; the last goes through the common path
+#pragma unroll
+          for (uint32_t u = 0; u + 1 < kTPS; ++u) {
+            if (u + 1 >= c_ntc) break;                           // warp-uniform
+            if (!__any_sync(0xffffffffu, Mu[u] != 0ull)) continue;
+            const uint32_t c = popc64(Mu[u]);
+            acc += c;
+            if constexpr (SEARCH) {
+              if (!waited) {
+                wait_ws(S);
+                waited = true;
+              }
+              st_keep_u64(scratch_cta + ((b * kChunkTiles + tpos + u) * kConsumerWarps + cw) * 32 + lane, Mu[u],
+                          keep_pol);
+              const uint32_t sc = __reduce_add_sync(0xffffffffu, c);
+              if (lane == 0) S.park[b].cnt[(tpos + u) * kConsumerWarps + cw] = sc;
+              slowbits |= 1u << (kChunkTiles * b + tpos + u);
+            }
+          }
+          Meq = c_ntc == 1 ? Mu[0] : c_ntc == 2 ? Mu[1] : kTPS > 2 && c_ntc == 3 ? Mu[kTPS > 2 ? 2 : 0]
+                                                                         : Mu[kTPS - 1];
+          tpos += c_ntc - 1;
+          sub = c_ntc - 1;
+        } else {
+          Meq = Mu[0];
         }
         slow = __any_sync(0xffffffffu, Meq != 0ull);
       } else if constexpr (SK > 0) {
