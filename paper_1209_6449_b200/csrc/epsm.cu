@@ -768,14 +768,19 @@ static uint32_t index_max_d() {
 
 // Does plans' search run over the index?  Its distinct bytes must all be in the index.  Speed
 // rule (B200, 256 MiB texts, us per search text -> index): the shift-AND over planes wins for
-// m <= 8 at every alphabet the index covers (sigma=2 m=8 137 -> 80, sigma=16 m=4 63 -> 52,
-// sigma=32 m=8 61 -> 56) and for m <= 16 with <= 4 distinct bytes (sigma=2 m=16 68 -> 52);
-// beyond that the text kernels are at the HBM roofline already (m=32: 38 us) and the
-// per-position shifts cost more than the sampled filter.
+// m <= 8 at every alphabet the index covers (sigma=2 m=8 137 -> 59, sigma=16 m=4 63 -> 27,
+// sigma=32 m=8 61 -> 51) and for m <= 24 with <= 4 distinct bytes (sigma=2 m=16 68 -> 43,
+// sigma=4 m=24 48 -> 36); at m = 32 the text kernels are at the HBM roofline already (38 us)
+// and the per-position shifts cost as much; m 9..24 with 5..8 distinct bytes loses to the
+// sampled filter.
 static bool index_worthwhile(const epsm_plan_t* pl) {
+  static const uint32_t max_m = [] {   // EPSM_INDEX_MAX_M: longest pattern with <= 4 bytes (A/B)
+    const char* e = getenv("EPSM_INDEX_MAX_M");
+    return e && e[0] ? static_cast<uint32_t>(strtoul(e, nullptr, 0)) : 24u;
+  }();
   const epsm::JobDesc& D = *pl->h_desc;
   if (pl->m > EPSM_MAX_M || D.np == 0 || D.np > index_max_d()) return false;
-  return pl->m <= 8 || (pl->m <= 16 && D.np <= 4);
+  return pl->m <= 8 || (pl->m <= max_m && D.np <= 4);
 }
 
 static bool use_index(const epsm_plan_t* pl, const epsm_eqidx_t* ix) {
