@@ -156,6 +156,7 @@ KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
   if (sk == epsm::kPlaneMode) return pick<4, 4, 1, epsm::kPlaneMode, 0>(search);   // EPSMa, index
   if (sk == epsm::kPlaneModeC) return pick<4, 4, 1, epsm::kPlaneModeC, 0>(search);
   if (sk == epsm::kPlaneModeC2) return pick<4, 4, 1, epsm::kPlaneModeC2, 0>(search);
+  if (sk == epsm::kPlaneModeC8) return pick<4, 4, 1, epsm::kPlaneModeC8, 0>(search);
   if (sk == 4 && sq == 8) return m == 12 ? pick<4, 4, 3, 4, 8>(search) : pick<4, 4, 4, 4, 8>(search);
   if (sk == 4 && sq == 12) {
     if (m == 16) return pick<4, 4, 4, 4, 12>(search);
@@ -503,11 +504,19 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
     const char* v = getenv("EPSM_INDEXC");
     return !(v && v[0] == '0');
   }();
+  static const bool index8 = [] {
+    const char* v = getenv("EPSM_INDEX8");
+    return !(v && v[0] == '0');
+  }();
   const int pmode = !multi_tile ? epsm::kPlaneMode
                     : max_np <= 2 ? epsm::kPlaneModeC
-                    : max_np <= 4 ? epsm::kPlaneModeC2 : epsm::kPlaneMode;
+                    : max_np <= 4 ? epsm::kPlaneModeC2
+                    : index8      ? epsm::kPlaneModeC8 : epsm::kPlaneMode;
   KernelFn fn = index ? kernel_for(plan0->m, pmode, 0, search) : kernel_for(plan0->m, plan0->sk, plan0->sq, search);
-  const int smem = search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
+  const int smem = (index && pmode == epsm::kPlaneModeC8)
+                       ? (search ? static_cast<int>(sizeof(epsm::Index8Smem<true>))
+                                 : static_cast<int>(sizeof(epsm::Index8Smem<false>)))
+                   : search ? static_cast<int>(sizeof(epsm::SearchSmem)) : static_cast<int>(sizeof(epsm::CountSmem));
   rc = set_smem_attr(fn, plan0->device, smem);
   if (rc) return rc;
   // programmatic dependent launch: the kernel starts while the previous grid on the stream
@@ -841,7 +850,7 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
   for (uint32_t j = 0; j < k; ++j)
     variant[j] = !use_index(plans[j], index) ? plans[j]->sk
                  : plans[j]->h_desc->np <= 2 ? epsm::kPlaneModeC
-                 : plans[j]->h_desc->np <= 4 ? epsm::kPlaneModeC2 : epsm::kPlaneMode;
+                 : plans[j]->h_desc->np <= 4 ? epsm::kPlaneModeC2 : epsm::kPlaneModeC8;
   std::vector<uint32_t> order(k);
   for (uint32_t j = 0; j < k; ++j) order[j] = j;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {

@@ -146,12 +146,13 @@ constexpr int kEqMode = -1;                                       // SK value of
 constexpr int kPlaneMode = -2;                                    // SK of the index variant (<= 8 planes)
 constexpr int kPlaneModeC = -4;                                   // ... <= 2 planes: a chunk per stage
 constexpr int kPlaneModeC2 = -5;                                  // ... <= 4 planes: 2 tiles per stage
+constexpr int kPlaneModeC8 = -6;                                  // ... <= 8 planes: 2 tiles, 2 big stages
 __host__ __device__ constexpr bool is_plane(int sk) {
-  return sk == kPlaneMode || sk == kPlaneModeC || sk == kPlaneModeC2;
+  return sk == kPlaneMode || sk == kPlaneModeC || sk == kPlaneModeC2 || sk == kPlaneModeC8;
 }
 // tiles per ring stage and bytes per plane in a stage (tiles' words + the halo word)
 __host__ __device__ constexpr uint32_t plane_tps(int sk) {
-  return sk == kPlaneModeC ? 4u : sk == kPlaneModeC2 ? 2u : 1u;
+  return sk == kPlaneModeC ? 4u : (sk == kPlaneModeC2 || sk == kPlaneModeC8) ? 2u : 1u;
 }
 __host__ __device__ constexpr uint32_t plane_stride(int sk) { return plane_tps(sk) * (kTile / 8) + 16; }
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
@@ -258,6 +259,12 @@ using SearchSmem = SmemLayoutT<kStagesSearch, true>;
 using CountSmem = SmemLayoutT<kStagesCount, false>;
 template <bool SEARCH>
 using SmemFor = typename std::conditional<SEARCH, SearchSmem, CountSmem>::type;
+// index variant for 5..8 planes: 2 stages of 2 tiles of 8 planes each
+template <bool SEARCH>
+using Index8Smem = SmemLayoutT<2, SEARCH, kMaxPlaneSlots * (2 * (kTile / 8) + 16)>;
+static_assert(sizeof(Index8Smem<true>) <= 232448, "index-8 layout fits 227 KB of shared memory");
+template <bool SEARCH, int SK>
+using SmemForK = typename std::conditional<SK == kPlaneModeC8, Index8Smem<SEARCH>, SmemFor<SEARCH>>::type;
 
 // ------------------------------------------------------------------ PTX helpers
 
@@ -906,7 +913,7 @@ __device__ __forceinline__ void load_segment(const uint8_t* seg, uint32_t rot, u
 template <int F, int F2, int MW, int SK, int SQ, bool SEARCH>
 __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using Smem = SmemFor<SEARCH>;
+  using Smem = SmemForK<SEARCH, SK>;
   constexpr int kStages = Smem::kStages;
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
