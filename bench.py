@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--breakdown", action="store_true", help="per-(sigma, m) timing pass (stderr)")
     ap.add_argument("--no-index", dest="index", action="store_false",
                     help="no equality-mask index (every search scans the text)")
+    ap.add_argument("--index-max-sigma", type=int, default=1 << 30,
+                    help="no index for texts of a larger alphabet (profiling runs with few patterns "
+                         "use 64 to mirror the default sweep, where sigma >= 128 needs > 64 values)")
     ap.add_argument("--no-batch", dest="batch", action="store_false",
                     help="one launch per search (epsm_search_async) instead of the batch API")
     return ap.parse_args()
@@ -249,6 +252,8 @@ def run_epsm(args, world, rank, local):
     idx_vals, ixs = {}, {}
     if use_batch and args.index:
         for ti in range(len(texts)):
+            if texts[ti][0] > args.index_max_sigma:
+                continue
             v = epsm.index_values([pl for tj, pl in jobs if tj == ti])
             if v:
                 idx_vals[ti] = v

@@ -23,6 +23,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="3,4,5a,5b")
 ap.add_argument("--patterns", type=int, default=40, help="patterns per (config, m)")
 ap.add_argument("--reps", type=int, default=2, help="timed repetitions (best is reported)")
+ap.add_argument("--no-index", dest="index", action="store_false",
+                help="text kernels only (no equality-mask index)")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 stream = torch.cuda.current_stream(dev)
@@ -30,6 +32,26 @@ result = {}
 for cfg in a.configs.split(","):
     for w in synth.config_workloads(cfg):
         text = synth.text_torch(w.spec, 0, w.n, device=dev)
+        # the text's equality-mask index over the values its qualifying searches need (built
+        # once per text, timed separately: its cost is shared by every search of the text)
+        ix, build_us = None, 0.0
+        if a.index:
+            allp = [epsm.plan(p) for m in w.ms
+                    for p in synth.extract_patterns_torch(text, w.start_seed(m), m,
+                                                          min(a.patterns, w.patterns_per_m))[0]]
+            vals = epsm.index_values(allp)
+            for p in allp:
+                p.close()
+            if vals:
+                ix = epsm.EqIndex()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                ix.build_async(text, vals, stream=stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                build_us = e0.elapsed_time(e1) * 1e3
+                result[f"{w.name}/index_build"] = {"us": round(build_us, 1), "values": len(vals)}
+                print(f"{w.name}: index of {len(vals)} values built in {build_us:.1f} us", file=sys.stderr)
         for m in w.ms:
             count = min(a.patterns, w.patterns_per_m)
             pats, _ = synth.extract_patterns_torch(text, w.start_seed(m), m, count)
@@ -47,7 +69,7 @@ for cfg in a.configs.split(","):
             for _ in range(a.reps + 1):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                epsm.search_batch_async(plans, text, occ, outs=outs, stream=stream)
+                epsm.search_batch_async(plans, text, occ, outs=outs, stream=stream, index=ix)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 t = e0.elapsed_time(e1) * 1e-3 / len(plans)
@@ -63,6 +85,8 @@ for cfg in a.configs.split(","):
             del pool, outs
             for p in plans:
                 p.close()
+        if ix is not None:
+            ix.close()
         del text
         torch.cuda.empty_cache()
 print(json.dumps(result))

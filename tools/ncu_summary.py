@@ -31,6 +31,17 @@ def traffic(path, out_json, out_txt):
             continue
         per.setdefault(r["ID"], {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
     allk = [per[k] for k in sorted(per, key=int)]
+    # keep the last len(SIGMAS) * len(MS) scans and the index builds among them (the capture
+    # may hold earlier passes: the count pass, warm-up steps)
+    nscan = 0
+    for i in range(len(allk) - 1, -1, -1):
+        if "epsm_scan" in allk[i]["kernel"]:
+            nscan += 1
+            if nscan == len(SIGMAS) * len(MS):
+                while i > 0 and "epsm_eqidx" in allk[i - 1]["kernel"]:
+                    i -= 1
+                allk = allk[i:]
+                break
     lines = ["sigma m  time_us  dram_read_MB  dram_write_MB   (m = 0: equality-mask index build)"]
     tot = 0.0
     launches = []
