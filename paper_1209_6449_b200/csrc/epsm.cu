@@ -104,7 +104,8 @@ void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
     if (m <= 11) *sk = 4, *sq = 4;
     else if (m <= 15) *sk = 8, *sq = 4;
     else if (m <= 23) *sk = 8, *sq = 8;
-    else if (m <= 31) *sk = 8, *sq = 16;
+    else if (m <= 27) *sk = 16, *sq = 8;     // one 8-byte gram per 16-byte unit (SK + SQ <= m)
+    else if (m <= 31) *sk = 16, *sq = 12;    // one 12-byte gram per unit
     else *sk = 16, *sq = 16;
     // small alphabets (few distinct bytes): longer grams at a 4-byte stride -- four lookups
     // per unit, but far fewer candidates to check (genome-like m = 12: 300 -> ~240 us/GiB)
@@ -163,6 +164,8 @@ KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
     if (m <= 20) return pick<4, 4, 5, 4, 12>(search);
     return pick<4, 4, 6, 4, 12>(search);
   }
+  if (sk == 16 && sq == 8) return m <= 24 ? pick<4, 4, 6, 16, 8>(search) : pick<4, 4, 7, 16, 8>(search);
+  if (sk == 16 && sq == 12) return pick<4, 4, 8, 16, 12>(search);
   if (sk > 0) {
     switch (m) {
       case 8: return pick<4, 4, 2, 4, 4>(search);

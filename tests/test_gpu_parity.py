@@ -286,7 +286,7 @@ def test_sampled_filter_repeated_and_periodic_grams(epsm, dev):
     and periodic texts where every sample hits: the sampled filter's candidate masks."""
     rng = np.random.default_rng(4242)
     n = 2 * CHUNK + 12345
-    for m in (9, 11, 12, 15, 16, 17, 23, 24, 25, 31, 32):
+    for m in (9, 11, 12, 15, 16, 17, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32):
         for unit in (b"a", b"ab", b"abc", b"abcd", b"aab", b"abcdefgh"):
             p = (unit * 40)[:m]
             t = np.frombuffer((unit * (n // len(unit) + 1))[:n], dtype=np.uint8).copy()
