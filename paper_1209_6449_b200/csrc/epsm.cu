@@ -103,14 +103,26 @@ void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
   } else if (m >= 8 && (mid ? (take_mid || sample_min_m() <= 8) : m >= sample_min_m())) {
     if (m <= 11) *sk = 4, *sq = 4;
     else if (m <= 15) *sk = 8, *sq = 4;
-    else if (m <= 23) *sk = 8, *sq = 8;
-    else if (m <= 27) *sk = 16, *sq = 8;     // one 8-byte gram per 16-byte unit (SK + SQ <= m)
+    else if (m <= 19) *sk = 8, *sq = 8;
+    else if (m <= 23) *sk = 16, *sq = 4;     // one 4-byte gram per 16-byte unit (SK + SQ <= m)
+    else if (m <= 27) *sk = 16, *sq = 8;     // one 8-byte gram per unit
     else if (m <= 31) *sk = 16, *sq = 12;    // one 12-byte gram per unit
     else *sk = 16, *sq = 16;
     // small alphabets (few distinct bytes): longer grams at a 4-byte stride -- four lookups
     // per unit, but far fewer candidates to check (genome-like m = 12: 300 -> ~240 us/GiB)
     if (m >= 12 && m <= 15 && d <= 5) *sk = 4, *sq = 8;
     else if (m >= 16 && m <= 23 && d <= 2) *sk = 4, *sq = 12;
+  }
+  // EPSM_GEOM="m:sk:sq" overrides the geometry of one pattern length (A/B timing; the kernel
+  // must exist for it -- see kernel_for)
+  static const int g_m = [] {
+    const char* e = getenv("EPSM_GEOM");
+    return e && e[0] ? atoi(e) : 0;
+  }();
+  if (g_m > 0 && static_cast<uint32_t>(g_m) == m) {
+    const char* e = getenv("EPSM_GEOM");
+    int a = 0, b = 0, c = 0;
+    if (sscanf(e, "%d:%d:%d", &a, &b, &c) == 3 && b + c <= static_cast<int>(m)) *sk = b, *sq = c;
   }
 }
 
@@ -164,6 +176,8 @@ KernelFn kernel_for(uint32_t m, int sk, int sq, bool search) {
     if (m <= 20) return pick<4, 4, 5, 4, 12>(search);
     return pick<4, 4, 6, 4, 12>(search);
   }
+  if (sk == 16 && sq == 4) return m <= 20 ? pick<4, 4, 5, 16, 4>(search) : pick<4, 4, 6, 16, 4>(search);
+  if (sk == 8 && sq == 4 && m == 16) return pick<4, 4, 4, 8, 4>(search);
   if (sk == 16 && sq == 8) return m <= 24 ? pick<4, 4, 6, 16, 8>(search) : pick<4, 4, 7, 16, 8>(search);
   if (sk == 16 && sq == 12) return pick<4, 4, 8, 16, 12>(search);
   if (sk > 0) {
