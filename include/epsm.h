@@ -63,7 +63,7 @@ extern "C" {
 
 typedef struct epsm_plan_s epsm_plan_t;   /* opaque, host-owned */
 typedef struct epsm_eqidx_s epsm_eqidx_t; /* opaque, host-owned (equality-mask index) */
-#define EPSM_MAX_PLANES 64u  /* byte values one equality-mask index holds                  */
+#define EPSM_MAX_PLANES 256u /* byte values one equality-mask index holds (all of them)    */
 #define EPSM_INDEX_MAX_D 8u  /* distinct pattern bytes a search over an index may have     */
 typedef void *epsm_stream_t;              /* a cudaStream_t     */
 
@@ -163,7 +163,7 @@ int epsm_count_batch_async(epsm_plan_t *const *plans, uint32_t k,
  *   same text.  Growing the planes re-allocates (synchronises the stream).
  *   Returns EPSM_OK or EPSM_EINVAL (NULL, nv out of range, duplicate values,
  *   n > 2^38), EPSM_EALIGN, EPSM_ENOMEM, EPSM_ECUDA.
- * epsm_eqidx_values -- the values the index holds: writes up to 64 bytes into
+ * epsm_eqidx_values -- the values the index holds: writes up to 256 bytes into
  *   out_values and returns nv (0 before the first build).
  */
 int epsm_eqidx_create(epsm_eqidx_t **out);

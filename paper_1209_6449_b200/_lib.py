@@ -100,7 +100,7 @@ EXPORTED_SYMBOLS = (
     "epsm_search_batch_index_async", "epsm_count_batch_index_async", "epsm_plan_index_values",
     "epsm_search_range_batch_index_async",
 )
-MAX_PLANES = 64
+MAX_PLANES = 256
 INDEX_MAX_D = 8
 
 

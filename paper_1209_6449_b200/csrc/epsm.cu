@@ -1033,7 +1033,7 @@ int epsm_eqidx_build_async(epsm_eqidx_t* ix, const uint8_t* d_text, uint64_t n, 
   for (uint32_t q = 0; q < nv; ++q) {
     ix->vals[q] = values[q];
     ix->plane_of[values[q]] = static_cast<int16_t>(q);
-    P.vb[q] = 0x01010101u * values[q];
+    P.vals[q] = values[q];
   }
   int sms = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1041,7 +1041,11 @@ int epsm_eqidx_build_async(epsm_eqidx_t* ix, const uint8_t* d_text, uint64_t n, 
   const uint64_t want = (pstride + 255) / 256;
   const uint64_t cap = static_cast<uint64_t>(sms) * 16;
   const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
-  epsm::epsm_eqidx_kernel<<<grid, 256, 0, s>>>(P);
+  // few values: compare the bytes per value; many: bit-slice once, then 16 logic ops per value
+  if (nv >= 8)
+    epsm::epsm_eqidx_bits_kernel<<<grid, 256, 0, s>>>(P);
+  else
+    epsm::epsm_eqidx_kernel<<<grid, 256, 0, s>>>(P);
   epsm_count_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_eqidx_kernel launch");

@@ -1657,15 +1657,74 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 // of a batch over that text reads the masks of its own distinct bytes instead of recomputing
 // them from the text: plane k, word w, bit i = [t[64w + i] == vals[k]]; zero past n and in the
 // padding words up to pstride (the search kernel streams whole tiles + one halo word).
-constexpr int kMaxPlanes = 64;
+constexpr int kMaxPlanes = 256;
 struct IdxParams {
   const uint8_t* text;          // 16-byte aligned
   uint64_t n;
   uint64_t* planes;             // nv planes of pstride words
   uint64_t pstride;
   uint32_t nv;
-  uint32_t vb[kMaxPlanes];      // vals[k] * 0x01010101
+  uint8_t vals[kMaxPlanes];     // the byte value of plane k
 };
+
+// The 64 bytes of text word w (bytes past n read as 0; `valid` masks their starts).
+__device__ __forceinline__ void idx_load_word(const IdxParams& P, uint64_t w, uint32_t (&W)[16], uint64_t& valid) {
+  const uint64_t b0 = w * 64;
+  valid = ~0ull;
+  if (b0 + 64 <= P.n) {
+    const uint4* src = reinterpret_cast<const uint4*>(P.text + b0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint4 v = __ldg(src + r);
+      W[4 * r] = v.x;
+      W[4 * r + 1] = v.y;
+      W[4 * r + 2] = v.z;
+      W[4 * r + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) W[q] = 0;
+    const uint32_t have = b0 < P.n ? static_cast<uint32_t>(P.n - b0) : 0u;
+    for (uint32_t i = 0; i < have; ++i) W[i >> 2] |= static_cast<uint32_t>(P.text[b0 + i]) << (8 * (i & 3));
+    valid = have ? (1ull << have) - 1ull : 0ull;
+  }
+}
+
+// Many values: bit-slice the 64 bytes once (8 masks: bit b of every byte), then every value's
+// plane word is an AND of 8 masks or their complements -- ~16 logic ops per value instead of
+// ~110 for comparing the bytes again.
+__global__ void __launch_bounds__(256) epsm_eqidx_bits_kernel(const __grid_constant__ IdxParams P) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < P.pstride; w += stride) {
+    uint32_t W[16];
+    uint64_t valid;
+    idx_load_word(P, w, W, valid);
+    uint32_t lo[8], hi[8];                                  // bit b of the bytes at 0-31, 32-63
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      uint32_t l = 0, h = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        l |= ((((W[k] >> b) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+        h |= ((((W[k + 8] >> b) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+      }
+      lo[b] = l;
+      hi[b] = h;
+    }
+    const uint32_t vl = static_cast<uint32_t>(valid), vh = static_cast<uint32_t>(valid >> 32);
+    for (uint32_t q = 0; q < P.nv; ++q) {
+      const uint32_t v = P.vals[q];
+      uint32_t rl = vl, rh = vh;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t flip = ((v >> b) & 1u) - 1u;          // 0: bit set, ~0: bit clear
+        rl &= lo[b] ^ flip;
+        rh &= hi[b] ^ flip;
+      }
+      P.planes[q * P.pstride + w] = (static_cast<uint64_t>(rh) << 32) | rl;
+    }
+  }
+}
 
 __global__ void __launch_bounds__(256) epsm_eqidx_kernel(const __grid_constant__ IdxParams P) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -1689,7 +1748,7 @@ __global__ void __launch_bounds__(256) epsm_eqidx_kernel(const __grid_constant__
       valid = have ? (1ull << have) - 1ull : 0ull;
     }
     for (uint32_t k = 0; k < P.nv; ++k) {
-      const uint32_t vb = P.vb[k];
+      const uint32_t vb = 0x01010101u * P.vals[k];
       uint64_t M = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {

@@ -164,7 +164,7 @@ def test_index_build_errors(epsm, dev):
             ix.build_async(buf, b"\x00\x00")            # duplicate value
         assert e.value.code == epsm.EPSM_EINVAL
         with pytest.raises(epsm.EpsmError):
-            ix.build_async(buf, bytes(range(65)))       # more than 64 planes
+            ix.build_async(buf, bytes(range(256)) + b"\x00")   # more than 256 planes (and a duplicate)
         with pytest.raises(epsm.EpsmError):
             ix.build_async(buf, b"")
     finally:
@@ -189,3 +189,19 @@ def test_index_many_values(epsm, dev):
     with epsm.eq_index(td, bytes(range(100, 164))) as ix:   # none of these bytes occur
         res = run_batch(epsm, [bytes([100, 101]), bytes([100]) * 5], td, ix)
     assert all(k == 0 for k, _ in res)
+
+
+def test_index_all_256_values(epsm, dev):
+    """Every byte value has a plane (bit-sliced build); short patterns over a 256-letter text,
+    including bytes 0x00 and 0xFF and a ragged tail."""
+    rng = np.random.default_rng(256)
+    n = 3 * TILE + 4321
+    t = rng.integers(0, 256, size=n, dtype=np.uint8)
+    pats = [t[s:s + m].tobytes() for m in (1, 2, 3, 4, 8) for s in rng.integers(0, n - m, 5)]
+    pats += [b"\x00\xff", b"\xff\x00", b"\x00" * 3, t[n - 4:].tobytes()]
+    t = planted_text(rng, n, 256, pats)
+    td = torch.from_numpy(t).to(dev)
+    with epsm.eq_index(td, bytes(range(256))) as ix:
+        assert ix.values == bytes(range(256))
+        res = run_batch(epsm, pats, td, ix)
+    assert_parity(pats, res, t, "256 planes")
