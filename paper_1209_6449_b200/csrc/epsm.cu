@@ -806,7 +806,11 @@ static bool index_worthwhile(const epsm_plan_t* pl) {
   }();
   const epsm::JobDesc& D = *pl->h_desc;
   if (pl->m > EPSM_MAX_M || D.np == 0 || D.np > index_max_d()) return false;
-  return pl->m <= 8 || (pl->m <= max_m && D.np <= 4);
+  static const uint32_t any_d_m = [] {   // EPSM_INDEX_ANYD_M: longest pattern with any d <= 8 (A/B)
+    const char* e = getenv("EPSM_INDEX_ANYD_M");
+    return e && e[0] ? static_cast<uint32_t>(strtoul(e, nullptr, 0)) : 8u;
+  }();
+  return pl->m <= any_d_m || (pl->m <= max_m && D.np <= 4);
 }
 
 static bool use_index(const epsm_plan_t* pl, const epsm_eqidx_t* ix) {

@@ -1277,15 +1277,17 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         const uint32_t wi = cw * 32u + lane;                 // the lane's word in each plane tile
         constexpr uint32_t kPS = plane_stride(SK);
         constexpr uint32_t kTPS = plane_tps(SK);             // tiles of this stage (<= c_ntc used)
+        constexpr uint32_t kPosMax = 8;                      // position by position up to this m
+                                                             // (16 measured slower at d = 8)
         uint64_t Mu[kTPS];
-        if (P.m <= 8) {
+        if (P.m <= kPosMax) {
           // short patterns: position by position, each reading the words of its own plane
           // (compile-time shifts, no list); the stage's tiles side by side (independent chains)
           uint32_t rl[kTPS], rh[kTPS];
 #pragma unroll
           for (uint32_t u = 0; u < kTPS; ++u) rl[u] = rh[u] = 0xFFFFFFFFu;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < static_cast<int>(kPosMax); ++i) {
             if (i >= static_cast<int>(P.m)) break;
             const uint8_t* pp = ts + JD->pslot[i] * kPS;
 #pragma unroll
