@@ -165,7 +165,8 @@ class Plan:
         """epsm_plan_index_values: the bytes this search reads from an index (b"" if it never
         runs over one)."""
         buf = ctypes.create_string_buffer(8)
-        return buf.raw[:_lib.epsm_plan_index_values(self.handle, buf)]
+        d = _lib.epsm_plan_index_values(self.handle, buf)
+        return buf.raw[:d]
 
     @property
     def handle(self):
