@@ -205,3 +205,45 @@ def test_index_all_256_values(epsm, dev):
         assert ix.values == bytes(range(256))
         res = run_batch(epsm, pats, td, ix)
     assert_parity(pats, res, t, "256 planes")
+
+
+def test_index_empty_and_short_texts(epsm, dev):
+    """n = 0 and n < m over an index: no occurrence, occ written as 0."""
+    buf = torch.zeros(64, dtype=torch.uint8, device=dev)
+    for n in (0, 1, 3):
+        td = buf[:n]
+        plans = [epsm.plan(p) for p in (b"\x00", b"\x00\x00", b"\x00\x00\x00\x00", b"\x01\x00")]
+        occ = torch.full((len(plans),), -1, dtype=torch.int64, device=dev)
+        outs = [torch.empty(4, dtype=torch.int64, device=dev) for _ in plans]
+        with epsm.eq_index(td, b"\x00\x01") as ix:
+            epsm.search_batch_async(plans, td, occ, outs=outs, index=ix)
+            torch.cuda.synchronize()
+        want = [max(0, n - len(p.pattern) + 1) if set(p.pattern) == {0} else 0 for p in plans]
+        assert occ.cpu().tolist() == want, (n, occ.cpu().tolist())
+        for j, w in enumerate(want):
+            assert outs[j][:w].cpu().tolist() == list(range(w))
+
+
+def test_index_on_another_stream(epsm, dev):
+    """Build and searches ordered on a side stream (the index is stream-ordered like the rest)."""
+    rng = np.random.default_rng(9)
+    n = CHUNK + 777
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    pats = [t[s:s + m].tobytes() for m in (2, 4, 8) for s in (5, n // 3)]
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    plans = [epsm.plan(p) for p in pats]
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    outs = [torch.empty(n, dtype=torch.int64, device=dev) for _ in pats]
+    ix = epsm.EqIndex()
+    try:
+        ix.build_async(td, epsm.index_values(plans), stream=side)
+        epsm.search_batch_async(plans, td, occ, outs=outs, stream=side, index=ix)
+        side.synchronize()
+        for j, p in enumerate(pats):
+            want = oracle.search(p, t)
+            assert int(occ[j]) == want.size
+            assert np.array_equal(outs[j][:want.size].cpu().numpy().astype(np.uint64), want)
+    finally:
+        ix.close()
