@@ -175,7 +175,7 @@ int epsm_eqidx_values(const epsm_eqidx_t *index, uint8_t *out_values);
 /* epsm_plan_index_values -- the byte values a search with this plan would read
  * from an index: writes its d <= EPSM_INDEX_MAX_D distinct pattern bytes (in order
  * of first occurrence) into out_values and returns d, or returns 0 if the plan
- * never runs over an index (m > 24, more than 4 distinct bytes at 9 <= m <= 24,
+ * never runs over an index (m > 31, more than 4 distinct bytes at 9 <= m <= 31,
  * or more than EPSM_INDEX_MAX_D; there the text kernels are faster). */
 int epsm_plan_index_values(const epsm_plan_t *plan, uint8_t *out_values);
 

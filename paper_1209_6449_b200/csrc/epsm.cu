@@ -104,9 +104,11 @@ void sampled_geometry(uint32_t m, const uint8_t* pattern, int* sk, int* sq) {
     if (m <= 11) *sk = 4, *sq = 4;
     else if (m <= 15) *sk = 8, *sq = 4;
     else if (m <= 19) *sk = 8, *sq = 8;
-    else if (m <= 23) *sk = 16, *sq = 4;     // one 4-byte gram per 16-byte unit (SK + SQ <= m)
-    else if (m <= 27) *sk = 16, *sq = 8;     // one 8-byte gram per unit
-    else if (m <= 31) *sk = 16, *sq = 12;    // one 12-byte gram per unit
+    // one gram per 16-byte unit (SK + SQ <= m) where the pattern's bytes carry enough entropy
+    // for a short gram; binary patterns keep two longer grams per unit
+    else if (m <= 23) *sk = d <= 2 ? 8 : 16, *sq = d <= 2 ? 8 : 4;
+    else if (m <= 27) *sk = d <= 2 ? 8 : 16, *sq = d <= 2 ? 16 : 8;
+    else if (m <= 31) *sk = d <= 2 ? 8 : 16, *sq = d <= 2 ? 16 : 12;
     else *sk = 16, *sq = 16;
     // small alphabets (few distinct bytes): longer grams at a 4-byte stride -- four lookups
     // per unit, but far fewer candidates to check (genome-like m = 12: 300 -> ~240 us/GiB)
@@ -795,14 +797,14 @@ static uint32_t index_max_d() {
 // Does plans' search run over the index?  Its distinct bytes must all be in the index.  Speed
 // rule (B200, 256 MiB texts, us per search text -> index): the shift-AND over planes wins for
 // m <= 8 at every alphabet the index covers (sigma=2 m=8 137 -> 59, sigma=16 m=4 63 -> 27,
-// sigma=32 m=8 61 -> 51) and for m <= 24 with <= 4 distinct bytes (sigma=2 m=16 68 -> 43,
-// sigma=4 m=24 48 -> 36); at m = 32 the text kernels are at the HBM roofline already (38 us)
-// and the per-position shifts cost as much; m 9..24 with 5..8 distinct bytes loses to the
-// sampled filter.
+// sigma=32 m=8 61 -> 51) and for m <= 31 with <= 4 distinct bytes (sigma=2 m=16 68 -> 43,
+// sigma=2 m=24 48 -> 40, sigma=4 m=24 38 -> 36); at m = 32 the text kernels are at the HBM
+// roofline already (38 us) and the per-position shifts cost as much (binary texts: 38 -> 39);
+// m 9..31 with 5..8 distinct bytes loses to the sampled filter.
 static bool index_worthwhile(const epsm_plan_t* pl) {
   static const uint32_t max_m = [] {   // EPSM_INDEX_MAX_M: longest pattern with <= 4 bytes (A/B)
     const char* e = getenv("EPSM_INDEX_MAX_M");
-    return e && e[0] ? static_cast<uint32_t>(strtoul(e, nullptr, 0)) : 24u;
+    return e && e[0] ? static_cast<uint32_t>(strtoul(e, nullptr, 0)) : 31u;
   }();
   const epsm::JobDesc& D = *pl->h_desc;
   if (pl->m > EPSM_MAX_M || D.np == 0 || D.np > index_max_d()) return false;

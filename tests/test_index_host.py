@@ -1,7 +1,7 @@
 """Host-side logic of the equality-mask index (no GPU: plans are built on the host).
 
 Which searches of a batch run over an index (epsm_plan_index_values): the pattern's distinct
-bytes in order of first occurrence, for m <= 8 with at most 8 distinct bytes, or m <= 24 with
+bytes in order of first occurrence, for m <= 8 with at most 8 distinct bytes, or m <= 31 with
 at most 4; everything else keeps the text kernels.  index_values() is the union a batch needs.
 Also the C-side argument checks of the index entry points that fail before any device work.
 """
@@ -26,7 +26,8 @@ def epsm():
     (b"abcdefghi", b""),                                 # m = 9, d = 9: text kernels
     (b"abcdabcdabcdabcdabcdabcd", b"abcd"),               # m = 24, d = 4
     (b"abcdeabcdeabcdeabcdeabcd", b""),                  # m = 24, d = 5
-    (b"ab" * 12 + b"a", b""),                            # m = 25: text kernels
+    (b"ab" * 12 + b"a", b"ab"),                          # m = 25, d = 2
+    (b"ab" * 16, b""),                                   # m = 32: text kernels
     (b"aaaaaaaaaaaaaaaa", b"a"),                         # m = 16, d = 1
     (b"x" * 33, b""),                                    # long pattern
 ])
