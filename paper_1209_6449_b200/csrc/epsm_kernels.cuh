@@ -1089,6 +1089,30 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         mbar_wait_suspend(&S.lb_full[q], par);
         const ChunkSlot sl = S.slot[q];
         if (sl.chunk == kInfoEnd) break;
+        {
+          // exclusive prefix over the chunk's 64 slice counts in text order (tile, warp), for
+          // the consumers' write-out (they wait for lb_done before reading it)
+          ParkedChunk& pk = S.park[sl.park];
+          const uint32_t ntiles = pk.ntiles;
+          constexpr int kPerLane = (kSlices + 31) / 32;
+          uint32_t v[kPerLane], sum = 0;
+#pragma unroll
+          for (int i = 0; i < kPerLane; ++i) {
+            const uint32_t si = lane * kPerLane + i;
+            const uint32_t t = si / kConsumerWarps;
+            const uint32_t w = si % kConsumerWarps;
+            v[i] = (si < static_cast<uint32_t>(kSlices) && t < ntiles && ((pk.slow[w] >> t) & 1u)) ? pk.cnt[si] : 0u;
+            sum += v[i];
+          }
+          const uint32_t incl = warp_inclusive_scan(sum, lane);
+          uint32_t run = incl - sum;
+#pragma unroll
+          for (int i = 0; i < kPerLane; ++i) {
+            if (lane * kPerLane + i < static_cast<uint32_t>(kSlices)) pk.off[lane * kPerLane + i] = run;
+            run += v[i];
+          }
+          __syncwarp();
+        }
         // a chunk without occurrences needs no prefix of its own; its look-back only helps
         // successors (an inclusive status shortens their walks), so it is dropped once every
         // consumer warp of this CTA is done and the CTA could otherwise exit
@@ -1561,27 +1585,19 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       prev = __shfl_sync(0xffffffffu, prev, 0);
       if (prev == kConsumerWarps - 1) {
         __threadfence_block();
-        // exclusive prefix over the 64 slice counts in text order (tile, warp); slices of
-        // warps that parked nothing for a tile count zero
+        // the chunk's total over the 64 slice counts (slices of warps that parked nothing for
+        // a tile count zero); the exclusive slice offsets are left to the look-back warp
         constexpr int kPerLane = (kSlices + 31) / 32;
-        uint32_t v[kPerLane], sum = 0;
+        uint32_t sum = 0;
 #pragma unroll
         for (int i = 0; i < kPerLane; ++i) {
           const uint32_t sl = lane * kPerLane + i;              // text order (>= kSlices: none)
           const uint32_t t = sl / kConsumerWarps;
           const uint32_t w = sl % kConsumerWarps;
-          v[i] = (sl < static_cast<uint32_t>(kSlices) && t < ntiles && ((S.park[b].slow[w] >> t) & 1u))
+          sum += (sl < static_cast<uint32_t>(kSlices) && t < ntiles && ((S.park[b].slow[w] >> t) & 1u))
                      ? S.park[b].cnt[sl] : 0u;
-          sum += v[i];
         }
-        const uint32_t incl = warp_inclusive_scan(sum, lane);
-        uint32_t run = incl - sum;
-#pragma unroll
-        for (int i = 0; i < kPerLane; ++i) {
-          if (lane * kPerLane + i < static_cast<uint32_t>(kSlices)) S.park[b].off[lane * kPerLane + i] = run;
-          run += v[i];
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t total = __reduce_add_sync(0xffffffffu, sum);
         if (seq >= kSlots) wait_done(seq - kSlots);          // slot seq % kSlots is free again
         if (lane == 0) {
           S.park[b].done = 0;
