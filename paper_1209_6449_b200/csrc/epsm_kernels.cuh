@@ -232,6 +232,8 @@ struct __align__(16) ParkedChunk {   // per parking slot
   uint32_t total;               // occurrences (hand-off warp)
   uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
   uint32_t done;                // consumer warps finished with the chunk (smem atomic)
+  uint32_t job;                 // search of the chunk, chunk / nchunks  (look-back warp)
+  uint32_t cidx;                // chunk index inside its search, chunk % nchunks
   uint8_t slow[kConsumerWarps]; // bit t: the warp parked masks for tile t (else all zero)
 };
 
@@ -820,7 +822,7 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
   const ParkedChunk& pk = S.park[b];
   if (pk.total == 0 || slow == 0) return;                      // warp-uniform
   const unsigned long long prefix = pk.prefix;
-  const JobRef& J = P.jobs[pk.chunk / P.nchunks];
+  const JobRef& J = P.jobs[pk.job];
   if (prefix >= J.cap) return;
   if (!out_ok) {                      // the previous grid on the stream may write the same output
     griddep_wait();
@@ -828,7 +830,7 @@ __device__ __forceinline__ void flush_slices(const KParams& P, Smem& S, const ui
   }
   uint64_t* const pos = J.pos;
   const uint64_t cap = J.cap;
-  const uint64_t cbase = static_cast<uint64_t>(pk.chunk % P.nchunks) * kChunkBytes + P.pos_bias;
+  const uint64_t cbase = static_cast<uint64_t>(pk.cidx) * kChunkBytes + P.pos_bias;
   uint16_t* stage = S.wstage[cw];
   const uint32_t nt = pk.ntiles;
   uint64_t mk4[kChunkTiles];
@@ -1116,7 +1118,12 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         // a chunk without occurrences needs no prefix of its own; its look-back only helps
         // successors (an inclusive status shortens their walks), so it is dropped once every
         // consumer warp of this CTA is done and the CTA could otherwise exit
-        const bool last = (sl.chunk % P.nchunks) + 1 == P.nchunks;   // its prefix gives occ
+        const uint32_t cidx = sl.chunk % P.nchunks;
+        const bool last = cidx + 1 == P.nchunks;                  // its prefix gives occ
+        if (lane == 0) {                                          // (no divisions in the write-out)
+          S.park[sl.park].job = sl.chunk / P.nchunks;
+          S.park[sl.park].cidx = cidx;
+        }
         const volatile uint32_t* fin = (sl.total == 0 && !last) ? &S.fin : nullptr;
         const bool skip = fin && *fin == static_cast<uint32_t>(kConsumerWarps);
         const unsigned long long pre = skip ? kAborted : lookback(P, sl.chunk, sl.total, lane, fin);
