@@ -233,6 +233,7 @@ struct __align__(16) ParkedChunk {   // per parking slot
   uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
   uint32_t done;                // consumer warps finished with the chunk (smem atomic)
   uint32_t job;                 // search of the chunk, chunk / nchunks  (look-back warp)
+  uint32_t scanned;             // sequence number of the chunk whose counts were last scanned
   uint32_t cidx;                // chunk index inside its search, chunk % nchunks
   uint8_t slow[kConsumerWarps]; // bit t: the warp parked masks for tile t (else all zero)
 };
@@ -935,6 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     fence_mbar_init();
   } else if (tid >= 64 && tid < 64 + static_cast<uint32_t>(Smem::kPark)) {
     S.park[tid - 64].done = 0;
+    S.park[tid - 64].scanned = 0xFFFFFFFFu;
   } else if (tid >= 96 && tid < 98) {
     mbar_init(&S.job_full[tid - 96], 1);
     mbar_init(&S.job_free[tid - 96], kConsumerWarps);
@@ -1086,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     // ================================================================ look-back
     if constexpr (SEARCH) {
       // (chunks reach this queue only after the consumers saw the workspace free)
-      uint32_t q = 0, par = 0;
+      uint32_t q = 0, par = 0, lbk = 0;                   // lbk: sequence number of the chunk
       while (true) {
         mbar_wait_suspend(&S.lb_full[q], par);
         const ChunkSlot sl = S.slot[q];
@@ -1114,6 +1116,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
             run += v[i];
           }
           __syncwarp();
+          __threadfence_block();
+          if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&pk.scanned) = lbk;
+          ++lbk;
         }
         // a chunk without occurrences needs no prefix of its own; its look-back only helps
         // successors (an inclusive status shortens their walks), so it is dropped once every
@@ -1167,12 +1172,16 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     };
     // write out chunk #k's slices (parked in slot k % kParked) once its prefix is known
     // (a warp that parked no masks for the chunk has nothing to write and needs no prefix)
+    // (with nothing to write the warp still waits until the look-back warp has scanned chunk
+    // #k's slice counts: it is about to park chunk #k + kParked in the same slot)
     auto flush_chunk_seq = [&](uint32_t k) {
       const uint32_t b = k % kParked;
       const uint32_t sb = (slowbits >> (kChunkTiles * b)) & kTileBitsMask;
       if (sb) {
         wait_done(k);
         flush_slices(P, S, scratch_cta, b, sb, cw, lane, keep_pol, out_ok);
+      } else {
+        while (*reinterpret_cast<volatile const uint32_t*>(&S.park[b].scanned) != k) __nanosleep(32);
       }
       slowbits &= ~(kTileBitsMask << (kChunkTiles * b));
     };
