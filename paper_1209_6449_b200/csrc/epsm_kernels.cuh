@@ -193,7 +193,9 @@ struct KParams {
   uint32_t desc_bytes;          // bytes of JobDesc the producer copies (header [+ gram table])
   uint32_t flags;               // EPSM_FLAGS (A/B timing): bit 1 = L2 prefetch of the next chunk
                                 // (off by default: measured no gain, and under dense position
-                                // writes the prefetched lines are evicted and read twice)
+                                // writes the prefetched lines are evicted and read twice);
+                                // bit 2 = slow the look-back warp down (test hook: consumers
+                                // then run up to the parking slots' limit)
   unsigned long long* trace;    // diagnostics (epsm_debug_trace): 8 stamps per CTA, or NULL
   unsigned long long* exit_ctr; // CTAs of all launches on this workspace parity that have exited
   unsigned long long exit_expect;   // value meaning "launch L-2 (same parity) has retired"
@@ -1091,6 +1093,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
       uint32_t q = 0, par = 0, lbk = 0;                   // lbk: sequence number of the chunk
       while (true) {
         mbar_wait_suspend(&S.lb_full[q], par);
+        if (P.flags & 4u) {                     // test hook: a lagging look-back warp
+          for (int i = 0; i < 16; ++i) __nanosleep(1000);
+        }
         const ChunkSlot sl = S.slot[q];
         if (sl.chunk == kInfoEnd) break;
         {
