@@ -235,7 +235,8 @@ struct __align__(16) ParkedChunk {   // per parking slot
   uint32_t ntiles;              // tiles in the chunk (last chunk may be short)
   uint32_t done;                // consumer warps finished with the chunk (smem atomic)
   uint32_t job;                 // search of the chunk, chunk / nchunks  (look-back warp)
-  uint32_t scanned;             // sequence number of the chunk whose counts were last scanned
+  uint32_t scanned;             // 1 + sequence number of the last chunk whose counts were scanned
+                                // (or that had none: marked at hand-off); only grows
   uint32_t cidx;                // chunk index inside its search, chunk % nchunks
   uint8_t slow[kConsumerWarps]; // bit t: the warp parked masks for tile t (else all zero)
 };
@@ -938,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
     fence_mbar_init();
   } else if (tid >= 64 && tid < 64 + static_cast<uint32_t>(Smem::kPark)) {
     S.park[tid - 64].done = 0;
-    S.park[tid - 64].scanned = 0xFFFFFFFFu;
+    S.park[tid - 64].scanned = 0;
   } else if (tid >= 96 && tid < 98) {
     mbar_init(&S.job_full[tid - 96], 1);
     mbar_init(&S.job_free[tid - 96], kConsumerWarps);
@@ -1122,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
           }
           __syncwarp();
           __threadfence_block();
-          if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&pk.scanned) = lbk;
+          if (lane == 0) atomicMax(&pk.scanned, lbk + 1);
           ++lbk;
         }
         // a chunk without occurrences needs no prefix of its own; its look-back only helps
@@ -1186,7 +1187,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
         wait_done(k);
         flush_slices(P, S, scratch_cta, b, sb, cw, lane, keep_pol, out_ok);
       } else {
-        while (*reinterpret_cast<volatile const uint32_t*>(&S.park[b].scanned) != k) __nanosleep(32);
+        while (*reinterpret_cast<volatile const uint32_t*>(&S.park[b].scanned) <= k) __nanosleep(32);
       }
       slowbits &= ~(kTileBitsMask << (kChunkTiles * b));
     };
@@ -1619,6 +1620,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
                      ? S.park[b].cnt[sl] : 0u;
         }
         const uint32_t total = __reduce_add_sync(0xffffffffu, sum);
+        // a chunk without occurrences has no offsets to scan: its slot may be reused at once
+        if (total == 0 && lane == 0) atomicMax(&S.park[b].scanned, seq + 1);
         if (seq >= kSlots) wait_done(seq - kSlots);          // slot seq % kSlots is free again
         if (lane == 0) {
           S.park[b].done = 0;
