@@ -161,6 +161,8 @@ int epsm_count_batch_async(epsm_plan_t *const *plans, uint32_t k,
  *   (ordered before later work on that stream).  d_text must be 16-byte aligned
  *   (EPSM_EALIGN otherwise).  The index remembers (d_text, n): searches name the
  *   same text.  Growing the planes re-allocates (synchronises the stream).
+ *   Searches on other streams that read the planes must be ordered before a
+ *   rebuild by the caller (events), as for any buffer shared across streams.
  *   Returns EPSM_OK or EPSM_EINVAL (NULL, nv out of range, duplicate values,
  *   n > 2^38), EPSM_EALIGN, EPSM_ENOMEM, EPSM_ECUDA.
  * epsm_eqidx_values -- the values the index holds: writes up to 256 bytes into
