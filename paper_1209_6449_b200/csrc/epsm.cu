@@ -1045,7 +1045,7 @@ int epsm_eqidx_build_async(epsm_eqidx_t* ix, const uint8_t* d_text, uint64_t n, 
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
   const uint64_t want = (pstride + 255) / 256;
-  const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 64;   // (enough loads in flight)
   const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
   // few values: compare the bytes per value; many: bit-slice once, then 16 logic ops per value
   if (nv >= 8)
