@@ -275,7 +275,7 @@ def run_epsm(args, world, rank, local):
             # sharded batch: local scan of the owned starts (global positions), then ONE
             # all-gather of the group's counts -> global occ and this rank's output offsets;
             # positions stay on the rank that found them (a distributed, ordered result)
-            epsm.search_range_batch_async(plans_, t_, owned_, base_, occ_loc[j0:j1], outs=outs, stream=stream,
+            epsm.search_range_batch_async(plans_, t_, owned_, base_, n_total_, occ_loc[j0:j1], outs=outs, stream=stream,
                                           index=ixs.get(ti))
             occ_g, _off = sharding.exchange_batch_counts(occ_loc[j0:j1])
             occ_buf[j0:j1].copy_(occ_g)

@@ -201,6 +201,7 @@ int epsm_search_range_batch_index_async(epsm_plan_t *const *plans, uint32_t k,
                                         const epsm_eqidx_t *index,
                                         const uint8_t *d_text, uint64_t n,
                                         uint64_t owned_len, uint64_t base,
+                                        uint64_t n_total,
                                         uint64_t *const *d_pos, const uint64_t *caps,
                                         uint64_t *d_occ, epsm_stream_t stream);
 
@@ -214,13 +215,18 @@ int epsm_count_batch_index_async(epsm_plan_t *const *plans, uint32_t k,
 /*
  * epsm_search_range_batch_async -- the local step of a sharded batch: as
  * epsm_search_batch_async over the shard d_text[0..n-1], reporting only starts
- * s < owned_len, each as s + base (the rank's global offset).  With the per-rank
- * counts exchanged (every rank learns each search's global occ and its own
- * offset), the union of the ranks' outputs is each search's Occ, in rank order.
+ * s < owned_len, each as s + base (the rank's global offset).  The global text
+ * has n_total bytes: base + owned_len <= n_total, and for every plan the shard
+ * must hold the (m-1)-byte overlap, n >= min(owned_len + m - 1, n_total - base)
+ * (EPSM_EINVAL otherwise: an owned start whose window runs past the shard would
+ * be silently dropped).  With the per-rank counts exchanged (every rank learns
+ * each search's global occ and its own offset), the union of the ranks' outputs
+ * is each search's Occ, in rank order.
  */
 int epsm_search_range_batch_async(epsm_plan_t *const *plans, uint32_t k,
                                   const uint8_t *d_text, uint64_t n,
                                   uint64_t owned_len, uint64_t base,
+                                  uint64_t n_total,
                                   uint64_t *const *d_pos, const uint64_t *caps,
                                   uint64_t *d_occ, epsm_stream_t stream);
 
@@ -259,10 +265,13 @@ int64_t epsm_search_sharded(epsm_plan_t *plan, const uint8_t *d_shard,
  * that a host runtime (e.g. torch.distributed) can do the exchange itself:
  * scans d_shard[0..shard_len-1], reports only starts s < owned_len, and writes
  * s + base into d_pos (first min(occ_local, cap)); occ_local goes to *d_occ.
+ * n_total is the global text length; the shard must hold the overlap,
+ * shard_len >= min(owned_len + m - 1, n_total - base), else EPSM_EINVAL.
  */
 int epsm_search_range_async(epsm_plan_t *plan, const uint8_t *d_shard,
                             uint64_t shard_len, uint64_t owned_len,
-                            uint64_t base, uint64_t *d_pos, uint64_t cap,
+                            uint64_t base, uint64_t n_total,
+                            uint64_t *d_pos, uint64_t cap,
                             uint64_t *d_occ, epsm_stream_t stream);
 
 /* epsm_strerror -- static name/description of an EPSM_E* code. */

@@ -54,13 +54,13 @@ _lib.epsm_search_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _
 _lib.epsm_search_batch_async.restype = ctypes.c_int
 _lib.epsm_count_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _vp]
 _lib.epsm_count_batch_async.restype = ctypes.c_int
-_lib.epsm_search_range_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_search_range_batch_async.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_search_range_batch_async.restype = ctypes.c_int
 _lib.epsm_search_host.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
 _lib.epsm_search_host.restype = _i64
 _lib.epsm_search_sharded.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _u64, _vp, _vp]
 _lib.epsm_search_sharded.restype = _i64
-_lib.epsm_search_range_async.argtypes = [_vp, _vp, _u64, _u64, _u64, _vp, _u64, _vp, _vp]
+_lib.epsm_search_range_async.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _u64, _vp, _vp]
 _lib.epsm_search_range_async.restype = ctypes.c_int
 _lib.epsm_strerror.argtypes = [_i64]
 _lib.epsm_strerror.restype = ctypes.c_char_p
@@ -82,8 +82,8 @@ _lib.epsm_eqidx_values.argtypes = [_vp, _vp]
 _lib.epsm_eqidx_values.restype = ctypes.c_int
 _lib.epsm_plan_index_values.argtypes = [_vp, _vp]
 _lib.epsm_plan_index_values.restype = ctypes.c_int
-_lib.epsm_search_range_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _u64, _u64, _vp, _vp,
-                                                     _vp, _vp]
+_lib.epsm_search_range_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _u64, _u64, _u64, _vp,
+                                                     _vp, _vp, _vp]
 _lib.epsm_search_range_batch_index_async.restype = ctypes.c_int
 _lib.epsm_count_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp]
 _lib.epsm_count_batch_index_async.restype = ctypes.c_int
@@ -414,35 +414,38 @@ def count_batch_async(plans, text: torch.Tensor, occ_out: torch.Tensor, stream=N
                                        _stream_handle(stream, text.device)), "epsm_count_batch_async")
 
 
-def search_range_batch_async(plans, shard: torch.Tensor, owned_len: int, base: int, occ_out: torch.Tensor,
-                             outs=None, caps=None, stream=None, index: "EqIndex | None" = None) -> None:
-    """Local step of a sharded batch: starts s < owned_len of ``shard``, reported as s + base
-    (with an EqIndex built over ``shard``, qualifying searches stream its planes)."""
+def search_range_batch_async(plans, shard: torch.Tensor, owned_len: int, base: int, n_total: int,
+                             occ_out: torch.Tensor, outs=None, caps=None, stream=None,
+                             index: "EqIndex | None" = None) -> None:
+    """Local step of a sharded batch: starts s < owned_len of ``shard``, reported as s + base;
+    n_total = the global text length (the shard must hold every owned window; with an EqIndex
+    built over ``shard``, qualifying searches stream its planes)."""
     if len(plans) == 0:
         return
     plans, k, hp, pos_arr, caps_arr = _batch_args(plans, shard, occ_out, outs, caps)
     if index is not None:
         _check(_lib.epsm_search_range_batch_index_async(hp, k, index.handle, shard.data_ptr(), shard.numel(),
-                                                        int(owned_len), int(base), pos_arr, caps_arr,
+                                                        int(owned_len), int(base), int(n_total), pos_arr, caps_arr,
                                                         occ_out.data_ptr(), _stream_handle(stream, shard.device)),
                "epsm_search_range_batch_index_async")
         return
     _check(_lib.epsm_search_range_batch_async(hp, k, shard.data_ptr(), shard.numel(), int(owned_len), int(base),
-                                              pos_arr, caps_arr, occ_out.data_ptr(),
+                                              int(n_total), pos_arr, caps_arr, occ_out.data_ptr(),
                                               _stream_handle(stream, shard.device)),
            "epsm_search_range_batch_async")
 
 
-def search_range_async(p: Plan, shard: torch.Tensor, owned_len: int, base: int,
+def search_range_async(p: Plan, shard: torch.Tensor, owned_len: int, base: int, n_total: int,
                        out: torch.Tensor | None, occ_out: torch.Tensor, cap: int | None = None,
                        stream=None) -> None:
-    """Local step of a sharded search: starts s < owned_len of ``shard``, reported as s + base."""
+    """Local step of a sharded search: starts s < owned_len of ``shard``, reported as s + base
+    (n_total = the global text length; the shard must hold every owned window)."""
     _check_text(shard)
     _check_out(out, "out")
     _check_out(occ_out, "occ_out")
     c = 0 if out is None else (out.numel() if cap is None else min(int(cap), out.numel()))
     _check(_lib.epsm_search_range_async(p.handle, shard.data_ptr(), shard.numel(), int(owned_len), int(base),
-                                        out.data_ptr() if (out is not None and c) else None, c,
+                                        int(n_total), out.data_ptr() if (out is not None and c) else None, c,
                                         occ_out.data_ptr(), _stream_handle(stream, shard.device)),
            "epsm_search_range_async")
 

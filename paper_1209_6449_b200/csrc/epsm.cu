@@ -487,15 +487,19 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   const uint64_t grid = gchunks < static_cast<uint64_t>(ws->num_sms) ? gchunks : ws->num_sms;
   int rc = ensure_workspace(ws, gchunks, grid, search, s);
   if (rc) return rc;
-  // launch L uses parity L & 1; its status tag is L (24 bits); on wrap every word is cleared
-  // (in stream order) so a stale tag can never match
+  // launch L uses parity L & 1; its status tag is L mod 2^24.  The first search launch of
+  // every epoch (L >> 24) clears both status buffers (in stream order) before it runs, so a
+  // word left by an earlier epoch can never carry a live tag -- whatever launch (count or
+  // search) happened to take the number at the epoch boundary.  Tag 0 is skipped (a zeroed
+  // word must never look like a valid status).
   uint64_t L = ws->launches;
-  if (search && (L & 0xFFFFFFull) == 0) {
+  if (search && ((L >> 24) != ws->status_epoch || (L & 0xFFFFFFull) == 0)) {
     for (auto* p : ws->d_status) {
       cudaError_t e = cudaMemsetAsync(p, 0, ws->status_cap * sizeof(unsigned long long), s);
       if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(status)");
     }
-    ws->launches = ++L;
+    if ((L & 0xFFFFFFull) == 0) ws->launches = ++L;
+    ws->status_epoch = L >> 24;
   }
   const int par = static_cast<int>(L & 1u);
   P.ntiles = static_cast<uint32_t>(tiles);
@@ -830,9 +834,28 @@ int epsm_plan_index_values(const epsm_plan_t* plan, uint8_t* out_values) {
   return static_cast<int>(D.np);
 }
 
+// A shard [base, base + n) of a text of n_total bytes that owns the starts [base, base +
+// owned_len) must hold every owned window: n >= min(owned_len + m - 1, n_total - base).
+static int check_overlap(uint64_t n, uint64_t owned_len, uint64_t base, uint64_t n_total, uint32_t m) {
+  if (base > n_total || owned_len > n_total - base || n > n_total - base) {
+    epsm_set_error("shard [%llu, +%llu) owning %llu starts lies outside the text of %llu bytes",
+                   (unsigned long long)base, (unsigned long long)n, (unsigned long long)owned_len,
+                   (unsigned long long)n_total);
+    return EPSM_EINVAL;
+  }
+  if (owned_len == 0) return EPSM_OK;
+  const uint64_t need = owned_len + m - 1 < n_total - base ? owned_len + m - 1 : n_total - base;
+  if (n < need) {
+    epsm_set_error("shard of %llu bytes is shorter than its owned starts plus the (m-1)-byte overlap "
+                   "(%llu bytes for m = %u)", (unsigned long long)n, (unsigned long long)need, m);
+    return EPSM_EINVAL;
+  }
+  return EPSM_OK;
+}
+
 static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n, uint64_t owned_len,
                         uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
-                        epsm_stream_t stream, const epsm_eqidx_t* index = nullptr) {
+                        epsm_stream_t stream, const epsm_eqidx_t* index = nullptr, uint64_t n_total = 0) {
   if (k == 0) return EPSM_OK;
   if (index && (index->text != d_text || index->n != n)) {
     epsm_set_error("the index was built over another text (pointer or length differ)");
@@ -856,6 +879,10 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
     if (!plans[j]) {
       epsm_set_error("epsm_search_batch_async: plans[%u] is NULL", j);
       return EPSM_EINVAL;
+    }
+    if (n_total) {                     // a shard: every plan's window must fit its overlap
+      int rc = check_overlap(n, owned_len, base, n_total, plans[j]->m);
+      if (rc) return rc;
     }
     uint64_t* pos = d_pos ? d_pos[j] : nullptr;
     const uint64_t cap = (pos && caps) ? caps[j] : 0;
@@ -903,9 +930,13 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
 }
 
 int epsm_search_range_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
-                                  uint64_t owned_len, uint64_t base, uint64_t* const* d_pos, const uint64_t* caps,
-                                  uint64_t* d_occ, epsm_stream_t stream) {
-  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, true, stream);
+                                  uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos,
+                                  const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
+  if (n_total == 0 && (n > 0 || owned_len > 0)) {
+    epsm_set_error("epsm_search_range_batch_async: n_total = 0");
+    return EPSM_EINVAL;
+  }
+  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, true, stream, nullptr, n_total);
 }
 
 int epsm_search_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
@@ -920,9 +951,13 @@ int epsm_count_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t*
 
 int epsm_search_range_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,
                                         const uint8_t* d_text, uint64_t n, uint64_t owned_len, uint64_t base,
-                                        uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ,
-                                        epsm_stream_t stream) {
-  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, true, stream, index);
+                                        uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
+                                        uint64_t* d_occ, epsm_stream_t stream) {
+  if (n_total == 0 && (n > 0 || owned_len > 0)) {
+    epsm_set_error("epsm_search_range_batch_index_async: n_total = 0");
+    return EPSM_EINVAL;
+  }
+  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, true, stream, index, n_total);
 }
 
 int epsm_count_batch_index_async(epsm_plan_t* const* plans, uint32_t k, const epsm_eqidx_t* index,
@@ -1059,8 +1094,11 @@ int epsm_eqidx_build_async(epsm_eqidx_t* ix, const uint8_t* d_text, uint64_t n, 
 }
 
 int epsm_search_range_async(epsm_plan_t* plan, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,
-                            uint64_t base, uint64_t* d_pos, uint64_t cap, uint64_t* d_occ, epsm_stream_t stream) {
+                            uint64_t base, uint64_t n_total, uint64_t* d_pos, uint64_t cap, uint64_t* d_occ,
+                            epsm_stream_t stream) {
   int rc = check_common(plan, d_shard, shard_len);
+  if (rc) return rc;
+  rc = check_overlap(shard_len, owned_len, base, n_total, plan->m);
   if (rc) return rc;
   if (!d_occ || (cap > 0 && !d_pos)) {
     epsm_set_error("d_occ required; d_pos required when cap > 0");
@@ -1187,7 +1225,7 @@ const char* epsm_last_error(void) { return g_last_error; }
 
 uint64_t epsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int epsm_version(void) { return 100; }
+int epsm_version(void) { return 200; }
 
 int64_t epsm_debug_trace(uint64_t* h_out, uint64_t max_words) {
   if (!g_trace) return 0;

@@ -46,6 +46,8 @@ struct epsm_workspace {
   cudaStream_t stream = nullptr;
   int num_sms = 0;
   uint64_t launches = 0;                      // launch sequence number of the next launch
+  uint64_t status_epoch = 0;                  // epoch (launches >> 24) the status words were
+                                              // last cleared in (0: zeroed at allocation)
   unsigned long long* d_status[2] = {nullptr, nullptr};   // one status word per chunk
   uint64_t status_cap = 0;
   uint64_t* d_scratch[2] = {nullptr, nullptr};            // parked masks, per CTA

@@ -108,7 +108,7 @@ def search_sharded_torch(shard: torch.Tensor, base: int, owned_len: int, n_total
     ``local_search(shard, owned_len, base) -> (global_positions, occ_local)`` is the
     per-rank scan (the CUDA path via ``local_search_cuda``; tests may inject the
     oracle to exercise this host logic on CPU)."""
-    pos, occ_local = local_search(shard, owned_len, base)
+    pos, occ_local = local_search(shard, owned_len, base, n_total)
     return exchange_positions(pos, occ_local, group=group, cap=cap)
 
 
@@ -116,15 +116,15 @@ def local_search_cuda(plan):
     """The per-rank scan through the C ABI (epsm_search_range_async)."""
     from . import _lib
 
-    def run(shard: torch.Tensor, owned_len: int, base: int):
+    def run(shard: torch.Tensor, owned_len: int, base: int, n_total: int):
         occ_dev = torch.zeros(1, dtype=torch.int64, device=shard.device)
         nst = max(0, min(owned_len, shard.numel() - plan.m + 1))
         out = torch.empty(min(nst, 1 << 20), dtype=torch.int64, device=shard.device)
-        _lib.search_range_async(plan, shard, owned_len, base, out, occ_dev)
+        _lib.search_range_async(plan, shard, owned_len, base, n_total, out, occ_dev)
         occ = int(occ_dev.item())
         if occ > out.numel():
             out = torch.empty(occ, dtype=torch.int64, device=shard.device)
-            _lib.search_range_async(plan, shard, owned_len, base, out, occ_dev)
+            _lib.search_range_async(plan, shard, owned_len, base, n_total, out, occ_dev)
         return out[:occ], occ
 
     return run

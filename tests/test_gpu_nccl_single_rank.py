@@ -73,7 +73,7 @@ def test_batch_counts_exchange_over_nccl(nccl_group):
     pats = [t[s:s + m].tobytes() for s, m in ((10, 2), (2000, 8), (70000, 16))]
     plans = [epsm.plan(p) for p in pats]
     occ_loc = torch.zeros(len(pats), dtype=torch.int64, device=dev)
-    epsm.search_range_batch_async(plans, td, n, 0, occ_loc)
+    epsm.search_range_batch_async(plans, td, n, 0, n, occ_loc)
     occ, off = sharding.exchange_batch_counts(occ_loc)
     want = [oracle.search(p, t).size for p in pats]
     assert occ.cpu().tolist() == want and off.cpu().tolist() == [0] * len(pats)

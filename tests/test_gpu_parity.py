@@ -211,7 +211,7 @@ def test_emulated_shards_compose(epsm, dev, world):
         parts, total = [], 0
         for r in range(world):
             base, owned, slen = sharding.shard_layout(n, world, r)
-            pos, occ = run(td[base:base + slen], owned, base)
+            pos, occ = run(td[base:base + slen], owned, base, n)
             parts.append(pos.cpu().numpy().astype(np.uint64))
             total += occ
         want = oracle.search(p.tobytes(), t)
@@ -502,10 +502,34 @@ def test_emulated_shards_batch_compose(epsm, dev, world):
             # each rank's shard in its own (aligned) buffer, as make_texts builds it
             shard = td[base:base + slen].clone()
             ix = epsm.eq_index(shard, epsm.index_values(plans)) if use_index else None
-            epsm.search_range_batch_async(plans, shard, owned, base, occ, outs=outs, index=ix)
+            epsm.search_range_batch_async(plans, shard, owned, base, n, occ, outs=outs, index=ix)
             torch.cuda.synchronize()
             for j in range(len(pats)):
                 k = int(occ[j])
                 parts[j].append(outs[j][:k].cpu().numpy().astype(np.uint64))
         for j, w in enumerate(wants):
             assert np.array_equal(np.concatenate(parts[j]), w), (use_index, len(pats[j]))
+
+
+def test_range_calls_reject_a_short_overlap(epsm, dev):
+    """A shard that cannot hold every owned window (shard_len < owned + m - 1 while the text
+    goes on) is an error, not a silent drop of the occurrences at the cut."""
+    n_total = 10_000
+    shard = torch.zeros(1000 + 31, dtype=torch.uint8, device=dev)
+    occ = torch.zeros(1, dtype=torch.int64, device=dev)
+    out = torch.empty(64, dtype=torch.int64, device=dev)
+    long_pl = epsm.plan(b"\x00" * 40)                  # needs 39 halo bytes, the shard has 31
+    with pytest.raises(epsm.EpsmError) as ei:
+        epsm.search_range_async(long_pl, shard, 1000, 0, n_total, out, occ)
+    assert ei.value.code == epsm.EPSM_EINVAL
+    with pytest.raises(epsm.EpsmError) as ei:
+        epsm.search_range_batch_async([long_pl], shard, 1000, 0, n_total, occ)
+    assert ei.value.code == epsm.EPSM_EINVAL
+    # the same shard at the end of the text (no bytes beyond it) is fine
+    epsm.search_range_async(long_pl, shard, 1000, n_total - 1031, n_total, out, occ)
+    torch.cuda.synchronize()
+    assert int(occ[0]) == 1031 - 40 + 1
+    # m <= 32 fits the 31-byte halo
+    epsm.search_range_batch_async([epsm.plan(b"\x00" * 32)], shard, 1000, 0, n_total, occ)
+    torch.cuda.synchronize()
+    assert int(occ[0]) == 1000

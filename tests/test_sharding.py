@@ -47,7 +47,7 @@ def _worker(rank, world, port, cases, q):
             base, owned, slen = sharding.shard_layout(n, world, rank)
             shard = torch.from_numpy(text[base:base + slen].copy())
 
-            def local(sh, owned_len, b, p=pattern):
+            def local(sh, owned_len, b, n_total, p=pattern):
                 # oracle over the shard, owned starts only, shifted to global
                 pos = oracle.search(p, sh.numpy())
                 pos = pos[pos < owned_len].astype(np.int64) + b
