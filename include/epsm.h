@@ -274,6 +274,71 @@ int epsm_search_range_async(epsm_plan_t *plan, const uint8_t *d_shard,
                             uint64_t *d_pos, uint64_t cap,
                             uint64_t *d_occ, epsm_stream_t stream);
 
+/*
+ * Group search: k searches of one pattern length m over one text in ONE pass.
+ * The paper's protocol searches sets of 1000 patterns of fixed length m, randomly
+ * extracted from each text (Sec. 4); every search of a group
+ * returns exactly its own Occ(p_j, t), as if searched alone, but
+ * the text is streamed once for the group: identical patterns are searched once,
+ * and the distinct ones share one EPSMc-style table of sampled q-grams
+ * (Fig. 1 lines 1-12: one table lookup per sample names
+ * candidate (start, pattern) pairs, each naively checked).
+ */
+typedef struct epsm_group_s epsm_group_t;   /* opaque, host-owned */
+
+/*
+ * epsm_group_create -- preprocess k patterns of length m (1 <= m <= EPSM_MAX_M,
+ * 1 <= k <= 1024) stored back to back in patterns[0 .. k*m).  Search j of the
+ * group is pattern j.  Copies the patterns; no device work (the group's tables
+ * are uploaded on first use, to the device of that call).  More than 255
+ * distinct patterns are split internally into passes of <= 255.
+ * Returns EPSM_OK, EPSM_EINVAL (NULL argument, m = 0, k = 0), EPSM_EUNSUP
+ * (m > 32 or k > 1024) or EPSM_ENOMEM.
+ */
+int epsm_group_create(const uint8_t *patterns, uint32_t m, uint32_t k,
+                      epsm_group_t **out);
+
+/* epsm_group_free -- release a group (synchronises its device first). NULL-safe. */
+void epsm_group_free(epsm_group_t *g);
+
+/* epsm_group_info -- diagnostics: writes min(nout, 4 + 2*P) values
+ * [m, k, distinct patterns, passes P, then (q, SK) per pass: the sampled gram
+ * length and stride] to out and returns 4 + 2*P (EPSM_EINVAL on NULL). */
+int epsm_group_info(const epsm_group_t *g, uint32_t *out, uint32_t nout);
+
+/* epsm_group_set_geometry -- tuning / test hook: use sampled q-grams (1 <= q <=
+ * min(m, 16)) every SK bytes (SK in {1, 2, 4, 8, 16}, SK + q - 1 <= m, SK times
+ * the distinct patterns of a pass <= 4096) instead of the cost model's choice.
+ * Every geometry returns the same results.  Synchronises the group's device if
+ * it was used.  Returns EPSM_OK or EPSM_EINVAL. */
+int epsm_group_set_geometry(epsm_group_t *g, uint32_t q, uint32_t sk);
+
+/*
+ * epsm_group_search_async -- all k searches of the group over d_text[0..n-1]
+ * (any alignment): search j writes its first min(occ_j, caps[j]) positions,
+ * ascending, to the device array d_pos[j] (d_pos[j] may be NULL, or d_pos
+ * itself NULL: counts only) and occ_j to d_occ[j] (device, k entries, 8-byte
+ * aligned).  Scratch (per-chunk counts, prefixes and occurrence lists, ~1/30 of
+ * n bytes) belongs to the (device, stream) workspace.  Does not synchronise.
+ */
+int epsm_group_search_async(epsm_group_t *g, const uint8_t *d_text, uint64_t n,
+                            uint64_t *const *d_pos, const uint64_t *caps,
+                            uint64_t *d_occ, epsm_stream_t stream);
+
+/* epsm_group_count_async -- occ_j of every search into d_occ[j] (no positions). */
+int epsm_group_count_async(epsm_group_t *g, const uint8_t *d_text, uint64_t n,
+                           uint64_t *d_occ, epsm_stream_t stream);
+
+/* epsm_group_search_range_async -- the local step of a sharded group search: as
+ * epsm_search_range_batch_async (starts s < owned_len of the shard, reported as
+ * s + base; shard_len >= min(owned_len + m - 1, n_total - base), else
+ * EPSM_EINVAL) for every search of the group in one pass. */
+int epsm_group_search_range_async(epsm_group_t *g, const uint8_t *d_shard,
+                                  uint64_t shard_len, uint64_t owned_len,
+                                  uint64_t base, uint64_t n_total,
+                                  uint64_t *const *d_pos, const uint64_t *caps,
+                                  uint64_t *d_occ, epsm_stream_t stream);
+
 /* epsm_strerror -- static name/description of an EPSM_E* code. */
 const char *epsm_strerror(int64_t code);
 

@@ -6,7 +6,7 @@ include/epsm.h; this package is the thin Python binding over it.
 """
 from ._lib import (  # noqa: F401
     EPSM_EALIGN, EPSM_ECUDA, EPSM_EINVAL, EPSM_ENCCL, EPSM_ENOMEM, EPSM_EUNSUP, EPSM_OK,
-    EXPORTED_SYMBOLS, INDEX_MAX_D, LIB_PATH, MAX_M, MAX_M_LONG, MAX_PLANES, EpsmError, EqIndex, Plan, count,
+    EXPORTED_SYMBOLS, INDEX_MAX_D, Group, group, LIB_PATH, MAX_M, MAX_M_LONG, MAX_PLANES, EpsmError, EqIndex, Plan, count,
     eq_index, index_values, count_async, count_batch_async, find_all,
     debug_trace, launch_count, nccl_comm_ptr, plan, search, search_async, search_batch_async, search_host, search_range_async,
     search_range_batch_async,

@@ -90,6 +90,21 @@ _lib.epsm_count_batch_index_async.restype = ctypes.c_int
 _lib.epsm_search_batch_index_async.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_search_batch_index_async.restype = ctypes.c_int
 
+_lib.epsm_group_create.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(_vp)]
+_lib.epsm_group_create.restype = ctypes.c_int
+_lib.epsm_group_free.argtypes = [_vp]
+_lib.epsm_group_free.restype = None
+_lib.epsm_group_set_geometry.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32]
+_lib.epsm_group_set_geometry.restype = ctypes.c_int
+_lib.epsm_group_info.argtypes = [_vp, _vp, ctypes.c_uint32]
+_lib.epsm_group_info.restype = ctypes.c_int
+_lib.epsm_group_search_async.argtypes = [_vp, _vp, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_group_search_async.restype = ctypes.c_int
+_lib.epsm_group_count_async.argtypes = [_vp, _vp, _u64, _vp, _vp]
+_lib.epsm_group_count_async.restype = ctypes.c_int
+_lib.epsm_group_search_range_async.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_group_search_range_async.restype = ctypes.c_int
+
 EXPORTED_SYMBOLS = (
     "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
     "epsm_search", "epsm_search_async", "epsm_search_batch_async", "epsm_search_range_batch_async", "epsm_count_batch_async",
@@ -99,6 +114,8 @@ EXPORTED_SYMBOLS = (
     "epsm_eqidx_create", "epsm_eqidx_free", "epsm_eqidx_build_async", "epsm_eqidx_values",
     "epsm_search_batch_index_async", "epsm_count_batch_index_async", "epsm_plan_index_values",
     "epsm_search_range_batch_index_async",
+    "epsm_group_create", "epsm_group_free", "epsm_group_info", "epsm_group_set_geometry", "epsm_group_search_async",
+    "epsm_group_count_async", "epsm_group_search_range_async",
 )
 MAX_PLANES = 256
 INDEX_MAX_D = 8
@@ -499,3 +516,115 @@ def search_sharded(p, shard: torch.Tensor, base: int, owned_len: int, n_total: i
                                            out.data_ptr() if (out is not None and c) else None, c,
                                            comm, _stream_handle(stream, shard.device)),
                   "epsm_search_sharded")
+
+
+class Group:
+    """epsm_group_*: k patterns of one length searched in ONE pass over a text (the paper's
+    protocol of many patterns per text); search j is patterns[j]."""
+
+    def __init__(self, patterns):
+        pats = [_pattern_bytes(p) for p in patterns]
+        if not pats:
+            raise ValueError("a group needs at least one pattern")
+        m = len(pats[0])
+        if any(len(p) != m for p in pats):
+            raise ValueError("all patterns of a group have the same length")
+        self.patterns = pats
+        buf = ctypes.create_string_buffer(b"".join(pats), max(1, m * len(pats)))
+        h = _vp()
+        _check(_lib.epsm_group_create(buf, m, len(pats), ctypes.byref(h)), "epsm_group_create")
+        self._h = h
+
+    @property
+    def m(self) -> int:
+        return len(self.patterns[0])
+
+    @property
+    def k(self) -> int:
+        return len(self.patterns)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("group is closed")
+        return self._h
+
+    def info(self) -> dict:
+        """{m, k, distinct, passes: [(q, SK), ...]} (epsm_group_info)."""
+        out = (ctypes.c_uint32 * 64)()
+        c = _check(_lib.epsm_group_info(self.handle, out, 64), "epsm_group_info")
+        v = list(out[:min(c, 64)])
+        return {"m": v[0], "k": v[1], "distinct": v[2],
+                "passes": [(v[4 + 2 * i], v[5 + 2 * i]) for i in range(v[3])]}
+
+    def set_geometry(self, q: int, sk: int) -> "Group":
+        """Force sampled q-grams every SK bytes (tests / tuning; results never change)."""
+        _check(_lib.epsm_group_set_geometry(self.handle, int(q), int(sk)), "epsm_group_set_geometry")
+        return self
+
+    def _outs(self, outs, caps):
+        k = self.k
+        if outs is None:
+            return None, None
+        if len(outs) != k:
+            raise ValueError("one output (or None) per search")
+        ptrs, cs = [], []
+        for j, o in enumerate(outs):
+            _check_out(o, f"outs[{j}]")
+            c = 0 if o is None else (o.numel() if caps is None else min(int(caps[j]), o.numel()))
+            ptrs.append(o.data_ptr() if (o is not None and c) else None)
+            cs.append(c)
+        return (ctypes.c_void_p * k)(*ptrs), (ctypes.c_uint64 * k)(*cs)
+
+    def search_async(self, text: torch.Tensor, occ_out: torch.Tensor, outs=None, caps=None, stream=None):
+        """Enqueue every search over ``text``: occ of search j -> occ_out[j], positions -> outs[j]."""
+        _check_text(text)
+        _check_out(occ_out, "occ_out")
+        if occ_out.numel() < self.k:
+            raise ValueError("occ_out needs one element per search")
+        pa, ca = self._outs(outs, caps)
+        _check(_lib.epsm_group_search_async(self.handle, text.data_ptr(), text.numel(), pa, ca,
+                                            occ_out.data_ptr(), _stream_handle(stream, text.device)),
+               "epsm_group_search_async")
+
+    def count_async(self, text: torch.Tensor, occ_out: torch.Tensor, stream=None):
+        _check_text(text)
+        _check_out(occ_out, "occ_out")
+        if occ_out.numel() < self.k:
+            raise ValueError("occ_out needs one element per search")
+        _check(_lib.epsm_group_count_async(self.handle, text.data_ptr(), text.numel(), occ_out.data_ptr(),
+                                           _stream_handle(stream, text.device)), "epsm_group_count_async")
+
+    def search_range_async(self, shard: torch.Tensor, owned_len: int, base: int, n_total: int,
+                           occ_out: torch.Tensor, outs=None, caps=None, stream=None):
+        """Local step of a sharded group search (starts s < owned_len, reported as s + base)."""
+        _check_text(shard)
+        _check_out(occ_out, "occ_out")
+        if occ_out.numel() < self.k:
+            raise ValueError("occ_out needs one element per search")
+        pa, ca = self._outs(outs, caps)
+        _check(_lib.epsm_group_search_range_async(self.handle, shard.data_ptr(), shard.numel(), int(owned_len),
+                                                  int(base), int(n_total), pa, ca, occ_out.data_ptr(),
+                                                  _stream_handle(stream, shard.device)),
+               "epsm_group_search_range_async")
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.epsm_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def group(patterns) -> Group:
+    return Group(patterns)

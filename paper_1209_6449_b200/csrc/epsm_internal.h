@@ -55,6 +55,18 @@ struct epsm_workspace {
   unsigned long long* d_ctr = nullptr;        // [parity][kCtrWords]: chunk counter, -, count
                                               // ticket, CTA exit counter, -, per-search counts
   unsigned long long ctr_base[2] = {0, 0};    // chunk counter value at the next launch
+  // group search (epsm_multi.cu): per-(chunk, distinct pattern) counts and prefixes, per-chunk
+  // occurrence lists, the chunks with occurrences (capacities in bytes)
+  uint16_t* m_counts = nullptr;
+  uint64_t m_counts_cap = 0;
+  unsigned long long* m_prefix = nullptr;
+  uint64_t m_prefix_cap = 0;
+  uint32_t* m_listlen = nullptr;
+  uint64_t m_listlen_cap = 0;
+  uint32_t* m_lists = nullptr;
+  uint64_t m_lists_cap = 0;
+  uint32_t* m_work = nullptr;
+  uint64_t m_work_cap = 0;
   unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
 };
 
@@ -62,6 +74,7 @@ epsm_workspace* epsm_get_workspace(int device, cudaStream_t s);
 
 void epsm_set_error(const char* fmt, ...);
 int epsm_cuda_fail(cudaError_t e, const char* what);
+void epsm_count_launch();   // one more kernel launched by this library (epsm_launch_count)
 int epsm_bind_device(epsm_plan_t* plan, const void* dptr);
 int epsm_ensure_occ(epsm_plan_t* plan);
 int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,

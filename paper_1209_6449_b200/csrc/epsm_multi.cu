@@ -1,0 +1,555 @@
+// epsm_multi.cu -- host side of the group search (many patterns of one length over one text
+// in one pass): group construction (deduplication, the shared EPSMc-style
+// gram table, the choice of gram length and sampling stride), workspace and the three launches.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "epsm.h"
+#include "epsm_internal.h"
+#include "epsm_multi.cuh"
+
+namespace mp = epsm::mp;
+
+namespace {
+
+// One pass over the text serves at most kMaxD distinct patterns (u8 ids in shared memory);
+// a group of more is split into subgroups (one pass each).
+struct Subgroup {
+  uint32_t D = 0, k = 0;               // distinct patterns, searches
+  int q = 1, sk = 1, qw = 1;
+  uint32_t qmask = 0xFFu, hmul[4] = {0, 0, 0, 0};
+  std::vector<uint32_t> jobs;          // the caller's search index of local search j
+  mp::GroupDesc* h_desc = nullptr;
+  mp::GroupDesc* d_desc = nullptr;
+  double cost = 0;                     // model estimate (instructions per 64 text bytes)
+};
+
+constexpr uint32_t kMul[4] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du, 0x27D4EB2Fu};
+
+uint32_t hash_key(const uint8_t* g, int q, const Subgroup& S) {
+  uint32_t h = 0;
+  for (int r = 0; r < S.qw; ++r) {
+    uint32_t w = 0;
+    for (int b = 0; b < 4 && 4 * r + b < q; ++b) w |= static_cast<uint32_t>(g[4 * r + b]) << (8 * b);
+    h += w * S.hmul[r];
+  }
+  return h;
+}
+
+// Sampling geometry (q-gram length, stride SK) for D distinct patterns of length m whose bytes
+// have collision probability p2 (a pair of random text bytes is equal with probability ~p2 if
+// the text looks like the patterns -- they are extracted from it).  Cost model in
+// lane instructions per 64 text bytes: samples (key extraction, hash, bitmap test), bitmap
+// hits (bucket walk), candidates (naive check).  Speed only: every geometry is exact.
+void choose_geometry(uint32_t m, uint32_t D, double p2, Subgroup& S) {
+  double best = 1e300;
+  const int mw = static_cast<int>((m + 3) / 4);
+  for (int q = 1; q <= static_cast<int>(std::min<uint32_t>(m, 16)); ++q) {
+    const int qw = (q + 3) / 4;
+    const double pq = std::pow(p2, q);                       // a sample equals a given gram
+    for (int sk = 1; sk <= 16; sk *= 2) {
+      if (sk > static_cast<int>(m) - q + 1 || static_cast<uint64_t>(sk) * D > mp::kMaxEntries) continue;
+      const double nsamp = 64.0 / sk + (sk > 1 ? 1 : 0);
+      const double entries = static_cast<double>(sk) * D;
+      const double p_true = std::min(1.0, entries * pq);
+      const double p_false = q <= 2 ? 0.0 : std::min(1.0, entries / 65536.0);
+      const double p_hit = std::min(1.0, p_true + p_false);
+      const double c_sample = 8 + 2 * qw;
+      const double c_hit = 14 + 3 * qw + 3 * (entries / 4096.0);
+      const double cand_per_start = std::min(64.0, D * pq);  // true gram matches per start
+      const double c_verify = 10 + 4 * mw;
+      const double cost = nsamp * (c_sample + p_hit * c_hit) + 64.0 * cand_per_start * c_verify;
+      if (cost < best * 0.999 || (cost <= best * 1.001 && q > S.q)) {
+        best = std::min(best, cost);
+        S.q = q;
+        S.sk = sk;
+        S.qw = qw;
+      }
+    }
+  }
+  S.cost = best;
+  S.qmask = (S.q % 4 == 0) ? 0xFFFFFFFFu : ((1u << (8 * (S.q % 4))) - 1u);
+  if (S.q <= 2) {
+    S.hmul[0] = 1u << 16;                                    // the key itself: an exact bitmap
+  } else {
+    for (int r = 0; r < 4; ++r) S.hmul[r] = kMul[r];
+  }
+}
+
+using MKernel = void (*)(mp::MParams);
+
+template <int SK, int QW>
+MKernel pick_mk(bool write) {
+  return write ? &mp::epsm_multi_kernel<SK, QW, true> : &mp::epsm_multi_kernel<SK, QW, false>;
+}
+
+template <int SK>
+MKernel pick_qw(int qw, bool write) {
+  switch (qw) {
+    case 1: return pick_mk<SK, 1>(write);
+    case 2: return pick_mk<SK, 2>(write);
+    case 3: return pick_mk<SK, 3>(write);
+    default: return pick_mk<SK, 4>(write);
+  }
+}
+
+MKernel multi_kernel_for(int sk, int qw, bool write) {
+  switch (sk) {
+    case 1: return pick_qw<1>(qw, write);
+    case 2: return pick_qw<2>(qw, write);
+    case 4: return pick_qw<4>(qw, write);
+    case 8: return pick_qw<8>(qw, write);
+    default: return pick_qw<16>(qw, write);
+  }
+}
+
+// EPSM_MULTI_GEOM="q:sk" forces the geometry of every subgroup (A/B timing; must satisfy
+// sk + q - 1 <= m and D * sk <= 4096, else ignored).
+void geometry_override(uint32_t m, uint32_t D, Subgroup& S) {
+  static const char* e = getenv("EPSM_MULTI_GEOM");
+  if (!e || !e[0]) return;
+  int q = 0, sk = 0;
+  if (sscanf(e, "%d:%d", &q, &sk) != 2) return;
+  if (q < 1 || q > 16 || (sk & (sk - 1)) || sk < 1 || sk > 16 || sk + q - 1 > static_cast<int>(m) ||
+      static_cast<uint64_t>(sk) * D > mp::kMaxEntries)
+    return;
+  S.q = q;
+  S.sk = sk;
+  S.qw = (q + 3) / 4;
+  S.qmask = (q % 4 == 0) ? 0xFFFFFFFFu : ((1u << (8 * (q % 4))) - 1u);
+  if (q <= 2) {
+    S.hmul[0] = 1u << 16;
+    S.hmul[1] = S.hmul[2] = S.hmul[3] = 0;
+  } else {
+    for (int r = 0; r < 4; ++r) S.hmul[r] = kMul[r];
+  }
+}
+
+}  // namespace
+
+struct epsm_group_s {
+  uint32_t m = 0, k = 0, D = 0;
+  int device = -1;
+  std::vector<Subgroup> subs;
+  std::vector<std::string> pats;                  // distinct patterns
+  std::vector<std::vector<uint32_t>> dups;        // searches per distinct pattern
+};
+
+static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subgroup& S,
+                          const std::vector<std::vector<uint32_t>>& dups, int force_q = 0, int force_sk = 0) {
+  const uint32_t D = static_cast<uint32_t>(pats.size());
+  // collision probability of the patterns' bytes (unbiased: pairs of distinct positions)
+  uint64_t cnt[256] = {};
+  uint64_t N = 0;
+  for (const auto& p : pats)
+    for (unsigned char ch : p) ++cnt[ch], ++N;
+  double p2 = 1.0;
+  if (N > 1) {
+    double num = 0;
+    for (int c = 0; c < 256; ++c) num += static_cast<double>(cnt[c]) * (cnt[c] ? cnt[c] - 1 : 0);
+    p2 = std::max(num / (static_cast<double>(N) * (N - 1)), 1.0 / 256.0);
+  }
+  S.D = D;
+  choose_geometry(m, D, p2, S);
+  geometry_override(m, D, S);
+  if (force_q) {
+    S.q = force_q;
+    S.sk = force_sk;
+    S.qw = (force_q + 3) / 4;
+    S.qmask = (force_q % 4 == 0) ? 0xFFFFFFFFu : ((1u << (8 * (force_q % 4))) - 1u);
+    for (int r = 0; r < 4; ++r) S.hmul[r] = force_q <= 2 ? (r == 0 ? 1u << 16 : 0u) : kMul[r];
+  }
+  if (!S.h_desc) S.h_desc = new (std::nothrow) mp::GroupDesc();
+  if (!S.h_desc) return EPSM_ENOMEM;
+  mp::GroupDesc& G = *S.h_desc;
+  std::memset(&G, 0, sizeof(G));
+  // patterns, zero padded, and the byte masks of their words
+  for (uint32_t d = 0; d < D; ++d)
+    for (uint32_t b = 0; b < m; ++b)
+      G.pat[d][b / 4] |= static_cast<uint32_t>(static_cast<unsigned char>(pats[d][b])) << (8 * (b % 4));
+  for (uint32_t b = 0; b < m; ++b) G.pmask[b / 4] |= 0xFFu << (8 * (b % 4));
+  // the table (EPSMc's L, for every pattern at once): gram p_d[i .. i+q) of
+  // every distinct pattern d and offset i < SK, bucketed by the top 12 bits of its hash
+  std::vector<std::vector<uint16_t>> buckets(1u << mp::kBucketLog);
+  for (uint32_t d = 0; d < D; ++d) {
+    for (int i = 0; i < S.sk; ++i) {
+      const uint32_t h = hash_key(reinterpret_cast<const uint8_t*>(pats[d].data()) + i, S.q, S);
+      G.bitmap[h >> (32 - mp::kBitmapLog + 5)] |= 1u << ((h >> (32 - mp::kBitmapLog)) & 31u);
+      buckets[h >> (32 - mp::kBucketLog)].push_back(
+          static_cast<uint16_t>((d << 8) | (static_cast<uint32_t>(i) << 4) | ((h >> (32 - mp::kBitmapLog)) & 15u)));
+    }
+  }
+  uint32_t e = 0;
+  for (uint32_t b = 0; b < (1u << mp::kBucketLog); ++b) {
+    G.boff[b] = static_cast<uint16_t>(e);
+    for (uint16_t v : buckets[b]) G.ent[e++] = v;
+  }
+  for (uint32_t b = (1u << mp::kBucketLog); b < (1u << mp::kBucketLog) + 8; ++b) G.boff[b] = static_cast<uint16_t>(e);
+  // searches per distinct pattern
+  uint32_t q = 0;
+  S.jobs.clear();
+  for (uint32_t d = 0; d < D; ++d) {
+    G.dup_off[d] = static_cast<uint16_t>(q);
+    for (uint32_t j : dups[d]) {
+      G.dup_list[q] = static_cast<uint16_t>(S.jobs.size());
+      G.job_d[S.jobs.size()] = static_cast<uint16_t>(d);
+      G.job_g[S.jobs.size()] = static_cast<uint16_t>(j);
+      S.jobs.push_back(j);
+      ++q;
+    }
+  }
+  G.dup_off[D] = static_cast<uint16_t>(q);
+  G.dup_off[D + 1] = static_cast<uint16_t>(q);
+  S.k = q;
+  return EPSM_OK;
+}
+
+static void group_release(epsm_group_t* g) {
+  if (!g) return;
+  bool synced = false;
+  for (auto& S : g->subs) {
+    if (S.d_desc) {
+      if (!synced && g->device >= 0) {
+        cudaSetDevice(g->device);
+        cudaDeviceSynchronize();
+        synced = true;
+      }
+      cudaFree(S.d_desc);
+    }
+    delete S.h_desc;
+  }
+  delete g;
+}
+
+// Make the workspace of stream s hold the group buffers for `chunks` chunks of D patterns.
+static int ensure_multi_ws(epsm_workspace* ws, uint64_t chunks, uint32_t D, cudaStream_t s) {
+  auto grow = [&](void** p, uint64_t& cap, uint64_t want, const char* what) -> int {
+    if (want <= cap) return EPSM_OK;
+    if (*p) {
+      cudaStreamSynchronize(s);
+      cudaFree(*p);
+      *p = nullptr;
+      cap = 0;
+    }
+    const uint64_t bytes = std::max<uint64_t>(want, 4096);
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      *p = nullptr;
+      epsm_set_error("cudaMalloc(%s, %llu bytes): %s", what, (unsigned long long)bytes, cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    cap = bytes;
+    return EPSM_OK;
+  };
+  int rc = grow(reinterpret_cast<void**>(&ws->m_counts), ws->m_counts_cap, chunks * D * sizeof(uint16_t), "counts");
+  if (!rc) rc = grow(reinterpret_cast<void**>(&ws->m_prefix), ws->m_prefix_cap, chunks * D * 8, "prefix");
+  if (!rc) rc = grow(reinterpret_cast<void**>(&ws->m_listlen), ws->m_listlen_cap, chunks * 4, "list lengths");
+  if (!rc)
+    rc = grow(reinterpret_cast<void**>(&ws->m_lists), ws->m_lists_cap, chunks * mp::kListCap * 4ull, "chunk lists");
+  if (!rc) rc = grow(reinterpret_cast<void**>(&ws->m_work), ws->m_work_cap, (chunks + 1) * 4, "work list");
+  return rc;
+}
+
+static int set_multi_smem(MKernel fn) {
+  static std::vector<MKernel> done;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), fn) != done.end()) return EPSM_OK;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(mp::MSmem)));
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(group kernel smem)");
+  done.push_back(fn);
+  return EPSM_OK;
+}
+
+// The three launches of one subgroup over d_text[0..nbytes): starts [0, nstarts) reported as
+// start + base.  pos/caps/occ are the caller's batch arrays (indexed by the caller's search).
+static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
+                           uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
+                           cudaStream_t s) {
+  if (!S.d_desc) {
+    cudaError_t e = cudaMalloc(&S.d_desc, sizeof(mp::GroupDesc));
+    if (e != cudaSuccess) {
+      S.d_desc = nullptr;
+      epsm_set_error("cudaMalloc(group descriptor): %s", cudaGetErrorString(e));
+      return EPSM_ENOMEM;
+    }
+    e = cudaMemcpy(S.d_desc, S.h_desc, sizeof(mp::GroupDesc), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpy(group descriptor)");
+  }
+  if (nstarts == 0) {
+    for (uint32_t j : S.jobs) {
+      cudaError_t e = cudaMemsetAsync(d_occ + j, 0, 8, s);
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
+    }
+    return EPSM_OK;
+  }
+  const uint64_t mis = reinterpret_cast<uintptr_t>(d_text) & 15u;
+  mp::MParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.text = d_text - mis;
+  P.nbytes = nbytes + mis;
+  P.s_lo = mis;
+  P.s_hi = mis + nstarts;
+  P.pos_bias = base - mis;
+  const uint64_t chunks = (P.s_hi + mp::kTile - 1) / mp::kTile;
+  if (chunks > 0x7FFFFFFFull) {
+    epsm_set_error("text too large for a group search");
+    return EPSM_EINVAL;
+  }
+  P.nchunks = static_cast<uint32_t>(chunks);
+  P.it_lo = mis ? 1u : 0u;
+  P.it_hi = static_cast<uint32_t>(P.s_hi / mp::kTile);
+  P.m = g->m;
+  P.mw = (g->m + 3) / 4;
+  P.D = S.D;
+  P.k = S.k;
+  P.qmask = S.qmask;
+  for (int r = 0; r < 4; ++r) P.hmul[r] = S.hmul[r];
+  P.desc = S.d_desc;
+  P.desc_bytes = sizeof(mp::GroupDesc);
+  epsm_workspace* ws = epsm_get_workspace(g->device, s);
+  if (!ws) return EPSM_ENOMEM;
+  if (ws->num_sms <= 0) {
+    cudaError_t e = cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, g->device);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  }
+  int rc = ensure_multi_ws(ws, chunks, S.D, s);
+  if (rc) return rc;
+  P.counts = ws->m_counts;
+  P.listlen = ws->m_listlen;
+  P.lists = ws->m_lists;
+  P.prefix = ws->m_prefix;
+  P.work = ws->m_work;
+  for (uint32_t j = 0; j < S.k; ++j) {
+    const uint32_t gj = S.jobs[j];
+    P.pos[j] = (search && d_pos) ? d_pos[gj] : nullptr;
+    P.cap[j] = (search && d_pos && d_pos[gj] && caps) ? caps[gj] : 0;
+  }
+  const int smem = static_cast<int>(sizeof(mp::MSmem));
+  // pass 1: counts per (chunk, distinct pattern), lists of sparse chunks
+  MKernel k1 = multi_kernel_for(S.sk, S.qw, false);
+  rc = set_multi_smem(k1);
+  if (rc) return rc;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(chunks, static_cast<uint64_t>(ws->num_sms)));
+  k1<<<grid, mp::kThreads, smem, s>>>(P);
+  epsm_count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_kernel (pass 1) launch");
+  // pass 2: prefixes, totals (occ), chunks with occurrences
+  mp::ScanParams Q;
+  Q.counts = ws->m_counts;
+  Q.listlen = ws->m_listlen;
+  Q.prefix = search ? ws->m_prefix : nullptr;
+  Q.work = ws->m_work;
+  Q.occ = reinterpret_cast<unsigned long long*>(d_occ);
+  Q.desc = S.d_desc;
+  Q.nchunks = P.nchunks;
+  Q.D = S.D;
+  Q.k = S.k;
+  mp::epsm_multi_scan_kernel<<<(S.D + 31) / 32, 32 * mp::kScanWarps, 0, s>>>(Q);
+  epsm_count_launch();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_scan_kernel launch");
+  if (!search) return EPSM_OK;
+  // pass 3: positions of the chunks with occurrences
+  MKernel k3 = multi_kernel_for(S.sk, S.qw, true);
+  rc = set_multi_smem(k3);
+  if (rc) return rc;
+  k3<<<ws->num_sms, mp::kThreads, smem, s>>>(P);
+  epsm_count_launch();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_kernel (pass 3) launch");
+  return EPSM_OK;
+}
+
+static int group_bind(epsm_group_t* g, const void* dptr) {
+  int dev = -1;
+  cudaPointerAttributes attr;
+  cudaError_t e = dptr ? cudaPointerGetAttributes(&attr, dptr) : cudaErrorInvalidValue;
+  if (e == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+    dev = attr.device;
+  } else {
+    cudaGetLastError();
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaGetDevice");
+  }
+  if (g->device < 0) g->device = dev;
+  if (g->device != dev) {
+    epsm_set_error("group is bound to device %d but the buffer is on device %d", g->device, dev);
+    return EPSM_EINVAL;
+  }
+  e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaSetDevice");
+  return EPSM_OK;
+}
+
+static int group_run(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t owned_len, uint64_t base,
+                     uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search, epsm_stream_t stream) {
+  if (!g || !d_occ || (!d_text && n > 0)) {
+    epsm_set_error("epsm_group_*: NULL group, d_occ or text");
+    return EPSM_EINVAL;
+  }
+  if (n > (1ull << 38)) {
+    epsm_set_error("n = %llu exceeds 2^38", (unsigned long long)n);
+    return EPSM_EINVAL;
+  }
+  if (reinterpret_cast<uintptr_t>(d_occ) & 7u) {
+    epsm_set_error("d_occ must be 8-byte aligned");
+    return EPSM_EALIGN;
+  }
+  if (search && d_pos)
+    for (uint32_t j = 0; j < g->k; ++j)
+      if (d_pos[j] && (reinterpret_cast<uintptr_t>(d_pos[j]) & 7u)) {
+        epsm_set_error("d_pos[%u] must be 8-byte aligned", j);
+        return EPSM_EALIGN;
+      }
+  int rc = group_bind(g, d_occ);
+  if (rc) return rc;
+  uint64_t ns = n >= g->m ? n - g->m + 1 : 0;
+  if (owned_len < ns) ns = owned_len;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (auto& S : g->subs) {
+    rc = subgroup_launch(g, S, d_text, n, ns, base, d_pos, caps, d_occ, search, s);
+    if (rc) return rc;
+  }
+  return EPSM_OK;
+}
+
+extern "C" {
+
+int epsm_group_create(const uint8_t* patterns, uint32_t m, uint32_t k, epsm_group_t** out) {
+  if (!out) {
+    epsm_set_error("epsm_group_create: NULL out");
+    return EPSM_EINVAL;
+  }
+  *out = nullptr;
+  if (!patterns || m == 0 || k == 0) {
+    epsm_set_error("epsm_group_create: NULL patterns, m = 0 or k = 0");
+    return EPSM_EINVAL;
+  }
+  if (m > EPSM_MAX_M || k > static_cast<uint32_t>(mp::kMaxJobs)) {
+    epsm_set_error("epsm_group_create: m = %u > %u or k = %u > %d", m, EPSM_MAX_M, k, mp::kMaxJobs);
+    return EPSM_EUNSUP;
+  }
+  epsm_group_t* g = new (std::nothrow) epsm_group_t();
+  if (!g) return EPSM_ENOMEM;
+  g->m = m;
+  g->k = k;
+  // distinct patterns in order of first occurrence, and the searches asking for each
+  std::map<std::string, uint32_t> seen;
+  std::vector<std::string> pats;
+  std::vector<std::vector<uint32_t>> dups;
+  for (uint32_t j = 0; j < k; ++j) {
+    std::string p(reinterpret_cast<const char*>(patterns) + static_cast<size_t>(j) * m, m);
+    auto it = seen.find(p);
+    if (it == seen.end()) {
+      it = seen.emplace(p, static_cast<uint32_t>(pats.size())).first;
+      pats.push_back(p);
+      dups.emplace_back();
+    }
+    dups[it->second].push_back(j);
+  }
+  g->D = static_cast<uint32_t>(pats.size());
+  g->pats = pats;
+  g->dups = dups;
+  for (uint32_t a = 0; a < g->D; a += mp::kMaxD) {
+    const uint32_t b = std::min<uint32_t>(g->D, a + mp::kMaxD);
+    std::vector<std::string> sp(pats.begin() + a, pats.begin() + b);
+    std::vector<std::vector<uint32_t>> sd(dups.begin() + a, dups.begin() + b);
+    g->subs.emplace_back();
+    int rc = build_subgroup(sp, m, g->subs.back(), sd);
+    if (rc) {
+      group_release(g);
+      return rc;
+    }
+  }
+  *out = g;
+  return EPSM_OK;
+}
+
+void epsm_group_free(epsm_group_t* g) { group_release(g); }
+
+int epsm_group_set_geometry(epsm_group_t* g, uint32_t q, uint32_t sk) {
+  if (!g || q < 1 || q > 16 || q > g->m || sk < 1 || sk > 16 || (sk & (sk - 1)) || sk + q - 1 > g->m) {
+    epsm_set_error("epsm_group_set_geometry: need 1 <= q <= min(m, 16), SK in {1,2,4,8,16}, SK + q - 1 <= m");
+    return EPSM_EINVAL;
+  }
+  for (const auto& S : g->subs)
+    if (static_cast<uint64_t>(S.D) * sk > mp::kMaxEntries) {
+      epsm_set_error("epsm_group_set_geometry: %u patterns x SK = %u exceeds %d table entries", S.D, sk,
+                     mp::kMaxEntries);
+      return EPSM_EINVAL;
+    }
+  if (g->device >= 0) {
+    cudaSetDevice(g->device);
+    cudaDeviceSynchronize();
+  }
+  uint32_t a = 0;
+  for (auto& S : g->subs) {
+    if (S.d_desc) cudaFree(S.d_desc);
+    S.d_desc = nullptr;
+    const uint32_t b = a + S.D;
+    std::vector<std::string> sp(g->pats.begin() + a, g->pats.begin() + b);
+    std::vector<std::vector<uint32_t>> sd(g->dups.begin() + a, g->dups.begin() + b);
+    int rc = build_subgroup(sp, g->m, S, sd, static_cast<int>(q), static_cast<int>(sk));
+    if (rc) return rc;
+    a = b;
+  }
+  return EPSM_OK;
+}
+
+int epsm_group_info(const epsm_group_t* g, uint32_t* out, uint32_t nout) {
+  if (!g || !out) return EPSM_EINVAL;
+  std::vector<uint32_t> v = {g->m, g->k, g->D, static_cast<uint32_t>(g->subs.size())};
+  for (const auto& S : g->subs) {
+    v.push_back(static_cast<uint32_t>(S.q));
+    v.push_back(static_cast<uint32_t>(S.sk));
+  }
+  const uint32_t c = std::min<uint32_t>(nout, static_cast<uint32_t>(v.size()));
+  for (uint32_t i = 0; i < c; ++i) out[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+int epsm_group_search_async(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t* const* d_pos,
+                            const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
+  return group_run(g, d_text, n, n, 0, d_pos, caps, d_occ, true, stream);
+}
+
+int epsm_group_count_async(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t* d_occ,
+                           epsm_stream_t stream) {
+  return group_run(g, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream);
+}
+
+int epsm_group_search_range_async(epsm_group_t* g, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,
+                                  uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
+                                  uint64_t* d_occ, epsm_stream_t stream) {
+  if (!g) {
+    epsm_set_error("NULL group");
+    return EPSM_EINVAL;
+  }
+  if (base > n_total || owned_len > n_total - base || shard_len > n_total - base) {
+    epsm_set_error("shard [%llu, +%llu) owning %llu starts lies outside the text of %llu bytes",
+                   (unsigned long long)base, (unsigned long long)shard_len, (unsigned long long)owned_len,
+                   (unsigned long long)n_total);
+    return EPSM_EINVAL;
+  }
+  if (owned_len) {
+    const uint64_t need = std::min<uint64_t>(owned_len + g->m - 1, n_total - base);
+    if (shard_len < need) {
+      epsm_set_error("shard of %llu bytes is shorter than its owned starts plus the (m-1)-byte overlap (%llu)",
+                     (unsigned long long)shard_len, (unsigned long long)need);
+      return EPSM_EINVAL;
+    }
+  }
+  return group_run(g, d_shard, shard_len, owned_len, base, d_pos, caps, d_occ, true, stream);
+}
+
+}  // extern "C"

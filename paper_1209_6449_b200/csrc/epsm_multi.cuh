@@ -1,0 +1,532 @@
+// epsm_multi.cuh -- sm_100a kernels of the single-pass GROUP search: many patterns of one
+// length m over one text, the paper's own workload (100 / 1000 patterns "randomly extracted"
+// from each text, Sec. 4), with the text streamed once for the whole group.
+//
+// Every search of a group still returns exactly its own Occ(p_j, t): the
+// group only shares the work.  Three observations make that cheap on a GPU:
+//   * identical patterns have identical results: the group keeps its D distinct patterns and,
+//     per distinct pattern, the searches that asked for it;
+//   * all patterns have the same length m, so at a start s at most ONE distinct pattern
+//     matches -- a start carries one id (0..D-1) or none;
+//   * EPSMc's block fingerprints (Fig. 1 lines 1-12) generalise to many
+//     patterns: sample one q-gram every SK text bytes (SK + q - 1 <= m, so every window holds
+//     exactly one sample at an offset i < SK), and look the sample up in ONE table holding
+//     the q-grams p_d[i .. i+q) of every distinct pattern d and offset i (EPSMc's L[v], there
+//     per pattern).  A hit names candidate (s = x - i, d); the naive check
+//     of the window against p_d decides.  For q = m (m <= 16) a hit is the whole pattern.
+//
+// Passes of a group search (host: epsm_multi.cu):
+//   1. epsm_multi_kernel<SK, QW, false>  streams the text (TMA ring, as the single-pattern
+//      scan) and filters it; per chunk (one 32 KiB tile) it writes the count of every
+//      distinct pattern and, where the chunk holds at most kListCap occurrences, the list of
+//      them as (chunk offset, id) -- so the positions of sparse chunks are never recomputed;
+//   2. epsm_multi_scan_kernel            exclusive prefix over the chunks per distinct pattern
+//      (where each chunk's positions go in each output), the totals (every search's occ),
+//      and the list of chunks that hold occurrences at all;
+//   3. epsm_multi_kernel<SK, QW, true>   visits only those chunks: a chunk with a list is
+//      rebuilt from it (no text read), a dense chunk is streamed and filtered again; then the
+//      positions of each distinct pattern are ranked in text order and written to every
+//      search that asked for that pattern (Fig. 1 line 11: i*alpha + {r}).
+// DRAM traffic of a group: the text once (plus dense chunks once more -- those are the
+// chunks whose output is many bytes per text byte anyway) + the positions.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "epsm_ptx.cuh"
+
+namespace epsm {
+namespace mp {
+
+constexpr int kTile = 32768;                      // bytes per chunk (one TMA stage)
+constexpr int kHalo = 32;                         // >= m - 1 (m <= 32)
+constexpr int kStageBytes = kTile + 128;          // tile + halo + unaligned-read slack
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = 16;
+constexpr int kThreads = 32 + 32 * kConsumerWarps;   // producer warp + consumers
+constexpr int kSegBytes = 64;                     // starts per lane
+constexpr int kSliceBytes = 32 * kSegBytes;       // starts per warp and tile (2048)
+constexpr int kBatches = kSliceBytes / 32;        // 32-start batches per slice (64)
+constexpr int kMaxD = 255;                        // distinct patterns per group (u8 ids)
+constexpr uint8_t kNoId = 0xFF;
+constexpr int kBitmapLog = 16;                    // sample filter: 2^16 bits
+constexpr int kBucketLog = 12;                    // table buckets: 2^12
+constexpr int kMaxEntries = 4096;                 // (d, i) pairs: D * SK
+constexpr int kMaxJobs = 1024;                    // searches per group
+constexpr int kListCap = 256;                     // (offset, id) entries kept per chunk
+constexpr int kMaxPW = 8;                         // pattern words (m <= 32)
+static_assert(kSegBytes * 32 * kConsumerWarps == kTile, "lanes tile the chunk");
+
+// The group's preprocessing (built on the host, copied into shared memory once per CTA).
+struct __align__(16) GroupDesc {
+  uint32_t bitmap[(1 << kBitmapLog) / 32];        // bit h >> 16 set <=> some gram hashes there
+  uint16_t boff[(1 << kBucketLog) + 8];           // CSR offsets of bucket h >> 20 into ent
+  uint16_t ent[kMaxEntries];                      // d << 8 | i << 4 | (h >> 16) & 15
+  uint32_t pat[kMaxD + 1][kMaxPW];                // distinct patterns, zero padded, LE words
+  uint32_t pmask[kMaxPW];                         // byte masks of the words (m bytes)
+  uint16_t dup_off[kMaxD + 2];                    // searches of pattern d: dup_list[off[d] .. off[d+1])
+  uint16_t dup_list[kMaxJobs];
+  uint16_t job_d[kMaxJobs];                       // distinct pattern of (local) search j
+  uint16_t job_g[kMaxJobs];                       // its index in the caller's batch (occ slot)
+};
+
+struct MParams {
+  const uint8_t* text;          // 16-byte aligned virtual base
+  uint64_t nbytes;              // readable bytes from text
+  uint64_t s_lo, s_hi;          // valid virtual starts [s_lo, s_hi)
+  uint64_t pos_bias;            // reported = virtual start + pos_bias
+  uint32_t nchunks;             // tiles covering [0, s_hi)
+  uint32_t it_lo, it_hi;        // interior tiles: every start in [s_lo, s_hi)
+  uint32_t m, mw, D, k;         // pattern length, words, distinct patterns, searches
+  uint32_t qmask;               // byte mask of the last key word
+  uint32_t hmul[4];             // key word multipliers of the sample hash
+  uint32_t desc_bytes;
+  const GroupDesc* desc;
+  uint16_t* counts;             // [nchunks][D]: pass 1 out
+  uint32_t* listlen;            // [nchunks]: occurrences per chunk (pass 1 out)
+  uint32_t* lists;              // [nchunks][kListCap]: offset | id << 16 (pass 1 out)
+  const unsigned long long* prefix;   // [nchunks][D]: pass 3 in (scan out)
+  uint32_t* work;               // [0] chunks with occurrences, [1 ..] their ids (scan out)
+  uint64_t* pos[kMaxJobs];      // pass 3: output of search j
+  uint64_t cap[kMaxJobs];
+};
+
+struct ScanParams {
+  const uint16_t* counts;
+  const uint32_t* listlen;
+  unsigned long long* prefix;   // NULL: totals only (count)
+  uint32_t* work;
+  unsigned long long* occ;      // the batch's occ array (slot job_g[j] for local search j)
+  const GroupDesc* desc;        // job_d, job_g
+  uint32_t nchunks, D, k;
+};
+
+template <int SK>
+struct Geo {
+  static constexpr int kSamples = kSegBytes / SK + (SK > 1 ? 1 : 0);   // sample offsets 0, SK, ..
+};
+
+__device__ __forceinline__ void bar_consumers() {   // named barrier over the 16 consumer warps
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+}
+
+// 4 bytes at an arbitrary shared-memory byte offset (4-byte aligned base)
+__device__ __forceinline__ uint32_t lds_u32_any(const uint8_t* base, uint32_t off) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
+  return __funnelshift_r(w[0], w[1], 8 * (off & 3u));
+}
+
+template <int QW>
+__device__ __forceinline__ uint32_t hash_words(const uint32_t (&k)[4], const MParams& P) {
+  uint32_t h = k[0] * P.hmul[0];
+#pragma unroll
+  for (int r = 1; r < QW; ++r) h += k[r] * P.hmul[r];
+  return h;
+}
+
+// Shared-memory layout of the group kernel.
+struct __align__(128) MSmem {
+  uint8_t ring[kStages][kStageBytes];
+  GroupDesc g;
+  uint8_t ids[kConsumerWarps][kSliceBytes];           // id of the pattern at each start, kNoId
+  uint16_t hist[kConsumerWarps][kMaxD + 1];          // per-slice counts -> exclusive offsets
+  unsigned long long pre[kMaxD + 1];                 // pass 3: the chunk's global prefix
+  uint32_t ccnt[kStages][kMaxD + 1];                 // pass 1: chunk counts (by stage)
+  uint32_t lcur[kStages];                            // pass 1: list cursor (by stage)
+  uint32_t done[kStages];                            // pass 1: warps finished with the stage
+  uint32_t nbw[kConsumerWarps][2];                   // nonempty batches of a slice (list path)
+  alignas(8) uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t gfull;
+  uint32_t info[kStages];                            // chunk | kInfoList, or kEnd
+  uint32_t ilen[kStages];                            // list length (list stages)
+};
+static_assert(sizeof(MSmem) <= 232448, "group kernel fits 227 KB of shared memory");
+constexpr uint32_t kEnd = 0xFFFFFFFFu;
+constexpr uint32_t kInfoList = 0x80000000u;
+
+// Naive check of the window at stage offset st against distinct pattern d.
+__device__ __forceinline__ bool verify_window(const uint8_t* ts, uint32_t st, const GroupDesc& G, uint32_t d,
+                                              uint32_t mw) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(ts + (st & ~3u));
+  const uint32_t sh = 8 * (st & 3u);
+  uint32_t lo = w[0];
+  for (uint32_t r = 0; r < mw; ++r) {
+    const uint32_t hi = w[r + 1];
+    if ((__funnelshift_r(lo, hi, sh) ^ G.pat[d][r]) & G.pmask[r]) return false;
+    lo = hi;
+  }
+  return true;
+}
+
+template <int SK, int QW, bool WRITE>
+__global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_constant__ MParams P) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  MSmem& S = *reinterpret_cast<MSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31u;
+  const uint32_t warp = tid >> 5;
+
+  if (tid < static_cast<uint32_t>(kStages)) {
+    mbar_init(&S.full[tid], 1);
+    mbar_init(&S.empty[tid], kConsumerWarps);
+    S.lcur[tid] = 0;
+    S.done[tid] = 0;
+    fence_mbar_init();
+  } else if (tid == 32) {
+    mbar_init(&S.gfull, 1);
+    fence_mbar_init();
+  }
+  // ids start empty; chunk counters zero
+  for (uint32_t i = tid; i < kConsumerWarps * kSliceBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(&S.ids[0][0])[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  for (uint32_t i = tid; i < kStages * (kMaxD + 1); i += blockDim.x) (&S.ccnt[0][0])[i] = 0;
+  for (uint32_t i = tid; i < kConsumerWarps * (kMaxD + 1); i += blockDim.x) (&S.hist[0][0])[i] = 0;
+  if (!WRITE && blockIdx.x == 0 && tid == 0) P.work[0] = 0;   // (the scan appends; runs after)
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================================================================ producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&S.gfull, P.desc_bytes);
+      bulk_g2s_plain(&S.g, P.desc, P.desc_bytes, &S.gfull);
+    }
+    const uint64_t policy = policy_evict_first();
+    uint32_t stage = 0, phase = 0;
+    const uint32_t nwork = WRITE ? *reinterpret_cast<volatile const uint32_t*>(P.work) : P.nchunks;
+    for (uint32_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+      const uint32_t c = WRITE ? P.work[1 + w] : w;
+      uint32_t len = 0;
+      if (WRITE) len = P.listlen[c];
+      mbar_wait(&S.empty[stage], phase ^ 1u);
+      if (WRITE && len <= static_cast<uint32_t>(kListCap)) {
+        // a sparse chunk: its occurrences were listed by pass 1; the text is not needed
+        if (lane == 0) {
+          S.info[stage] = c | kInfoList;
+          S.ilen[stage] = len;
+          const uint32_t bytes = (len * 4u + 15u) & ~15u;
+          mbar_arrive_expect_tx(&S.full[stage], bytes);
+          bulk_g2s_plain(S.ring[stage], P.lists + static_cast<uint64_t>(c) * kListCap, bytes, &S.full[stage]);
+        }
+      } else {
+        const uint64_t base = static_cast<uint64_t>(c) * kTile;
+        const uint64_t want_end = base + kTile + kHalo;
+        const uint64_t end = want_end < P.nbytes ? want_end : P.nbytes;
+        const uint32_t bulk = static_cast<uint32_t>((end & ~15ull) - base);
+        const uint32_t tail = static_cast<uint32_t>(end - base) - bulk;
+        if (lane < tail) S.ring[stage][bulk + lane] = P.text[base + bulk + lane];
+        __syncwarp();
+        if (lane == 0) {
+          S.info[stage] = c;
+          if (bulk) {
+            mbar_arrive_expect_tx(&S.full[stage], bulk);
+            bulk_g2s(S.ring[stage], P.text + base, bulk, &S.full[stage], policy);
+          } else {
+            mbar_arrive(&S.full[stage]);
+          }
+        }
+      }
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    mbar_wait(&S.empty[stage], phase ^ 1u);
+    if (lane == 0) {
+      S.info[stage] = kEnd;
+      mbar_arrive(&S.full[stage]);
+    }
+    return;
+  }
+
+  // ================================================================== consumers
+  const uint32_t cw = warp - 1;
+  const uint32_t seg = cw * kSliceBytes + lane * kSegBytes;    // the lane's 64 starts in a tile
+  const uint32_t lt = (1u << lane) - 1u;
+  mbar_wait(&S.gfull, 0);
+  const GroupDesc& G = S.g;
+  uint32_t stage = 0, phase = 0;
+  uint8_t* const ids = S.ids[cw];
+  while (true) {
+    mbar_wait(&S.full[stage], phase);
+    const uint32_t info = S.info[stage];
+    if (info == kEnd) break;
+    const uint32_t c = info & ~kInfoList;
+    const uint8_t* ts = S.ring[stage];
+    uint32_t nb_lo = 0, nb_hi = 0;      // nonempty 32-start batches of this warp's slice
+    if (WRITE && (info & kInfoList)) {
+      // ---- rebuild the chunk's ids from its list (pass 1 kept it: no text)
+      if (lane < 2) S.nbw[cw][lane] = 0;
+      bar_consumers();
+      const uint32_t len = S.ilen[stage];
+      const uint32_t* L = reinterpret_cast<const uint32_t*>(ts);
+      for (uint32_t e = tid - 32; e < len; e += 32 * kConsumerWarps) {
+        const uint32_t v = L[e];
+        const uint32_t off = v & 0xFFFFu, d = v >> 16;
+        S.ids[off / kSliceBytes][off % kSliceBytes] = static_cast<uint8_t>(d);
+        const uint32_t b = (off % kSliceBytes) >> 5;
+        atomicOr(&S.nbw[off / kSliceBytes][b >> 5], 1u << (b & 31u));
+      }
+      bar_consumers();
+      nb_lo = S.nbw[cw][0];
+      nb_hi = S.nbw[cw][1];
+    } else {
+      // ---- filter the warp's slice: one sample every SK bytes (EPSMc)
+      uint32_t W[20];
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(ts + seg);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint4 v = src[r];
+          W[4 * r] = v.x;
+          W[4 * r + 1] = v.y;
+          W[4 * r + 2] = v.z;
+          W[4 * r + 3] = v.w;
+        }
+        // bytes 64..79: the next lane's first 16 (lane 31: the next slice / the tile halo)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) W[16 + r] = __shfl_down_sync(0xffffffffu, W[r], 1);
+        if (lane == 31) {
+          const uint4 v = src[4];
+          W[16] = v.x;
+          W[17] = v.y;
+          W[18] = v.z;
+          W[19] = v.w;
+        }
+      }
+      constexpr int NS = Geo<SK>::kSamples;
+      uint64_t hits = 0;
+      uint32_t hit64 = 0;                         // the sample at offset 64 (SK > 1)
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        // key words r < QW at the compile-time byte offset j * SK + 4r of the lane's registers
+        uint32_t k[4];
+#pragma unroll
+        for (int r = 0; r < QW; ++r) {
+          const int b = j * SK + 4 * r;
+          const int wi = b >> 2, sh = b & 3;
+          k[r] = sh == 0 ? W[wi] : __funnelshift_r(W[wi], W[wi + 1], 8 * sh);
+        }
+        k[QW - 1] &= P.qmask;
+        const uint32_t h = hash_words<QW>(k, P);
+        const uint32_t bw = G.bitmap[h >> (32 - kBitmapLog + 5)];
+        const uint32_t bit = __funnelshift_r(bw, bw, h >> (32 - kBitmapLog)) & 1u;
+        if (j < 64) hits |= static_cast<uint64_t>(bit) << j;
+        else hit64 = bit;
+      }
+      uint64_t M = 0;                             // matched starts of the lane
+      if (__any_sync(0xffffffffu, (hits | hit64) != 0)) {
+        const uint64_t tbase = static_cast<uint64_t>(c) * kTile;
+        const bool interior = c >= P.it_lo && c < P.it_hi;
+        // candidates: every table entry (d, i) of the sample's bucket with
+        // the sample's fingerprint bits names the start x - i of pattern d; naive check
+        uint64_t hm = hits;
+        uint32_t h64 = hit64;
+        while (hm | h64) {
+          uint32_t o;
+          if (hm) {
+            o = (__ffsll(static_cast<long long>(hm)) - 1) * SK;
+            hm &= hm - 1;
+          } else {
+            o = 64;
+            h64 = 0;
+          }
+          const uint32_t xt = seg + o;               // the sample's stage offset
+          uint32_t k[4];
+#pragma unroll
+          for (int r = 0; r < QW; ++r) k[r] = lds_u32_any(ts, xt + 4 * r);
+          k[QW - 1] &= P.qmask;
+          const uint32_t h = hash_words<QW>(k, P);
+          const uint32_t bk = h >> (32 - kBucketLog);
+          const uint32_t fp = (h >> (32 - kBitmapLog)) & 15u;
+          const uint32_t e1 = G.boff[bk + 1];
+          for (uint32_t e = G.boff[bk]; e < e1; ++e) {
+            const uint32_t v = G.ent[e];
+            if ((v & 15u) != fp) continue;
+            const uint32_t i = (v >> 4) & 15u, d = v >> 8;
+            if (i > o || o - i >= static_cast<uint32_t>(kSegBytes)) continue;   // not the lane's start
+            const uint32_t st = xt - i;                   // start, stage offset
+            if (!interior) {
+              const uint64_t vs = tbase + st;
+              if (vs < P.s_lo || vs >= P.s_hi) continue;
+            }
+            if (verify_window(ts, st, G, d, P.mw)) {
+              ids[lane * kSegBytes + (o - i)] = static_cast<uint8_t>(d);
+              M |= 1ull << (o - i);
+            }
+          }
+        }
+      }
+      // nonempty batches: batch b = slice starts [32b, 32b + 32) = lane b/2, half b&1
+      const uint32_t blo = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M) != 0u);
+      const uint32_t bhi = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M >> 32) != 0u);
+      // interleave: batch 2l <- blo bit l, batch 2l + 1 <- bhi bit l
+#pragma unroll
+      for (int l = 0; l < 16; ++l) {
+        nb_lo |= ((blo >> l) & 1u) << (2 * l);
+        nb_lo |= ((bhi >> l) & 1u) << (2 * l + 1);
+        nb_hi |= ((blo >> (l + 16)) & 1u) << (2 * l);
+        nb_hi |= ((bhi >> (l + 16)) & 1u) << (2 * l + 1);
+      }
+      __syncwarp();
+    }
+
+    if constexpr (!WRITE) {
+      // ---- pass 1: counts per distinct pattern, and the chunk's list while it is short
+      uint64_t nbm = (static_cast<uint64_t>(nb_hi) << 32) | nb_lo;
+      uint32_t* const cc = S.ccnt[stage];
+      while (nbm) {
+        const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
+        nbm &= nbm - 1;
+        const uint32_t id = ids[32 * b + lane];
+        ids[32 * b + lane] = kNoId;
+        const bool act = id != kNoId;
+        const uint32_t peers = __match_any_sync(0xffffffffu, id);
+        if (act && (peers & lt) == 0) atomicAdd(&cc[id], static_cast<uint32_t>(__popc(peers)));
+        const uint32_t am = __ballot_sync(0xffffffffu, act);
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&S.lcur[stage], static_cast<uint32_t>(__popc(am)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const uint32_t r = base + __popc(am & lt);
+        if (act && r < static_cast<uint32_t>(kListCap))
+          P.lists[static_cast<uint64_t>(c) * kListCap + r] = (cw * kSliceBytes + 32 * b + lane) | (id << 16);
+      }
+      __syncwarp();
+      uint32_t prev = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        prev = atomicAdd(&S.done[stage], 1u);
+      }
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == kConsumerWarps - 1) {
+        // the last warp of the chunk publishes its counts and resets the stage's counters
+        __threadfence_block();
+        for (uint32_t d = lane; d < P.D; d += 32) {
+          P.counts[static_cast<uint64_t>(c) * P.D + d] = static_cast<uint16_t>(cc[d]);
+          cc[d] = 0;
+        }
+        if (lane == 0) {
+          P.listlen[c] = S.lcur[stage];
+          S.lcur[stage] = 0;
+          S.done[stage] = 0;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive(&S.empty[stage]);
+    } else {
+      // ---- pass 3: rank every occurrence among its pattern's in text order, then write it to
+      // each search that asked for that pattern at prefix + rank
+      uint16_t* const hw = S.hist[cw];
+      uint64_t nbm = (static_cast<uint64_t>(nb_hi) << 32) | nb_lo;
+      {
+        uint64_t t = nbm;
+        while (t) {
+          const uint32_t b = __ffsll(static_cast<long long>(t)) - 1;
+          t &= t - 1;
+          const uint32_t id = ids[32 * b + lane];
+          const uint32_t peers = __match_any_sync(0xffffffffu, id);
+          if (id != kNoId && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
+          __syncwarp();
+        }
+      }
+      if (lane == 0) mbar_arrive(&S.empty[stage]);   // (lists and text both consumed)
+      bar_consumers();
+      // exclusive offsets of every slice inside the chunk, per pattern; the chunk's prefix
+      for (uint32_t d = tid - 32; d < P.D; d += 32 * kConsumerWarps) {
+        uint32_t run = 0;
+#pragma unroll 4
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          const uint32_t v = S.hist[w][d];
+          S.hist[w][d] = static_cast<uint16_t>(run);
+          run += v;
+        }
+        S.pre[d] = P.prefix[static_cast<uint64_t>(c) * P.D + d];
+      }
+      bar_consumers();
+      const uint64_t cbase = static_cast<uint64_t>(c) * kTile + P.pos_bias + cw * kSliceBytes;
+      while (nbm) {
+        const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
+        nbm &= nbm - 1;
+        const uint32_t id = ids[32 * b + lane];
+        ids[32 * b + lane] = kNoId;
+        const uint32_t peers = __match_any_sync(0xffffffffu, id);
+        const bool act = id != kNoId;
+        uint64_t g = 0;
+        if (act) g = S.pre[id] + hw[id] + __popc(peers & lt);
+        __syncwarp();
+        if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
+        if (act) {
+          const uint64_t pos = cbase + 32 * b + lane;
+          const uint32_t j1 = G.dup_off[id + 1];
+          for (uint32_t q = G.dup_off[id]; q < j1; ++q) {
+            const uint32_t j = G.dup_list[q];
+            if (g < P.cap[j]) st_stream_u64(P.pos[j] + g, pos);
+          }
+        }
+      }
+      __syncwarp();
+      // the warp's offsets are spent: zero its row for the next chunk (no other warp reads it
+      // before the next chunk's first barrier)
+      for (uint32_t d = lane; d < P.D; d += 32) hw[d] = 0;
+      __syncwarp();
+    }
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
+// Pass 2: per distinct pattern, the exclusive prefix of its chunk counts (where each chunk's
+// positions start in every output of that pattern) and its total (the occ of every search of
+// that pattern); plus the list of chunks with occurrences.  Block b scans
+// patterns [32b, 32b + 32) -- lane = pattern, warp w = a contiguous run of chunks.
+constexpr int kScanWarps = 32;
+__global__ void __launch_bounds__(32 * kScanWarps) epsm_multi_scan_kernel(const __grid_constant__ ScanParams P) {
+  __shared__ unsigned long long part[kScanWarps][32];
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  const uint32_t d = blockIdx.x * 32 + lane;
+  const bool live = d < P.D;
+  const uint32_t per = (P.nchunks + kScanWarps - 1) / kScanWarps;
+  const uint32_t c0 = min(P.nchunks, w * per), c1 = min(P.nchunks, c0 + per);
+  unsigned long long s = 0;
+  if (live)
+    for (uint32_t c = c0; c < c1; ++c) s += P.counts[static_cast<uint64_t>(c) * P.D + d];
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long run = 0;
+    for (int q = 0; q < kScanWarps; ++q) {
+      const unsigned long long v = part[q][lane];
+      part[q][lane] = run;
+      run += v;
+    }
+    if (live) {
+      for (uint32_t j = 0; j < P.k; ++j)
+        if (P.desc->job_d[j] == d) P.occ[P.desc->job_g[j]] = run;
+    }
+  }
+  __syncthreads();
+  if (live && P.prefix) {
+    unsigned long long run = part[w][lane];
+    for (uint32_t c = c0; c < c1; ++c) {
+      P.prefix[static_cast<uint64_t>(c) * P.D + d] = run;
+      run += P.counts[static_cast<uint64_t>(c) * P.D + d];
+    }
+  }
+  // chunks with occurrences (order irrelevant: each is handled on its own); block 0 only
+  if (blockIdx.x == 0 && P.prefix) {
+    for (uint32_t c0b = 0; c0b < P.nchunks; c0b += blockDim.x) {
+      const uint32_t cc = c0b + threadIdx.x;
+      const bool ne = cc < P.nchunks && P.listlen[cc] > 0;
+      const uint32_t bal = __ballot_sync(0xffffffffu, ne);
+      uint32_t base = 0;
+      if (lane == 0 && bal) base = atomicAdd(P.work, static_cast<uint32_t>(__popc(bal)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (ne) P.work[1 + base + __popc(bal & ((1u << lane) - 1u))] = cc;
+    }
+  }
+}
+
+}  // namespace mp
+}  // namespace epsm

@@ -1,0 +1,215 @@
+"""GPU parity of the group search (epsm_group_*): k patterns of one length in one pass.
+
+Every search of a group must return exactly its own Occ(p_j, t), as the
+oracle computes it pattern by pattern.  Cases: every alphabet / pattern length class, every
+(gram length, stride) geometry the kernels are compiled for, duplicate and absent patterns,
+occurrences planted at every lane (64 B), slice (2 KiB) and chunk (32 KiB) edge and at the text
+ends, dense texts whose chunks overflow the per-chunk occurrence lists (positions recomputed
+from the text) mixed with sparse chunks (positions from the lists), misaligned text pointers,
+capacities below occ, count-only calls, shards, and groups of more than 255 distinct patterns
+(several passes).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TILE = 32768
+
+
+@pytest.fixture(scope="module")
+def epsm():
+    import paper_1209_6449_b200 as e
+    return e
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda:0")
+
+
+def run_group(epsm, pats, td, caps=None, geom=None, count_only=False):
+    g = epsm.group(pats)
+    if geom is not None:
+        g.set_geometry(*geom)
+    n = td.numel()
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=td.device)
+    if count_only:
+        g.count_async(td, occ)
+        torch.cuda.synchronize()
+        g.close()
+        return [(int(o), None) for o in occ.cpu().tolist()]
+    outs = [torch.full((max(n, 1),), -7, dtype=torch.int64, device=td.device) for _ in pats]
+    g.search_async(td, occ, outs=outs, caps=caps)
+    torch.cuda.synchronize()
+    res = []
+    for j in range(len(pats)):
+        k = int(occ[j])
+        c = k if caps is None else min(k, caps[j])
+        got = outs[j][:c].cpu().numpy().astype(np.uint64)
+        if caps is not None and caps[j] < outs[j].numel():
+            assert int(outs[j][caps[j]]) == -7, "wrote past the capacity"
+        res.append((k, got))
+    g.close()
+    return res
+
+
+def check(pats, res, t, label, caps=None):
+    cache = {}
+    for j, (p, (k, got)) in enumerate(zip(pats, res)):
+        if p not in cache:
+            cache[p] = oracle.search(p, t)
+        want = cache[p]
+        assert k == want.size, (label, j, len(p), k, want.size)
+        if got is not None:
+            c = want.size if caps is None else min(want.size, caps[j])
+            assert np.array_equal(got, want[:c]), (label, j, len(p), got[:8], want[:8])
+
+
+def planted(rng, n, sigma, m, count, absent=3):
+    t = rng.integers(0, sigma, size=n, dtype=np.uint8)
+    starts = rng.integers(0, n - m + 1, size=count)
+    pats = [t[s:s + m].tobytes() for s in starts]
+    # plant the first patterns across lane / slice / chunk edges and at both ends
+    edges = [0, n - m]
+    for e in (64, 128, 2048, 4096, TILE, 2 * TILE, 3 * TILE + 2048, 4 * TILE - 64):
+        for d in (-m + 1, -1, 0):
+            if 0 <= e + d <= n - m:
+                edges.append(e + d)
+    for i, e in enumerate(edges):
+        p = np.frombuffer(pats[i % min(len(pats), 5)], np.uint8)
+        t[e:e + m] = p
+    pats = [t[s:s + m].tobytes() for s in starts]            # (re-read after planting)
+    pats += [pats[0], pats[1], pats[0]]                      # duplicates
+    pats += [rng.integers(0, 256, size=m, dtype=np.uint8).tobytes() for _ in range(absent)]
+    return t, pats
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 20, 256])
+def test_group_alphabets_and_lengths(epsm, dev, sigma):
+    rng = np.random.default_rng(sigma)
+    n = 5 * TILE + 777
+    for m in (1, 2, 3, 4, 5, 7, 8, 9, 12, 16, 17, 20, 24, 31, 32):
+        t, pats = planted(rng, n, sigma, m, 30)
+        td = torch.from_numpy(t).to(dev)
+        check(pats, run_group(epsm, pats, td), t, (sigma, m))
+
+
+GEOMS = [(q, sk) for q in (1, 2, 3, 4, 5, 7, 8, 9, 12, 13, 16) for sk in (1, 2, 4, 8, 16) if sk + q - 1 <= 32]
+
+
+@pytest.mark.parametrize("q,sk", GEOMS)
+def test_group_every_geometry(epsm, dev, q, sk):
+    """Every compiled (key words, stride) variant, forced: same results."""
+    rng = np.random.default_rng(100 + 17 * q + sk)
+    n = 3 * TILE + 4321
+    for sigma, m in ((4, 32), (2, max(17, q + sk - 1)), (256, max(q + sk - 1, 1))):
+        t, pats = planted(rng, n, sigma, m, 20)
+        td = torch.from_numpy(t).to(dev)
+        check(pats, run_group(epsm, pats, td, geom=(q, sk)), t, (q, sk, sigma, m))
+
+
+def test_group_dense_and_sparse_chunks_mixed(epsm, dev):
+    """Chunks over the occurrence-list capacity (positions recomputed from the text) next to
+    sparse chunks (positions from the lists) in one launch."""
+    rng = np.random.default_rng(5)
+    n = 8 * TILE + 99
+    t = rng.integers(0, 256, size=n, dtype=np.uint8)
+    t[2 * TILE + 100: 5 * TILE - 7] = ord("a")              # dense run over 3 chunks
+    t[6 * TILE: 6 * TILE + 3000] = np.tile(np.frombuffer(b"ab", np.uint8), 1500)
+    for m in (2, 4, 16, 32):
+        pats = [b"a" * m, (b"ab" * 16)[:m], (b"ba" * 16)[:m], b"a" * m,
+                t[100:100 + m].tobytes(), t[7 * TILE:7 * TILE + m].tobytes(), b"\x00" * m]
+        td = torch.from_numpy(t).to(dev)
+        check(pats, run_group(epsm, pats, td), t, ("mixed", m))
+
+
+def test_group_unary_closed_form(epsm, dev):
+    n = 6 * TILE + 13
+    td = torch.full((n,), ord("a"), dtype=torch.uint8, device=dev)
+    for m in (1, 2, 16, 32):
+        pats = [b"a" * m] * 4 + [b"b" * m]
+        res = run_group(epsm, pats, td)
+        for j in range(4):
+            k, got = res[j]
+            assert k == n - m + 1 and np.array_equal(got, np.arange(n - m + 1, dtype=np.uint64))
+        assert res[4][0] == 0
+
+
+@pytest.mark.parametrize("offset", [1, 3, 8, 15])
+def test_group_misaligned_text(epsm, dev, offset):
+    rng = np.random.default_rng(offset)
+    n = 2 * TILE + 555
+    big = rng.integers(0, 4, size=n + 32, dtype=np.uint8)
+    t = big[offset:offset + n]
+    bd = torch.from_numpy(big).to(dev)
+    td = bd[offset:offset + n]
+    for m in (2, 5, 16, 32):
+        pats = [t[s:s + m].tobytes() for s in (0, 1, n - m, 12345, 40000)]
+        check(pats, run_group(epsm, pats, td), t, ("mis", offset, m))
+
+
+def test_group_caps_and_counts(epsm, dev):
+    rng = np.random.default_rng(9)
+    n = 4 * TILE + 1
+    t = rng.integers(0, 2, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    pats = [t[s:s + 3].tobytes() for s in (0, 10, 20, 30, 40, 50)]
+    occs = [oracle.count(p, t) for p in pats]
+    caps = [0, 1, occs[2] // 2, occs[3], occs[4] + 5, 7]
+    check(pats, run_group(epsm, pats, td, caps=caps), t, "caps", caps=caps)
+    check(pats, run_group(epsm, pats, td, count_only=True), t, "count")
+
+
+def test_group_short_texts(epsm, dev):
+    for n in (0, 1, 2, 15, 16, 17, 31, 32, 33, 64, 65):
+        t = np.frombuffer((b"abcabcabca" * 8)[:n], np.uint8).copy()
+        td = torch.from_numpy(t).to(dev) if n else torch.empty(0, dtype=torch.uint8, device=dev)
+        for m in (1, 2, 3, 16, 32):
+            pats = [(b"abc" * 11)[:m], (b"bca" * 11)[:m], b"z" * m]
+            check(pats, run_group(epsm, pats, td), t, ("short", n, m))
+
+
+def test_group_many_distinct_patterns(epsm, dev):
+    """More than 255 distinct patterns: several passes, each search still exact."""
+    rng = np.random.default_rng(11)
+    n = 3 * TILE + 17
+    t = rng.integers(0, 256, size=n, dtype=np.uint8)
+    starts = rng.integers(0, n - 4, size=700)
+    pats = [t[s:s + 4].tobytes() for s in starts] + [b"\x01\x02\x03\x04"] * 3
+    g = epsm.group(pats)
+    assert len(g.info()["passes"]) >= 3
+    g.close()
+    check(pats, run_group(epsm, pats, torch.from_numpy(t).to(dev)), t, "many")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_group_shards_compose(epsm, dev, world):
+    from paper_1209_6449_b200 import sharding
+    rng = np.random.default_rng(50 + world)
+    n = 6 * TILE + 345
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    for m in (2, 8, 32):
+        pats = [t[s:s + m].tobytes() for s in rng.integers(0, n - m, size=12)]
+        for r in range(1, world):                              # straddle every cut
+            b = sharding.shard_base(n, world, r)
+            t[b - m // 2:b - m // 2 + m] = np.frombuffer(pats[0], np.uint8)
+        wants = [oracle.search(p, t) for p in pats]
+        td = torch.from_numpy(t).to(dev)
+        g = epsm.group(pats)
+        parts = [[] for _ in pats]
+        for r in range(world):
+            base, owned, slen = sharding.shard_layout(n, world, r)
+            shard = td[base:base + slen].clone()
+            occ = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+            outs = [torch.empty(w.size + 1, dtype=torch.int64, device=dev) for w in wants]
+            g.search_range_async(shard, owned, base, n, occ, outs=outs)
+            torch.cuda.synchronize()
+            for j in range(len(pats)):
+                parts[j].append(outs[j][:int(occ[j])].cpu().numpy().astype(np.uint64))
+        g.close()
+        for j, w in enumerate(wants):
+            assert np.array_equal(np.concatenate(parts[j]), w), (world, m, j)
