@@ -5,7 +5,10 @@
 
 #include "epsm.h"
 
-namespace epsm { struct JobDesc; }
+namespace epsm {
+struct JobDesc;
+namespace mp { struct JobOut; }
+}  // namespace epsm
 
 struct epsm_plan_s {
   uint32_t m = 0;
@@ -67,6 +70,8 @@ struct epsm_workspace {
   uint64_t m_lists_cap = 0;
   uint32_t* m_work = nullptr;
   uint64_t m_work_cap = 0;
+  epsm::mp::JobOut* m_jobs = nullptr;         // outputs of the searches of a pass
+  uint64_t m_jobs_cap = 0;
   unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
 };
 

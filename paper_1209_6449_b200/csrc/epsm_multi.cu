@@ -254,6 +254,8 @@ static int ensure_multi_ws(epsm_workspace* ws, uint64_t chunks, uint32_t D, cuda
   if (!rc)
     rc = grow(reinterpret_cast<void**>(&ws->m_lists), ws->m_lists_cap, chunks * mp::kListCap * 4ull, "chunk lists");
   if (!rc) rc = grow(reinterpret_cast<void**>(&ws->m_work), ws->m_work_cap, (chunks + 1) * 4, "work list");
+  if (!rc)
+    rc = grow(reinterpret_cast<void**>(&ws->m_jobs), ws->m_jobs_cap, mp::kMaxJobs * sizeof(mp::JobOut), "job table");
   return rc;
 }
 
@@ -328,10 +330,18 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   P.lists = ws->m_lists;
   P.prefix = ws->m_prefix;
   P.work = ws->m_work;
-  for (uint32_t j = 0; j < S.k; ++j) {
-    const uint32_t gj = S.jobs[j];
-    P.pos[j] = (search && d_pos) ? d_pos[gj] : nullptr;
-    P.cap[j] = (search && d_pos && d_pos[gj] && caps) ? caps[gj] : 0;
+  if (search) {
+    // the searches' outputs, in stream order into the workspace's job table (a pageable copy
+    // is staged before cudaMemcpyAsync returns, so the host vector may go)
+    std::vector<mp::JobOut> jt(S.k);
+    for (uint32_t j = 0; j < S.k; ++j) {
+      const uint32_t gj = S.jobs[j];
+      jt[j].pos = d_pos ? d_pos[gj] : nullptr;
+      jt[j].cap = (d_pos && d_pos[gj] && caps) ? caps[gj] : 0;
+    }
+    cudaError_t e = cudaMemcpyAsync(ws->m_jobs, jt.data(), S.k * sizeof(mp::JobOut), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(group job table)");
+    P.jobs = ws->m_jobs;
   }
   const int smem = static_cast<int>(sizeof(mp::MSmem));
   // pass 1: counts per (chunk, distinct pattern), lists of sparse chunks

@@ -70,6 +70,11 @@ struct __align__(16) GroupDesc {
   uint16_t job_g[kMaxJobs];                       // its index in the caller's batch (occ slot)
 };
 
+struct JobOut {                 // where search j's positions go
+  uint64_t* pos;
+  uint64_t cap;
+};
+
 struct MParams {
   const uint8_t* text;          // 16-byte aligned virtual base
   uint64_t nbytes;              // readable bytes from text
@@ -87,8 +92,7 @@ struct MParams {
   uint32_t* lists;              // [nchunks][kListCap]: offset | id << 16 (pass 1 out)
   const unsigned long long* prefix;   // [nchunks][D]: pass 3 in (scan out)
   uint32_t* work;               // [0] chunks with occurrences, [1 ..] their ids (scan out)
-  uint64_t* pos[kMaxJobs];      // pass 3: output of search j
-  uint64_t cap[kMaxJobs];
+  const JobOut* jobs;           // pass 3: output of (local) search j (device memory)
 };
 
 struct ScanParams {
@@ -100,6 +104,20 @@ struct ScanParams {
   const GroupDesc* desc;        // job_d, job_g
   uint32_t nchunks, D, k;
 };
+
+#ifdef EPSM_MULTI_DEBUG
+#include <cstdio>
+#define MP_CHECK(cond, tag, a, b)                                                              \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("MP_CHECK %s failed: %s a=%llu b=%llu blk=%d tid=%d\n", #cond, tag,               \
+             (unsigned long long)(a), (unsigned long long)(b), (int)blockIdx.x, (int)threadIdx.x); \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define MP_CHECK(cond, tag, a, b) do { } while (0)
+#endif
 
 template <int SK>
 struct Geo {
@@ -189,11 +207,19 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
     // ================================================================ producer
     if (lane == 0) {
       mbar_arrive_expect_tx(&S.gfull, P.desc_bytes);
-      bulk_g2s_plain(&S.g, P.desc, P.desc_bytes, &S.gfull);
+      // (in pieces of at most 8 KiB)
+      for (uint32_t a = 0; a < P.desc_bytes; a += 8192u) {
+        const uint32_t b = P.desc_bytes - a < 8192u ? P.desc_bytes - a : 8192u;
+        bulk_g2s_plain(reinterpret_cast<uint8_t*>(&S.g) + a, reinterpret_cast<const uint8_t*>(P.desc) + a, b,
+                       &S.gfull);
+      }
     }
     const uint64_t policy = policy_evict_first();
     uint32_t stage = 0, phase = 0;
-    const uint32_t nwork = WRITE ? *reinterpret_cast<volatile const uint32_t*>(P.work) : P.nchunks;
+    // (the work count is read through its own pointer: a ternary between a volatile load and a
+    // __grid_constant__ member once compiled into a volatile load from the parameter's address)
+    uint32_t nwork = P.nchunks;
+    if constexpr (WRITE) nwork = *reinterpret_cast<volatile const uint32_t*>(P.work);
     for (uint32_t w = blockIdx.x; w < nwork; w += gridDim.x) {
       const uint32_t c = WRITE ? P.work[1 + w] : w;
       uint32_t len = 0;
@@ -309,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         }
         k[QW - 1] &= P.qmask;
         const uint32_t h = hash_words<QW>(k, P);
+        MP_CHECK((h >> (32 - kBitmapLog + 5)) < 2048u, "bitmap", h, j);
         const uint32_t bw = G.bitmap[h >> (32 - kBitmapLog + 5)];
         const uint32_t bit = __funnelshift_r(bw, bw, h >> (32 - kBitmapLog)) & 1u;
         if (j < 64) hits |= static_cast<uint64_t>(bit) << j;
@@ -340,8 +367,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           const uint32_t bk = h >> (32 - kBucketLog);
           const uint32_t fp = (h >> (32 - kBitmapLog)) & 15u;
           const uint32_t e1 = G.boff[bk + 1];
+          MP_CHECK(e1 <= 4096u && G.boff[bk] <= e1, "boff", bk, e1);
           for (uint32_t e = G.boff[bk]; e < e1; ++e) {
             const uint32_t v = G.ent[e];
+            MP_CHECK((v >> 8) < P.D, "ent", v, e);
             if ((v & 15u) != fp) continue;
             const uint32_t i = (v >> 4) & 15u, d = v >> 8;
             if (i > o || o - i >= static_cast<uint32_t>(kSegBytes)) continue;   // not the lane's start
@@ -350,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
               const uint64_t vs = tbase + st;
               if (vs < P.s_lo || vs >= P.s_hi) continue;
             }
+            MP_CHECK(st < static_cast<uint32_t>(kTile + 64), "st", st, o);
             if (verify_window(ts, st, G, d, P.mw)) {
               ids[lane * kSegBytes + (o - i)] = static_cast<uint8_t>(d);
               M |= 1ull << (o - i);
@@ -378,9 +408,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       while (nbm) {
         const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
         nbm &= nbm - 1;
+        MP_CHECK(b < 64u, "batch", b, 0);
         const uint32_t id = ids[32 * b + lane];
         ids[32 * b + lane] = kNoId;
         const bool act = id != kNoId;
+        MP_CHECK(!act || id < P.D, "id", id, b);
         const uint32_t peers = __match_any_sync(0xffffffffu, id);
         if (act && (peers & lt) == 0) atomicAdd(&cc[id], static_cast<uint32_t>(__popc(peers)));
         const uint32_t am = __ballot_sync(0xffffffffu, act);
@@ -388,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         if (lane == 0) base = atomicAdd(&S.lcur[stage], static_cast<uint32_t>(__popc(am)));
         base = __shfl_sync(0xffffffffu, base, 0);
         const uint32_t r = base + __popc(am & lt);
+        MP_CHECK(c < P.nchunks, "chunk", c, r);
         if (act && r < static_cast<uint32_t>(kListCap))
           P.lists[static_cast<uint64_t>(c) * kListCap + r] = (cw * kSliceBytes + 32 * b + lane) | (id << 16);
       }
@@ -459,8 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           const uint64_t pos = cbase + 32 * b + lane;
           const uint32_t j1 = G.dup_off[id + 1];
           for (uint32_t q = G.dup_off[id]; q < j1; ++q) {
-            const uint32_t j = G.dup_list[q];
-            if (g < P.cap[j]) st_stream_u64(P.pos[j] + g, pos);
+            const JobOut J = P.jobs[G.dup_list[q]];
+            if (g < J.cap) st_stream_u64(J.pos + g, pos);
           }
         }
       }
