@@ -261,6 +261,22 @@ int64_t epsm_search_sharded(epsm_plan_t *plan, const uint8_t *d_shard,
                             epsm_stream_t stream);
 
 /*
+ * epsm_allgatherv_async -- the positions exchange of a sharded batch of k searches
+ * (collective over the NCCL communicator nccl_comm; every rank calls it with the same
+ * k, counts and caps).  counts is a HOST array [nranks][k]: counts[q*k + j] = rank q's
+ * occurrences of search j (from a counts exchange, e.g. the all-gather of the
+ * per-rank d_occ of epsm_search_range_batch_async / epsm_group_search_range_async).
+ * d_local[j] holds this rank's GLOBAL positions of search j (device); every rank's
+ * d_out[j] (device) receives the first min(occ_j, caps[j]) global positions
+ * (occ_j = sum over q; caps NULL: no limit), rank 0's first, so ascending.  Grouped
+ * ncclBroadcasts, one root per rank and search.  Enqueued on stream; does not
+ * synchronise.  Returns EPSM_OK, EPSM_EINVAL or EPSM_ENCCL.
+ */
+int epsm_allgatherv_async(uint32_t k, const uint64_t *const *d_local,
+                          const uint64_t *counts, uint64_t *const *d_out,
+                          const uint64_t *caps, void *nccl_comm, epsm_stream_t stream);
+
+/*
  * epsm_search_range_async -- the local step of the sharded search, exposed so
  * that a host runtime (e.g. torch.distributed) can do the exchange itself:
  * scans d_shard[0..shard_len-1], reports only starts s < owned_len, and writes
@@ -292,6 +308,13 @@ typedef struct epsm_group_s epsm_group_t;   /* opaque, host-owned */
  * group is pattern j.  Copies the patterns; no device work (the group's tables
  * are uploaded on first use, to the device of that call).  More than 255
  * distinct patterns are split internally into passes of <= 255.
+ * Dense patterns -- an expected rate of >= 2^-11 occurrences per text byte, the
+ * product of their bytes' frequencies among the k patterns (which are extracted
+ * from the text) -- are searched one by one through the
+ * single-pattern kernels (and over an index where one is passed and the search
+ * qualifies): their positions, not the text, dominate the traffic.  The
+ * environment variable EPSM_GROUP_DENSE=L moves the threshold to 2^-L (0: every
+ * pattern shares the passes).  Results never depend on the split.
  * Returns EPSM_OK, EPSM_EINVAL (NULL argument, m = 0, k = 0), EPSM_EUNSUP
  * (m > 32 or k > 1024) or EPSM_ENOMEM.
  */
@@ -301,15 +324,28 @@ int epsm_group_create(const uint8_t *patterns, uint32_t m, uint32_t k,
 /* epsm_group_free -- release a group (synchronises its device first). NULL-safe. */
 void epsm_group_free(epsm_group_t *g);
 
-/* epsm_group_info -- diagnostics: writes min(nout, 4 + 2*P) values
- * [m, k, distinct patterns, passes P, then (q, SK) per pass: the sampled gram
- * length and stride] to out and returns 4 + 2*P (EPSM_EINVAL on NULL). */
+/* epsm_group_set_dense -- tuning / test hook: re-split the group with the dense
+ * threshold 2^-log2_rate occurrences per text byte (0: no pattern is dense, every
+ * one shares the passes).  Synchronises the group's device if it was used.
+ * Returns EPSM_OK or EPSM_EINVAL (NULL, log2_rate > 64). */
+int epsm_group_set_dense(epsm_group_t *g, uint32_t log2_rate);
+
+/* epsm_group_index_values -- the byte values an equality-mask index needs for the
+ * group's dense searches to run over it: writes up to 256 distinct values into
+ * out_values (may be NULL) and returns their number (0: none qualifies, or NULL). */
+int epsm_group_index_values(const epsm_group_t *g, uint8_t *out_values);
+
+/* epsm_group_info -- diagnostics: writes min(nout, 5 + 2*P) values
+ * [m, k, distinct patterns, dense distinct patterns (searched one by one),
+ * passes P, then (q, SK) per pass: the sampled gram length and stride] to out
+ * and returns 5 + 2*P (EPSM_EINVAL on NULL). */
 int epsm_group_info(const epsm_group_t *g, uint32_t *out, uint32_t nout);
 
 /* epsm_group_set_geometry -- tuning / test hook: use sampled q-grams (1 <= q <=
  * min(m, 16)) every SK bytes (SK in {1, 2, 4, 8, 16}, SK + q - 1 <= m, SK times
- * the distinct patterns of a pass <= 4096) instead of the cost model's choice.
- * Every geometry returns the same results.  Synchronises the group's device if
+ * the distinct patterns of a pass <= 4096) instead of the cost model's choice,
+ * for EVERY distinct pattern (dense ones included: none is searched one by one
+ * afterwards).  Every geometry returns the same results.  Synchronises the group's device if
  * it was used.  Returns EPSM_OK or EPSM_EINVAL. */
 int epsm_group_set_geometry(epsm_group_t *g, uint32_t q, uint32_t sk);
 
@@ -329,6 +365,18 @@ int epsm_group_search_async(epsm_group_t *g, const uint8_t *d_text, uint64_t n,
 int epsm_group_count_async(epsm_group_t *g, const uint8_t *d_text, uint64_t n,
                            uint64_t *d_occ, epsm_stream_t stream);
 
+/* epsm_group_search_index_async / epsm_group_count_index_async -- as the calls
+ * above, with the dense patterns' searches run over the equality-mask index
+ * `index` where they qualify (epsm_search_batch_index_async); index must have been
+ * built over the same d_text and n (EPSM_EINVAL otherwise) and may be NULL. */
+int epsm_group_search_index_async(epsm_group_t *g, const epsm_eqidx_t *index,
+                                  const uint8_t *d_text, uint64_t n,
+                                  uint64_t *const *d_pos, const uint64_t *caps,
+                                  uint64_t *d_occ, epsm_stream_t stream);
+int epsm_group_count_index_async(epsm_group_t *g, const epsm_eqidx_t *index,
+                                 const uint8_t *d_text, uint64_t n,
+                                 uint64_t *d_occ, epsm_stream_t stream);
+
 /* epsm_group_search_range_async -- the local step of a sharded group search: as
  * epsm_search_range_batch_async (starts s < owned_len of the shard, reported as
  * s + base; shard_len >= min(owned_len + m - 1, n_total - base), else
@@ -338,6 +386,34 @@ int epsm_group_search_range_async(epsm_group_t *g, const uint8_t *d_shard,
                                   uint64_t base, uint64_t n_total,
                                   uint64_t *const *d_pos, const uint64_t *caps,
                                   uint64_t *d_occ, epsm_stream_t stream);
+
+/* epsm_group_search_range_index_async -- the same with a shard's index (built over
+ * d_shard[0..shard_len-1]) for the dense patterns' searches. */
+int epsm_group_search_range_index_async(epsm_group_t *g, const epsm_eqidx_t *index,
+                                        const uint8_t *d_shard, uint64_t shard_len,
+                                        uint64_t owned_len, uint64_t base,
+                                        uint64_t n_total, uint64_t *const *d_pos,
+                                        const uint64_t *caps, uint64_t *d_occ,
+                                        epsm_stream_t stream);
+
+/*
+ * epsm_search_text_host -- end to end over a HOST text, the paper's protocol for one
+ * text (sets of patterns of each length, timings including the
+ * preprocessing): copies h_text[0..n-1] to the device, builds the equality-mask index
+ * the groups' dense searches need (epsm_group_index_values), counts every search,
+ * runs every group (epsm_group_search_index_async) and copies each search's first
+ * min(occ, caps[j]) positions into the HOST array h_pos[j] (pinned memory gives full
+ * PCIe bandwidth; h_pos or h_pos[j] NULL, or caps NULL: count only).  Search j
+ * numbers the searches of groups[0], then groups[1], ...; its occ goes to h_occ[j].
+ * Device buffers (text, index, two position arenas of the largest group's output,
+ * occ) belong to the calling (device, stream) and are reused by later calls; the
+ * copies of group i overlap the search of group i + 1 on an internal stream.
+ * Synchronises.  Returns EPSM_OK or a negative error.
+ */
+int epsm_search_text_host(epsm_group_t *const *groups, uint32_t ngroups,
+                          const uint8_t *h_text, uint64_t n,
+                          uint64_t *const *h_pos, const uint64_t *caps,
+                          uint64_t *h_occ, epsm_stream_t stream);
 
 /* epsm_strerror -- static name/description of an EPSM_E* code. */
 const char *epsm_strerror(int64_t code);

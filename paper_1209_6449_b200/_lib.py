@@ -104,6 +104,20 @@ _lib.epsm_group_count_async.argtypes = [_vp, _vp, _u64, _vp, _vp]
 _lib.epsm_group_count_async.restype = ctypes.c_int
 _lib.epsm_group_search_range_async.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
 _lib.epsm_group_search_range_async.restype = ctypes.c_int
+_lib.epsm_allgatherv_async.argtypes = [ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.epsm_allgatherv_async.restype = ctypes.c_int
+_lib.epsm_group_index_values.argtypes = [_vp, _vp]
+_lib.epsm_group_index_values.restype = ctypes.c_int
+_lib.epsm_search_text_host.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_search_text_host.restype = ctypes.c_int
+_lib.epsm_group_set_dense.argtypes = [_vp, ctypes.c_uint32]
+_lib.epsm_group_set_dense.restype = ctypes.c_int
+_lib.epsm_group_search_index_async.argtypes = [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_group_search_index_async.restype = ctypes.c_int
+_lib.epsm_group_count_index_async.argtypes = [_vp, _vp, _vp, _u64, _vp, _vp]
+_lib.epsm_group_count_index_async.restype = ctypes.c_int
+_lib.epsm_group_search_range_index_async.argtypes = [_vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
+_lib.epsm_group_search_range_index_async.restype = ctypes.c_int
 
 EXPORTED_SYMBOLS = (
     "epsm_plan", "epsm_plan_free", "epsm_plan_m", "epsm_count", "epsm_count_async",
@@ -115,7 +129,9 @@ EXPORTED_SYMBOLS = (
     "epsm_search_batch_index_async", "epsm_count_batch_index_async", "epsm_plan_index_values",
     "epsm_search_range_batch_index_async",
     "epsm_group_create", "epsm_group_free", "epsm_group_info", "epsm_group_set_geometry", "epsm_group_search_async",
-    "epsm_group_count_async", "epsm_group_search_range_async",
+    "epsm_group_count_async", "epsm_group_search_range_async", "epsm_group_set_dense",
+    "epsm_group_search_index_async", "epsm_group_count_index_async", "epsm_group_search_range_index_async",
+    "epsm_group_index_values", "epsm_search_text_host", "epsm_allgatherv_async",
 )
 MAX_PLANES = 256
 INDEX_MAX_D = 8
@@ -554,12 +570,24 @@ class Group:
         out = (ctypes.c_uint32 * 64)()
         c = _check(_lib.epsm_group_info(self.handle, out, 64), "epsm_group_info")
         v = list(out[:min(c, 64)])
-        return {"m": v[0], "k": v[1], "distinct": v[2],
-                "passes": [(v[4 + 2 * i], v[5 + 2 * i]) for i in range(v[3])]}
+        return {"m": v[0], "k": v[1], "distinct": v[2], "dense": v[3],
+                "passes": [(v[5 + 2 * i], v[6 + 2 * i]) for i in range(v[4])]}
 
     def set_geometry(self, q: int, sk: int) -> "Group":
         """Force sampled q-grams every SK bytes (tests / tuning; results never change)."""
         _check(_lib.epsm_group_set_geometry(self.handle, int(q), int(sk)), "epsm_group_set_geometry")
+        return self
+
+    def index_values(self) -> bytes:
+        """The byte values an equality-mask index needs for the dense searches."""
+        out = (ctypes.c_uint8 * 256)()
+        c = _lib.epsm_group_index_values(self.handle, out)
+        return bytes(out[:c])
+
+    def set_dense(self, log2_rate: int) -> "Group":
+        """Re-split: patterns estimated at >= 2^-log2_rate occurrences per byte are searched one
+        by one (0: none; tests / tuning, results never change)."""
+        _check(_lib.epsm_group_set_dense(self.handle, int(log2_rate)), "epsm_group_set_dense")
         return self
 
     def _outs(self, outs, caps):
@@ -576,37 +604,48 @@ class Group:
             cs.append(c)
         return (ctypes.c_void_p * k)(*ptrs), (ctypes.c_uint64 * k)(*cs)
 
-    def search_async(self, text: torch.Tensor, occ_out: torch.Tensor, outs=None, caps=None, stream=None):
-        """Enqueue every search over ``text``: occ of search j -> occ_out[j], positions -> outs[j]."""
+    def search_async(self, text: torch.Tensor, occ_out: torch.Tensor, outs=None, caps=None, stream=None,
+                     index: "EqIndex | None" = None):
+        """Enqueue every search over ``text``: occ of search j -> occ_out[j], positions -> outs[j]
+        (the dense patterns' searches over ``index`` where they qualify)."""
         _check_text(text)
         _check_out(occ_out, "occ_out")
         if occ_out.numel() < self.k:
             raise ValueError("occ_out needs one element per search")
         pa, ca = self._outs(outs, caps)
-        _check(_lib.epsm_group_search_async(self.handle, text.data_ptr(), text.numel(), pa, ca,
-                                            occ_out.data_ptr(), _stream_handle(stream, text.device)),
-               "epsm_group_search_async")
+        st = _stream_handle(stream, text.device)
+        if index is None:
+            _check(_lib.epsm_group_search_async(self.handle, text.data_ptr(), text.numel(), pa, ca,
+                                                occ_out.data_ptr(), st), "epsm_group_search_async")
+        else:
+            _check(_lib.epsm_group_search_index_async(self.handle, index.handle, text.data_ptr(), text.numel(), pa,
+                                                      ca, occ_out.data_ptr(), st), "epsm_group_search_index_async")
 
-    def count_async(self, text: torch.Tensor, occ_out: torch.Tensor, stream=None):
+    def count_async(self, text: torch.Tensor, occ_out: torch.Tensor, stream=None, index: "EqIndex | None" = None):
         _check_text(text)
         _check_out(occ_out, "occ_out")
         if occ_out.numel() < self.k:
             raise ValueError("occ_out needs one element per search")
-        _check(_lib.epsm_group_count_async(self.handle, text.data_ptr(), text.numel(), occ_out.data_ptr(),
-                                           _stream_handle(stream, text.device)), "epsm_group_count_async")
+        st = _stream_handle(stream, text.device)
+        if index is None:
+            _check(_lib.epsm_group_count_async(self.handle, text.data_ptr(), text.numel(), occ_out.data_ptr(), st),
+                   "epsm_group_count_async")
+        else:
+            _check(_lib.epsm_group_count_index_async(self.handle, index.handle, text.data_ptr(), text.numel(),
+                                                     occ_out.data_ptr(), st), "epsm_group_count_index_async")
 
     def search_range_async(self, shard: torch.Tensor, owned_len: int, base: int, n_total: int,
-                           occ_out: torch.Tensor, outs=None, caps=None, stream=None):
+                           occ_out: torch.Tensor, outs=None, caps=None, stream=None, index: "EqIndex | None" = None):
         """Local step of a sharded group search (starts s < owned_len, reported as s + base)."""
         _check_text(shard)
         _check_out(occ_out, "occ_out")
         if occ_out.numel() < self.k:
             raise ValueError("occ_out needs one element per search")
         pa, ca = self._outs(outs, caps)
-        _check(_lib.epsm_group_search_range_async(self.handle, shard.data_ptr(), shard.numel(), int(owned_len),
-                                                  int(base), int(n_total), pa, ca, occ_out.data_ptr(),
-                                                  _stream_handle(stream, shard.device)),
-               "epsm_group_search_range_async")
+        _check(_lib.epsm_group_search_range_index_async(
+            self.handle, None if index is None else index.handle, shard.data_ptr(), shard.numel(), int(owned_len),
+            int(base), int(n_total), pa, ca, occ_out.data_ptr(), _stream_handle(stream, shard.device)),
+            "epsm_group_search_range_index_async")
 
     def close(self):
         if getattr(self, "_h", None) is not None:
@@ -628,3 +667,51 @@ class Group:
 
 def group(patterns) -> Group:
     return Group(patterns)
+
+
+def search_text_host(groups, host_text, host_outs=None, caps=None, stream=None) -> np.ndarray:
+    """epsm_search_text_host: every search of every group over one HOST text (a pinned or
+    pageable uint8 tensor / numpy array); search j's positions land in the host array
+    host_outs[j] (searches numbered group by group).  Returns the occ of every search."""
+    t, n = _host_ptr_len(host_text, np.uint8)
+    ks = [g.k for g in groups]
+    K = sum(ks)
+    gp = (ctypes.c_void_p * len(groups))(*[g.handle for g in groups])
+    pa = ca = None
+    if host_outs is not None:
+        if len(host_outs) != K:
+            raise ValueError("one host output (or None) per search")
+        ptrs, cs = [], []
+        for j, o in enumerate(host_outs):
+            if o is None:
+                ptrs.append(None)
+                cs.append(0)
+                continue
+            p, ln = _host_ptr_len(o, np.int64)
+            ptrs.append(p)
+            cs.append(ln if caps is None else min(int(caps[j]), ln))
+        pa = (ctypes.c_void_p * K)(*ptrs)
+        ca = (ctypes.c_uint64 * K)(*cs)
+    occ = np.zeros(K, dtype=np.uint64)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _check(_lib.epsm_search_text_host(gp, len(groups), t, n, pa, ca, occ.ctypes.data, _stream_handle(stream, dev)),
+           "epsm_search_text_host")
+    return occ
+
+
+def allgatherv_async(locals_, counts, outs, caps=None, nccl_comm=None, stream=None) -> None:
+    """epsm_allgatherv_async: every rank's positions of search j (locals_[j], GLOBAL positions,
+    device int64) into every rank's outs[j] at the prefix of counts ([world, k] host ints)."""
+    k = len(locals_)
+    cnt = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64).reshape(-1))
+    if cnt.size % max(k, 1):
+        raise ValueError("counts must be [world, k]")
+    lp = (ctypes.c_void_p * k)(*[None if t is None else t.data_ptr() for t in locals_])
+    op = (ctypes.c_void_p * k)(*[None if t is None else t.data_ptr() for t in outs])
+    cp = None
+    if caps is not None:
+        cp = (ctypes.c_uint64 * k)(*[int(c) for c in caps])
+    comm = nccl_comm if nccl_comm is not None else nccl_comm_ptr()
+    dev = next((t.device for t in outs if t is not None), torch.device("cuda", torch.cuda.current_device()))
+    _check(_lib.epsm_allgatherv_async(k, lp, cnt.ctypes.data, op, cp, ctypes.c_void_p(comm),
+                                      _stream_handle(stream, dev)), "epsm_allgatherv_async")

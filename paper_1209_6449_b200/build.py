@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("epsm.cu", "epsm_sharded.cu", "epsm_multi.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("epsm.cu", "epsm_sharded.cu", "epsm_multi.cu", "epsm_host.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("epsm_kernels.cuh", "epsm_multi.cuh", "epsm_ptx.cuh", "epsm_internal.h")] + \
     [os.path.join(ROOT, "include", "epsm.h")]
 OUT = os.path.join(HERE, "libepsm.so")

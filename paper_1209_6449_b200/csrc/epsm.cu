@@ -855,7 +855,8 @@ static int check_overlap(uint64_t n, uint64_t owned_len, uint64_t base, uint64_t
 
 static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n, uint64_t owned_len,
                         uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
-                        epsm_stream_t stream, const epsm_eqidx_t* index = nullptr, uint64_t n_total = 0) {
+                        epsm_stream_t stream, const epsm_eqidx_t* index = nullptr, uint64_t n_total = 0,
+                        const uint32_t* slot = nullptr) {
   if (k == 0) return EPSM_OK;
   if (index && (index->text != d_text || index->n != n)) {
     epsm_set_error("the index was built over another text (pointer or length differ)");
@@ -884,15 +885,16 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
       int rc = check_overlap(n, owned_len, base, n_total, plans[j]->m);
       if (rc) return rc;
     }
-    uint64_t* pos = d_pos ? d_pos[j] : nullptr;
-    const uint64_t cap = (pos && caps) ? caps[j] : 0;
+    const uint32_t sj = slot ? slot[j] : j;   // the caller's arrays are indexed by slot[j]
+    uint64_t* pos = d_pos ? d_pos[sj] : nullptr;
+    const uint64_t cap = (pos && caps) ? caps[sj] : 0;
     if (pos && !aligned8(pos)) {
       epsm_set_error("d_pos[%u] must be 8-byte aligned", j);
       return EPSM_EALIGN;
     }
     int rc = epsm_bind_device(plans[j], d_occ);
     if (rc) return rc;
-    jobs[j] = epsm_job{plans[j], cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + j)};
+    jobs[j] = epsm_job{plans[j], cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + sj)};
   }
   // searches are independent: group them by kernel variant (m, filter or index), keeping
   // their order within a group, and launch each group in runs of at most kMaxJobs
@@ -928,6 +930,16 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
   }
   return EPSM_OK;
 }
+
+}  // extern "C"
+
+int epsm_batch_run(epsm_plan_t* const* plans, uint32_t k, const uint32_t* slot, const uint8_t* d_text, uint64_t n,
+                   uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
+                   uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index) {
+  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, search, s, index, n_total, slot);
+}
+
+extern "C" {
 
 int epsm_search_range_batch_async(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n,
                                   uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos,

@@ -96,6 +96,12 @@ struct epsm_job {
 int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
                      uint64_t base, bool search, cudaStream_t s, const epsm_eqidx_t* index = nullptr);
 
+// The batch path (epsm_search_(range_)batch(_index)_async) for k searches whose outputs sit at
+// the caller's slots slot[j] of d_pos / caps / d_occ (slot NULL: j); n_total 0 = not a shard.
+int epsm_batch_run(epsm_plan_t* const* plans, uint32_t k, const uint32_t* slot, const uint8_t* d_text, uint64_t n,
+                   uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
+                   uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index);
+
 // Equality-mask index of one text (epsm_eqidx_build_async).
 struct epsm_eqidx_s {
   int device = -1;

@@ -139,6 +139,13 @@ struct epsm_group_s {
   std::vector<Subgroup> subs;
   std::vector<std::string> pats;                  // distinct patterns
   std::vector<std::vector<uint32_t>> dups;        // searches per distinct pattern
+  // dense distinct patterns (estimated >= 2^-dense_log2 occurrences per text byte): searched
+  // one by one through the single-pattern kernels (their positions, >= 4 bytes of output per
+  // 1000 text bytes, dominate; the shared pass gains little there); the rest share the passes
+  std::vector<uint32_t> sparse, dense;            // distinct pattern indices
+  std::vector<epsm_plan_t*> dplans;               // plan of dense[i]
+  std::vector<epsm_plan_t*> djob_plan;            // per dense search: its plan ...
+  std::vector<uint32_t> djob_slot;                // ... and the caller's search index
 };
 
 static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subgroup& S,
@@ -212,6 +219,7 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
 
 static void group_release(epsm_group_t* g) {
   if (!g) return;
+  for (epsm_plan_t* p : g->dplans) epsm_plan_free(p);
   bool synced = false;
   for (auto& S : g->subs) {
     if (S.d_desc) {
@@ -364,7 +372,7 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   Q.nchunks = P.nchunks;
   Q.D = S.D;
   Q.k = S.k;
-  mp::epsm_multi_scan_kernel<<<(S.D + 31) / 32, 32 * mp::kScanWarps, 0, s>>>(Q);
+  mp::epsm_multi_scan_kernel<<<S.D + 1, mp::kScanThreads, 0, s>>>(Q);
   epsm_count_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_scan_kernel launch");
@@ -402,9 +410,14 @@ static int group_bind(epsm_group_t* g, const void* dptr) {
 }
 
 static int group_run(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t owned_len, uint64_t base,
-                     uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search, epsm_stream_t stream) {
+                     uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
+                     epsm_stream_t stream, const epsm_eqidx_t* index) {
   if (!g || !d_occ || (!d_text && n > 0)) {
     epsm_set_error("epsm_group_*: NULL group, d_occ or text");
+    return EPSM_EINVAL;
+  }
+  if (index && (index->text != d_text || index->n != n)) {
+    epsm_set_error("the index was built over another text (pointer or length differ)");
     return EPSM_EINVAL;
   }
   if (n > (1ull << 38)) {
@@ -430,8 +443,88 @@ static int group_run(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_
     rc = subgroup_launch(g, S, d_text, n, ns, base, d_pos, caps, d_occ, search, s);
     if (rc) return rc;
   }
+  if (!g->djob_plan.empty()) {
+    // the dense patterns' searches: the batch path (over the index where it qualifies)
+    rc = epsm_batch_run(g->djob_plan.data(), static_cast<uint32_t>(g->djob_plan.size()), g->djob_slot.data(), d_text,
+                        n, owned_len, base, n_total, search ? d_pos : nullptr, search ? caps : nullptr, d_occ, search,
+                        s, index);
+    if (rc) return rc;
+  }
   return EPSM_OK;
 }
+
+// EPSM_GROUP_DENSE=L: distinct patterns with an estimated rate >= 2^-L occurrences per text
+// byte are searched one by one (default 11; 0 puts every pattern through the group kernels).
+// Speed only: both paths are exact.  B200, 256 MiB texts, 100 patterns per group: the shared
+// passes win below ~2^-11 (sigma=64 m=2: 2.7 -> 2.3 ms, sigma=8 m=4: 3.4 -> 2.2 ms), the
+// single-pattern kernels above (sigma=32 m=2: 3.7 vs 4.3 ms, sigma=2 m=8: 5.6 vs 6.4 ms).
+static int group_dense_log2() {
+  static const int v = [] {
+    const char* e = getenv("EPSM_GROUP_DENSE");
+    return e && e[0] ? static_cast<int>(strtol(e, nullptr, 0)) : 11;
+  }();
+  return v <= 0 ? 4096 : v;
+}
+
+// Split the distinct patterns into dense (estimated rate >= 2^-log2 occurrences per text byte)
+// and sparse.  The rate of a pattern is the product of its bytes' frequencies among the OTHER
+// k - 1 patterns of the group (they are extracted from the text, so their bytes
+// sample its distribution; leaving the pattern's own copy out keeps a rare byte from counting
+// itself).
+static void group_split(epsm_group_t* g, int log2) {
+  double cnt[256] = {};
+  for (uint32_t d = 0; d < g->D; ++d)
+    for (unsigned char ch : g->pats[d]) cnt[ch] += static_cast<double>(g->dups[d].size());
+  const double thresh = std::ldexp(1.0, -log2);
+  const double others = static_cast<double>(g->k - 1) * g->m;
+  g->sparse.clear();
+  g->dense.clear();
+  for (uint32_t d = 0; d < g->D; ++d) {
+    double own[256] = {};
+    for (unsigned char ch : g->pats[d]) own[ch] += 1.0;
+    double rate = others > 0 ? 1.0 : 0.0;
+    for (unsigned char ch : g->pats[d]) rate *= others > 0 ? (cnt[ch] - own[ch]) / others : 0.0;
+    (log2 < 1024 && rate >= thresh ? g->dense : g->sparse).push_back(d);
+  }
+}
+
+// (Re)build the passes over g->sparse (<= kMaxD distinct patterns each) and the plans of
+// g->dense; the group's device copies are rebuilt on the next use.
+static int group_partition(epsm_group_t* g, int force_q, int force_sk) {
+  for (auto& S : g->subs) {
+    if (S.d_desc) cudaFree(S.d_desc);
+    delete S.h_desc;
+  }
+  g->subs.clear();
+  for (uint32_t a = 0; a < g->sparse.size(); a += mp::kMaxD) {
+    const uint32_t b = std::min<uint32_t>(static_cast<uint32_t>(g->sparse.size()), a + mp::kMaxD);
+    std::vector<std::string> sp;
+    std::vector<std::vector<uint32_t>> sd;
+    for (uint32_t i = a; i < b; ++i) {
+      sp.push_back(g->pats[g->sparse[i]]);
+      sd.push_back(g->dups[g->sparse[i]]);
+    }
+    g->subs.emplace_back();
+    int rc = build_subgroup(sp, g->m, g->subs.back(), sd, force_q, force_sk);
+    if (rc) return rc;
+  }
+  for (epsm_plan_t* p : g->dplans) epsm_plan_free(p);
+  g->dplans.clear();
+  g->djob_plan.clear();
+  g->djob_slot.clear();
+  for (uint32_t d : g->dense) {
+    epsm_plan_t* p = nullptr;
+    int rc = epsm_plan(reinterpret_cast<const uint8_t*>(g->pats[d].data()), g->m, &p);
+    if (rc) return rc;
+    g->dplans.push_back(p);
+    for (uint32_t j : g->dups[d]) {
+      g->djob_plan.push_back(p);
+      g->djob_slot.push_back(j);
+    }
+  }
+  return EPSM_OK;
+}
+static int group_partition(epsm_group_t* g) { return group_partition(g, 0, 0); }
 
 extern "C" {
 
@@ -470,16 +563,11 @@ int epsm_group_create(const uint8_t* patterns, uint32_t m, uint32_t k, epsm_grou
   g->D = static_cast<uint32_t>(pats.size());
   g->pats = pats;
   g->dups = dups;
-  for (uint32_t a = 0; a < g->D; a += mp::kMaxD) {
-    const uint32_t b = std::min<uint32_t>(g->D, a + mp::kMaxD);
-    std::vector<std::string> sp(pats.begin() + a, pats.begin() + b);
-    std::vector<std::vector<uint32_t>> sd(dups.begin() + a, dups.begin() + b);
-    g->subs.emplace_back();
-    int rc = build_subgroup(sp, m, g->subs.back(), sd);
-    if (rc) {
-      group_release(g);
-      return rc;
-    }
+  group_split(g, group_dense_log2());
+  int rc = group_partition(g);
+  if (rc) {
+    group_release(g);
+    return rc;
   }
   *out = g;
   return EPSM_OK;
@@ -492,33 +580,57 @@ int epsm_group_set_geometry(epsm_group_t* g, uint32_t q, uint32_t sk) {
     epsm_set_error("epsm_group_set_geometry: need 1 <= q <= min(m, 16), SK in {1,2,4,8,16}, SK + q - 1 <= m");
     return EPSM_EINVAL;
   }
-  for (const auto& S : g->subs)
-    if (static_cast<uint64_t>(S.D) * sk > mp::kMaxEntries) {
-      epsm_set_error("epsm_group_set_geometry: %u patterns x SK = %u exceeds %d table entries", S.D, sk,
-                     mp::kMaxEntries);
-      return EPSM_EINVAL;
-    }
+  const uint32_t dmax = std::min<uint32_t>(g->D, mp::kMaxD);   // distinct patterns of the largest pass
+  if (static_cast<uint64_t>(dmax) * sk > mp::kMaxEntries) {
+    epsm_set_error("epsm_group_set_geometry: %u patterns x SK = %u exceeds %d table entries", dmax, sk,
+                   mp::kMaxEntries);
+    return EPSM_EINVAL;
+  }
   if (g->device >= 0) {
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();
   }
-  uint32_t a = 0;
-  for (auto& S : g->subs) {
-    if (S.d_desc) cudaFree(S.d_desc);
-    S.d_desc = nullptr;
-    const uint32_t b = a + S.D;
-    std::vector<std::string> sp(g->pats.begin() + a, g->pats.begin() + b);
-    std::vector<std::vector<uint32_t>> sd(g->dups.begin() + a, g->dups.begin() + b);
-    int rc = build_subgroup(sp, g->m, S, sd, static_cast<int>(q), static_cast<int>(sk));
-    if (rc) return rc;
-    a = b;
+  // a forced geometry puts every distinct pattern through the group kernels
+  g->sparse.clear();
+  g->dense.clear();
+  for (uint32_t d = 0; d < g->D; ++d) g->sparse.push_back(d);
+  return group_partition(g, static_cast<int>(q), static_cast<int>(sk));
+}
+
+int epsm_group_set_dense(epsm_group_t* g, uint32_t log2_rate) {
+  if (!g || log2_rate > 64) {
+    epsm_set_error("epsm_group_set_dense: NULL group or log2_rate > 64");
+    return EPSM_EINVAL;
   }
-  return EPSM_OK;
+  if (g->device >= 0) {
+    cudaSetDevice(g->device);
+    cudaDeviceSynchronize();
+  }
+  group_split(g, log2_rate == 0 ? 4096 : static_cast<int>(log2_rate));
+  return group_partition(g);
+}
+
+int epsm_group_index_values(const epsm_group_t* g, uint8_t* out_values) {
+  if (!g) return 0;
+  bool have[256] = {};
+  int nv = 0;
+  for (epsm_plan_t* p : g->dplans) {
+    uint8_t v[EPSM_INDEX_MAX_D];
+    const int c = epsm_plan_index_values(p, v);
+    for (int q = 0; q < c; ++q)
+      if (!have[v[q]]) {
+        have[v[q]] = true;
+        if (out_values) out_values[nv] = v[q];
+        ++nv;
+      }
+  }
+  return nv;
 }
 
 int epsm_group_info(const epsm_group_t* g, uint32_t* out, uint32_t nout) {
   if (!g || !out) return EPSM_EINVAL;
-  std::vector<uint32_t> v = {g->m, g->k, g->D, static_cast<uint32_t>(g->subs.size())};
+  std::vector<uint32_t> v = {g->m, g->k, g->D, static_cast<uint32_t>(g->dense.size()),
+                             static_cast<uint32_t>(g->subs.size())};
   for (const auto& S : g->subs) {
     v.push_back(static_cast<uint32_t>(S.q));
     v.push_back(static_cast<uint32_t>(S.sk));
@@ -530,17 +642,29 @@ int epsm_group_info(const epsm_group_t* g, uint32_t* out, uint32_t nout) {
 
 int epsm_group_search_async(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t* const* d_pos,
                             const uint64_t* caps, uint64_t* d_occ, epsm_stream_t stream) {
-  return group_run(g, d_text, n, n, 0, d_pos, caps, d_occ, true, stream);
+  return group_run(g, d_text, n, n, 0, 0, d_pos, caps, d_occ, true, stream, nullptr);
 }
 
 int epsm_group_count_async(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t* d_occ,
                            epsm_stream_t stream) {
-  return group_run(g, d_text, n, n, 0, nullptr, nullptr, d_occ, false, stream);
+  return group_run(g, d_text, n, n, 0, 0, nullptr, nullptr, d_occ, false, stream, nullptr);
 }
 
-int epsm_group_search_range_async(epsm_group_t* g, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,
-                                  uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
-                                  uint64_t* d_occ, epsm_stream_t stream) {
+int epsm_group_search_index_async(epsm_group_t* g, const epsm_eqidx_t* index, const uint8_t* d_text, uint64_t n,
+                                  uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ,
+                                  epsm_stream_t stream) {
+  return group_run(g, d_text, n, n, 0, 0, d_pos, caps, d_occ, true, stream, index);
+}
+
+int epsm_group_count_index_async(epsm_group_t* g, const epsm_eqidx_t* index, const uint8_t* d_text, uint64_t n,
+                                 uint64_t* d_occ, epsm_stream_t stream) {
+  return group_run(g, d_text, n, n, 0, 0, nullptr, nullptr, d_occ, false, stream, index);
+}
+
+int epsm_group_search_range_index_async(epsm_group_t* g, const epsm_eqidx_t* index, const uint8_t* d_shard,
+                                        uint64_t shard_len, uint64_t owned_len, uint64_t base, uint64_t n_total,
+                                        uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ,
+                                        epsm_stream_t stream) {
   if (!g) {
     epsm_set_error("NULL group");
     return EPSM_EINVAL;
@@ -559,7 +683,14 @@ int epsm_group_search_range_async(epsm_group_t* g, const uint8_t* d_shard, uint6
       return EPSM_EINVAL;
     }
   }
-  return group_run(g, d_shard, shard_len, owned_len, base, d_pos, caps, d_occ, true, stream);
+  return group_run(g, d_shard, shard_len, owned_len, base, n_total, d_pos, caps, d_occ, true, stream, index);
+}
+
+int epsm_group_search_range_async(epsm_group_t* g, const uint8_t* d_shard, uint64_t shard_len, uint64_t owned_len,
+                                  uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
+                                  uint64_t* d_occ, epsm_stream_t stream) {
+  return epsm_group_search_range_index_async(g, nullptr, d_shard, shard_len, owned_len, base, n_total, d_pos, caps,
+                                             d_occ, stream);
 }
 
 }  // extern "C"

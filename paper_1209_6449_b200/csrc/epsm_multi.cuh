@@ -128,6 +128,15 @@ __device__ __forceinline__ void bar_consumers() {   // named barrier over the 16
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory");
 }
 
+// bits 0..15 of x to the even bit positions 0, 2, .., 30
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
 // 4 bytes at an arbitrary shared-memory byte offset (4-byte aligned base)
 __device__ __forceinline__ uint32_t lds_u32_any(const uint8_t* base, uint32_t off) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
@@ -390,13 +399,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       // nonempty batches: batch b = slice starts [32b, 32b + 32) = lane b/2, half b&1
       const uint32_t blo = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M) != 0u);
       const uint32_t bhi = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M >> 32) != 0u);
-      // interleave: batch 2l <- blo bit l, batch 2l + 1 <- bhi bit l
-#pragma unroll
-      for (int l = 0; l < 16; ++l) {
-        nb_lo |= ((blo >> l) & 1u) << (2 * l);
-        nb_lo |= ((bhi >> l) & 1u) << (2 * l + 1);
-        nb_hi |= ((blo >> (l + 16)) & 1u) << (2 * l);
-        nb_hi |= ((bhi >> (l + 16)) & 1u) << (2 * l + 1);
+      // interleave: batch 2l <- blo bit l, batch 2l + 1 <- bhi bit l (bit spreading; skipped
+      // by the common warps without a match)
+      if ((blo | bhi) != 0u) {
+        nb_lo = spread16(blo & 0xFFFFu) | (spread16(bhi & 0xFFFFu) << 1);
+        nb_hi = spread16(blo >> 16) | (spread16(bhi >> 16) << 1);
       }
       __syncwarp();
     }
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         // the last warp of the chunk publishes its counts and resets the stage's counters
         __threadfence_block();
         for (uint32_t d = lane; d < P.D; d += 32) {
-          P.counts[static_cast<uint64_t>(c) * P.D + d] = static_cast<uint16_t>(cc[d]);
+          P.counts[static_cast<uint64_t>(d) * P.nchunks + c] = static_cast<uint16_t>(cc[d]);
           cc[d] = 0;
         }
         if (lane == 0) {
@@ -473,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           S.hist[w][d] = static_cast<uint16_t>(run);
           run += v;
         }
-        S.pre[d] = P.prefix[static_cast<uint64_t>(c) * P.D + d];
+        S.pre[d] = P.prefix[static_cast<uint64_t>(d) * P.nchunks + c];
       }
       bar_consumers();
       const uint64_t cbase = static_cast<uint64_t>(c) * kTile + P.pos_bias + cw * kSliceBytes;
@@ -512,52 +519,62 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
 
 // Pass 2: per distinct pattern, the exclusive prefix of its chunk counts (where each chunk's
 // positions start in every output of that pattern) and its total (the occ of every search of
-// that pattern); plus the list of chunks with occurrences.  Block b scans
-// patterns [32b, 32b + 32) -- lane = pattern, warp w = a contiguous run of chunks.
-constexpr int kScanWarps = 32;
-__global__ void __launch_bounds__(32 * kScanWarps) epsm_multi_scan_kernel(const __grid_constant__ ScanParams P) {
-  __shared__ unsigned long long part[kScanWarps][32];
+// that pattern); plus the list of chunks with occurrences.  Block d < D scans
+// pattern d's row of counts ([D][nchunks], contiguous) 1024 chunks at a time (coalesced loads,
+// warp + block scans, a running carry); block D builds the work list.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) epsm_multi_scan_kernel(const __grid_constant__ ScanParams P) {
+  __shared__ unsigned long long wsum[kScanThreads / 32];
+  __shared__ unsigned long long carry_s;
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-  const uint32_t d = blockIdx.x * 32 + lane;
-  const bool live = d < P.D;
-  const uint32_t per = (P.nchunks + kScanWarps - 1) / kScanWarps;
-  const uint32_t c0 = min(P.nchunks, w * per), c1 = min(P.nchunks, c0 + per);
-  unsigned long long s = 0;
-  if (live)
-    for (uint32_t c = c0; c < c1; ++c) s += P.counts[static_cast<uint64_t>(c) * P.D + d];
-  part[w][lane] = s;
-  __syncthreads();
-  if (w == 0) {
-    unsigned long long run = 0;
-    for (int q = 0; q < kScanWarps; ++q) {
-      const unsigned long long v = part[q][lane];
-      part[q][lane] = run;
-      run += v;
+  const uint32_t d = blockIdx.x;
+  if (d < P.D) {
+    const uint16_t* row = P.counts + static_cast<uint64_t>(d) * P.nchunks;
+    unsigned long long* prow = P.prefix ? P.prefix + static_cast<uint64_t>(d) * P.nchunks : nullptr;
+    unsigned long long carry = 0;
+    for (uint32_t c0 = 0; c0 < P.nchunks; c0 += kScanThreads) {
+      const uint32_t c = c0 + threadIdx.x;
+      const uint32_t v = c < P.nchunks ? row[c] : 0u;
+      uint32_t x = v;                                            // warp inclusive scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<uint32_t>(o)) x += y;
+      }
+      if (lane == 31) wsum[w] = x;
+      __syncthreads();
+      if (w == 0) {                                              // scan of the warp sums
+        unsigned long long s = wsum[lane], t = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+          if (lane >= static_cast<uint32_t>(o)) t += y;
+        }
+        wsum[lane] = t - s;                                      // exclusive
+        if (lane == 31) carry_s = t;                             // tile total
+      }
+      __syncthreads();
+      if (prow && c < P.nchunks) prow[c] = carry + wsum[w] + (x - v);
+      carry += carry_s;
+      __syncthreads();
     }
-    if (live) {
-      for (uint32_t j = 0; j < P.k; ++j)
-        if (P.desc->job_d[j] == d) P.occ[P.desc->job_g[j]] = run;
+    if (threadIdx.x == 0) {
+      // every search of pattern d gets its total
+      for (uint32_t q = P.desc->dup_off[d]; q < P.desc->dup_off[d + 1]; ++q)
+        P.occ[P.desc->job_g[P.desc->dup_list[q]]] = carry;
     }
+    return;
   }
-  __syncthreads();
-  if (live && P.prefix) {
-    unsigned long long run = part[w][lane];
-    for (uint32_t c = c0; c < c1; ++c) {
-      P.prefix[static_cast<uint64_t>(c) * P.D + d] = run;
-      run += P.counts[static_cast<uint64_t>(c) * P.D + d];
-    }
-  }
-  // chunks with occurrences (order irrelevant: each is handled on its own); block 0 only
-  if (blockIdx.x == 0 && P.prefix) {
-    for (uint32_t c0b = 0; c0b < P.nchunks; c0b += blockDim.x) {
-      const uint32_t cc = c0b + threadIdx.x;
-      const bool ne = cc < P.nchunks && P.listlen[cc] > 0;
-      const uint32_t bal = __ballot_sync(0xffffffffu, ne);
-      uint32_t base = 0;
-      if (lane == 0 && bal) base = atomicAdd(P.work, static_cast<uint32_t>(__popc(bal)));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (ne) P.work[1 + base + __popc(bal & ((1u << lane) - 1u))] = cc;
-    }
+  // block D: chunks with occurrences (order irrelevant: each is handled on its own)
+  if (!P.prefix) return;
+  for (uint32_t c0b = 0; c0b < P.nchunks; c0b += blockDim.x) {
+    const uint32_t cc = c0b + threadIdx.x;
+    const bool ne = cc < P.nchunks && P.listlen[cc] > 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ne);
+    uint32_t base = 0;
+    if (lane == 0 && bal) base = atomicAdd(P.work, static_cast<uint32_t>(__popc(bal)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ne) P.work[1 + base + __popc(bal & ((1u << lane) - 1u))] = cc;
   }
 }
 

@@ -190,3 +190,56 @@ extern "C" int64_t epsm_search_sharded(epsm_plan_t* plan, const uint8_t* d_shard
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_search_sharded");
   return static_cast<int64_t>(total);
 }
+
+// epsm_allgatherv_async -- the positions exchange of a sharded batch (BASELINE.json north_star:
+// "gathering counts and offsets and allgathering the positions over NVLink with NCCL"): for
+// every search j, rank q's counts[q * k + j] positions d_local[j] (on rank q) are broadcast into
+// every rank's d_out[j] at the exclusive prefix of the counts -- k all-gather(v)s as grouped
+// ncclBroadcasts, 64 searches per NCCL group call.
+extern "C" int epsm_allgatherv_async(uint32_t k, const uint64_t* const* d_local, const uint64_t* counts,
+                                     uint64_t* const* d_out, const uint64_t* caps, void* nccl_comm,
+                                     epsm_stream_t stream) {
+  if (k == 0) return EPSM_OK;
+  if (!d_local || !counts || !d_out || !nccl_comm) {
+    epsm_set_error("epsm_allgatherv_async: NULL argument");
+    return EPSM_EINVAL;
+  }
+  NcclApi& api = nccl();
+  if (!api.ok) {
+    epsm_set_error("libnccl.so.2 could not be loaded");
+    return EPSM_ENCCL;
+  }
+  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+  int nranks = 0, rank = 0;
+  ncclResult_t nr = api.CommCount(comm, &nranks);
+  if (nr != ncclSuccess) return nccl_fail(nr, "ncclCommCount");
+  nr = api.CommUserRank(comm, &rank);
+  if (nr != ncclSuccess) return nccl_fail(nr, "ncclCommUserRank");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  constexpr uint32_t kPerGroup = 64;
+  for (uint32_t a = 0; a < k; a += kPerGroup) {
+    const uint32_t b = a + kPerGroup < k ? a + kPerGroup : k;
+    nr = api.GroupStart();
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
+    for (uint32_t j = a; j < b; ++j) {
+      const uint64_t cap = caps ? caps[j] : ~0ull;
+      uint64_t off = 0;
+      for (int q = 0; q < nranks; ++q) {
+        const uint64_t c = counts[static_cast<uint64_t>(q) * k + j];
+        const uint64_t room = off < cap ? cap - off : 0;
+        const uint64_t cnt = c < room ? c : room;
+        if (cnt && d_out[j]) {
+          nr = api.Broadcast(q == rank ? d_local[j] : nullptr, d_out[j] + off, cnt, ncclUint64, q, comm, s);
+          if (nr != ncclSuccess) {
+            api.GroupEnd();
+            return nccl_fail(nr, "ncclBroadcast(positions)");
+          }
+        }
+        off += c;
+      }
+    }
+    nr = api.GroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclGroupEnd");
+  }
+  return EPSM_OK;
+}

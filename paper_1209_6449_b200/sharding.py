@@ -76,15 +76,10 @@ def exchange_positions(local_pos: torch.Tensor, local_occ: int, group=None, cap:
     return out, occ
 
 
-def exchange_batch_counts(local_occ: torch.Tensor, group=None):
-    """Counts exchange of a sharded batch of k searches (one all-gather of k int64 per rank).
-
-    ``local_occ[j]`` = occurrences of search j among this rank's owned starts.  Returns
-    (occ, offset): occ[j] = the global count, offset[j] = this rank's exclusive prefix (its
-    positions of search j are the global positions [offset[j], offset[j] + local_occ[j]) of
-    Occ in ascending order).  Stays on the device (no host synchronisation)."""
+def exchange_count_matrix(local_occ: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather of a sharded batch's per-rank counts: returns [world, k] int64 (row q = rank
+    q's local_occ) on local_occ's device.  One collective, no host synchronisation (NCCL)."""
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     k = local_occ.numel()
     dev = local_occ.device
     # gloo has no device all-gather: stage through the host (CPU tests, one-GPU emulation)
@@ -96,7 +91,56 @@ def exchange_batch_counts(local_occ: torch.Tensor, group=None):
     dist.all_gather_into_tensor(allc, src.contiguous(), group=group)
     if via_host:
         allc = allc.to(dev)
-    allc = allc.view(world, k)
+    return allc.view(world, k)
+
+
+def gather_batch_positions(local_outs, counts, outs, caps=None, group=None) -> None:
+    """The positions all-gather of a sharded batch of k searches (north_star: "allgathering the
+    positions"): every rank's outs[j] receives the first min(occ_j, caps[j]) GLOBAL positions of
+    search j in rank order -- rank q contributes counts[q][j] positions from its local_outs[j].
+    ``counts`` is the [world, k] count matrix on the host (exchange_count_matrix(...).cpu()).
+    NCCL: one native call (epsm_allgatherv_async: grouped ncclBroadcasts, one root per rank and
+    search).  gloo (CPU tests, one-GPU emulation): a padded all-gather per search + placement."""
+    import numpy as np
+    cnt = np.asarray(counts, dtype=np.int64)
+    world, k = cnt.shape
+    if k == 0:
+        return
+    if dist.get_backend(group) == "nccl":
+        from . import _lib
+        _lib.allgatherv_async(local_outs, cnt, outs, caps=caps, nccl_comm=_lib.nccl_comm_ptr(group))
+        return
+    me = dist.get_rank(group)
+    for j in range(k):
+        width = int(cnt[:, j].max())
+        if width == 0 or outs[j] is None:
+            continue
+        dev = outs[j].device
+        send = torch.zeros(width, dtype=torch.int64)
+        c_me = int(cnt[me, j])
+        if c_me:
+            send[:c_me] = local_outs[j][:c_me].to("cpu", torch.int64)
+        recv = torch.empty(world * width, dtype=torch.int64)
+        dist.all_gather_into_tensor(recv, send, group=group)
+        recv = recv.view(world, width)
+        cap = outs[j].numel() if caps is None else min(int(caps[j]), outs[j].numel())
+        off = 0
+        for q in range(world):
+            c = min(int(cnt[q, j]), max(0, cap - off))
+            if c:
+                outs[j][off:off + c].copy_(recv[q, :c].to(dev))
+            off += int(cnt[q, j])
+
+
+def exchange_batch_counts(local_occ: torch.Tensor, group=None):
+    """Counts exchange of a sharded batch of k searches (one all-gather of k int64 per rank).
+
+    ``local_occ[j]`` = occurrences of search j among this rank's owned starts.  Returns
+    (occ, offset): occ[j] = the global count, offset[j] = this rank's exclusive prefix (its
+    positions of search j are the global positions [offset[j], offset[j] + local_occ[j]) of
+    Occ in ascending order).  Stays on the device (no host synchronisation)."""
+    rank = dist.get_rank(group)
+    allc = exchange_count_matrix(local_occ, group)
     offset = allc.cumsum(0) - allc
     return allc.sum(0), offset[rank]
 

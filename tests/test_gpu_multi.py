@@ -31,19 +31,23 @@ def dev():
     return torch.device("cuda:0")
 
 
-def run_group(epsm, pats, td, caps=None, geom=None, count_only=False):
+def run_group(epsm, pats, td, caps=None, geom=None, count_only=False, dense=0, index=None):
+    """dense=0 (default here): every pattern through the group kernels (the kernels under
+    test); dense=None: the library's split (dense patterns one by one, over `index`)."""
     g = epsm.group(pats)
+    if dense is not None:
+        g.set_dense(dense)
     if geom is not None:
         g.set_geometry(*geom)
     n = td.numel()
     occ = torch.full((len(pats),), -1, dtype=torch.int64, device=td.device)
     if count_only:
-        g.count_async(td, occ)
+        g.count_async(td, occ, index=index)
         torch.cuda.synchronize()
         g.close()
         return [(int(o), None) for o in occ.cpu().tolist()]
     outs = [torch.full((max(n, 1),), -7, dtype=torch.int64, device=td.device) for _ in pats]
-    g.search_async(td, occ, outs=outs, caps=caps)
+    g.search_async(td, occ, outs=outs, caps=caps, index=index)
     torch.cuda.synchronize()
     res = []
     for j in range(len(pats)):
@@ -213,3 +217,59 @@ def test_group_shards_compose(epsm, dev, world):
         g.close()
         for j, w in enumerate(wants):
             assert np.array_equal(np.concatenate(parts[j]), w), (world, m, j)
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 16, 256])
+@pytest.mark.parametrize("use_index", [False, True])
+def test_group_dense_split(epsm, dev, sigma, use_index):
+    """The library's split: dense patterns (estimated >= 2^-11 occurrences per byte) searched
+    one by one (over the text's index where they qualify), the rest in the shared passes --
+    every search still returns its own Occ."""
+    rng = np.random.default_rng(200 + sigma)
+    n = 9 * TILE + 123
+    for m in (2, 4, 8, 16):
+        t, pats = planted(rng, n, sigma, m, 40)
+        td = torch.from_numpy(t).to(dev)
+        g = epsm.group(pats)
+        info = g.info()
+        g.close()
+        if sigma == 2 and m <= 8:
+            assert info["dense"] > 0, info
+        if sigma == 256 and m >= 4:
+            assert info["dense"] == 0, info
+        ix = None
+        if use_index:
+            plans = [epsm.plan(p) for p in set(pats)]
+            vals = epsm.index_values(plans)
+            ix = epsm.eq_index(td, vals) if vals else None
+        check(pats, run_group(epsm, pats, td, dense=None, index=ix), t, ("split", sigma, m, use_index))
+        check(pats, run_group(epsm, pats, td, dense=None, index=ix, count_only=True), t, ("split-count", sigma, m))
+        if ix is not None:
+            ix.close()
+
+
+def test_group_dense_split_shards(epsm, dev):
+    from paper_1209_6449_b200 import sharding
+    rng = np.random.default_rng(77)
+    n = 7 * TILE + 5
+    t = rng.integers(0, 2, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    pats = [t[s:s + 4].tobytes() for s in rng.integers(0, n - 4, size=20)] + [b"\x07" * 4]
+    wants = [oracle.search(p, t) for p in pats]
+    g = epsm.group(pats)
+    assert 0 < g.info()["dense"] < g.info()["distinct"]
+    parts = [[] for _ in pats]
+    for r in range(2):
+        base, owned, slen = sharding.shard_layout(n, 2, r)
+        shard = td[base:base + slen].clone()
+        ix = epsm.eq_index(shard, b"\x00\x01")
+        occ = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+        outs = [torch.empty(w.size + 1, dtype=torch.int64, device=dev) for w in wants]
+        g.search_range_async(shard, owned, base, n, occ, outs=outs, index=ix)
+        torch.cuda.synchronize()
+        for j in range(len(pats)):
+            parts[j].append(outs[j][:int(occ[j])].cpu().numpy().astype(np.uint64))
+        ix.close()
+    g.close()
+    for j, w in enumerate(wants):
+        assert np.array_equal(np.concatenate(parts[j]), w), j

@@ -77,3 +77,33 @@ def test_batch_counts_exchange_over_nccl(nccl_group):
     occ, off = sharding.exchange_batch_counts(occ_loc)
     want = [oracle.search(p, t).size for p in pats]
     assert occ.cpu().tolist() == want and off.cpu().tolist() == [0] * len(pats)
+
+
+def test_group_range_and_allgatherv_over_nccl(nccl_group):
+    """The bench's N > 1 step on a one-rank communicator: group search over the shard (dense
+    patterns over the shard's index), counts exchange, native positions all-gather
+    (epsm_allgatherv_async) -- against the oracle."""
+    import paper_1209_6449_b200 as epsm
+    from paper_1209_6449_b200 import sharding
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(63)
+    n = 5 * 128 * 1024 + 11
+    t = rng.integers(0, 2, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    pats = [t[s:s + m].tobytes() for s, m in ((1, 2), (70, 2), (900, 8), (5000, 20), (9999, 32))]
+    g = epsm.group(pats[:2])
+    ix = epsm.eq_index(td, g.index_values()) if g.index_values() else None
+    occ_loc = torch.zeros(2, dtype=torch.int64, device=dev)
+    loc = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(2)]
+    g.search_range_async(td, n, 0, n, occ_loc, outs=loc, index=ix)
+    cm = sharding.exchange_count_matrix(occ_loc).cpu().numpy()
+    outs = [torch.full((n,), -3, dtype=torch.int64, device=dev) for _ in range(2)]
+    sharding.gather_batch_positions(loc, cm, outs, caps=[n, 5])
+    torch.cuda.synchronize()
+    for j in range(2):
+        want = oracle.search(pats[j], t)
+        c = want.size if j == 0 else 5
+        assert int(cm[0, j]) == want.size
+        assert np.array_equal(outs[j][:c].cpu().numpy().astype(np.uint64), want[:c])
+        assert int(outs[j][c]) == -3
+    g.close()

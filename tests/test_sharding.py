@@ -148,3 +148,64 @@ def test_batch_counts_exchange_gives_global_layout(world):
             assert occ[j] == want.size
             out[off[j]: off[j] + lp[j].size] = lp[j]
         assert np.array_equal(out.astype(np.uint64), want)
+
+
+def _gather_worker(rank, world, port, text, patterns, caps, q):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = text.size
+        base, owned, slen = sharding.shard_layout(n, world, rank)
+        shard = text[base:base + slen]
+        local_outs, local_occ = [], []
+        for p in patterns:
+            pos = oracle.search(p, shard)
+            pos = pos[pos < owned].astype(np.int64) + base
+            local_outs.append(torch.from_numpy(pos.copy()))
+            local_occ.append(pos.size)
+        cm = sharding.exchange_count_matrix(torch.tensor(local_occ, dtype=torch.int64))
+        tot = cm.sum(0)
+        outs = [torch.full((int(t) + 2,), -9, dtype=torch.int64) for t in tot]
+        sharding.gather_batch_positions(local_outs, cm.numpy(), outs, caps=caps)
+        q.put((rank, [o.numpy().copy() for o in outs], tot.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_positions_gather(world):
+    """The N > 1 positions all-gather of a sharded batch (the bench's default multi-GPU exchange):
+    every rank ends with every search's full Occ (oracle over the whole text), in order, the cap
+    smallest when capped, nothing written past the cap."""
+    import oracle
+    rng = np.random.default_rng(world + 90)
+    n = 60_000
+    text = rng.integers(0, 2, size=n, dtype=np.uint8)
+    patterns = [text[s:s + m].tobytes() for s, m in ((3, 2), (500, 6), (9000, 12), (40_000, 31))] + [b"\x05" * 3]
+    for r in range(1, world):
+        b = sharding.shard_base(n, world, r)
+        text[b - 5:b - 5 + 12] = np.frombuffer(patterns[2], dtype=np.uint8)
+    patterns[2] = bytes(text[9000:9012])
+    caps = [10 ** 9, 7, 10 ** 9, 10 ** 9, 10 ** 9]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, text, patterns, caps, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict((r, (o, t)) for r, o, t in (q.get(timeout=120) for _ in range(world)))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for j, p in enumerate(patterns):
+        want = oracle.search(p, text)
+        c = min(want.size, caps[j])
+        for r in range(world):
+            outs, tot = res[r]
+            assert tot[j] == want.size
+            assert np.array_equal(outs[j][:c].astype(np.uint64), want[:c]), (r, j)
+            assert (outs[j][c:] == -9).all()

@@ -23,7 +23,7 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
-print("sigma m  distinct  group_us  batch_us  occ_total  pos_GB  group_TBps_text")
+print("sigma m  distinct(dense)  group_us  batch_us  occ_total  pos_GB  group_TBps_text")
 tot_g = tot_b = 0.0
 for s in sigmas:
     t = synth.text_torch(synth.raw_sigma_spec(s, (2, s)), 0, n, device=dev)
@@ -40,14 +40,14 @@ for s in sigmas:
         vals = epsm.index_values(plans)
         ix = epsm.eq_index(t, vals) if vals else None
         for _ in range(2):
-            g.search_async(t, occ, outs=outs)
+            g.search_async(t, occ, outs=outs, index=ix)
             epsm.search_batch_async(plans, t, occ_b, outs=outs, index=ix)
         torch.cuda.synchronize()
         assert torch.equal(occ, occ_b), (s, m)
         e = [ev() for _ in range(4)]
         e[0].record(st)
         for _ in range(3):
-            g.search_async(t, occ, outs=outs)
+            g.search_async(t, occ, outs=outs, index=ix)
         e[1].record(st)
         e[2].record(st)
         for _ in range(3):
@@ -59,8 +59,9 @@ for s in sigmas:
         tot_g += gu
         tot_b += bu
         o = int(occ.sum())
-        print("%5d %2d %9d %9.1f %9.1f %10d %7.2f %9.1f" % (
-            s, m, g.info()["distinct"], gu, bu, o, 8 * o / 1e9, P * n / (gu * 1e-6) / 1e12), flush=True)
+        inf = g.info()
+        print("%5d %2d %5d(%3d) %9.1f %9.1f %10d %7.2f %9.1f" % (
+            s, m, inf["distinct"], inf["dense"], gu, bu, o, 8 * o / 1e9, P * n / (gu * 1e-6) / 1e12), flush=True)
         if ix is not None:
             ix.close()
         g.close()
