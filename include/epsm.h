@@ -330,6 +330,11 @@ void epsm_group_free(epsm_group_t *g);
  * Returns EPSM_OK or EPSM_EINVAL (NULL, log2_rate > 64). */
 int epsm_group_set_dense(epsm_group_t *g, uint32_t log2_rate);
 
+/* epsm_group_dense_searches -- which searches of the group are searched one by one
+ * (dense patterns): flags[j] = 1 for those, 0 for the shared passes (flags: k bytes,
+ * may be NULL).  Returns their number, or EPSM_EINVAL for NULL g. */
+int epsm_group_dense_searches(const epsm_group_t *g, uint8_t *flags);
+
 /* epsm_group_index_values -- the byte values an equality-mask index needs for the
  * group's dense searches to run over it: writes up to 256 distinct values into
  * out_values (may be NULL) and returns their number (0: none qualifies, or NULL). */

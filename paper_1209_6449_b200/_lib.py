@@ -106,6 +106,8 @@ _lib.epsm_group_search_range_async.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64,
 _lib.epsm_group_search_range_async.restype = ctypes.c_int
 _lib.epsm_allgatherv_async.argtypes = [ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.epsm_allgatherv_async.restype = ctypes.c_int
+_lib.epsm_group_dense_searches.argtypes = [_vp, _vp]
+_lib.epsm_group_dense_searches.restype = ctypes.c_int
 _lib.epsm_group_index_values.argtypes = [_vp, _vp]
 _lib.epsm_group_index_values.restype = ctypes.c_int
 _lib.epsm_search_text_host.argtypes = [_vp, ctypes.c_uint32, _vp, _u64, _vp, _vp, _vp, _vp]
@@ -131,7 +133,7 @@ EXPORTED_SYMBOLS = (
     "epsm_group_create", "epsm_group_free", "epsm_group_info", "epsm_group_set_geometry", "epsm_group_search_async",
     "epsm_group_count_async", "epsm_group_search_range_async", "epsm_group_set_dense",
     "epsm_group_search_index_async", "epsm_group_count_index_async", "epsm_group_search_range_index_async",
-    "epsm_group_index_values", "epsm_search_text_host", "epsm_allgatherv_async",
+    "epsm_group_index_values", "epsm_search_text_host", "epsm_allgatherv_async", "epsm_group_dense_searches",
 )
 MAX_PLANES = 256
 INDEX_MAX_D = 8
@@ -577,6 +579,12 @@ class Group:
         """Force sampled q-grams every SK bytes (tests / tuning; results never change)."""
         _check(_lib.epsm_group_set_geometry(self.handle, int(q), int(sk)), "epsm_group_set_geometry")
         return self
+
+    def dense_searches(self) -> list:
+        """flags[j] = True if search j is searched one by one (a dense pattern)."""
+        out = (ctypes.c_uint8 * max(1, self.k))()
+        _check(_lib.epsm_group_dense_searches(self.handle, out), "epsm_group_dense_searches")
+        return [bool(x) for x in out[:self.k]]
 
     def index_values(self) -> bytes:
         """The byte values an equality-mask index needs for the dense searches."""

@@ -58,13 +58,19 @@ void choose_geometry(uint32_t m, uint32_t D, double p2, Subgroup& S) {
       const double nsamp = 64.0 / sk + (sk > 1 ? 1 : 0);
       const double entries = static_cast<double>(sk) * D;
       const double p_true = std::min(1.0, entries * pq);
-      const double p_false = q <= 2 ? 0.0 : std::min(1.0, entries / 65536.0);
+      const double fill = 1.0 - std::exp(-2.0 * entries / 65536.0);   // two probes per gram
+      const double p_false = q <= 2 ? 0.0 : fill * fill;
       const double p_hit = std::min(1.0, p_true + p_false);
-      const double c_sample = 8 + 2 * qw;
+      const double c_sample = 14 + 2 * qw;
       const double c_hit = 14 + 3 * qw + 3 * (entries / 4096.0);
       const double cand_per_start = std::min(64.0, D * pq);  // true gram matches per start
       const double c_verify = 10 + 4 * mw;
-      const double cost = nsamp * (c_sample + p_hit * c_hit) + 64.0 * cand_per_start * c_verify;
+      // a bucket walk is divergent: a warp pays it when ANY of its 32 lanes hits, for as many
+      // rounds as its busiest lane has hits
+      const double lane_hits = nsamp * p_hit;
+      const double p_warp = 1.0 - std::pow(1.0 - std::min(1.0, lane_hits), 32.0);
+      const double cost = nsamp * c_sample + p_warp * c_hit * std::max(1.0, 2.0 * lane_hits) +
+                          64.0 * cand_per_start * c_verify;
       if (cost < best * 0.999 || (cost <= best * 1.001 && q > S.q)) {
         best = std::min(best, cost);
         S.q = q;
@@ -188,6 +194,10 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     for (int i = 0; i < S.sk; ++i) {
       const uint32_t h = hash_key(reinterpret_cast<const uint8_t*>(pats[d].data()) + i, S.q, S);
       G.bitmap[h >> (32 - mp::kBitmapLog + 5)] |= 1u << ((h >> (32 - mp::kBitmapLog)) & 31u);
+      if (S.q > 2) {
+        const uint32_t h2 = mp::bloom2(h);
+        G.bitmap[h2 >> (32 - mp::kBitmapLog + 5)] |= 1u << ((h2 >> (32 - mp::kBitmapLog)) & 31u);
+      }
       buckets[h >> (32 - mp::kBucketLog)].push_back(
           static_cast<uint16_t>((d << 8) | (static_cast<uint32_t>(i) << 4) | ((h >> (32 - mp::kBitmapLog)) & 15u)));
     }
@@ -322,6 +332,7 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   P.D = S.D;
   P.k = S.k;
   P.qmask = S.qmask;
+  P.bloom2 = S.q > 2 ? 1u : 0u;
   for (int r = 0; r < 4; ++r) P.hmul[r] = S.hmul[r];
   P.desc = S.d_desc;
   P.desc_bytes = sizeof(mp::GroupDesc);
@@ -608,6 +619,14 @@ int epsm_group_set_dense(epsm_group_t* g, uint32_t log2_rate) {
   }
   group_split(g, log2_rate == 0 ? 4096 : static_cast<int>(log2_rate));
   return group_partition(g);
+}
+
+int epsm_group_dense_searches(const epsm_group_t* g, uint8_t* flags) {
+  if (!g) return EPSM_EINVAL;
+  if (flags) std::memset(flags, 0, g->k);
+  for (uint32_t j : g->djob_slot)
+    if (flags) flags[j] = 1;
+  return static_cast<int>(g->djob_slot.size());
 }
 
 int epsm_group_index_values(const epsm_group_t* g, uint8_t* out_values) {

@@ -84,6 +84,7 @@ struct MParams {
   uint32_t it_lo, it_hi;        // interior tiles: every start in [s_lo, s_hi)
   uint32_t m, mw, D, k;         // pattern length, words, distinct patterns, searches
   uint32_t qmask;               // byte mask of the last key word
+  uint32_t bloom2;              // second bitmap probe on (q > 2: hashed keys)
   uint32_t hmul[4];             // key word multipliers of the sample hash
   uint32_t desc_bytes;
   const GroupDesc* desc;
@@ -142,6 +143,9 @@ __device__ __forceinline__ uint32_t lds_u32_any(const uint8_t* base, uint32_t of
   const uint32_t* w = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
   return __funnelshift_r(w[0], w[1], 8 * (off & 3u));
 }
+
+// the second probe of the sample bitmap: a remix of the gram hash (host and device alike)
+__host__ __device__ __forceinline__ uint32_t bloom2(uint32_t h) { return (h ^ (h >> 15)) * 0x2C1B3C6Du; }
 
 template <int QW>
 __device__ __forceinline__ uint32_t hash_words(const uint32_t (&k)[4], const MParams& P) {
@@ -345,8 +349,16 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         k[QW - 1] &= P.qmask;
         const uint32_t h = hash_words<QW>(k, P);
         MP_CHECK((h >> (32 - kBitmapLog + 5)) < 2048u, "bitmap", h, j);
+        // two-probe (Bloom) test: both bits set for every table gram (false positives
+        // D*SK/2^16 -> (that)^2: one warp in ~3 instead of every warp walks a bucket per chunk)
         const uint32_t bw = G.bitmap[h >> (32 - kBitmapLog + 5)];
-        const uint32_t bit = __funnelshift_r(bw, bw, h >> (32 - kBitmapLog)) & 1u;
+        uint32_t bit = __funnelshift_r(bw, bw, h >> (32 - kBitmapLog));
+        if (P.bloom2) {                           // (q <= 2: the key itself, exact already)
+          const uint32_t h2 = bloom2(h);
+          const uint32_t bw2 = G.bitmap[h2 >> (32 - kBitmapLog + 5)];
+          bit &= __funnelshift_r(bw2, bw2, h2 >> (32 - kBitmapLog));
+        }
+        bit &= 1u;
         if (j < 64) hits |= static_cast<uint64_t>(bit) << j;
         else hit64 = bit;
       }
