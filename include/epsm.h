@@ -308,7 +308,7 @@ typedef struct epsm_group_s epsm_group_t;   /* opaque, host-owned */
  * group is pattern j.  Copies the patterns; no device work (the group's tables
  * are uploaded on first use, to the device of that call).  More than 255
  * distinct patterns are split internally into passes of <= 255.
- * Dense patterns -- an expected rate of >= 2^-11 occurrences per text byte, the
+ * Dense patterns -- an expected rate of >= 2^-7 occurrences per text byte, the
  * product of their bytes' frequencies among the k patterns (which are extracted
  * from the text) -- are searched one by one through the
  * single-pattern kernels (and over an index where one is passed and the search

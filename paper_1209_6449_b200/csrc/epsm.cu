@@ -413,6 +413,8 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   if (nstarts == 0) {
     for (uint32_t j = 0; j < k; ++j) {
       cudaError_t e = cudaMemsetAsync(jobs[j].d_occ, 0, sizeof(unsigned long long), s);
+      for (uint32_t o = 0; o < jobs[j].nx && e == cudaSuccess; ++o)
+        e = cudaMemsetAsync(jobs[j].xh[o].occ, 0, sizeof(unsigned long long), s);
       if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
     }
     return EPSM_OK;
@@ -564,6 +566,30 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   ws->ctr_base[par] += gchunks + grid;
   ws->exit_total[par] += grid;
   ws->launches = L + 1;
+  // fan-out: occ and positions of a job to its further outputs (identical patterns)
+  for (uint32_t j = 0; j < k; ++j) {
+    if (jobs[j].nx == 0) continue;
+    const uint64_t have = (search && jobs[j].d_pos) ? jobs[j].cap : 0;
+    static bool rep_attr = false;
+    if (!rep_attr) {
+      e = cudaFuncSetAttribute(epsm::epsm_replicate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(epsm::RepSmem)));
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(replicate)");
+      rep_attr = true;
+    }
+    // (grid sized by the capacity; CTAs past the occ's chunks exit at once)
+    const uint64_t chunks = (have + epsm::kRepChunk / 8 - 1) / (epsm::kRepChunk / 8);
+    const unsigned blocks = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(2ull * ws->num_sms, chunks)));
+    for (uint32_t a = 0; a < jobs[j].nx; a += epsm::kRepMaxOut) {
+      const uint32_t nxa = std::min<uint32_t>(jobs[j].nx - a, epsm::kRepMaxOut);
+      epsm::epsm_replicate_kernel<<<blocks, epsm::kRepThreads, sizeof(epsm::RepSmem), s>>>(
+          search ? jobs[j].d_pos : nullptr, jobs[j].d_occ, have, jobs[j].x + a, nxa);
+      epsm_count_launch();
+    }
+    epsm_count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_replicate_kernel launch");
+  }
   return EPSM_OK;
 }
 
@@ -856,7 +882,7 @@ static int check_overlap(uint64_t n, uint64_t owned_len, uint64_t base, uint64_t
 static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_text, uint64_t n, uint64_t owned_len,
                         uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
                         epsm_stream_t stream, const epsm_eqidx_t* index = nullptr, uint64_t n_total = 0,
-                        const uint32_t* slot = nullptr) {
+                        const uint32_t* slot = nullptr, const std::vector<std::vector<uint32_t>>* fan = nullptr) {
   if (k == 0) return EPSM_OK;
   if (index && (index->text != d_text || index->n != n)) {
     epsm_set_error("the index was built over another text (pointer or length differ)");
@@ -895,6 +921,51 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
     int rc = epsm_bind_device(plans[j], d_occ);
     if (rc) return rc;
     jobs[j] = epsm_job{plans[j], cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + sj)};
+  }
+  // fan-out outputs: host table, then one upload into the stream's workspace (stream order
+  // keeps an earlier call's launches reading their table before this copy lands)
+  std::vector<epsm::XOut> xh;
+  std::vector<uint64_t> xoff(k, 0);
+  if (fan) {
+    for (uint32_t j = 0; j < k; ++j) {
+      xoff[j] = xh.size();
+      for (uint32_t q : (*fan)[j]) {
+        uint64_t* pos = d_pos ? d_pos[q] : nullptr;
+        const uint64_t cap = (pos && caps) ? caps[q] : 0;
+        if (pos && !aligned8(pos)) {
+          epsm_set_error("d_pos[%u] must be 8-byte aligned", q);
+          return EPSM_EALIGN;
+        }
+        xh.push_back(epsm::XOut{cap ? pos : nullptr, cap, reinterpret_cast<unsigned long long*>(d_occ + q)});
+      }
+    }
+  }
+  if (!xh.empty()) {
+    epsm_workspace* ws = epsm_get_workspace(plans[0]->device, s);
+    if (!ws) return EPSM_ENOMEM;
+    if (xh.size() > ws->xout_cap) {
+      if (ws->d_xout) {
+        cudaStreamSynchronize(s);
+        cudaFree(ws->d_xout);
+        ws->d_xout = nullptr;
+        ws->xout_cap = 0;
+      }
+      cudaError_t e = cudaMalloc(&ws->d_xout, xh.size() * sizeof(epsm::XOut));
+      if (e != cudaSuccess) {
+        epsm_set_error("cudaMalloc(fan-out table): %s", cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
+      ws->xout_cap = xh.size();
+    }
+    cudaError_t e = cudaMemcpyAsync(ws->d_xout, xh.data(), xh.size() * sizeof(epsm::XOut), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out table)");
+    for (uint32_t j = 0; j < k; ++j) {
+      jobs[j].nx = static_cast<uint32_t>((*fan)[j].size());
+      if (jobs[j].nx) {
+        jobs[j].x = ws->d_xout + xoff[j];
+        jobs[j].xh = xh.data() + xoff[j];
+      }
+    }
   }
   // searches are independent: group them by kernel variant (m, filter or index), keeping
   // their order within a group, and launch each group in runs of at most kMaxJobs
@@ -935,8 +1006,9 @@ static int batch_common(epsm_plan_t* const* plans, uint32_t k, const uint8_t* d_
 
 int epsm_batch_run(epsm_plan_t* const* plans, uint32_t k, const uint32_t* slot, const uint8_t* d_text, uint64_t n,
                    uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
-                   uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index) {
-  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, search, s, index, n_total, slot);
+                   uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index,
+                   const std::vector<std::vector<uint32_t>>* fan) {
+  return batch_common(plans, k, d_text, n, owned_len, base, d_pos, caps, d_occ, search, s, index, n_total, slot, fan);
 }
 
 extern "C" {

@@ -1,12 +1,14 @@
 // epsm_internal.h -- plan layout and helpers shared by the host translation units.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "epsm.h"
 
 namespace epsm {
 struct JobDesc;
+struct XOut;
 namespace mp { struct JobOut; }
 }  // namespace epsm
 
@@ -72,6 +74,8 @@ struct epsm_workspace {
   uint64_t m_work_cap = 0;
   epsm::mp::JobOut* m_jobs = nullptr;         // outputs of the searches of a pass
   uint64_t m_jobs_cap = 0;
+  epsm::XOut* d_xout = nullptr;               // fan-out outputs of a batch call (device)
+  uint64_t xout_cap = 0;                      // entries
   unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
 };
 
@@ -85,12 +89,17 @@ int epsm_ensure_occ(epsm_plan_t* plan);
 int epsm_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
                 uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s);
 
-// One search of a multi-search launch (all over the same text, same m).
+// One search of a multi-search launch (all over the same text, same m).  Fan-out: nx further
+// outputs (identical patterns of a batch) get the same positions -- x is their device array,
+// xh the host copy (for the occ of an empty range), capmax the largest capacity of all.
 struct epsm_job {
   epsm_plan_t* plan;
   uint64_t* d_pos;
   uint64_t cap;
   unsigned long long* d_occ;
+  const epsm::XOut* x = nullptr;
+  const epsm::XOut* xh = nullptr;
+  uint32_t nx = 0;
 };
 // index: run the searches over its equality-mask planes (every plan qualifies), else the text
 int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
@@ -98,9 +107,12 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
 
 // The batch path (epsm_search_(range_)batch(_index)_async) for k searches whose outputs sit at
 // the caller's slots slot[j] of d_pos / caps / d_occ (slot NULL: j); n_total 0 = not a shard.
+// fan (optional): fan[j] = further slots of the caller's arrays that receive search j's results
+// (their d_pos must have the same 16-byte phase as slot[j]'s)
 int epsm_batch_run(epsm_plan_t* const* plans, uint32_t k, const uint32_t* slot, const uint8_t* d_text, uint64_t n,
                    uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
-                   uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index);
+                   uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index,
+                   const std::vector<std::vector<uint32_t>>* fan = nullptr);
 
 // Equality-mask index of one text (epsm_eqidx_build_async).
 struct epsm_eqidx_s {

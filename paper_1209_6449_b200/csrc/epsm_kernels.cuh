@@ -159,6 +159,14 @@ __host__ __device__ constexpr uint32_t plane_tps(int sk) {
 __host__ __device__ constexpr uint32_t plane_stride(int sk) { return plane_tps(sk) * (kTile / 8) + 16; }
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
+// A further output of a search (fan-out: identical patterns of a batch share one scan, and
+// the replicate kernel below copies the positions and occ to each of them).
+struct XOut {
+  uint64_t* pos;                // output positions
+  uint64_t cap;                 // capacity of pos (<= the source's capacity)
+  unsigned long long* occ;      // device occ
+};
+
 // One search of a launch: its preprocessing and its outputs.
 struct JobRef {
   const JobDesc* desc;          // device copy of the plan's preprocessing
@@ -1559,6 +1567,112 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 // of a batch over that text reads the masks of its own distinct bytes instead of recomputing
 // them from the text: plane k, word w, bit i = [t[64w + i] == vals[k]]; zero past n and in the
 // padding words up to pstride (the search kernel streams whole tiles + one halo word).
+// Fan-out of one search's result (identical patterns have identical Occ): occ
+// and the first min(occ, cap_o) positions of src to every output o.  The source streams
+// through shared memory in 32 KiB chunks (TMA bulk loads, a 3-stage ring per CTA) and each
+// chunk leaves as ONE TMA bulk store per output (cp.async.bulk.global.shared::cta): long
+// contiguous writes, no register traffic -- a store of 8-byte words from registers to many
+// interleaved destinations reached only ~3.3 TB/s.  Outputs of another 16-byte phase than
+// the source (never produced by the library's own callers) take 8-byte stores from shared
+// memory.
+constexpr uint32_t kRepChunk = 32768;                              // bytes per chunk
+constexpr int kRepStages = 3;
+constexpr uint32_t kRepMaxOut = 1024;
+constexpr int kRepThreads = 128;
+struct RepSmem {
+  uint64_t buf[kRepStages][kRepChunk / 8];
+  uint64_t* pos[kRepMaxOut];
+  uint64_t cnt[kRepMaxOut];
+  alignas(8) uint64_t full[kRepStages];
+  uint32_t odd_phase;                                              // some output has the other phase
+};
+
+__global__ void __launch_bounds__(kRepThreads) epsm_replicate_kernel(const uint64_t* __restrict__ src,
+                                                                     const unsigned long long* __restrict__ src_occ,
+                                                                     uint64_t src_cap, const XOut* __restrict__ x,
+                                                                     uint32_t nx) {
+  extern __shared__ __align__(128) uint8_t rep_raw[];
+  RepSmem& S = *reinterpret_cast<RepSmem*>(rep_raw);
+  const unsigned long long occ = *src_occ;
+  if (nx > kRepMaxOut) nx = kRepMaxOut;                            // (the host splits larger fan-outs)
+  if (blockIdx.x == 0)
+    for (uint32_t o = threadIdx.x; o < nx; o += blockDim.x) *x[o].occ = occ;
+  const uint64_t have = occ < src_cap ? occ : src_cap;
+  if (!src || have == 0) return;
+  const uint64_t lead = (reinterpret_cast<uintptr_t>(src) >> 3) & 1u;   // src + lead: 16-byte aligned
+  if (threadIdx.x == 0) S.odd_phase = 0;
+  __syncthreads();
+  for (uint32_t o = threadIdx.x; o < nx; o += blockDim.x) {
+    S.pos[o] = x[o].pos;
+    S.cnt[o] = x[o].pos ? (x[o].cap < have ? x[o].cap : have) : 0;
+    if (x[o].pos && S.cnt[o] > lead && (((reinterpret_cast<uintptr_t>(x[o].pos) >> 3) & 1u) != lead))
+      S.odd_phase = 1;
+    if (lead && blockIdx.x == 0 && S.cnt[o]) x[o].pos[0] = src[0];      // the element before the body
+  }
+  if (threadIdx.x < kRepStages) mbar_init(&S.full[threadIdx.x], 1);
+  fence_mbar_init();
+  __syncthreads();
+  const bool odd = S.odd_phase != 0;
+  const uint64_t body = have - lead;                               // elements from src + lead
+  const uint64_t per = kRepChunk / 8;
+  const uint64_t nchunk = (body + per - 1) / per;
+  auto issue = [&](uint64_t c, int st) {                           // thread 0: chunk c -> stage st
+    const uint64_t e0 = lead + c * per;
+    const uint64_t ne = have - e0 < per ? have - e0 : per;
+    const uint32_t bytes = static_cast<uint32_t>((ne * 8) & ~15ull);
+    mbar_arrive_expect_tx(&S.full[st], bytes);
+    if (bytes) bulk_g2s_plain(S.buf[st], src + e0, bytes, &S.full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int st = 0; st < kRepStages; ++st) {
+      const uint64_t c = blockIdx.x + static_cast<uint64_t>(st) * gridDim.x;
+      if (c < nchunk) issue(c, st);
+    }
+  uint32_t phase = 0;
+  int st = 0;
+  for (uint64_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
+    mbar_wait(&S.full[st], phase);
+    const uint64_t e0 = lead + c * per;
+    const uint64_t ne = have - e0 < per ? have - e0 : per;
+    if (threadIdx.x == 0) {
+      const uint64_t last = (ne & 1u) ? src[e0 + ne - 1] : 0;      // (not in the 16-byte bulk part)
+      for (uint32_t o = 0; o < nx; ++o) {
+        const uint64_t cnt = S.cnt[o];
+        if (cnt <= e0) continue;
+        uint64_t* d = S.pos[o] + e0;
+        if ((reinterpret_cast<uintptr_t>(d) & 15u) != 0) continue;  // other phase: below
+        const uint64_t n = cnt - e0 < ne ? cnt - e0 : ne;
+        const uint32_t bytes = static_cast<uint32_t>((n * 8) & ~15ull);
+        if (bytes) bulk_s2g(d, S.buf[st], bytes);
+        if (n & 1u) d[n - 1] = (n == ne) ? last : S.buf[st][n - 1];
+      }
+      bulk_commit();
+    }
+    if (odd) {                                                     // 8-byte stores from shared memory
+      for (uint32_t o = 0; o < nx; ++o) {
+        const uint64_t cnt = S.cnt[o];
+        uint64_t* d = S.pos[o] + e0;
+        if (cnt <= e0 || (reinterpret_cast<uintptr_t>(d) & 15u) == 0) continue;
+        const uint64_t n = cnt - e0 < ne ? cnt - e0 : ne;
+        const uint64_t nb = n & ~1ull;                             // the bulk part of the stage
+        for (uint64_t i = threadIdx.x; i < nb; i += blockDim.x) d[i] = S.buf[st][i];
+        if ((n & 1u) && threadIdx.x == 0) d[n - 1] = src[e0 + n - 1];
+      }
+    }
+    __syncthreads();                                               // shared-memory reads done
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();                                           // ... and the bulk stores' reads
+      const uint64_t cn = c + static_cast<uint64_t>(kRepStages) * gridDim.x;
+      if (cn < nchunk) issue(cn, st);
+    }
+    if (++st == kRepStages) {
+      st = 0;
+      phase ^= 1u;
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
 constexpr int kMaxPlanes = 256;
 struct IdxParams {
   const uint8_t* text;          // 16-byte aligned

@@ -22,7 +22,8 @@ namespace {
 // a group of more is split into subgroups (one pass each).
 struct Subgroup {
   uint32_t D = 0, k = 0;               // distinct patterns, searches
-  int q = 1, sk = 1, qw = 1;
+  int q = 1, sk = 1, qw = 1;           // sk = 0: code mode (every start keyed, exact)
+  uint32_t cb = 0;                     // code mode: bits per symbol code
   uint32_t qmask = 0xFFu, hmul[4] = {0, 0, 0, 0};
   std::vector<uint32_t> jobs;          // the caller's search index of local search j
   mp::GroupDesc* h_desc = nullptr;
@@ -107,6 +108,7 @@ MKernel pick_qw(int qw, bool write) {
 
 MKernel multi_kernel_for(int sk, int qw, bool write) {
   switch (sk) {
+    case 0: return pick_mk<0, 1>(write);
     case 1: return pick_qw<1>(qw, write);
     case 2: return pick_qw<2>(qw, write);
     case 4: return pick_qw<4>(qw, write);
@@ -149,10 +151,21 @@ struct epsm_group_s {
   // one by one through the single-pattern kernels (their positions, >= 4 bytes of output per
   // 1000 text bytes, dominate; the shared pass gains little there); the rest share the passes
   std::vector<uint32_t> sparse, dense;            // distinct pattern indices
-  std::vector<epsm_plan_t*> dplans;               // plan of dense[i]
-  std::vector<epsm_plan_t*> djob_plan;            // per dense search: its plan ...
-  std::vector<uint32_t> djob_slot;                // ... and the caller's search index
+  std::vector<epsm_plan_t*> dplans;               // plan of dense[i] (one scan, fanned out to its
+                                                  // searches: they have the same positions)
 };
+
+// EPSM_MULTI_CODE=0 disables the code mode (A/B timing; every mode is exact)
+static bool code_disabled() {
+  static const bool v = [] {
+    const char* e = getenv("EPSM_MULTI_CODE");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+// the code mode's cost in the cost model's units (lane instructions per 64 text bytes): 80 key
+// steps of ~10 instructions
+constexpr double kCodeCost = 850.0;
 
 static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subgroup& S,
                           const std::vector<std::vector<uint32_t>>& dups, int force_q = 0, int force_sk = 0) {
@@ -171,7 +184,22 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
   S.D = D;
   choose_geometry(m, D, p2, S);
   geometry_override(m, D, S);
-  if (force_q) {
+  // code mode: the patterns' distinct bytes coded in cb bits, m * cb <= 14 bits of key; it
+  // costs ~10 instructions per start whatever the density, so it wins where the sampled filter
+  // meets many candidates (dense groups over small alphabets)
+  uint32_t sigp = 0;
+  for (int c = 0; c < 256; ++c) sigp += cnt[c] ? 1u : 0u;
+  uint32_t cb = 1;
+  while ((1u << cb) < sigp) ++cb;
+  const bool code_ok = m * cb <= static_cast<uint32_t>(mp::kCodeKeyBits) && !code_disabled();
+  const bool force_code = force_q && force_sk == 0;
+  if (force_code && !code_ok) return EPSM_EINVAL;
+  if ((code_ok && !force_q && S.cost > kCodeCost) || force_code) {
+    S.sk = 0;
+    S.q = static_cast<int>(m);
+    S.qw = 1;
+    S.cb = cb;
+  } else if (force_q) {
     S.q = force_q;
     S.sk = force_sk;
     S.qw = (force_q + 3) / 4;
@@ -187,10 +215,26 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     for (uint32_t b = 0; b < m; ++b)
       G.pat[d][b / 4] |= static_cast<uint32_t>(static_cast<unsigned char>(pats[d][b])) << (8 * (b % 4));
   for (uint32_t b = 0; b < m; ++b) G.pmask[b / 4] |= 0xFFu << (8 * (b % 4));
+  if (S.sk == 0) {
+    // code mode: byte -> code (pattern bytes in order of value), key table (the codes of a
+    // window, its LAST byte in the low bits -- the kernel's rolling key) -> pattern
+    std::memset(G.cmap, 0x80, sizeof(G.cmap));
+    uint32_t code = 0;
+    for (int c = 0; c < 256; ++c)
+      if (cnt[c]) G.cmap[c] = static_cast<uint8_t>(code++);
+    uint8_t* lut = reinterpret_cast<uint8_t*>(G.bitmap);
+    std::memset(lut, 0xFF, 1u << mp::kCodeKeyBits);
+    for (uint32_t d = 0; d < D; ++d) {
+      uint32_t key = 0;
+      for (uint32_t j = 0; j < m; ++j)
+        key = (key << S.cb) | G.cmap[static_cast<unsigned char>(pats[d][j])];
+      lut[key] = static_cast<uint8_t>(d);
+    }
+  }
   // the table (EPSMc's L, for every pattern at once): gram p_d[i .. i+q) of
   // every distinct pattern d and offset i < SK, bucketed by the top 12 bits of its hash
   std::vector<std::vector<uint16_t>> buckets(1u << mp::kBucketLog);
-  for (uint32_t d = 0; d < D; ++d) {
+  for (uint32_t d = 0; d < D && S.sk > 0; ++d) {
     for (int i = 0; i < S.sk; ++i) {
       const uint32_t h = hash_key(reinterpret_cast<const uint8_t*>(pats[d].data()) + i, S.q, S);
       G.bitmap[h >> (32 - mp::kBitmapLog + 5)] |= 1u << ((h >> (32 - mp::kBitmapLog)) & 31u);
@@ -203,11 +247,14 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     }
   }
   uint32_t e = 0;
-  for (uint32_t b = 0; b < (1u << mp::kBucketLog); ++b) {
-    G.boff[b] = static_cast<uint16_t>(e);
-    for (uint16_t v : buckets[b]) G.ent[e++] = v;
+  if (S.sk > 0) {
+    for (uint32_t b = 0; b < (1u << mp::kBucketLog); ++b) {
+      G.boff[b] = static_cast<uint16_t>(e);
+      for (uint16_t v : buckets[b]) G.ent[e++] = v;
+    }
+    for (uint32_t b = (1u << mp::kBucketLog); b < (1u << mp::kBucketLog) + 8; ++b)
+      G.boff[b] = static_cast<uint16_t>(e);
   }
-  for (uint32_t b = (1u << mp::kBucketLog); b < (1u << mp::kBucketLog) + 8; ++b) G.boff[b] = static_cast<uint16_t>(e);
   // searches per distinct pattern
   uint32_t q = 0;
   S.jobs.clear();
@@ -332,7 +379,10 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   P.D = S.D;
   P.k = S.k;
   P.qmask = S.qmask;
-  P.bloom2 = S.q > 2 ? 1u : 0u;
+  P.bloom2 = (S.sk > 0 && S.q > 2) ? 1u : 0u;
+  P.cb = S.cb;
+  P.kmask = S.sk == 0 ? (1u << (g->m * S.cb)) - 1u : 0u;
+  P.mmask = S.sk == 0 ? (1u << g->m) - 1u : 0u;
   for (int r = 0; r < 4; ++r) P.hmul[r] = S.hmul[r];
   P.desc = S.d_desc;
   P.desc_bytes = sizeof(mp::GroupDesc);
@@ -454,25 +504,51 @@ static int group_run(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_
     rc = subgroup_launch(g, S, d_text, n, ns, base, d_pos, caps, d_occ, search, s);
     if (rc) return rc;
   }
-  if (!g->djob_plan.empty()) {
-    // the dense patterns' searches: the batch path (over the index where it qualifies)
-    rc = epsm_batch_run(g->djob_plan.data(), static_cast<uint32_t>(g->djob_plan.size()), g->djob_slot.data(), d_text,
-                        n, owned_len, base, n_total, search ? d_pos : nullptr, search ? caps : nullptr, d_occ, search,
-                        s, index);
+  if (!g->dense.empty()) {
+    // the dense patterns: one single-pattern scan per distinct pattern (over the index where it
+    // qualifies), its occ and positions fanned out to every other search of that pattern by the
+    // replicate kernel -- one job per 16-byte phase of the outputs (16-byte copies)
+    std::vector<epsm_plan_t*> pl;
+    std::vector<uint32_t> primary;
+    std::vector<std::vector<uint32_t>> fan;
+    for (size_t i = 0; i < g->dense.size(); ++i) {
+      std::vector<uint32_t> cls[2], none;
+      for (uint32_t j : g->dups[g->dense[i]]) {
+        const bool has = search && d_pos && d_pos[j] && caps && caps[j];
+        if (has) cls[(reinterpret_cast<uintptr_t>(d_pos[j]) >> 3) & 1u].push_back(j);
+        else none.push_back(j);
+      }
+      if (cls[0].empty() && cls[1].empty()) cls[0].swap(none);
+      else (cls[0].empty() ? cls[1] : cls[0]).insert((cls[0].empty() ? cls[1] : cls[0]).end(), none.begin(), none.end());
+      for (auto& c : cls) {
+        if (c.empty()) continue;
+        // the primary (the scan's own output) is the largest capacity: the fan-out copies from it
+        size_t best = 0;
+        for (size_t q = 1; q < c.size(); ++q)
+          if (search && d_pos && caps && d_pos[c[q]] && (!d_pos[c[best]] || caps[c[q]] > caps[c[best]])) best = q;
+        std::swap(c[0], c[best]);
+        pl.push_back(g->dplans[i]);
+        primary.push_back(c[0]);
+        fan.emplace_back(c.begin() + 1, c.end());
+      }
+    }
+    rc = epsm_batch_run(pl.data(), static_cast<uint32_t>(pl.size()), primary.data(), d_text, n, owned_len, base,
+                        n_total, search ? d_pos : nullptr, search ? caps : nullptr, d_occ, search, s, index, &fan);
     if (rc) return rc;
   }
   return EPSM_OK;
 }
 
 // EPSM_GROUP_DENSE=L: distinct patterns with an estimated rate >= 2^-L occurrences per text
-// byte are searched one by one (default 11; 0 puts every pattern through the group kernels).
-// Speed only: both paths are exact.  B200, 256 MiB texts, 100 patterns per group: the shared
-// passes win below ~2^-11 (sigma=64 m=2: 2.7 -> 2.3 ms, sigma=8 m=4: 3.4 -> 2.2 ms), the
-// single-pattern kernels above (sigma=32 m=2: 3.7 vs 4.3 ms, sigma=2 m=8: 5.6 vs 6.4 ms).
+// byte are searched one by one, their positions fanned out to their duplicate searches by the
+// replicate kernel (default 7; 0 puts every pattern through the group kernels).  Speed only:
+// both paths are exact.  B200, 256 MiB texts, 100 patterns per group (ms, one by one vs shared
+// passes): sigma=8 m=2 (2^-6) 3.85 vs 8.7; sigma=2 m=8 (2^-8) 4.9 vs 4.0; sigma=16 m=2 (2^-8)
+// 4.2 vs 4.1; sigma=32 m=2 (2^-10) 4.4 vs 2.2-2.8; sigma=64 m=2 (2^-12) 2.3 vs 1.4.
 static int group_dense_log2() {
   static const int v = [] {
     const char* e = getenv("EPSM_GROUP_DENSE");
-    return e && e[0] ? static_cast<int>(strtol(e, nullptr, 0)) : 11;
+    return e && e[0] ? static_cast<int>(strtol(e, nullptr, 0)) : 7;
   }();
   return v <= 0 ? 4096 : v;
 }
@@ -521,17 +597,11 @@ static int group_partition(epsm_group_t* g, int force_q, int force_sk) {
   }
   for (epsm_plan_t* p : g->dplans) epsm_plan_free(p);
   g->dplans.clear();
-  g->djob_plan.clear();
-  g->djob_slot.clear();
   for (uint32_t d : g->dense) {
     epsm_plan_t* p = nullptr;
     int rc = epsm_plan(reinterpret_cast<const uint8_t*>(g->pats[d].data()), g->m, &p);
     if (rc) return rc;
     g->dplans.push_back(p);
-    for (uint32_t j : g->dups[d]) {
-      g->djob_plan.push_back(p);
-      g->djob_slot.push_back(j);
-    }
   }
   return EPSM_OK;
 }
@@ -587,8 +657,11 @@ int epsm_group_create(const uint8_t* patterns, uint32_t m, uint32_t k, epsm_grou
 void epsm_group_free(epsm_group_t* g) { group_release(g); }
 
 int epsm_group_set_geometry(epsm_group_t* g, uint32_t q, uint32_t sk) {
-  if (!g || q < 1 || q > 16 || q > g->m || sk < 1 || sk > 16 || (sk & (sk - 1)) || sk + q - 1 > g->m) {
-    epsm_set_error("epsm_group_set_geometry: need 1 <= q <= min(m, 16), SK in {1,2,4,8,16}, SK + q - 1 <= m");
+  const bool code = sk == 0;   // the code mode (q ignored)
+  if (code) q = g ? g->m : 1;
+  if (!g || (!code && (q < 1 || q > 16 || q > g->m || sk < 1 || sk > 16 || (sk & (sk - 1)) || sk + q - 1 > g->m))) {
+    epsm_set_error("epsm_group_set_geometry: need SK = 0 (code mode) or 1 <= q <= min(m, 16), SK in {1,2,4,8,16}, "
+                   "SK + q - 1 <= m");
     return EPSM_EINVAL;
   }
   const uint32_t dmax = std::min<uint32_t>(g->D, mp::kMaxD);   // distinct patterns of the largest pass
@@ -624,9 +697,13 @@ int epsm_group_set_dense(epsm_group_t* g, uint32_t log2_rate) {
 int epsm_group_dense_searches(const epsm_group_t* g, uint8_t* flags) {
   if (!g) return EPSM_EINVAL;
   if (flags) std::memset(flags, 0, g->k);
-  for (uint32_t j : g->djob_slot)
-    if (flags) flags[j] = 1;
-  return static_cast<int>(g->djob_slot.size());
+  int c = 0;
+  for (uint32_t d : g->dense)
+    for (uint32_t j : g->dups[d]) {
+      if (flags) flags[j] = 1;
+      ++c;
+    }
+  return c;
 }
 
 int epsm_group_index_values(const epsm_group_t* g, uint8_t* out_values) {

@@ -30,6 +30,7 @@
 // DRAM traffic of a group: the text once (plus dense chunks once more -- those are the
 // chunks whose output is many bytes per text byte anyway) + the positions.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -55,6 +56,7 @@ constexpr int kMaxEntries = 4096;                 // (d, i) pairs: D * SK
 constexpr int kMaxJobs = 1024;                    // searches per group
 constexpr int kListCap = 256;                     // (offset, id) entries kept per chunk
 constexpr int kMaxPW = 8;                         // pattern words (m <= 32)
+constexpr int kCodeKeyBits = 14;                  // code mode: m * (bits per symbol) <= 14
 static_assert(kSegBytes * 32 * kConsumerWarps == kTile, "lanes tile the chunk");
 
 // The group's preprocessing (built on the host, copied into shared memory once per CTA).
@@ -68,7 +70,13 @@ struct __align__(16) GroupDesc {
   uint16_t dup_list[kMaxJobs];
   uint16_t job_d[kMaxJobs];                       // distinct pattern of (local) search j
   uint16_t job_g[kMaxJobs];                       // its index in the caller's batch (occ slot)
+  uint8_t cmap[256];                              // code mode: byte -> symbol code, 0x80 = not a
+                                                  // pattern byte (the key table overlays bitmap
+                                                  // and boff: 2^14 bytes, key -> pattern or 0xFF)
 };
+static_assert(offsetof(GroupDesc, boff) == offsetof(GroupDesc, bitmap) + 8192 &&
+                  sizeof(GroupDesc::bitmap) + sizeof(GroupDesc::boff) >= (1u << kCodeKeyBits),
+              "code-mode key table overlays bitmap + boff");
 
 struct JobOut {                 // where search j's positions go
   uint64_t* pos;
@@ -85,6 +93,9 @@ struct MParams {
   uint32_t m, mw, D, k;         // pattern length, words, distinct patterns, searches
   uint32_t qmask;               // byte mask of the last key word
   uint32_t bloom2;              // second bitmap probe on (q > 2: hashed keys)
+  uint32_t cb;                  // code mode: bits per symbol code
+  uint32_t kmask;               // code mode: 2^(m * cb) - 1
+  uint32_t mmask;               // code mode: 2^m - 1
   uint32_t hmul[4];             // key word multipliers of the sample hash
   uint32_t desc_bytes;
   const GroupDesc* desc;
@@ -121,8 +132,8 @@ struct ScanParams {
 #endif
 
 template <int SK>
-struct Geo {
-  static constexpr int kSamples = kSegBytes / SK + (SK > 1 ? 1 : 0);   // sample offsets 0, SK, ..
+struct Geo {   // sample offsets 0, SK, .. (SK = 0: the code mode, every start keyed)
+  static constexpr int kSamples = SK > 0 ? kSegBytes / (SK > 0 ? SK : 1) + (SK > 1 ? 1 : 0) : 0;
 };
 
 __device__ __forceinline__ void bar_consumers() {   // named barrier over the 16 consumer warps
@@ -165,7 +176,8 @@ struct __align__(128) MSmem {
   uint32_t ccnt[kStages][kMaxD + 1];                 // pass 1: chunk counts (by stage)
   uint32_t lcur[kStages];                            // pass 1: list cursor (by stage)
   uint32_t done[kStages];                            // pass 1: warps finished with the stage
-  uint32_t nbw[kConsumerWarps][2];                   // nonempty batches of a slice (list path)
+  unsigned long long lm[kConsumerWarps][32];         // lane match masks of a slice (list path)
+  uint32_t rbuf[kConsumerWarps][32];                 // pass 3: a round of 32 matches (offset | id << 16)
   alignas(8) uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t gfull;
@@ -188,6 +200,44 @@ __device__ __forceinline__ bool verify_window(const uint8_t* ts, uint32_t st, co
     lo = hi;
   }
   return true;
+}
+
+// Code mode: the lane's 80 bytes (64 starts + halo) keyed through the patterns' symbol codes.
+// Byte t maps to its code (cmap); the rolling key over t holds the codes of bytes t-m+1 .. t
+// (byte t in the low bits), i.e. the window of start t-m+1, and the key table names the pattern
+// with exactly those m bytes (or 0xFF) -- EPSMa's per-position compare for all
+// patterns at once, exact, so no naive check.  Returns the lane's match mask (bit s: start s).
+// DIRECT: count each match into cc[pattern] (shared atomics); else store every start's id
+// (0xFF: none) into idb[0..63].
+template <bool DIRECT>
+__device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
+                                              uint8_t* idb, uint32_t* cc) {
+  const uint8_t* lut = reinterpret_cast<const uint8_t*>(G.bitmap);
+  const uint32_t m1 = P.m - 1, cb = P.cb, kmask = P.kmask;
+  uint32_t key = 0, e0 = 0, e1 = 0, e2 = 0;
+  int last_inv = -64;                            // last byte outside the patterns' alphabet
+  uint8_t* const ids0 = idb - m1;                // id slot of the start closed by byte t: ids0[t]
+#pragma unroll
+  for (int t = 0; t < 80; ++t) {
+    const uint32_t cm = G.cmap[(W[t >> 2] >> (8 * (t & 3))) & 0xFFu];
+    key = ((key << cb) | cm) & kmask;            // (an invalid byte's 0x80 is cut by the next
+    if (cm & 0x80u) last_inv = t;                //  mask or caught by last_inv)
+    const uint32_t d = (t - last_inv > static_cast<int>(m1)) ? lut[key] : 0xFFu;
+    const uint32_t s0 = static_cast<uint32_t>(t) - m1;
+    const bool mine = s0 < static_cast<uint32_t>(kSegBytes);
+    if constexpr (DIRECT) {
+      if (mine && d != 0xFFu) atomicAdd(&cc[d], 1u);
+    } else {
+      if (mine) ids0[t] = static_cast<uint8_t>(d);
+    }
+    const uint32_t hit = d != 0xFFu ? 1u : 0u;
+    if (t < 32) e0 |= hit << t;
+    else if (t < 64) e1 |= hit << (t - 32);
+    else e2 |= hit << (t - 64);
+  }
+  // starts = window ends - m1 (m1 <= 13): the lane's 64 starts out of the 80 ends
+  const uint64_t lo = (static_cast<uint64_t>(e1) << 32) | e0;
+  return m1 ? ((lo >> m1) | (static_cast<uint64_t>(e2) << (64 - m1))) : lo;
 }
 
 template <int SK, int QW, bool WRITE>
@@ -292,10 +342,11 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
     if (info == kEnd) break;
     const uint32_t c = info & ~kInfoList;
     const uint8_t* ts = S.ring[stage];
-    uint32_t nb_lo = 0, nb_hi = 0;      // nonempty 32-start batches of this warp's slice
+    uint64_t M = 0;                     // this lane's matched starts (bit i: slice offset 64 lane + i)
+    bool direct = false;                // pass 1, code mode: counted in the scan, no ids
     if (WRITE && (info & kInfoList)) {
       // ---- rebuild the chunk's ids from its list (pass 1 kept it: no text)
-      if (lane < 2) S.nbw[cw][lane] = 0;
+      S.lm[cw][lane] = 0;
       bar_consumers();
       const uint32_t len = S.ilen[stage];
       const uint32_t* L = reinterpret_cast<const uint32_t*>(ts);
@@ -303,12 +354,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         const uint32_t v = L[e];
         const uint32_t off = v & 0xFFFFu, d = v >> 16;
         S.ids[off / kSliceBytes][off % kSliceBytes] = static_cast<uint8_t>(d);
-        const uint32_t b = (off % kSliceBytes) >> 5;
-        atomicOr(&S.nbw[off / kSliceBytes][b >> 5], 1u << (b & 31u));
+        atomicOr(&S.lm[off / kSliceBytes][(off % kSliceBytes) / kSegBytes], 1ull << (off % kSegBytes));
       }
       bar_consumers();
-      nb_lo = S.nbw[cw][0];
-      nb_hi = S.nbw[cw][1];
+      M = S.lm[cw][lane];
     } else {
       // ---- filter the warp's slice: one sample every SK bytes (EPSMc)
       uint32_t W[20];
@@ -331,6 +380,38 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           W[17] = v.y;
           W[18] = v.z;
           W[19] = v.w;
+        }
+      }
+      if constexpr (SK == 0) {
+        // ---- code mode (dense groups, small pattern alphabets): every start keyed exactly.
+        // Byte t of the lane's window maps to its symbol code; the rolling key over t holds the
+        // codes of bytes t-m+1 .. t (byte t in the low bits), i.e. the window of start t-m+1;
+        // the key table names the pattern with exactly those m bytes (or none) -- EPSMa's
+        // per-position compare for all patterns at once, without a naive check.
+        // Every start of the lane gets its id (0xFF: none) -- no stale ids -- and bit t of
+        // E marks the window ENDING at byte t (compile-time bit positions).
+        uint8_t* const idb = ids + lane * kSegBytes;
+        if (!WRITE && c >= P.it_lo && c < P.it_hi) {
+          // pass 1 over an interior chunk: count straight into the chunk's counters (no ids,
+          // no list: the chunk is re-filtered by pass 3)
+          M = code_scan<true>(W, G, P, idb, S.ccnt[stage]);
+          direct = true;
+        } else {
+          M = code_scan<false>(W, G, P, idb, nullptr);
+        }
+        if (!(c >= P.it_lo && c < P.it_hi)) {
+          // a chunk at the text's ends: starts outside [s_lo, s_hi) do not count (their ids are
+          // cleared again below with the others)
+          const uint64_t ub = static_cast<uint64_t>(c) * kTile + seg;
+          uint64_t keep = ~0ull;
+          if (ub + 64 > P.s_hi) keep = P.s_hi <= ub ? 0ull : (~0ull >> (64 - (P.s_hi - ub)));
+          if (ub < P.s_lo) keep &= P.s_lo >= ub + 64 ? 0ull : (~0ull << (P.s_lo - ub));
+          uint64_t drop = M & ~keep;
+          M &= keep;
+          while (drop) {
+            idb[__ffsll(static_cast<long long>(drop)) - 1] = kNoId;
+            drop &= drop - 1;
+          }
         }
       }
       constexpr int NS = Geo<SK>::kSamples;
@@ -362,8 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         if (j < 64) hits |= static_cast<uint64_t>(bit) << j;
         else hit64 = bit;
       }
-      uint64_t M = 0;                             // matched starts of the lane
-      if (__any_sync(0xffffffffu, (hits | hit64) != 0)) {
+      if (SK > 0 && __any_sync(0xffffffffu, (hits | hit64) != 0)) {
         const uint64_t tbase = static_cast<uint64_t>(c) * kTile;
         const bool interior = c >= P.it_lo && c < P.it_hi;
         // candidates: every table entry (d, i) of the sample's bucket with
@@ -408,40 +488,42 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           }
         }
       }
-      // nonempty batches: batch b = slice starts [32b, 32b + 32) = lane b/2, half b&1
-      const uint32_t blo = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M) != 0u);
-      const uint32_t bhi = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M >> 32) != 0u);
-      // interleave: batch 2l <- blo bit l, batch 2l + 1 <- bhi bit l (bit spreading; skipped
-      // by the common warps without a match)
-      if ((blo | bhi) != 0u) {
-        nb_lo = spread16(blo & 0xFFFFu) | (spread16(bhi & 0xFFFFu) << 1);
-        nb_hi = spread16(blo >> 16) | (spread16(bhi >> 16) << 1);
-      }
       __syncwarp();
     }
+    // this lane's matches: count and exclusive offset among the warp slice's (text order)
+    const uint32_t cl = static_cast<uint32_t>(__popcll(static_cast<long long>(M)));
+    uint32_t incl = cl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += y;
+    }
+    const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);       // matches of the slice
+    uint8_t* const idl = ids + lane * kSegBytes;
 
     if constexpr (!WRITE) {
-      // ---- pass 1: counts per distinct pattern, and the chunk's list while it is short
-      uint64_t nbm = (static_cast<uint64_t>(nb_hi) << 32) | nb_lo;
+      // ---- pass 1: counts per distinct pattern (per-match shared atomics), and the chunk's
+      // list while it is short (order irrelevant here: one warp-aggregated slot reservation)
       uint32_t* const cc = S.ccnt[stage];
-      while (nbm) {
-        const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
-        nbm &= nbm - 1;
-        MP_CHECK(b < 64u, "batch", b, 0);
-        const uint32_t id = ids[32 * b + lane];
-        ids[32 * b + lane] = kNoId;
-        const bool act = id != kNoId;
-        MP_CHECK(!act || id < P.D, "id", id, b);
-        const uint32_t peers = __match_any_sync(0xffffffffu, id);
-        if (act && (peers & lt) == 0) atomicAdd(&cc[id], static_cast<uint32_t>(__popc(peers)));
-        const uint32_t am = __ballot_sync(0xffffffffu, act);
+      if (direct) {
+        // (counted already; a chunk with matches is marked dense: pass 3 re-filters it)
+        if (T && lane == 0) atomicAdd(&S.lcur[stage], T + kListCap + 1);
+      } else if (T) {
         uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&S.lcur[stage], static_cast<uint32_t>(__popc(am)));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const uint32_t r = base + __popc(am & lt);
-        MP_CHECK(c < P.nchunks, "chunk", c, r);
-        if (act && r < static_cast<uint32_t>(kListCap))
-          P.lists[static_cast<uint64_t>(c) * kListCap + r] = (cw * kSliceBytes + 32 * b + lane) | (id << 16);
+        if (lane == 0) base = atomicAdd(&S.lcur[stage], T);
+        uint32_t r = __shfl_sync(0xffffffffu, base, 0) + incl - cl;
+        uint64_t mm = M;
+        while (mm) {
+          const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
+          mm &= mm - 1;
+          const uint32_t id = idl[bit];
+          idl[bit] = kNoId;
+          MP_CHECK(id < P.D, "id", id, bit);
+          atomicAdd(&cc[id], 1u);
+          if (r < static_cast<uint32_t>(kListCap))
+            P.lists[static_cast<uint64_t>(c) * kListCap + r] = (cw * kSliceBytes + lane * kSegBytes + bit) | (id << 16);
+          ++r;
+        }
       }
       __syncwarp();
       uint32_t prev = 0;
@@ -469,17 +551,17 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       // ---- pass 3: rank every occurrence among its pattern's in text order, then write it to
       // each search that asked for that pattern at prefix + rank
       uint16_t* const hw = S.hist[cw];
-      uint64_t nbm = (static_cast<uint64_t>(nb_hi) << 32) | nb_lo;
       {
-        uint64_t t = nbm;
-        while (t) {
-          const uint32_t b = __ffsll(static_cast<long long>(t)) - 1;
-          t &= t - 1;
-          const uint32_t id = ids[32 * b + lane];
-          const uint32_t peers = __match_any_sync(0xffffffffu, id);
-          if (id != kNoId && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
-          __syncwarp();
+        // the slice's count of every pattern (u16 counters, two per 32-bit word)
+        uint32_t* const hw32 = reinterpret_cast<uint32_t*>(hw);
+        uint64_t mm = M;
+        while (mm) {
+          const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
+          mm &= mm - 1;
+          const uint32_t id = idl[bit];
+          atomicAdd(&hw32[id >> 1], 1u << (16 * (id & 1u)));
         }
+        __syncwarp();
       }
       if (lane == 0) mbar_arrive(&S.empty[stage]);   // (lists and text both consumed)
       bar_consumers();
@@ -496,25 +578,69 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       }
       bar_consumers();
       const uint64_t cbase = static_cast<uint64_t>(c) * kTile + P.pos_bias + cw * kSliceBytes;
-      while (nbm) {
-        const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
-        nbm &= nbm - 1;
-        const uint32_t id = ids[32 * b + lane];
-        ids[32 * b + lane] = kNoId;
+      // the slice's matches in text order, 32 per round: every lane emits its own (in bit order)
+      // into the round buffer, then lane i takes match R + i -- ranks by match_any on the ids
+      uint32_t* const rb = S.rbuf[cw];
+      uint64_t mm = M;
+      uint32_t idx = incl - cl;
+      if (T > 96) {
+        // a dense slice: 32-start batches instead (the matches of a round would come from one or
+        // two lanes, emitted one by one); batch b = slice starts [32b, 32b + 32) = lane b/2, half b&1
+        const uint32_t blo = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M) != 0u);
+        const uint32_t bhi = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M >> 32) != 0u);
+        uint64_t nbm = (static_cast<uint64_t>(spread16(blo >> 16) | (spread16(bhi >> 16) << 1)) << 32) |
+                       (spread16(blo & 0xFFFFu) | (spread16(bhi & 0xFFFFu) << 1));
+        while (nbm) {
+          const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
+          nbm &= nbm - 1;
+          const uint32_t id = ids[32 * b + lane];
+          ids[32 * b + lane] = kNoId;
+          const uint32_t peers = __match_any_sync(0xffffffffu, id);
+          const bool act = id != kNoId;
+          uint64_t g = 0;
+          if (act) g = S.pre[id] + hw[id] + __popc(peers & lt);
+          __syncwarp();
+          if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
+          if (act) {
+            const uint64_t pos = cbase + 32 * b + lane;
+            const uint32_t j1 = G.dup_off[id + 1];
+            for (uint32_t q = G.dup_off[id]; q < j1; ++q) {
+              const JobOut J = P.jobs[G.dup_list[q]];
+              if (g < J.cap) st_stream_u64(J.pos + g, pos);
+            }
+          }
+          __syncwarp();
+        }
+        mm = 0;
+        idx = T;                                      // (the round loop below has nothing left)
+      }
+      for (uint32_t R = T > 96 ? T : 0; R < T; R += 32) {
+        while (mm && idx < R + 32) {
+          const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
+          mm &= mm - 1;
+          const uint32_t id = idl[bit];
+          idl[bit] = kNoId;
+          rb[idx - R] = (lane * kSegBytes + bit) | (id << 16);
+          ++idx;
+        }
+        __syncwarp();
+        const bool act = R + lane < T;
+        const uint32_t e = act ? rb[lane] : 0u;
+        const uint32_t id = act ? (e >> 16) : static_cast<uint32_t>(kNoId);
         const uint32_t peers = __match_any_sync(0xffffffffu, id);
-        const bool act = id != kNoId;
         uint64_t g = 0;
         if (act) g = S.pre[id] + hw[id] + __popc(peers & lt);
         __syncwarp();
         if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
         if (act) {
-          const uint64_t pos = cbase + 32 * b + lane;
+          const uint64_t pos = cbase + (e & 0xFFFFu);
           const uint32_t j1 = G.dup_off[id + 1];
           for (uint32_t q = G.dup_off[id]; q < j1; ++q) {
             const JobOut J = P.jobs[G.dup_list[q]];
             if (g < J.cap) st_stream_u64(J.pos + g, pos);
           }
         }
+        __syncwarp();                                  // (the round buffer is refilled next)
       }
       __syncwarp();
       // the warp's offsets are spent: zero its row for the next chunk (no other warp reads it

@@ -222,7 +222,7 @@ def test_group_shards_compose(epsm, dev, world):
 @pytest.mark.parametrize("sigma", [2, 4, 16, 256])
 @pytest.mark.parametrize("use_index", [False, True])
 def test_group_dense_split(epsm, dev, sigma, use_index):
-    """The library's split: dense patterns (estimated >= 2^-11 occurrences per byte) searched
+    """The library's split: dense patterns (estimated >= 2^-7 occurrences per byte) searched
     one by one (over the text's index where they qualify), the rest in the shared passes --
     every search still returns its own Occ."""
     rng = np.random.default_rng(200 + sigma)
@@ -233,7 +233,7 @@ def test_group_dense_split(epsm, dev, sigma, use_index):
         g = epsm.group(pats)
         info = g.info()
         g.close()
-        if sigma == 2 and m <= 8:
+        if sigma == 2 and m <= 4:
             assert info["dense"] > 0, info
         if sigma == 256 and m >= 4:
             assert info["dense"] == 0, info
@@ -273,3 +273,70 @@ def test_group_dense_split_shards(epsm, dev):
     g.close()
     for j, w in enumerate(wants):
         assert np.array_equal(np.concatenate(parts[j]), w), j
+
+
+@pytest.mark.parametrize("use_index", [False, True])
+def test_group_dense_fanout_phases_and_caps(epsm, dev, use_index):
+    """Dense patterns are scanned once and their positions fanned out to every search of the
+    pattern: outputs of both 16-byte phases (one job per phase), capacities below occ, a
+    count-only slot (no output) -- every search still gets exactly its own Occ."""
+    rng = np.random.default_rng(410)
+    n = 13 * TILE + 77
+    t = rng.integers(0, 2, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    base = [t[s:s + 3].tobytes() for s in (5, 900, 7000)]
+    while len(set(base)) < 3:
+        base = [bytes(rng.integers(0, 2, size=3, dtype=np.uint8)) for _ in range(3)]
+    pats = [base[0]] * 6 + [base[1]] * 5 + [base[2]] * 3
+    wants = [oracle.search(p, t) for p in pats]
+    g = epsm.group(pats)
+    assert g.info()["dense"] == 3
+    ix = epsm.eq_index(td, g.index_values()) if use_index and g.index_values() else None
+    bufs = [torch.full((w.size + 8,), -4, dtype=torch.int64, device=dev) for w in wants]
+    outs = [b[j % 2:] for j, b in enumerate(bufs)]          # alternate 16-byte phases
+    caps = [w.size for w in wants]
+    caps[1] = wants[1].size // 3
+    caps[7] = 5
+    outs[4] = None                                           # count only
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    g.search_async(td, occ, outs=outs, caps=[c if o is not None else 0 for c, o in zip(caps, outs)], index=ix)
+    torch.cuda.synchronize()
+    for j, w in enumerate(wants):
+        assert int(occ[j]) == w.size, j
+        if outs[j] is None:
+            continue
+        c = min(w.size, caps[j])
+        got = outs[j][:c].cpu().numpy().astype(np.uint64)
+        assert np.array_equal(got, w[:c]), (j, got[:5], w[:5])
+        assert int(outs[j][c]) == -4, j                      # nothing past the capacity
+    g.close()
+
+
+@pytest.mark.parametrize("sigma", [2, 3, 4, 16, 100])
+def test_group_code_mode(epsm, dev, sigma):
+    """The code mode (every start keyed through the patterns' byte codes, exact): forced with
+    set_geometry(q, 0) wherever m * ceil(log2(distinct pattern bytes)) <= 14; bytes outside the
+    patterns' alphabet break windows; edges, duplicates and absent patterns as elsewhere."""
+    rng = np.random.default_rng(500 + sigma)
+    n = 7 * TILE + 1001
+    for m in (1, 2, 3, 4, 5, 7, 8, 12, 14):
+        t, pats = planted(rng, n, sigma, m, 25, absent=2)
+        sigp = len(set(b"".join(pats)))
+        cb = max(1, (sigp - 1).bit_length())
+        td = torch.from_numpy(t).to(dev)
+        if m * cb > 14:
+            g = epsm.group(pats).set_dense(0)
+            with pytest.raises(epsm.EpsmError):
+                g.set_geometry(m, 0)
+            g.close()
+            continue
+        check(pats, run_group(epsm, pats, td, geom=(m, 0)), t, ("code", sigma, m))
+
+
+def test_group_code_mode_chosen_for_dense_small_alphabets(epsm):
+    rng = np.random.default_rng(7)
+    t = rng.integers(0, 2, size=1 << 16, dtype=np.uint8)
+    pats = [t[s:s + 8].tobytes() for s in rng.integers(0, t.size - 8, size=100)]
+    g = epsm.group(pats).set_dense(5)          # none one by one at 1/256 per byte
+    assert g.info()["passes"] == [(8, 0)]
+    g.close()

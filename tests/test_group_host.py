@@ -52,6 +52,10 @@ def test_geometry_is_valid(sigma):
             info = epsm.group(pats).set_dense(0).info()
             assert info["distinct"] == len(set(pats))
             for q, sk in info["passes"]:
+                if sk == 0:                                      # code mode: m * code bits <= 14
+                    cb = max(1, (len(set(b"".join(pats))) - 1).bit_length())
+                    assert q == m and m * cb <= 14, (m, cb)
+                    continue
                 assert 1 <= q <= min(m, 16) and sk in (1, 2, 4, 8, 16)
                 assert sk + q - 1 <= m, (m, q, sk)               # one sample per window
                 assert sk * min(255, info["distinct"]) <= 4096
@@ -74,10 +78,20 @@ def test_set_geometry_validation():
     g = epsm.group([b"abcdefgh"] * 3)
     g.set_geometry(4, 4)
     assert g.info()["passes"] == [(4, 4)]
-    for q, sk in ((0, 1), (9, 1), (4, 3), (4, 8), (17, 1)):
+    for q, sk in ((0, 1), (9, 1), (4, 3), (4, 8), (17, 1), (8, 32)):
         with pytest.raises(epsm.EpsmError) as ei:
             g.set_geometry(q, sk)
         assert ei.value.code == epsm.EPSM_EINVAL
+    with pytest.raises(epsm.EpsmError):                       # 8 symbols x 8 bytes: 24 key bits
+        g.set_geometry(8, 0)
+    g.close()
+    g = epsm.group([b"abababab", b"bbbbaaaa"])
+    g.set_geometry(8, 0)                                      # the code mode (2 symbols: 8 key bits)
+    assert g.info()["passes"] == [(8, 0)]
+    g.close()
+    g = epsm.group([bytes(range(i, i + 16)) for i in range(0, 64, 16)])
+    with pytest.raises(epsm.EpsmError):                       # 64 symbols x 16 bytes: no code mode
+        g.set_geometry(16, 0)
     g.close()
 
 
