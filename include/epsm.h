@@ -73,8 +73,10 @@ typedef void *epsm_stream_t;              /* a cudaStream_t     */
  * PAPER.md:150-152).  Copies pattern[0..m-1] (1 <= m <= EPSM_MAX_M_LONG) into a
  * new plan, builds the broadcast words and selects the kernel variant for m
  * (m > 32: EPSMc's sampled block fingerprints with the naive check of each
- * candidate against the pattern in device memory; the plan
- * uploads the pattern on its first search).  No device work.  *out receives the
+ * candidate against the pattern in device memory, PAPER.md:576-603 -- for
+ * m >= 208 at EPSMc's own stride, one 16-byte block every (floor(m/16) - 1) * 16
+ * text bytes, so only part of the text is read; the plan
+ * uploads the pattern and its block table on its first search).  No device work.  *out receives the
  * plan (caller frees with epsm_plan_free).
  * Returns EPSM_OK, EPSM_EINVAL (NULL pattern/out, m = 0) or EPSM_EUNSUP
  * (m > EPSM_MAX_M_LONG).

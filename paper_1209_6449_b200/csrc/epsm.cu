@@ -385,19 +385,25 @@ static int ensure_plan_device(epsm_plan_t* plan, cudaStream_t s) {
     e = cudaMemcpyAsync(plan->d_desc, plan->h_desc, sizeof(epsm::JobDesc), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(plan descriptor)");
   }
-  if (plan->m > EPSM_MAX_M && !plan->d_pat) {   // long pattern: zero-padded words for the check
-    const size_t bytes = ((plan->m + 3) / 4 + 1) * sizeof(uint32_t);
-    cudaError_t e = cudaMalloc(&plan->d_pat, bytes);
-    if (e != cudaSuccess) {
-      plan->d_pat = nullptr;
-      epsm_set_error("cudaMalloc(pattern, %zu bytes): %s", bytes, cudaGetErrorString(e));
-      return EPSM_ENOMEM;
-    }
-    e = cudaMemcpyAsync(plan->d_pat, plan->pattern, bytes, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(pattern)");
-  }
+  if (plan->m > EPSM_MAX_M && !plan->d_pat) return epsm_upload_pattern(plan, s);
   return EPSM_OK;
 }
+
+// long patterns: the zero-padded pattern words in device memory (the naive check)
+int epsm_upload_pattern(epsm_plan_t* plan, cudaStream_t s) {
+  const size_t bytes = ((plan->m + 3) / 4 + 1) * sizeof(uint32_t);
+  cudaError_t e = cudaMalloc(&plan->d_pat, bytes);
+  if (e != cudaSuccess) {
+    plan->d_pat = nullptr;
+    epsm_set_error("cudaMalloc(pattern, %zu bytes): %s", bytes, cudaGetErrorString(e));
+    return EPSM_ENOMEM;
+  }
+  e = cudaMemcpyAsync(plan->d_pat, plan->pattern, bytes, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(pattern)");
+  return EPSM_OK;
+}
+
+static int launch_fanout(const epsm_job* jobs, uint32_t k, bool search, cudaStream_t s, epsm_workspace* ws);
 
 // Core launcher: k <= kMaxJobs searches of one pattern length over the device text
 // d_text[0..nbytes-1]; starts [0, nstarts) are reported (nstarts <= nbytes - m + 1), each
@@ -418,6 +424,17 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
       if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
     }
     return EPSM_OK;
+  }
+  if (!index && epsm_long_applies(plan0)) {
+    // long patterns at EPSMc's sampling stride: their own kernels, one search at a time
+    epsm_workspace* wsl = nullptr;
+    for (uint32_t j = 0; j < k; ++j) {
+      int rc = epsm_long_launch(jobs[j].plan, d_text, nbytes, nstarts, base, jobs[j].d_pos, jobs[j].cap,
+                                jobs[j].d_occ, search, s);
+      if (rc) return rc;
+    }
+    wsl = epsm_get_workspace(plan0->device, s);
+    return wsl ? launch_fanout(jobs, k, search, s, wsl) : EPSM_ENOMEM;
   }
   const uint64_t mis = reinterpret_cast<uintptr_t>(d_text) & 15u;
   epsm::KParams P;
@@ -566,7 +583,12 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
   ws->ctr_base[par] += gchunks + grid;
   ws->exit_total[par] += grid;
   ws->launches = L + 1;
-  // fan-out: occ and positions of a job to its further outputs (identical patterns)
+  return launch_fanout(jobs, k, search, s, ws);
+}
+
+// fan-out: occ and positions of a job to its further outputs (identical patterns)
+static int launch_fanout(const epsm_job* jobs, uint32_t k, bool search, cudaStream_t s, epsm_workspace* ws) {
+  cudaError_t e = cudaSuccess;
   for (uint32_t j = 0; j < k; ++j) {
     if (jobs[j].nx == 0) continue;
     const uint64_t have = (search && jobs[j].d_pos) ? jobs[j].cap : 0;
@@ -756,6 +778,8 @@ void epsm_plan_free(epsm_plan_t* plan) {
   if (plan->d_desc) cudaFree(plan->d_desc);
   delete plan->h_desc;
   if (plan->d_pat) cudaFree(plan->d_pat);
+  if (plan->d_long) cudaFree(plan->d_long);
+  delete plan->h_long;
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);
   if (plan->d_pos_buf) cudaFree(plan->d_pos_buf);

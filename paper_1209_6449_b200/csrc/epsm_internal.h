@@ -9,6 +9,7 @@
 namespace epsm {
 struct JobDesc;
 struct XOut;
+namespace lg { struct LongDesc; }
 namespace mp { struct JobOut; }
 }  // namespace epsm
 
@@ -16,6 +17,8 @@ struct epsm_plan_s {
   uint32_t m = 0;
   uint8_t pattern[EPSM_MAX_M_LONG] = {};
   uint32_t* d_pat = nullptr;  // m > 32: zero-padded pattern words in device memory
+  epsm::lg::LongDesc* h_long = nullptr;   // m >= 64: EPSMc table at the sampling stride (host)
+  epsm::lg::LongDesc* d_long = nullptr;   // ... and its device copy
   epsm::JobDesc* h_desc = nullptr;   // preprocessing (filter words, gram table), host copy
   epsm::JobDesc* d_desc = nullptr;   // ... and its device copy (uploaded on first search)
   int sk = 0, sq = 0;                // sampled-filter geometry (0: packed filter)
@@ -74,6 +77,10 @@ struct epsm_workspace {
   uint64_t m_work_cap = 0;
   epsm::mp::JobOut* m_jobs = nullptr;         // outputs of the searches of a pass
   uint64_t m_jobs_cap = 0;
+  uint32_t* l_counts = nullptr;               // long patterns: matches per chunk of samples
+  uint64_t l_counts_cap = 0;                  // (bytes)
+  unsigned long long* l_prefix = nullptr;     // ... and their exclusive prefix
+  uint64_t l_prefix_cap = 0;
   epsm::XOut* d_xout = nullptr;               // fan-out outputs of a batch call (device)
   uint64_t xout_cap = 0;                      // entries
   unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
@@ -113,6 +120,16 @@ int epsm_batch_run(epsm_plan_t* const* plans, uint32_t k, const uint32_t* slot, 
                    uint64_t owned_len, uint64_t base, uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps,
                    uint64_t* d_occ, bool search, cudaStream_t s, const epsm_eqidx_t* index,
                    const std::vector<std::vector<uint32_t>>* fan = nullptr);
+
+// Long patterns at EPSMc's sampling stride (epsm_long.cu): m >= kLongStrideMinM
+// (stride (floor(m/16) - 1) * 16 >= 192 bytes; a sample costs a 128-byte DRAM line, so below
+// that the full-text kernel is faster: B200, 1 GiB, us per search m=144 182 vs 158, m=256 112 vs 158).
+constexpr uint32_t kLongStrideMinM = 208;
+uint32_t epsm_long_stride(uint32_t m);
+bool epsm_long_applies(const epsm_plan_t* plan);
+int epsm_long_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
+                     uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s);
+int epsm_upload_pattern(epsm_plan_t* plan, cudaStream_t s);
 
 // Equality-mask index of one text (epsm_eqidx_build_async).
 struct epsm_eqidx_s {

@@ -533,3 +533,54 @@ def test_range_calls_reject_a_short_overlap(epsm, dev):
     epsm.search_range_batch_async([epsm.plan(b"\x00" * 32)], shard, 1000, 0, n_total, occ)
     torch.cuda.synchronize()
     assert int(occ[0]) == 1000
+
+
+@pytest.mark.parametrize("m", [64, 144, 207, 208, 209, 256, 1000, 4096])
+def test_long_stride_path(epsm, dev, m):
+    """m >= 64: EPSMc's sampling stride (one 16-byte block every (floor(m/16) - 1) * 16 bytes,
+    PAPER.md:600-601) -- planted occurrences at every phase relative to the sampled blocks and
+    at both ends, periodic texts (many candidates per block), the batch API with caps and
+    count-only searches, shards with an (m-1)-byte halo, misaligned texts."""
+    from paper_1209_6449_b200 import sharding
+    rng = np.random.default_rng(7000 + m)
+    L = 16 * (m // 16 - 1)
+    n = max(40 * m, 3 * 2048 * L // 8 + 777)
+    t = rng.integers(0, 4, size=n, dtype=np.uint8)
+    p = rng.integers(0, 4, size=m, dtype=np.uint8)
+    step = (m // L + 2) * L                                   # planted windows never overlap
+    starts = [0, n - m] + [(j + 1) * step + ph for j, ph in enumerate((0, 1, 15, 16, L - 1, L // 2))
+                           if (j + 1) * step + ph + m <= n - m]
+    for s in starts:
+        t[s:s + m] = p
+    td = torch.from_numpy(t).to(dev)
+    want = oracle.search(p.tobytes(), t)
+    assert set(starts) <= set(want.tolist())
+    check(epsm, p.tobytes(), t, td, label=f"stride m={m}")
+    assert epsm.count(p.tobytes(), td) == want.size
+    # periodic: every start matches a^m-like patterns with period 3
+    per = np.tile(np.array([1, 2, 3], np.uint8), n // 3 + 1)[:n]
+    check(epsm, per[5:5 + m].tobytes(), per, torch.from_numpy(per).to(dev), label=f"stride periodic m={m}")
+    # batch API: caps, count-only, an absent pattern, the same pattern twice
+    plans = [epsm.plan(p.tobytes()), epsm.plan(p.tobytes()), epsm.plan(bytes(9 for _ in range(m)))]
+    occ = torch.zeros(3, dtype=torch.int64, device=dev)
+    outs = [torch.full((want.size + 2,), -1, dtype=torch.int64, device=dev) for _ in range(3)]
+    epsm.search_batch_async(plans, td, occ, outs=outs, caps=[want.size + 2, 3, 5])
+    torch.cuda.synchronize()
+    assert occ.tolist() == [want.size, want.size, 0]
+    assert np.array_equal(outs[0][:want.size].cpu().numpy().astype(np.uint64), want)
+    assert np.array_equal(outs[1][:3].cpu().numpy().astype(np.uint64), want[:3]) and int(outs[1][3]) == -1
+    # shards with an (m-1)-byte halo
+    parts = []
+    for r in range(3):
+        base, owned, slen = sharding.shard_layout(n, 3, r, halo=m - 1)
+        o = torch.zeros(1, dtype=torch.int64, device=dev)
+        out = torch.empty(want.size + 1, dtype=torch.int64, device=dev)
+        epsm.search_range_async(plans[0], td[base:base + slen].clone(), owned, base, n, out, o)
+        torch.cuda.synchronize()
+        parts.append(out[:int(o)].cpu().numpy().astype(np.uint64))
+    assert np.array_equal(np.concatenate(parts), want)
+    # misaligned views
+    for off in (1, 7):
+        check(epsm, p.tobytes(), t[off:], td[off:], label=f"stride misaligned m={m} off={off}")
+    for pl in plans:
+        pl.close()
