@@ -516,7 +516,9 @@ def run_epsm(args, world, rank, local):
                                    "note": "n + 8*occ per search as SURVEY 8(d) writes it: every search "
                                            "counted as a full text pass, so frac > 1 where searches share "
                                            "one pass or read planes -- not HBM evidence"},
-                     "traffic_unit": (tf or {}).get("unit")},
+                     "traffic_unit": (tf or {}).get("unit"),
+                     "dominant_kernel": (tf or {}).get("dominant"),
+                     "kernel_shares_ncu": {k: v.get("share") for k, v in ((tf or {}).get("kernels") or {}).items()}},
         "clocks": clocks,
         "gpu_launches": int(launches),
         "total_occ_per_step": int(occ_g.sum()),
