@@ -566,12 +566,28 @@ static void group_split(epsm_group_t* g, int log2) {
   const double others = static_cast<double>(g->k - 1) * g->m;
   g->sparse.clear();
   g->dense.clear();
+  std::vector<double> rate(g->D, 0.0);
+  double lsum = 0;
+  uint32_t lcnt = 0;
   for (uint32_t d = 0; d < g->D; ++d) {
     double own[256] = {};
     for (unsigned char ch : g->pats[d]) own[ch] += 1.0;
-    double rate = others > 0 ? 1.0 : 0.0;
-    for (unsigned char ch : g->pats[d]) rate *= others > 0 ? (cnt[ch] - own[ch]) / others : 0.0;
-    (log2 < 1024 && rate >= thresh ? g->dense : g->sparse).push_back(d);
+    double r = others > 0 ? 1.0 : 0.0;
+    for (unsigned char ch : g->pats[d]) r *= others > 0 ? (cnt[ch] - own[ch]) / others : 0.0;
+    rate[d] = r;
+    if (r > 0) {
+      lsum += std::log2(r);
+      ++lcnt;
+    }
+  }
+  // the estimates of one group scatter (a handful of sampled bytes per symbol): a pattern within
+  // 8x of the group's geometric mean takes the mean, so that a uniform text's patterns, which
+  // have one common rate, are split the same way; outliers keep their own estimate
+  const double gmean = lcnt ? std::exp2(lsum / lcnt) : 0.0;
+  for (uint32_t d = 0; d < g->D; ++d) {
+    double r = rate[d];
+    if (r > 0 && gmean > 0 && std::fabs(std::log2(r / gmean)) <= 3.0) r = gmean;
+    (log2 < 1024 && r >= thresh ? g->dense : g->sparse).push_back(d);
   }
 }
 

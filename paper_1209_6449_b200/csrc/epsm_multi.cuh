@@ -178,6 +178,8 @@ struct __align__(128) MSmem {
   uint32_t done[kStages];                            // pass 1: warps finished with the stage
   unsigned long long lm[kConsumerWarps][32];         // lane match masks of a slice (list path)
   uint32_t rbuf[kConsumerWarps][32];                 // pass 3: a round of 32 matches (offset | id << 16)
+  uint64_t* opos[kMaxD + 1];                         // pass 3: the first output of each pattern ...
+  uint64_t ocap[kMaxD + 1];                          // ... and its capacity (0: none)
   alignas(8) uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t gfull;
@@ -333,6 +335,16 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
   const uint32_t seg = cw * kSliceBytes + lane * kSegBytes;    // the lane's 64 starts in a tile
   const uint32_t lt = (1u << lane) - 1u;
   mbar_wait(&S.gfull, 0);
+  if constexpr (WRITE) {
+    // the first output of every pattern, out of the job table (global) into shared memory: the
+    // store of a match then needs no dependent global load
+    for (uint32_t d = tid - 32; d < P.D; d += 32 * kConsumerWarps) {
+      const JobOut J = P.jobs[S.g.dup_list[S.g.dup_off[d]]];
+      S.opos[d] = J.pos;
+      S.ocap[d] = J.pos ? J.cap : 0;
+    }
+    bar_consumers();
+  }
   const GroupDesc& G = S.g;
   uint32_t stage = 0, phase = 0;
   uint8_t* const ids = S.ids[cw];
@@ -603,8 +615,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
           if (act) {
             const uint64_t pos = cbase + 32 * b + lane;
+            if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);
             const uint32_t j1 = G.dup_off[id + 1];
-            for (uint32_t q = G.dup_off[id]; q < j1; ++q) {
+            for (uint32_t q = G.dup_off[id] + 1; q < j1; ++q) {   // (further searches of the pattern)
               const JobOut J = P.jobs[G.dup_list[q]];
               if (g < J.cap) st_stream_u64(J.pos + g, pos);
             }
@@ -634,8 +647,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
         if (act) {
           const uint64_t pos = cbase + (e & 0xFFFFu);
+          if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);
           const uint32_t j1 = G.dup_off[id + 1];
-          for (uint32_t q = G.dup_off[id]; q < j1; ++q) {
+          for (uint32_t q = G.dup_off[id] + 1; q < j1; ++q) {
             const JobOut J = P.jobs[G.dup_list[q]];
             if (g < J.cap) st_stream_u64(J.pos + g, pos);
           }
