@@ -57,6 +57,11 @@ constexpr int kMaxJobs = 1024;                    // searches per group
 constexpr int kListCap = 256;                     // (offset, id) entries kept per chunk
 constexpr int kMaxPW = 8;                         // pattern words (m <= 32)
 constexpr int kCodeKeyBits = 14;                  // code mode: m * (bits per symbol) <= 14
+constexpr int kIdsLane = kSegBytes + 4;           // ids of one lane (padded: bank-conflict-free)
+constexpr int kIdsWarp = 32 * kIdsLane;
+__host__ __device__ constexpr uint32_t id_slot(uint32_t so) {   // slice offset -> ids index
+  return (so / kSegBytes) * kIdsLane + so % kSegBytes;
+}
 static_assert(kSegBytes * 32 * kConsumerWarps == kTile, "lanes tile the chunk");
 
 // The group's preprocessing (built on the host, copied into shared memory once per CTA).
@@ -170,7 +175,9 @@ __device__ __forceinline__ uint32_t hash_words(const uint32_t (&k)[4], const MPa
 struct __align__(128) MSmem {
   uint8_t ring[kStages][kStageBytes];
   GroupDesc g;
-  uint8_t ids[kConsumerWarps][kSliceBytes];           // id of the pattern at each start, kNoId
+  uint8_t ids[kConsumerWarps][kIdsWarp];             // id of the pattern at each start, kNoId
+                                                     // (lane l's 64 starts at l * 68: a lane stride of
+                                                     // 17 words keeps the lanes' stores conflict-free)
   uint16_t hist[kConsumerWarps][kMaxD + 1];          // per-slice counts -> exclusive offsets
   unsigned long long pre[kMaxD + 1];                 // pass 3: the chunk's global prefix
   uint32_t ccnt[kStages][kMaxD + 1];                 // pass 1: chunk counts (by stage)
@@ -261,8 +268,8 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
     fence_mbar_init();
   }
   // ids start empty; chunk counters zero
-  for (uint32_t i = tid; i < kConsumerWarps * kSliceBytes / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(&S.ids[0][0])[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  for (uint32_t i = tid; i < kConsumerWarps * kIdsWarp / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(&S.ids[0][0])[i] = make_uint4(~0u, ~0u, ~0u, ~0u);   // (kIdsWarp % 16 == 0)
   for (uint32_t i = tid; i < kStages * (kMaxD + 1); i += blockDim.x) (&S.ccnt[0][0])[i] = 0;
   for (uint32_t i = tid; i < kConsumerWarps * (kMaxD + 1); i += blockDim.x) (&S.hist[0][0])[i] = 0;
   if (!WRITE && blockIdx.x == 0 && tid == 0) P.work[0] = 0;   // (the scan appends; runs after)
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       for (uint32_t e = tid - 32; e < len; e += 32 * kConsumerWarps) {
         const uint32_t v = L[e];
         const uint32_t off = v & 0xFFFFu, d = v >> 16;
-        S.ids[off / kSliceBytes][off % kSliceBytes] = static_cast<uint8_t>(d);
+        S.ids[off / kSliceBytes][id_slot(off % kSliceBytes)] = static_cast<uint8_t>(d);
         atomicOr(&S.lm[off / kSliceBytes][(off % kSliceBytes) / kSegBytes], 1ull << (off % kSegBytes));
       }
       bar_consumers();
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         // per-position compare for all patterns at once, without a naive check.
         // Every start of the lane gets its id (0xFF: none) -- no stale ids -- and bit t of
         // E marks the window ENDING at byte t (compile-time bit positions).
-        uint8_t* const idb = ids + lane * kSegBytes;
+        uint8_t* const idb = ids + lane * kIdsLane;
         if (!WRITE && c >= P.it_lo && c < P.it_hi) {
           // pass 1 over an interior chunk: count straight into the chunk's counters (no ids,
           // no list: the chunk is re-filtered by pass 3)
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
             }
             MP_CHECK(st < static_cast<uint32_t>(kTile + 64), "st", st, o);
             if (verify_window(ts, st, G, d, P.mw)) {
-              ids[lane * kSegBytes + (o - i)] = static_cast<uint8_t>(d);
+              ids[lane * kIdsLane + (o - i)] = static_cast<uint8_t>(d);
               M |= 1ull << (o - i);
             }
           }
@@ -511,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       if (lane >= static_cast<uint32_t>(o)) incl += y;
     }
     const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);       // matches of the slice
-    uint8_t* const idl = ids + lane * kSegBytes;
+    uint8_t* const idl = ids + lane * kIdsLane;
 
     if constexpr (!WRITE) {
       // ---- pass 1: counts per distinct pattern (per-match shared atomics), and the chunk's
@@ -605,8 +612,9 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         while (nbm) {
           const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
           nbm &= nbm - 1;
-          const uint32_t id = ids[32 * b + lane];
-          ids[32 * b + lane] = kNoId;
+          uint8_t* const ib = ids + (b >> 1) * kIdsLane + 32 * (b & 1u) + lane;   // slice start 32b + lane
+          const uint32_t id = *ib;
+          *ib = kNoId;
           const uint32_t peers = __match_any_sync(0xffffffffu, id);
           const bool act = id != kNoId;
           uint64_t g = 0;
