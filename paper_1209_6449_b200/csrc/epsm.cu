@@ -588,10 +588,19 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
 
 // fan-out: occ and positions of a job to its further outputs (identical patterns)
 static int launch_fanout(const epsm_job* jobs, uint32_t k, bool search, cudaStream_t s, epsm_workspace* ws) {
-  cudaError_t e = cudaSuccess;
   for (uint32_t j = 0; j < k; ++j) {
     if (jobs[j].nx == 0) continue;
-    const uint64_t have = (search && jobs[j].d_pos) ? jobs[j].cap : 0;
+    int rc = epsm_replicate(jobs[j].d_pos, jobs[j].cap, jobs[j].d_occ, jobs[j].x, jobs[j].nx, search, s, ws);
+    if (rc) return rc;
+  }
+  return EPSM_OK;
+}
+
+int epsm_replicate(const uint64_t* d_pos, uint64_t cap, const unsigned long long* d_occ, const epsm::XOut* x,
+                   uint32_t nx, bool search, cudaStream_t s, epsm_workspace* ws) {
+  cudaError_t e = cudaSuccess;
+  {
+    const uint64_t have = (search && d_pos) ? cap : 0;
     static bool rep_attr = false;
     if (!rep_attr) {
       e = cudaFuncSetAttribute(epsm::epsm_replicate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -601,14 +610,17 @@ static int launch_fanout(const epsm_job* jobs, uint32_t k, bool search, cudaStre
     }
     // (grid sized by the capacity; CTAs past the occ's chunks exit at once)
     const uint64_t chunks = (have + epsm::kRepChunk / 8 - 1) / (epsm::kRepChunk / 8);
-    const unsigned blocks = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(2ull * ws->num_sms, chunks)));
-    for (uint32_t a = 0; a < jobs[j].nx; a += epsm::kRepMaxOut) {
-      const uint32_t nxa = std::min<uint32_t>(jobs[j].nx - a, epsm::kRepMaxOut);
+#ifndef EPSM_REP_CTAS_PER_SM
+#define EPSM_REP_CTAS_PER_SM 2
+#endif
+    const unsigned blocks = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>(EPSM_REP_CTAS_PER_SM * static_cast<uint64_t>(ws->num_sms), chunks)));
+    for (uint32_t a = 0; a < nx; a += epsm::kRepMaxOut) {
+      const uint32_t nxa = std::min<uint32_t>(nx - a, epsm::kRepMaxOut);
       epsm::epsm_replicate_kernel<<<blocks, epsm::kRepThreads, sizeof(epsm::RepSmem), s>>>(
-          search ? jobs[j].d_pos : nullptr, jobs[j].d_occ, have, jobs[j].x + a, nxa);
+          search ? d_pos : nullptr, d_occ, have, x + a, nxa);
       epsm_count_launch();
     }
-    epsm_count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_replicate_kernel launch");
   }

@@ -130,6 +130,10 @@ bool epsm_long_applies(const epsm_plan_t* plan);
 int epsm_long_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
                      uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s);
 int epsm_upload_pattern(epsm_plan_t* plan, cudaStream_t s);
+// occ and the first min(occ, cap_o) positions of d_pos (capacity cap) to nx further outputs x
+// (device XOut table), on stream s
+int epsm_replicate(const uint64_t* d_pos, uint64_t cap, const unsigned long long* d_occ, const epsm::XOut* x,
+                   uint32_t nx, bool search, cudaStream_t s, epsm_workspace* ws);
 
 // Equality-mask index of one text (epsm_eqidx_build_async).
 struct epsm_eqidx_s {

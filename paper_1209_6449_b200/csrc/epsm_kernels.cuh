@@ -159,14 +159,6 @@ __host__ __device__ constexpr uint32_t plane_tps(int sk) {
 __host__ __device__ constexpr uint32_t plane_stride(int sk) { return plane_tps(sk) * (kTile / 8) + 16; }
 static_assert(sizeof(JobDesc) == kJobHeader + 4 * kGramTab, "JobDesc layout");
 
-// A further output of a search (fan-out: identical patterns of a batch share one scan, and
-// the replicate kernel below copies the positions and occ to each of them).
-struct XOut {
-  uint64_t* pos;                // output positions
-  uint64_t cap;                 // capacity of pos (<= the source's capacity)
-  unsigned long long* occ;      // device occ
-};
-
 // One search of a launch: its preprocessing and its outputs.
 struct JobRef {
   const JobDesc* desc;          // device copy of the plan's preprocessing
@@ -1575,9 +1567,18 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_scan_kernel(const __grid_con
 // interleaved destinations reached only ~3.3 TB/s.  Outputs of another 16-byte phase than
 // the source (never produced by the library's own callers) take 8-byte stores from shared
 // memory.
-constexpr uint32_t kRepChunk = 32768;                              // bytes per chunk
-constexpr int kRepStages = 3;
-constexpr uint32_t kRepMaxOut = 1024;
+#ifndef EPSM_REP_CHUNK
+#define EPSM_REP_CHUNK 32768
+#endif
+#ifndef EPSM_REP_STAGES
+#define EPSM_REP_STAGES 3
+#endif
+#ifndef EPSM_REP_MAXOUT
+#define EPSM_REP_MAXOUT 1024
+#endif
+constexpr uint32_t kRepChunk = EPSM_REP_CHUNK;                     // bytes per chunk
+constexpr int kRepStages = EPSM_REP_STAGES;
+constexpr uint32_t kRepMaxOut = EPSM_REP_MAXOUT;
 constexpr int kRepThreads = 128;
 struct RepSmem {
   uint64_t buf[kRepStages][kRepChunk / 8];

@@ -20,6 +20,13 @@ namespace {
 
 // One pass over the text serves at most kMaxD distinct patterns (u8 ids in shared memory);
 // a group of more is split into subgroups (one pass each).
+struct RepJob {                        // a pattern with duplicate searches: its first output ...
+  uint64_t* pos;
+  uint64_t cap;
+  unsigned long long* occ;
+  uint32_t nx;                         // ... and the number of further outputs (rep_x, in order)
+};
+
 struct Subgroup {
   uint32_t D = 0, k = 0;               // distinct patterns, searches
   int q = 1, sk = 1, qw = 1;           // sk = 0: code mode (every start keyed, exact)
@@ -29,6 +36,8 @@ struct Subgroup {
   mp::GroupDesc* h_desc = nullptr;
   mp::GroupDesc* d_desc = nullptr;
   double cost = 0;                     // model estimate (instructions per 64 text bytes)
+  std::vector<RepJob> rep_jobs;        // per call: duplicate searches to copy after pass 3
+  std::vector<epsm::XOut> rep_x;
 };
 
 constexpr uint32_t kMul[4] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du, 0x27D4EB2Fu};
@@ -408,6 +417,33 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
       jt[j].pos = d_pos ? d_pos[gj] : nullptr;
       jt[j].cap = (d_pos && d_pos[gj] && caps) ? caps[gj] : 0;
     }
+    // pass 3 writes each pattern's FIRST output only (the largest capacity: the outputs are
+    // swapped among the pattern's searches -- their occ is the same); the others are copied from
+    // it afterwards by the replicate kernel (fan-out, like the dense patterns' searches)
+    const mp::GroupDesc& Gh = *S.h_desc;
+    std::vector<epsm::XOut> xo;
+    std::vector<std::pair<uint32_t, uint32_t>> rep;   // (first local job, number of further outputs)
+    for (uint32_t d = 0; d < S.D; ++d) {
+      const uint32_t a = Gh.dup_off[d], b = Gh.dup_off[d + 1];
+      if (b - a < 2) continue;
+      uint32_t best = a;
+      for (uint32_t q = a + 1; q < b; ++q)
+        if (jt[Gh.dup_list[q]].cap > jt[Gh.dup_list[best]].cap) best = q;
+      std::swap(jt[Gh.dup_list[a]], jt[Gh.dup_list[best]]);
+      rep.emplace_back(Gh.dup_list[a], b - a - 1);
+      for (uint32_t q = a + 1; q < b; ++q) {
+        const mp::JobOut& J = jt[Gh.dup_list[q]];
+        xo.push_back(epsm::XOut{J.cap ? J.pos : nullptr, J.cap,
+                                reinterpret_cast<unsigned long long*>(d_occ + Gh.job_g[Gh.dup_list[q]])});
+      }
+    }
+    S.rep_jobs.clear();
+    for (const auto& r : rep) {
+      const mp::JobOut& J = jt[r.first];
+      S.rep_jobs.push_back(RepJob{J.pos, J.cap, reinterpret_cast<unsigned long long*>(d_occ + Gh.job_g[r.first]),
+                                  r.second});
+    }
+    S.rep_x = xo;
     cudaError_t e = cudaMemcpyAsync(ws->m_jobs, jt.data(), S.k * sizeof(mp::JobOut), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(group job table)");
     P.jobs = ws->m_jobs;
@@ -446,6 +482,31 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   epsm_count_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_kernel (pass 3) launch");
+  if (!S.rep_x.empty()) {
+    // duplicate searches: copies of their pattern's first output (one replicate per pattern)
+    if (S.rep_x.size() > ws->xout_cap) {
+      if (ws->d_xout) {
+        cudaStreamSynchronize(s);
+        cudaFree(ws->d_xout);
+        ws->d_xout = nullptr;
+        ws->xout_cap = 0;
+      }
+      e = cudaMalloc(&ws->d_xout, S.rep_x.size() * sizeof(epsm::XOut));
+      if (e != cudaSuccess) {
+        epsm_set_error("cudaMalloc(fan-out table): %s", cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
+      ws->xout_cap = S.rep_x.size();
+    }
+    e = cudaMemcpyAsync(ws->d_xout, S.rep_x.data(), S.rep_x.size() * sizeof(epsm::XOut), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out table)");
+    uint64_t off = 0;
+    for (const RepJob& r : S.rep_jobs) {
+      rc = epsm_replicate(r.pos, r.cap, r.occ, ws->d_xout + off, r.nx, true, s, ws);
+      if (rc) return rc;
+      off += r.nx;
+    }
+  }
   return EPSM_OK;
 }
 

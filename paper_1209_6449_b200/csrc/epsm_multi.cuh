@@ -623,12 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
           if (act) {
             const uint64_t pos = cbase + 32 * b + lane;
-            if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);
-            const uint32_t j1 = G.dup_off[id + 1];
-            for (uint32_t q = G.dup_off[id] + 1; q < j1; ++q) {   // (further searches of the pattern)
-              const JobOut J = P.jobs[G.dup_list[q]];
-              if (g < J.cap) st_stream_u64(J.pos + g, pos);
-            }
+            if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);   // (duplicates: copied after)
           }
           __syncwarp();
         }
@@ -655,12 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
         if (act) {
           const uint64_t pos = cbase + (e & 0xFFFFu);
-          if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);
-          const uint32_t j1 = G.dup_off[id + 1];
-          for (uint32_t q = G.dup_off[id] + 1; q < j1; ++q) {
-            const JobOut J = P.jobs[G.dup_list[q]];
-            if (g < J.cap) st_stream_u64(J.pos + g, pos);
-          }
+          if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);   // (duplicates: copied after)
         }
         __syncwarp();                                  // (the round buffer is refilled next)
       }

@@ -162,4 +162,12 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 // ... and has completed (writes visible)
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// A further output of a search (fan-out: identical patterns share one scan; the replicate
+// kernel copies the positions and occ to each of them).
+struct XOut {
+  uint64_t* pos;                // output positions
+  uint64_t cap;                 // capacity of pos (<= the source's capacity)
+  unsigned long long* occ;      // device occ
+};
+
 }  // namespace epsm
