@@ -15,12 +15,14 @@ n = 256 * synth.MiB
 t = synth.text_torch(synth.raw_sigma_spec(s, (2, s)), 0, n, device=dev)
 pats, _ = synth.extract_patterns_torch(t, (2, s, m), m, 100)
 g = epsm.group(pats)
+vals = g.index_values()
+ix = epsm.eq_index(t, vals) if vals else None
 occ = torch.zeros(100, dtype=torch.int64, device=dev)
-g.count_async(t, occ)
+g.count_async(t, occ, index=ix)
 torch.cuda.synchronize()
 cap = int(occ.max()) + 1
 outs = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in range(100)]
 for _ in range(reps):
-    g.search_async(t, occ, outs=outs)
+    g.search_async(t, occ, outs=outs, index=ix)
 torch.cuda.synchronize()
 print("info", g.info(), "occ total", int(occ.sum()))
