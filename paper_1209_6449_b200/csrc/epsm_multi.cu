@@ -13,6 +13,7 @@
 #include "epsm.h"
 #include "epsm_internal.h"
 #include "epsm_multi.cuh"
+#include "epsm_mask.cuh"
 
 namespace mp = epsm::mp;
 
@@ -531,6 +532,135 @@ static int group_bind(epsm_group_t* g, const void* dptr) {
   return EPSM_OK;
 }
 
+constexpr uint32_t kMaskMinPatterns = 24;
+
+// EPSM_MASK=0: the dense patterns keep the one-by-one scans (A/B)
+static bool mask_disabled() {
+  static const bool v = [] {
+    const char* e = getenv("EPSM_MASK");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+
+// The dense patterns of a group in ONE pass over the index (epsm_mask.cuh) when they fit: m <= 8,
+// <= 64 patterns, <= 8 distinct bytes, all in the index, m * bytes <= 16.  Each pattern's
+// largest-capacity search gets the positions, its other searches a copy (replicate kernel).
+// Returns 1 when the set does not fit (the caller scans the patterns one by one).
+static int mask_run(epsm_group_t* g, const epsm_eqidx_t* index, const uint8_t* d_text, uint64_t n, uint64_t ns,
+                    uint64_t base, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
+                    cudaStream_t s) {
+  namespace mk = epsm::mk;
+  const uint32_t D = static_cast<uint32_t>(g->dense.size());
+  // (only for many dense patterns: a few are faster one by one, their scans write the bulk of
+  // their positions with staged 16-byte stores -- sigma=2 m=4, 16 patterns: 4.0 ms either way;
+  // sigma=8 m=2, 50 patterns: 2.8 vs 3.8 ms)
+  if (mask_disabled() || D < kMaskMinPatterns || D > static_cast<uint32_t>(mk::kMaxD) ||
+      g->m > static_cast<uint32_t>(mk::kMaxM))
+    return 1;
+  if (reinterpret_cast<uintptr_t>(d_text) & 15u) return 1;
+  int slot_of[256];
+  for (int& v : slot_of) v = -1;
+  uint32_t nval = 0, pid[mk::kMaxVals];
+  for (uint32_t d : g->dense)
+    for (unsigned char ch : g->pats[d])
+      if (slot_of[ch] < 0) {
+        if (nval == static_cast<uint32_t>(mk::kMaxVals) || index->plane_of[ch] < 0) return 1;
+        pid[nval] = static_cast<uint32_t>(index->plane_of[ch]);
+        slot_of[ch] = static_cast<int>(nval++);
+      }
+  if (g->m * nval > static_cast<uint32_t>(mk::kMaxSh)) return 1;
+  mk::MaskParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.planes = index->d_planes;
+  P.pstride = index->pstride;
+  P.nval = nval;
+  P.m = g->m;
+  P.D = D;
+  for (uint32_t v = 0; v < nval; ++v) P.pid[v] = pid[v];
+  P.nstarts = ns;
+  P.pos_bias = base;
+  P.nwords = (ns + 63) / 64;
+  P.ntasks = (P.nwords + mk::kTaskWords - 1) / mk::kTaskWords;
+  // outputs: per pattern the largest-capacity search first, the others fanned out afterwards
+  std::vector<epsm::XOut> xo;
+  std::vector<std::pair<uint32_t, uint32_t>> rep;   // (pattern, further outputs)
+  for (uint32_t k = 0; k < D; ++k) {
+    const uint32_t d = g->dense[k];
+    for (uint32_t i = 0; i < g->m; ++i)
+      P.sh[k][i] = static_cast<uint8_t>(i * nval + slot_of[static_cast<unsigned char>(g->pats[d][i])]);
+    const auto& js = g->dups[d];
+    uint32_t best = js[0];
+    auto capof = [&](uint32_t j) -> uint64_t { return (search && d_pos && d_pos[j] && caps) ? caps[j] : 0; };
+    for (uint32_t j : js)
+      if (capof(j) > capof(best)) best = j;
+    P.pos[k] = capof(best) ? d_pos[best] : nullptr;
+    P.cap[k] = capof(best);
+    P.occ[k] = reinterpret_cast<unsigned long long*>(d_occ + best);
+    uint32_t nx = 0;
+    for (uint32_t j : js) {
+      if (j == best) continue;
+      xo.push_back(epsm::XOut{capof(j) ? d_pos[j] : nullptr, capof(j), reinterpret_cast<unsigned long long*>(d_occ + j)});
+      ++nx;
+    }
+    if (nx) rep.emplace_back(k, nx);
+  }
+  epsm_workspace* ws = epsm_get_workspace(g->device, s);
+  if (!ws) return EPSM_ENOMEM;
+  if (ws->num_sms <= 0) {
+    cudaError_t e = cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, g->device);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  }
+  int rc = ensure_multi_ws(ws, P.ntasks, D, s);
+  if (rc) return rc;
+  P.counts = ws->m_counts;
+  P.prefix = ws->m_prefix;
+  if (ns == 0) {
+    for (uint32_t k = 0; k < D; ++k) {
+      cudaError_t e = cudaMemsetAsync(P.occ[k], 0, 8, s);
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemsetAsync(occ)");
+    }
+  } else {
+    const unsigned grid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((P.ntasks + mk::kWarps - 1) / mk::kWarps, 4ull * ws->num_sms)));
+    mk::epsm_mask_count_kernel<<<grid, mk::kThreads, 0, s>>>(P);
+    epsm_count_launch();
+    mk::epsm_mask_scan_kernel<<<D, 1024, 0, s>>>(P);
+    epsm_count_launch();
+    if (search) {
+      mk::epsm_mask_write_kernel<<<grid, mk::kThreads, 0, s>>>(P);
+      epsm_count_launch();
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "mask kernels launch");
+  }
+  if (!xo.empty()) {
+    if (xo.size() > ws->xout_cap) {
+      if (ws->d_xout) {
+        cudaStreamSynchronize(s);
+        cudaFree(ws->d_xout);
+        ws->d_xout = nullptr;
+        ws->xout_cap = 0;
+      }
+      cudaError_t e = cudaMalloc(&ws->d_xout, xo.size() * sizeof(epsm::XOut));
+      if (e != cudaSuccess) {
+        epsm_set_error("cudaMalloc(fan-out table): %s", cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
+      ws->xout_cap = xo.size();
+    }
+    cudaError_t e = cudaMemcpyAsync(ws->d_xout, xo.data(), xo.size() * sizeof(epsm::XOut), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out table)");
+    uint64_t off = 0;
+    for (const auto& r : rep) {
+      rc = epsm_replicate(P.pos[r.first], P.cap[r.first], P.occ[r.first], ws->d_xout + off, r.second, search, s, ws);
+      if (rc) return rc;
+      off += r.second;
+    }
+  }
+  return 0;
+}
+
 static int group_run(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_t owned_len, uint64_t base,
                      uint64_t n_total, uint64_t* const* d_pos, const uint64_t* caps, uint64_t* d_occ, bool search,
                      epsm_stream_t stream, const epsm_eqidx_t* index) {
@@ -564,6 +694,10 @@ static int group_run(epsm_group_t* g, const uint8_t* d_text, uint64_t n, uint64_
   for (auto& S : g->subs) {
     rc = subgroup_launch(g, S, d_text, n, ns, base, d_pos, caps, d_occ, search, s);
     if (rc) return rc;
+  }
+  if (!g->dense.empty() && index) {
+    rc = mask_run(g, index, d_text, n, ns, base, d_pos, caps, d_occ, search, s);
+    if (rc != 1) return rc;          // done (or an error); 1: the dense set does not fit the mask pass
   }
   if (!g->dense.empty()) {
     // the dense patterns: one single-pattern scan per distinct pattern (over the index where it

@@ -340,3 +340,56 @@ def test_group_code_mode_chosen_for_dense_small_alphabets(epsm):
     g = epsm.group(pats).set_dense(5)          # none one by one at 1/256 per byte
     assert g.info()["passes"] == [(8, 0)]
     g.close()
+
+
+@pytest.mark.parametrize("sigma,m", [(8, 2), (6, 2), (3, 3), (2, 5)])
+def test_group_mask_pass(epsm, dev, sigma, m):
+    """>= 24 dense patterns over an index: the mask pass (all dense patterns' shift-ANDs over the
+    planes in one pass, epsm_mask.cuh) -- every search exact, with duplicates (copied by the
+    replicate kernel), capacities, count-only, misaligned outputs and shards."""
+    from paper_1209_6449_b200 import sharding
+    rng = np.random.default_rng(600 + 10 * sigma + m)
+    n = 21 * TILE + 301
+    t = rng.integers(0, sigma, size=n, dtype=np.uint8)
+    td = torch.from_numpy(t).to(dev)
+    grams = sorted({t[s:s + m].tobytes() for s in range(0, n - m, 7)})
+    pats = grams[:40] + grams[:5] + [bytes([0] * (m - 1) + [200])]      # dups and an absent one
+    wants = [oracle.search(p, t) for p in pats]
+    g = epsm.group(pats)
+    info = g.info()
+    assert info["dense"] >= 24, info
+    ix = epsm.eq_index(td, g.index_values())
+    bufs = [torch.full((w.size + 6,), -2, dtype=torch.int64, device=dev) for w in wants]
+    outs = [b[j % 2:] for j, b in enumerate(bufs)]
+    caps = [w.size for w in wants]
+    caps[3] = wants[3].size // 2
+    caps[len(pats) - 2] = 1
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    g.search_async(td, occ, outs=outs, caps=caps, index=ix)
+    torch.cuda.synchronize()
+    for j, w in enumerate(wants):
+        assert int(occ[j]) == w.size, (j, int(occ[j]), w.size)
+        c = min(w.size, caps[j])
+        assert np.array_equal(outs[j][:c].cpu().numpy().astype(np.uint64), w[:c]), j
+        assert int(outs[j][c]) == -2, j
+    occ2 = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    g.count_async(td, occ2, index=ix)
+    torch.cuda.synchronize()
+    assert occ2.cpu().tolist() == [w.size for w in wants]
+    ix.close()
+    # shards, each with its own index
+    parts = [[] for _ in pats]
+    for r in range(3):
+        base, owned, slen = sharding.shard_layout(n, 3, r)
+        shard = td[base:base + slen].clone()
+        six = epsm.eq_index(shard, g.index_values())
+        o = torch.zeros(len(pats), dtype=torch.int64, device=dev)
+        so = [torch.empty(w.size + 1, dtype=torch.int64, device=dev) for w in wants]
+        g.search_range_async(shard, owned, base, n, o, outs=so, index=six)
+        torch.cuda.synchronize()
+        for j in range(len(pats)):
+            parts[j].append(so[j][:int(o[j])].cpu().numpy().astype(np.uint64))
+        six.close()
+    for j, w in enumerate(wants):
+        assert np.array_equal(np.concatenate(parts[j]), w), ("shard", j)
+    g.close()
