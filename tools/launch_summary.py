@@ -1,0 +1,46 @@
+"""Summarise an ncu launch list of bench.py (--metrics gpu__time_duration.sum,dram__bytes_read.sum,
+dram__bytes_write.sum --csv): per-launch lines of the repo's kernels, per-kernel shares, and
+profiles/traffic.json (DRAM bytes per launch of the dominant kernel, read by bench.py).
+usage: python tools/launch_summary.py launches.csv out.txt [traffic.json]"""
+import collections
+import csv
+import json
+import sys
+
+src, out_path = sys.argv[1], sys.argv[2]
+tj = sys.argv[3] if len(sys.argv) > 3 else None
+lines = [ln for ln in open(src) if ln.startswith('"')]
+rows = collections.OrderedDict()
+for r in csv.DictReader(lines):
+    rows.setdefault((r["ID"], r["Kernel Name"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+with open(out_path, "w") as out:
+    out.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+              "--clock-control none (cold-cache, serialised launches: shares, not absolutes)\n")
+    out.write("# id kernel time_us dram_read_MB dram_write_MB\n")
+    for (i, name), m in rows.items():
+        short = name.split("(")[0].replace("void ", "").replace("epsm::", "")
+        if "epsm" not in short:
+            continue
+        t, rd, wr = m.get("gpu__time_duration.sum", 0), m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)
+        out.write(f"{i} {short[:70]} {t / 1e3:.1f} {rd / 1e6:.1f} {wr / 1e6:.1f}\n")
+        a = agg[short.split("<")[0]]
+        a[0] += 1
+        a[1] += t
+        a[2] += rd
+        a[3] += wr
+    tot = sum(a[1] for a in agg.values())
+    out.write("\n# per kernel (repo kernels only)\n")
+    summ = {"source": out_path, "kernels": {}}
+    for k, a in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.write(f"# {k}: launches {a[0]}, {a[1] / 1e6:.2f} ms ({100 * a[1] / tot:.1f}%), DRAM {a[2] / 1e9:.2f} GB "
+                  f"read + {a[3] / 1e9:.2f} GB written, {(a[2] + a[3]) / a[0] / 1e6:.1f} MB per launch\n")
+        summ["kernels"][k] = {"launches": a[0], "share": round(a[1] / tot, 4),
+                              "dram_bytes_per_launch": int((a[2] + a[3]) / a[0])}
+dom = max(summ["kernels"].items(), key=lambda x: x[1]["share"])
+summ["dominant"] = dom[0]
+summ["dram_bytes_per_launch"] = dom[1]["dram_bytes_per_launch"]
+summ["unit"] = "DRAM bytes (read + write) per launch of the dominant kernel (" + dom[0] + "), ncu launch list of the bench"
+if tj:
+    json.dump(summ, open(tj, "w"), indent=1)
+print(open(out_path).read().split("# per kernel")[1])
