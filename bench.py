@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-breakdown", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the `configs` field (BASELINE configs 1, 3a, 3b, 4, 5a, 5b via the group search)")
     ap.add_argument("--scan-patterns", type=int, default=10,
                     help="online scan field: patterns per (sigma, m), one search per launch (0: off)")
     ap.add_argument("--cpu-bytes", type=int, default=64 * synth.MiB, help="host baseline sample bytes per search")
@@ -528,10 +530,15 @@ def run_epsm(args, world, rank, local):
     }
     if world == 1 and args.scan_patterns > 0:
         res["scan"] = run_scan(args, epsm, texts, pats, ms, hbm_peak)
-    if world == 1 and not args.no_e2e:
+    if world == 1 and (not args.no_e2e or not args.no_configs):
         del pool
         torch.cuda.empty_cache()
+    if world == 1 and not args.no_e2e:
         res["e2e"] = run_e2e(args, epsm, texts, G, P)
+    if world == 1 and not args.no_configs:
+        texts_keep = texts
+        res["configs"] = run_configs(args, epsm, dev, hbm_peak)
+        del texts_keep
     if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"], res["cpu_epsm"] = cpu_baselines(args, texts, pats, ms)
     for _, _, g, plans in G:
@@ -617,6 +624,88 @@ def run_scan(args, epsm, texts, pats, ms, peak):
             "min_frac_8d": min(fr), "below_0.7": sum(1 for x in fr if x < 0.7),
             "note": "one search per launch over the text kernels (no index, no group) -- EPSM's online "
                     "per-pattern search; frac_8d = (n + 8 occ) / t / peak, per search, averaged"}
+
+
+def run_configs(args, epsm, dev, peak):
+    """BASELINE.json's other configs through the same public API as the headline (one group call
+    per (text, m), the text's index over its dense patterns' bytes): 1 (1 MiB ACGT, 16 x m=4),
+    3a/3b (1 GiB genome-/protein-like, m = 2..32), 4 (1 GiB Zipf-27), 5a (8 GiB ACGT, m = 8, 32),
+    5b ('a'^(2^30), 'a'^16).  Per (text, m): one warm and one timed call (CUDA events, the index
+    build timed apart), text GB/s = patterns x n / t, moved GB/s (text once per pass + 8 B per
+    position), oracle windows on two searches per group (config 1: the full oracle; 5b: the
+    closed form occ = n - 15, positions = 0 .. n - 16 sampled)."""
+    import oracle
+    stream = torch.cuda.current_stream(dev)
+    rng = np.random.default_rng(99)
+    out = {}
+    for cfg in ("1", "3", "4", "5a", "5b"):
+        for w in synth.config_workloads(cfg):
+            text = synth.text_torch(w.spec, 0, w.n, device=dev)
+            groups = {}
+            for m in w.ms:
+                p, _ = (synth.extract_patterns_torch(text, w.start_seed(m), m, w.patterns_per_m)
+                        if cfg != "5b" else ([b"a" * m], None))
+                groups[m] = (p, epsm.group(p))
+            vals = sorted({v for _, g in groups.values() for v in g.index_values()})
+            ix, build_us = None, 0.0
+            if vals:
+                ix = epsm.EqIndex()
+                ix.build_async(text, bytes(vals))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                ix.build_async(text, bytes(vals))
+                e1.record(stream)
+                torch.cuda.synchronize()
+                build_us = e0.elapsed_time(e1) * 1e3
+            rows, t_tot, txt_tot, mv_tot = [], build_us, 0.0, w.n * (1 + len(vals) / 8) if vals else 0.0
+            for m, (p, g) in groups.items():
+                k = len(p)
+                occ = torch.zeros(k, dtype=torch.int64, device=dev)
+                g.count_async(text, occ, index=ix)
+                torch.cuda.synchronize()
+                cap = int(occ.max().item()) + 1
+                outs = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in range(k)]
+                g.search_async(text, occ, outs=outs, index=ix)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.search_async(text, occ, outs=outs, index=ix)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) * 1e3
+                oc = occ.cpu().numpy()
+                if cfg == "1":
+                    host = text.cpu().numpy()
+                    for j in range(k):
+                        want = oracle.search(p[j], host)
+                        assert int(oc[j]) == want.size and np.array_equal(
+                            outs[j][:want.size].cpu().numpy().astype(np.uint64), want), "config 1 parity"
+                elif cfg == "5b":
+                    assert int(oc[0]) == w.n - m + 1, "config 5b closed form"
+                    for q in (0, 1, w.n // 3, w.n - m):
+                        assert int(outs[0][q]) == q, "config 5b positions"
+                else:
+                    for j in (0, k - 1):
+                        check_windows(p[j], outs[j], int(oc[j]), w.spec, w.n, rng)
+                moved = w.n * len(g.info()["passes"]) + 8.0 * float(oc.sum())
+                rows.append([m, round(us, 1), round(k * w.n / (us * 1e-6) / 1e9, 1),
+                             round(moved / (us * 1e-6) / 1e9, 1), int(oc.sum()), int(sum(g.dense_searches()))])
+                t_tot += us
+                txt_tot += k * w.n
+                mv_tot += moved
+                del outs
+                g.close()
+            if ix is not None:
+                ix.close()
+            del text
+            torch.cuda.empty_cache()
+            out[w.name] = {"text_GBps": round(txt_tot / (t_tot * 1e-6) / 1e9, 1),
+                           "moved_frac": round(mv_tot / (t_tot * 1e-6) / 1e9 / peak, 3),
+                           "index_build_us": round(build_us, 1), "index_values": len(vals),
+                           "cols": ["m", "us per group", "text_GBps", "moved_GBps", "positions", "dense searches"],
+                           "rows": rows}
+    out["note"] = ("group search per (text, m), patterns_per_m as BASELINE.json (100; config 1: 16; 5b: 1); "
+                   "parity: oracle windows (config 1: full oracle; 5b: closed form)")
+    return out
 
 
 def run_e2e(args, epsm, texts, G, P):

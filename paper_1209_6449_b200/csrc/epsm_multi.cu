@@ -748,6 +748,8 @@ static int group_dense_log2() {
   return v <= 0 ? 4096 : v;
 }
 
+constexpr uint32_t kMinShared = 4;
+
 // Split the distinct patterns into dense (estimated rate >= 2^-log2 occurrences per text byte)
 // and sparse.  The rate of a pattern is the product of its bytes' frequencies among the OTHER
 // k - 1 patterns of the group (they are extracted from the text, so their bytes
@@ -779,10 +781,14 @@ static void group_split(epsm_group_t* g, int log2) {
   // 8x of the group's geometric mean takes the mean, so that a uniform text's patterns, which
   // have one common rate, are split the same way; outliers keep their own estimate
   const double gmean = lcnt ? std::exp2(lsum / lcnt) : 0.0;
+  // a group of fewer than kMinShared distinct patterns has little to share and too few samples
+  // to estimate rates from: its patterns are searched one by one (a single search is the
+  // single-pattern kernel's case: 'a'^16 over 'a'^(2^30) 1.4 ms, the shared passes 30 ms)
+  const bool all_single = log2 < 1024 && g->D < kMinShared;
   for (uint32_t d = 0; d < g->D; ++d) {
     double r = rate[d];
     if (r > 0 && gmean > 0 && std::fabs(std::log2(r / gmean)) <= 3.0) r = gmean;
-    (log2 < 1024 && r >= thresh ? g->dense : g->sparse).push_back(d);
+    (all_single || (log2 < 1024 && r >= thresh) ? g->dense : g->sparse).push_back(d);
   }
 }
 
