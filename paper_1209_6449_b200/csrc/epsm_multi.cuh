@@ -179,14 +179,15 @@ struct __align__(128) MSmem {
                                                      // (lane l's 64 starts at l * 68: a lane stride of
                                                      // 17 words keeps the lanes' stores conflict-free)
   uint16_t hist[kConsumerWarps][kMaxD + 1];          // per-slice counts -> exclusive offsets
-  unsigned long long pre[kMaxD + 1];                 // pass 3: the chunk's global prefix
+  uint64_t* cptr[kMaxD + 1];                         // pass 3: the chunk's first slot of each pattern
+                                                     // (its first output + the chunk's prefix)
   uint32_t ccnt[kStages][kMaxD + 1];                 // pass 1: chunk counts (by stage)
   uint32_t lcur[kStages];                            // pass 1: list cursor (by stage)
   uint32_t done[kStages];                            // pass 1: warps finished with the stage
   unsigned long long lm[kConsumerWarps][32];         // lane match masks of a slice (list path)
   uint32_t rbuf[kConsumerWarps][32];                 // pass 3: a round of 32 matches (offset | id << 16)
   uint64_t* opos[kMaxD + 1];                         // pass 3: the first output of each pattern ...
-  uint64_t ocap[kMaxD + 1];                          // ... and its capacity (0: none)
+  uint64_t* oend[kMaxD + 1];                         // ... and its end (first + capacity)
   alignas(8) uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t gfull;
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
     for (uint32_t d = tid - 32; d < P.D; d += 32 * kConsumerWarps) {
       const JobOut J = P.jobs[S.g.dup_list[S.g.dup_off[d]]];
       S.opos[d] = J.pos;
-      S.ocap[d] = J.pos ? J.cap : 0;
+      S.oend[d] = J.pos ? J.pos + J.cap : J.pos;
     }
     bar_consumers();
   }
@@ -444,19 +445,20 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         for (int r = 0; r < QW; ++r) {
           const int b = j * SK + 4 * r;
           const int wi = b >> 2, sh = b & 3;
-          k[r] = sh == 0 ? W[wi] : __funnelshift_r(W[wi], W[wi + 1], 8 * sh);
+          k[r] = sh == 0 ? W[wi] : ((W[wi] >> (8 * sh)) | (W[wi + 1] << (32 - 8 * sh)));
         }
         k[QW - 1] &= P.qmask;
         const uint32_t h = hash_words<QW>(k, P);
         MP_CHECK((h >> (32 - kBitmapLog + 5)) < 2048u, "bitmap", h, j);
         // two-probe (Bloom) test: both bits set for every table gram (false positives
         // D*SK/2^16 -> (that)^2: one warp in ~3 instead of every warp walks a bucket per chunk)
+        // (plain shifts, not the volatile shf asm of __funnelshift_r: the samples' chains interleave)
         const uint32_t bw = G.bitmap[h >> (32 - kBitmapLog + 5)];
-        uint32_t bit = __funnelshift_r(bw, bw, h >> (32 - kBitmapLog));
+        uint32_t bit = bw >> ((h >> (32 - kBitmapLog)) & 31u);
         if (P.bloom2) {                           // (q <= 2: the key itself, exact already)
           const uint32_t h2 = bloom2(h);
           const uint32_t bw2 = G.bitmap[h2 >> (32 - kBitmapLog + 5)];
-          bit &= __funnelshift_r(bw2, bw2, h2 >> (32 - kBitmapLog));
+          bit &= bw2 >> ((h2 >> (32 - kBitmapLog)) & 31u);
         }
         bit &= 1u;
         if (j < 64) hits |= static_cast<uint64_t>(bit) << j;
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           S.hist[w][d] = static_cast<uint16_t>(run);
           run += v;
         }
-        S.pre[d] = P.prefix[static_cast<uint64_t>(d) * P.nchunks + c];
+        S.cptr[d] = S.opos[d] + P.prefix[static_cast<uint64_t>(d) * P.nchunks + c];
       }
       bar_consumers();
       const uint64_t cbase = static_cast<uint64_t>(c) * kTile + P.pos_bias + cw * kSliceBytes;
@@ -617,13 +619,13 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           *ib = kNoId;
           const uint32_t peers = __match_any_sync(0xffffffffu, id);
           const bool act = id != kNoId;
-          uint64_t g = 0;
-          if (act) g = S.pre[id] + hw[id] + __popc(peers & lt);
+          uint64_t* dst = nullptr;
+          if (act) dst = S.cptr[id] + hw[id] + __popc(peers & lt);
           __syncwarp();
           if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
           if (act) {
             const uint64_t pos = cbase + 32 * b + lane;
-            if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);   // (duplicates: copied after)
+            if (dst < S.oend[id]) st_stream_u64(dst, pos);   // (duplicates: copied after)
           }
           __syncwarp();
         }
@@ -644,13 +646,13 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         const uint32_t e = act ? rb[lane] : 0u;
         const uint32_t id = act ? (e >> 16) : static_cast<uint32_t>(kNoId);
         const uint32_t peers = __match_any_sync(0xffffffffu, id);
-        uint64_t g = 0;
-        if (act) g = S.pre[id] + hw[id] + __popc(peers & lt);
+        uint64_t* dst = nullptr;
+        if (act) dst = S.cptr[id] + hw[id] + __popc(peers & lt);
         __syncwarp();
         if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
         if (act) {
           const uint64_t pos = cbase + (e & 0xFFFFu);
-          if (g < S.ocap[id]) st_stream_u64(S.opos[id] + g, pos);   // (duplicates: copied after)
+          if (dst < S.oend[id]) st_stream_u64(dst, pos);   // (duplicates: copied after)
         }
         __syncwarp();                                  // (the round buffer is refilled next)
       }
