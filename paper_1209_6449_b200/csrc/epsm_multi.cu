@@ -118,6 +118,7 @@ MKernel pick_qw(int qw, bool write) {
 
 MKernel multi_kernel_for(int sk, int qw, bool write) {
   switch (sk) {
+    case -1: return pick_mk<-1, 1>(write);
     case 0: return pick_mk<0, 1>(write);
     case 1: return pick_qw<1>(qw, write);
     case 2: return pick_qw<2>(qw, write);
@@ -201,11 +202,16 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
   for (int c = 0; c < 256; ++c) sigp += cnt[c] ? 1u : 0u;
   uint32_t cb = 1;
   while ((1u << cb) < sigp) ++cb;
-  const bool code_ok = m * cb <= static_cast<uint32_t>(mp::kCodeKeyBits) && !code_disabled();
+  // (the wide mode -- keys of 15-16 bits in a bitmap + buckets -- only when forced: its ~1.3 ms
+  // per 256 MiB never beat the sampled filter in the measured cases, sigma=4 m=8 1.32 vs 0.39 ms,
+  // sigma=256 m=2 1.44 vs 0.36 ms; the table mode does where the sampled filter meets many
+  // candidates: sigma=64 m=2 0.96 vs 2.3 ms)
+  const bool code_ok = m * cb <= static_cast<uint32_t>(mp::kWideKeyBits) && !code_disabled();
+  const bool wide = m * cb > static_cast<uint32_t>(mp::kCodeKeyBits);   // bitmap + buckets, no table
   const bool force_code = force_q && force_sk == 0;
   if (force_code && !code_ok) return EPSM_EINVAL;
-  if ((code_ok && !force_q && S.cost > kCodeCost) || force_code) {
-    S.sk = 0;
+  if ((code_ok && !wide && !force_q && S.cost > kCodeCost) || force_code) {
+    S.sk = wide ? -1 : 0;
     S.q = static_cast<int>(m);
     S.qw = 1;
     S.cb = cb;
@@ -225,20 +231,29 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     for (uint32_t b = 0; b < m; ++b)
       G.pat[d][b / 4] |= static_cast<uint32_t>(static_cast<unsigned char>(pats[d][b])) << (8 * (b % 4));
   for (uint32_t b = 0; b < m; ++b) G.pmask[b / 4] |= 0xFFu << (8 * (b % 4));
-  if (S.sk == 0) {
+  std::vector<std::vector<uint16_t>> wide_buckets;
+  if (S.sk <= 0) {
     // code mode: byte -> code (pattern bytes in order of value), key table (the codes of a
-    // window, its LAST byte in the low bits -- the kernel's rolling key) -> pattern
+    // window, its LAST byte in the low bits -- the kernel's rolling key) -> pattern; the wide
+    // mode (keys of 15-16 bits) keeps an exact 2^16-bit bitmap of the keys and buckets by key >> 4
+    // whose entries hold the pattern and the key's low 4 bits
     std::memset(G.cmap, 0x80, sizeof(G.cmap));
     uint32_t code = 0;
     for (int c = 0; c < 256; ++c)
       if (cnt[c]) G.cmap[c] = static_cast<uint8_t>(code++);
     uint8_t* lut = reinterpret_cast<uint8_t*>(G.bitmap);
-    std::memset(lut, 0xFF, 1u << mp::kCodeKeyBits);
+    if (S.sk == 0) std::memset(lut, 0xFF, 1u << mp::kCodeKeyBits);
+    else wide_buckets.assign(1u << mp::kBucketLog, {});
     for (uint32_t d = 0; d < D; ++d) {
       uint32_t key = 0;
       for (uint32_t j = 0; j < m; ++j)
         key = (key << S.cb) | G.cmap[static_cast<unsigned char>(pats[d][j])];
-      lut[key] = static_cast<uint8_t>(d);
+      if (S.sk == 0) {
+        lut[key] = static_cast<uint8_t>(d);
+      } else {
+        G.bitmap[key >> 5] |= 1u << (key & 31u);
+        wide_buckets[key >> 4].push_back(static_cast<uint16_t>((d << 8) | (key & 15u)));
+      }
     }
   }
   // the table (EPSMc's L, for every pattern at once): gram p_d[i .. i+q) of
@@ -257,10 +272,11 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     }
   }
   uint32_t e = 0;
-  if (S.sk > 0) {
+  if (S.sk != 0) {
+    const auto& bks = S.sk > 0 ? buckets : wide_buckets;
     for (uint32_t b = 0; b < (1u << mp::kBucketLog); ++b) {
       G.boff[b] = static_cast<uint16_t>(e);
-      for (uint16_t v : buckets[b]) G.ent[e++] = v;
+      for (uint16_t v : bks[b]) G.ent[e++] = v;
     }
     for (uint32_t b = (1u << mp::kBucketLog); b < (1u << mp::kBucketLog) + 8; ++b)
       G.boff[b] = static_cast<uint16_t>(e);
@@ -391,8 +407,8 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   P.qmask = S.qmask;
   P.bloom2 = (S.sk > 0 && S.q > 2) ? 1u : 0u;
   P.cb = S.cb;
-  P.kmask = S.sk == 0 ? (1u << (g->m * S.cb)) - 1u : 0u;
-  P.mmask = S.sk == 0 ? (1u << g->m) - 1u : 0u;
+  P.kmask = S.sk <= 0 ? (1u << (g->m * S.cb)) - 1u : 0u;
+  P.mmask = S.sk <= 0 ? (1u << g->m) - 1u : 0u;
   for (int r = 0; r < 4; ++r) P.hmul[r] = S.hmul[r];
   P.desc = S.d_desc;
   P.desc_bytes = sizeof(mp::GroupDesc);
@@ -946,7 +962,7 @@ int epsm_group_info(const epsm_group_t* g, uint32_t* out, uint32_t nout) {
                              static_cast<uint32_t>(g->subs.size())};
   for (const auto& S : g->subs) {
     v.push_back(static_cast<uint32_t>(S.q));
-    v.push_back(static_cast<uint32_t>(S.sk));
+    v.push_back(static_cast<uint32_t>(S.sk < 0 ? 0 : S.sk));   // (0: code mode, table or wide)
   }
   const uint32_t c = std::min<uint32_t>(nout, static_cast<uint32_t>(v.size()));
   for (uint32_t i = 0; i < c; ++i) out[i] = v[i];

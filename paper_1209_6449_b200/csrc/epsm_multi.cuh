@@ -56,7 +56,8 @@ constexpr int kMaxEntries = 4096;                 // (d, i) pairs: D * SK
 constexpr int kMaxJobs = 1024;                    // searches per group
 constexpr int kListCap = 256;                     // (offset, id) entries kept per chunk
 constexpr int kMaxPW = 8;                         // pattern words (m <= 32)
-constexpr int kCodeKeyBits = 14;                  // code mode: m * (bits per symbol) <= 14
+constexpr int kCodeKeyBits = 14;                  // code mode: m * (bits per symbol) <= 14 (table)
+constexpr int kWideKeyBits = 16;                  // ... <= 16 (bitmap + buckets: the wide code mode)
 constexpr int kIdsLane = kSegBytes + 4;           // ids of one lane (padded: bank-conflict-free)
 constexpr int kIdsWarp = 32 * kIdsLane;
 __host__ __device__ constexpr uint32_t id_slot(uint32_t so) {   // slice offset -> ids index
@@ -219,10 +220,27 @@ __device__ __forceinline__ bool verify_window(const uint8_t* ts, uint32_t st, co
 // patterns at once, exact, so no naive check.  Returns the lane's match mask (bit s: start s).
 // DIRECT: count each match into cc[pattern] (shared atomics); else store every start's id
 // (0xFF: none) into idb[0..63].
-template <bool DIRECT>
+// WIDE (keys of 15-16 bits): the key's bit in the bitmap (exact membership), and on a hit (rare:
+// the mode is chosen for sparse groups) the pattern from the key's bucket (key >> 4) whose entry
+// holds the key's low 4 bits -- the bucket and the fingerprint together are the whole key.
+template <bool WIDE>
+__device__ __forceinline__ uint32_t code_lookup(const GroupDesc& G, uint32_t key) {
+  if constexpr (!WIDE) {
+    return reinterpret_cast<const uint8_t*>(G.bitmap)[key];
+  } else {
+    if (((G.bitmap[key >> 5] >> (key & 31u)) & 1u) == 0) return 0xFFu;
+    const uint32_t bk = key >> 4, e1 = G.boff[bk + 1];
+    for (uint32_t e = G.boff[bk]; e < e1; ++e) {
+      const uint32_t v = G.ent[e];
+      if ((v & 15u) == (key & 15u)) return v >> 8;
+    }
+    return 0xFFu;
+  }
+}
+
+template <bool DIRECT, bool WIDE>
 __device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
                                               uint8_t* idb, uint32_t* cc) {
-  const uint8_t* lut = reinterpret_cast<const uint8_t*>(G.bitmap);
   const uint32_t m1 = P.m - 1, cb = P.cb, kmask = P.kmask;
   uint32_t key = 0, e0 = 0, e1 = 0, e2 = 0;
   int last_inv = -64;                            // last byte outside the patterns' alphabet
@@ -232,7 +250,7 @@ __device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const Gro
     const uint32_t cm = G.cmap[(W[t >> 2] >> (8 * (t & 3))) & 0xFFu];
     key = ((key << cb) | cm) & kmask;            // (an invalid byte's 0x80 is cut by the next
     if (cm & 0x80u) last_inv = t;                //  mask or caught by last_inv)
-    const uint32_t d = (t - last_inv > static_cast<int>(m1)) ? lut[key] : 0xFFu;
+    const uint32_t d = (t - last_inv > static_cast<int>(m1)) ? code_lookup<WIDE>(G, key) : 0xFFu;
     const uint32_t s0 = static_cast<uint32_t>(t) - m1;
     const bool mine = s0 < static_cast<uint32_t>(kSegBytes);
     if constexpr (DIRECT) {
@@ -402,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           W[19] = v.w;
         }
       }
-      if constexpr (SK == 0) {
+      if constexpr (SK <= 0) {
         // ---- code mode (dense groups, small pattern alphabets): every start keyed exactly.
         // Byte t of the lane's window maps to its symbol code; the rolling key over t holds the
         // codes of bytes t-m+1 .. t (byte t in the low bits), i.e. the window of start t-m+1;
@@ -414,10 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         if (!WRITE && c >= P.it_lo && c < P.it_hi) {
           // pass 1 over an interior chunk: count straight into the chunk's counters (no ids,
           // no list: the chunk is re-filtered by pass 3)
-          M = code_scan<true>(W, G, P, idb, S.ccnt[stage]);
+          M = code_scan<true, (SK < 0)>(W, G, P, idb, S.ccnt[stage]);
           direct = true;
         } else {
-          M = code_scan<false>(W, G, P, idb, nullptr);
+          M = code_scan<false, (SK < 0)>(W, G, P, idb, nullptr);
         }
         if (!(c >= P.it_lo && c < P.it_hi)) {
           // a chunk at the text's ends: starts outside [s_lo, s_hi) do not count (their ids are

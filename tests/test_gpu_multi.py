@@ -315,16 +315,17 @@ def test_group_dense_fanout_phases_and_caps(epsm, dev, use_index):
 @pytest.mark.parametrize("sigma", [2, 3, 4, 16, 100])
 def test_group_code_mode(epsm, dev, sigma):
     """The code mode (every start keyed through the patterns' byte codes, exact): forced with
-    set_geometry(q, 0) wherever m * ceil(log2(distinct pattern bytes)) <= 14; bytes outside the
+    set_geometry(q, 0) wherever m * ceil(log2(distinct pattern bytes)) <= 16 (<= 14: key table;
+    15-16: the wide mode's bitmap + buckets); bytes outside the
     patterns' alphabet break windows; edges, duplicates and absent patterns as elsewhere."""
     rng = np.random.default_rng(500 + sigma)
     n = 7 * TILE + 1001
-    for m in (1, 2, 3, 4, 5, 7, 8, 12, 14):
+    for m in (1, 2, 3, 4, 5, 7, 8, 12, 14, 15, 16):
         t, pats = planted(rng, n, sigma, m, 25, absent=2)
         sigp = len(set(b"".join(pats)))
         cb = max(1, (sigp - 1).bit_length())
         td = torch.from_numpy(t).to(dev)
-        if m * cb > 14:
+        if m * cb > 16:
             g = epsm.group(pats).set_dense(0)
             with pytest.raises(epsm.EpsmError):
                 g.set_geometry(m, 0)

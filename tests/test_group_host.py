@@ -52,7 +52,7 @@ def test_geometry_is_valid(sigma):
             info = epsm.group(pats).set_dense(0).info()
             assert info["distinct"] == len(set(pats))
             for q, sk in info["passes"]:
-                if sk == 0:                                      # code mode: m * code bits <= 14
+                if sk == 0:                                      # code mode (auto: the table, <= 14 bits)
                     cb = max(1, (len(set(b"".join(pats))) - 1).bit_length())
                     assert q == m and m * cb <= 14, (m, cb)
                     continue
