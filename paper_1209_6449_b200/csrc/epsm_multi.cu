@@ -32,6 +32,7 @@ struct Subgroup {
   uint32_t D = 0, k = 0;               // distinct patterns, searches
   int q = 1, sk = 1, qw = 1;           // sk = 0: code mode (every start keyed, exact)
   uint32_t cb = 0;                     // code mode: bits per symbol code
+  bool spare = false;                  // code mode: a spare code marks bytes outside the alphabet
   uint32_t qmask = 0xFFu, hmul[4] = {0, 0, 0, 0};
   std::vector<uint32_t> jobs;          // the caller's search index of local search j
   mp::GroupDesc* h_desc = nullptr;
@@ -162,6 +163,7 @@ struct epsm_group_s {
   // one by one through the single-pattern kernels (their positions, >= 4 bytes of output per
   // 1000 text bytes, dominate; the shared pass gains little there); the rest share the passes
   std::vector<uint32_t> sparse, dense;            // distinct pattern indices
+  double sparse_rate = 0;                         // estimated matches per text byte of the sparse ones
   std::vector<epsm_plan_t*> dplans;               // plan of dense[i] (one scan, fanned out to its
                                                   // searches: they have the same positions)
 };
@@ -215,6 +217,13 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     S.q = static_cast<int>(m);
     S.qw = 1;
     S.cb = cb;
+    // a spare code (one more bit if the key still fits the table) spares the kernel the
+    // tracking of bytes outside the alphabet
+    S.spare = (1u << cb) > sigp;
+    if (!S.spare && !wide && m * (cb + 1) <= static_cast<uint32_t>(mp::kCodeKeyBits)) {
+      S.cb = cb + 1;
+      S.spare = true;
+    }
   } else if (force_q) {
     S.q = force_q;
     S.sk = force_sk;
@@ -237,8 +246,10 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     // window, its LAST byte in the low bits -- the kernel's rolling key) -> pattern; the wide
     // mode (keys of 15-16 bits) keeps an exact 2^16-bit bitmap of the keys and buckets by key >> 4
     // whose entries hold the pattern and the key's low 4 bits
-    std::memset(G.cmap, 0x80, sizeof(G.cmap));
     uint32_t code = 0;
+    for (int c = 0; c < 256; ++c) code += cnt[c] ? 1u : 0u;
+    std::memset(G.cmap, S.spare ? static_cast<int>(code) : 0x80, sizeof(G.cmap));   // (spare code = sigma')
+    code = 0;
     for (int c = 0; c < 256; ++c)
       if (cnt[c]) G.cmap[c] = static_cast<uint8_t>(code++);
     uint8_t* lut = reinterpret_cast<uint8_t*>(G.bitmap);
@@ -409,6 +420,10 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   P.cb = S.cb;
   P.kmask = S.sk <= 0 ? (1u << (g->m * S.cb)) - 1u : 0u;
   P.mmask = S.sk <= 0 ? (1u << g->m) - 1u : 0u;
+  P.spare = S.sk <= 0 && S.spare ? 1u : 0u;
+  // direct counting in pass 1 only where the chunks would overflow their lists anyway (> 256
+  // expected matches per 32 KiB chunk); sparser groups keep the lists (pass 3 without the text)
+  P.direct = (S.sk <= 0 && g->sparse_rate * mp::kTile > static_cast<double>(mp::kListCap)) ? 1u : 0u;
   for (int r = 0; r < 4; ++r) P.hmul[r] = S.hmul[r];
   P.desc = S.d_desc;
   P.desc_bytes = sizeof(mp::GroupDesc);
@@ -801,10 +816,13 @@ static void group_split(epsm_group_t* g, int log2) {
   // to estimate rates from: its patterns are searched one by one (a single search is the
   // single-pattern kernel's case: 'a'^16 over 'a'^(2^30) 1.4 ms, the shared passes 30 ms)
   const bool all_single = log2 < 1024 && g->D < kMinShared;
+  g->sparse_rate = 0;
   for (uint32_t d = 0; d < g->D; ++d) {
     double r = rate[d];
     if (r > 0 && gmean > 0 && std::fabs(std::log2(r / gmean)) <= 3.0) r = gmean;
-    (all_single || (log2 < 1024 && r >= thresh) ? g->dense : g->sparse).push_back(d);
+    const bool dn = all_single || (log2 < 1024 && r >= thresh);
+    (dn ? g->dense : g->sparse).push_back(d);
+    if (!dn) g->sparse_rate += r;
   }
 }
 

@@ -102,6 +102,9 @@ struct MParams {
   uint32_t cb;                  // code mode: bits per symbol code
   uint32_t kmask;               // code mode: 2^(m * cb) - 1
   uint32_t mmask;               // code mode: 2^m - 1
+  uint32_t spare;               // code mode: bytes outside the alphabet map to a spare code
+  uint32_t direct;              // code mode, pass 1: count in the scan, no lists (dense groups: the
+                                // chunks overflow their lists anyway and pass 3 re-filters them)
   uint32_t hmul[4];             // key word multipliers of the sample hash
   uint32_t desc_bytes;
   const GroupDesc* desc;
@@ -238,34 +241,50 @@ __device__ __forceinline__ uint32_t code_lookup(const GroupDesc& G, uint32_t key
   }
 }
 
-template <bool DIRECT, bool WIDE>
-__device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
-                                              uint8_t* idb, uint32_t* cc) {
+template <bool DIRECT, bool WIDE, bool SPARE>
+__device__ __forceinline__ uint64_t code_scan_t(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
+                                                uint8_t* idb, uint32_t* cc) {
   const uint32_t m1 = P.m - 1, cb = P.cb, kmask = P.kmask;
-  uint32_t key = 0, e0 = 0, e1 = 0, e2 = 0;
+  uint32_t key = 0, e0 = 0, e1 = 0, e2 = 0, any = 0;
   int last_inv = -64;                            // last byte outside the patterns' alphabet
   uint8_t* const ids0 = idb - m1;                // id slot of the start closed by byte t: ids0[t]
 #pragma unroll
   for (int t = 0; t < 80; ++t) {
     const uint32_t cm = G.cmap[(W[t >> 2] >> (8 * (t & 3))) & 0xFFu];
-    key = ((key << cb) | cm) & kmask;            // (an invalid byte's 0x80 is cut by the next
-    if (cm & 0x80u) last_inv = t;                //  mask or caught by last_inv)
-    const uint32_t d = (t - last_inv > static_cast<int>(m1)) ? code_lookup<WIDE>(G, key) : 0xFFu;
+    key = ((key << cb) | cm) & kmask;
+    uint32_t d;
+    if constexpr (SPARE) {
+      // bytes outside the alphabet have the spare code: no pattern key holds it (table: 0xFF)
+      d = code_lookup<WIDE>(G, key);
+    } else {
+      if (cm & 0x80u) last_inv = t;              // (its 0x80 leaves the key within m bytes)
+      d = (t - last_inv > static_cast<int>(m1)) ? code_lookup<WIDE>(G, key) : 0xFFu;
+    }
     const uint32_t s0 = static_cast<uint32_t>(t) - m1;
     const bool mine = s0 < static_cast<uint32_t>(kSegBytes);
     if constexpr (DIRECT) {
-      if (mine && d != 0xFFu) atomicAdd(&cc[d], 1u);
+      if (mine && d != 0xFFu) {
+        atomicAdd(&cc[d], 1u);
+        any = 1u;
+      }
     } else {
       if (mine) ids0[t] = static_cast<uint8_t>(d);
+      const uint32_t hit = d != 0xFFu ? 1u : 0u;
+      if (t < 32) e0 |= hit << t;
+      else if (t < 64) e1 |= hit << (t - 32);
+      else e2 |= hit << (t - 64);
     }
-    const uint32_t hit = d != 0xFFu ? 1u : 0u;
-    if (t < 32) e0 |= hit << t;
-    else if (t < 64) e1 |= hit << (t - 32);
-    else e2 |= hit << (t - 64);
   }
+  if constexpr (DIRECT) return any;              // (pass 1 counts directly: only "any match")
   // starts = window ends - m1 (m1 <= 13): the lane's 64 starts out of the 80 ends
   const uint64_t lo = (static_cast<uint64_t>(e1) << 32) | e0;
   return m1 ? ((lo >> m1) | (static_cast<uint64_t>(e2) << (64 - m1))) : lo;
+}
+
+template <bool DIRECT, bool WIDE>
+__device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
+                                              uint8_t* idb, uint32_t* cc) {
+  return P.spare ? code_scan_t<DIRECT, WIDE, true>(W, G, P, idb, cc) : code_scan_t<DIRECT, WIDE, false>(W, G, P, idb, cc);
 }
 
 template <int SK, int QW, bool WRITE>
@@ -429,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         // Every start of the lane gets its id (0xFF: none) -- no stale ids -- and bit t of
         // E marks the window ENDING at byte t (compile-time bit positions).
         uint8_t* const idb = ids + lane * kIdsLane;
-        if (!WRITE && c >= P.it_lo && c < P.it_hi) {
+        if (!WRITE && P.direct && c >= P.it_lo && c < P.it_hi) {
           // pass 1 over an interior chunk: count straight into the chunk's counters (no ids,
           // no list: the chunk is re-filtered by pass 3)
           M = code_scan<true, (SK < 0)>(W, G, P, idb, S.ccnt[stage]);
