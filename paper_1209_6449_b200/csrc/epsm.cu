@@ -601,12 +601,16 @@ int epsm_replicate(const uint64_t* d_pos, uint64_t cap, const unsigned long long
   cudaError_t e = cudaSuccess;
   {
     const uint64_t have = (search && d_pos) ? cap : 0;
-    static bool rep_attr = false;
-    if (!rep_attr) {
-      e = cudaFuncSetAttribute(epsm::epsm_replicate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(sizeof(epsm::RepSmem)));
-      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(replicate)");
-      rep_attr = true;
+    {                                                  // (per device: the attribute is per device)
+      static std::mutex mu;
+      static std::vector<int> devs;
+      std::lock_guard<std::mutex> lk(mu);
+      if (std::find(devs.begin(), devs.end(), ws->device) == devs.end()) {
+        e = cudaFuncSetAttribute(epsm::epsm_replicate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(epsm::RepSmem)));
+        if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(replicate)");
+        devs.push_back(ws->device);
+      }
     }
     // (grid sized by the capacity; CTAs past the occ's chunks exit at once)
     const uint64_t chunks = (have + epsm::kRepChunk / 8 - 1) / (epsm::kRepChunk / 8);

@@ -362,14 +362,17 @@ static int ensure_multi_ws(epsm_workspace* ws, uint64_t chunks, uint32_t D, cuda
 }
 
 static int set_multi_smem(MKernel fn) {
-  static std::vector<MKernel> done;
+  // (the attribute is per device: remember (kernel, device) pairs)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::vector<std::pair<MKernel, int>> done;
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
-  if (std::find(done.begin(), done.end(), fn) != done.end()) return EPSM_OK;
+  if (std::find(done.begin(), done.end(), std::make_pair(fn, dev)) != done.end()) return EPSM_OK;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(mp::MSmem)));
   if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(group kernel smem)");
-  done.push_back(fn);
+  done.emplace_back(fn, dev);
   return EPSM_OK;
 }
 
