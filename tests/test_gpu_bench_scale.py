@@ -99,3 +99,56 @@ def test_index_batch_at_bench_scale(epsm, dev, sigma):
             del outs
     for pl in allplans:
         pl.close()
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 8, 16, 64, 128, 256])
+def test_group_search_at_bench_scale(epsm, dev, sigma):
+    """The bench's step as it runs: per (sigma, m) ONE group call over the 256 MiB text with its
+    100 extracted patterns, the index over the dense patterns' bytes -- every path at full size:
+    the shared sampled / code-mode passes (thousands of chunks per CTA, lists and re-filtered
+    chunks), the dense patterns one by one or in the mask pass, the duplicates' copies.  Checks:
+    the oracle's full count of two searches per group, window parity of every distinct pattern
+    (first, last, two random 1 MiB windows), the per-search properties (ascending, in range,
+    every position verifies, the extraction start reported), duplicates equal."""
+    spec = synth.raw_sigma_spec(sigma, (2, sigma))
+    text = synth.text_torch(spec, 0, N, device=dev)
+    host = text.cpu().numpy()
+    rng = np.random.default_rng(2000 + sigma)
+    P = 100
+    groups = {}
+    for m in (2, 4, 8, 16, 32):
+        pats, starts = synth.extract_patterns_torch(text, (2, sigma, m), m, P)
+        groups[m] = (epsm.group(pats), pats, starts)
+    vals = sorted({v for g, _, _ in groups.values() for v in g.index_values()})
+    ix = epsm.eq_index(text, bytes(vals)) if vals else None
+    for m, (g, pats, starts) in groups.items():
+        occ_c = torch.zeros(P, dtype=torch.int64, device=dev)
+        g.count_async(text, occ_c, index=ix)
+        torch.cuda.synchronize()
+        caps = occ_c.cpu().tolist()
+        outs = [torch.empty(max(c, 1), dtype=torch.int64, device=dev) for c in caps]
+        occ = torch.full((P,), -1, dtype=torch.int64, device=dev)
+        g.search_async(text, occ, outs=outs, index=ix)
+        torch.cuda.synchronize()
+        occ = occ.cpu().tolist()
+        assert occ == caps, (sigma, m)
+        first = {}
+        for j in range(P):
+            pos = outs[j][: occ[j]]
+            if pats[j] in first:                                          # a duplicate: equal
+                assert torch.equal(pos, outs[first[pats[j]]][: occ[j]]), (sigma, m, j)
+                continue
+            first[pats[j]] = j
+            if occ[j] > 1:
+                assert bool((pos[1:] > pos[:-1]).all()), (sigma, m, j)
+            assert int(pos[0]) >= 0 and int(pos[-1]) <= N - m
+            assert bool((pos == int(starts[j])).any()), (sigma, m, j)    # recall
+            verify_all(pos, text, pats[j])                                # precision
+            for a in [0, N - W] + rng.integers(0, N - W, size=2).tolist():
+                window_parity(pos, host, pats[j], int(a))
+        for j in (0, P - 1):
+            assert occ[j] == oracle.count(pats[j], host), (sigma, m, j)
+        del outs
+        g.close()
+    if ix is not None:
+        ix.close()
