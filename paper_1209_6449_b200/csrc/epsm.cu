@@ -795,7 +795,7 @@ void epsm_plan_free(epsm_plan_t* plan) {
   delete plan->h_desc;
   if (plan->d_pat) cudaFree(plan->d_pat);
   if (plan->d_long) cudaFree(plan->d_long);
-  delete plan->h_long;
+  epsm_long_free(plan);
   if (plan->h_occ) cudaFreeHost(plan->h_occ);
   if (plan->d_text_buf) cudaFree(plan->d_text_buf);
   if (plan->d_pos_buf) cudaFree(plan->d_pos_buf);

@@ -127,6 +127,7 @@ int epsm_batch_run(epsm_plan_t* const* plans, uint32_t k, const uint32_t* slot, 
 constexpr uint32_t kLongStrideMinM = 208;
 uint32_t epsm_long_stride(uint32_t m);
 bool epsm_long_applies(const epsm_plan_t* plan);
+void epsm_long_free(epsm_plan_t* plan);   // the host table (its type is complete only in epsm_long.cu)
 int epsm_long_launch(epsm_plan_t* plan, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts, uint64_t base,
                      uint64_t* d_pos, uint64_t cap, unsigned long long* d_occ, bool search, cudaStream_t s);
 int epsm_upload_pattern(epsm_plan_t* plan, cudaStream_t s);

@@ -15,6 +15,11 @@ namespace lg = epsm::lg;
 
 uint32_t epsm_long_stride(uint32_t m) { return m >= 32 ? 16u * (m / 16u - 1u) : 0u; }
 
+void epsm_long_free(epsm_plan_t* plan) {
+  delete plan->h_long;
+  plan->h_long = nullptr;
+}
+
 bool epsm_long_applies(const epsm_plan_t* plan) {
   // EPSM_LONG_STRIDE=0 keeps every long pattern on the full-text sampled kernel (A/B)
   static const bool off = [] {

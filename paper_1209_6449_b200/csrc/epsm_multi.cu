@@ -361,7 +361,11 @@ static int ensure_multi_ws(epsm_workspace* ws, uint64_t chunks, uint32_t D, cuda
   return rc;
 }
 
-static int set_multi_smem(MKernel fn) {
+static int multi_smem_bytes(bool write) {
+  return static_cast<int>(write ? sizeof(mp::MSmemT<true>) : sizeof(mp::MSmemT<false>));
+}
+
+static int set_multi_smem(MKernel fn, bool write) {
   // (the attribute is per device: remember (kernel, device) pairs)
   int dev = 0;
   cudaGetDevice(&dev);
@@ -370,7 +374,7 @@ static int set_multi_smem(MKernel fn) {
   std::lock_guard<std::mutex> lk(mu);
   if (std::find(done.begin(), done.end(), std::make_pair(fn, dev)) != done.end()) return EPSM_OK;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sizeof(mp::MSmem)));
+                                       multi_smem_bytes(write));
   if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(group kernel smem)");
   done.emplace_back(fn, dev);
   return EPSM_OK;
@@ -483,10 +487,10 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(group job table)");
     P.jobs = ws->m_jobs;
   }
-  const int smem = static_cast<int>(sizeof(mp::MSmem));
+  const int smem = multi_smem_bytes(false), smem3 = multi_smem_bytes(true);
   // pass 1: counts per (chunk, distinct pattern), lists of sparse chunks
   MKernel k1 = multi_kernel_for(S.sk, S.qw, false);
-  rc = set_multi_smem(k1);
+  rc = set_multi_smem(k1, false);
   if (rc) return rc;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(chunks, static_cast<uint64_t>(ws->num_sms)));
   k1<<<grid, mp::kThreads, smem, s>>>(P);
@@ -511,9 +515,9 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   if (!search) return EPSM_OK;
   // pass 3: positions of the chunks with occurrences
   MKernel k3 = multi_kernel_for(S.sk, S.qw, true);
-  rc = set_multi_smem(k3);
+  rc = set_multi_smem(k3, true);
   if (rc) return rc;
-  k3<<<ws->num_sms, mp::kThreads, smem, s>>>(P);
+  k3<<<ws->num_sms, mp::kThreads, smem3, s>>>(P);
   epsm_count_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_kernel (pass 3) launch");

@@ -176,8 +176,10 @@ __device__ __forceinline__ uint32_t hash_words(const uint32_t (&k)[4], const MPa
 }
 
 // Shared-memory layout of the group kernel.
-struct __align__(128) MSmem {
-  uint8_t ring[kStages][kStageBytes];
+template <bool WRITE>
+struct __align__(128) MSmemT {
+  static constexpr int kS = WRITE ? kStages - 1 : kStages;   // pass 3 gives a stage to lbuf
+  uint8_t ring[kS][kStageBytes];
   GroupDesc g;
   uint8_t ids[kConsumerWarps][kIdsWarp];             // id of the pattern at each start, kNoId
                                                      // (lane l's 64 starts at l * 68: a lane stride of
@@ -185,20 +187,23 @@ struct __align__(128) MSmem {
   uint16_t hist[kConsumerWarps][kMaxD + 1];          // per-slice counts -> exclusive offsets
   uint64_t* cptr[kMaxD + 1];                         // pass 3: the chunk's first slot of each pattern
                                                      // (its first output + the chunk's prefix)
-  uint32_t ccnt[kStages][kMaxD + 1];                 // pass 1: chunk counts (by stage)
-  uint32_t lcur[kStages];                            // pass 1: list cursor (by stage)
-  uint32_t done[kStages];                            // pass 1: warps finished with the stage
+  uint32_t ccnt[kS][kMaxD + 1];                 // pass 1: chunk counts (by stage)
+  uint32_t lcur[kS];                            // pass 1: list cursor (by stage)
+  uint32_t done[kS];                            // pass 1: warps finished with the stage
   unsigned long long lm[kConsumerWarps][32];         // lane match masks of a slice (list path)
   uint32_t rbuf[kConsumerWarps][32];                 // pass 3: a round of 32 matches (offset | id << 16)
+  uint16_t lbuf[WRITE ? kConsumerWarps : 1][WRITE ? kSliceBytes / 2 : 1];   // pass 3: a half slice's
+                                                     // matches (slice offsets), text order
   uint64_t* opos[kMaxD + 1];                         // pass 3: the first output of each pattern ...
   uint64_t* oend[kMaxD + 1];                         // ... and its end (first + capacity)
-  alignas(8) uint64_t full[kStages];
-  uint64_t empty[kStages];
+  alignas(8) uint64_t full[kS];
+  uint64_t empty[kS];
   uint64_t gfull;
-  uint32_t info[kStages];                            // chunk | kInfoList, or kEnd
-  uint32_t ilen[kStages];                            // list length (list stages)
+  uint32_t info[kS];                            // chunk | kInfoList, or kEnd
+  uint32_t ilen[kS];                            // list length (list stages)
 };
-static_assert(sizeof(MSmem) <= 232448, "group kernel fits 227 KB of shared memory");
+static_assert(sizeof(MSmemT<false>) <= 232448 && sizeof(MSmemT<true>) <= 232448,
+              "group kernel fits 227 KB of shared memory");
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 constexpr uint32_t kInfoList = 0x80000000u;
 
@@ -290,6 +295,8 @@ __device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const Gro
 template <int SK, int QW, bool WRITE>
 __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_constant__ MParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  using MSmem = MSmemT<WRITE>;
+  constexpr int kStages = MSmem::kS;
   MSmem& S = *reinterpret_cast<MSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
@@ -641,35 +648,51 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       uint32_t* const rb = S.rbuf[cw];
       uint64_t mm = M;
       uint32_t idx = incl - cl;
-      if (T > 96) {
-        // a dense slice: 32-start batches instead (the matches of a round would come from one or
-        // two lanes, emitted one by one); batch b = slice starts [32b, 32b + 32) = lane b/2, half b&1
-        const uint32_t blo = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M) != 0u);
-        const uint32_t bhi = __ballot_sync(0xffffffffu, static_cast<uint32_t>(M >> 32) != 0u);
-        uint64_t nbm = (static_cast<uint64_t>(spread16(blo >> 16) | (spread16(bhi >> 16) << 1)) << 32) |
-                       (spread16(blo & 0xFFFFu) | (spread16(bhi & 0xFFFFu) << 1));
-        while (nbm) {
-          const uint32_t b = __ffsll(static_cast<long long>(nbm)) - 1;
-          nbm &= nbm - 1;
-          uint8_t* const ib = ids + (b >> 1) * kIdsLane + 32 * (b & 1u) + lane;   // slice start 32b + lane
-          const uint32_t id = *ib;
-          *ib = kNoId;
-          const uint32_t peers = __match_any_sync(0xffffffffu, id);
-          const bool act = id != kNoId;
-          uint64_t* dst = nullptr;
-          if (act) dst = S.cptr[id] + hw[id] + __popc(peers & lt);
-          __syncwarp();
-          if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
-          if (act) {
-            const uint64_t pos = cbase + 32 * b + lane;
-            if (dst < S.oend[id]) st_stream_u64(dst, pos);   // (duplicates: copied after)
+      if (T > 32) {
+        // more than one round: each half slice's matches (lanes 16h .. 16h + 15) are compacted into
+        // lbuf in text order (every lane writes its own run at its exclusive offset), then ranked 32
+        // per round -- a round costs one match_any however the matches spread over the lanes
+        uint16_t* const lb = S.lbuf[cw];
+        const uint32_t t15 = __shfl_sync(0xffffffffu, incl, 15);
+#pragma unroll 1
+        for (uint32_t h = 0; h < 2; ++h) {
+          const uint32_t hb = h ? t15 : 0u, th = h ? T - t15 : t15;
+          if (th == 0) continue;
+          if ((lane >> 4) == h) {
+            uint32_t k = incl - cl - hb;
+            while (mm) {
+              const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
+              mm &= mm - 1;
+              lb[k++] = static_cast<uint16_t>(lane * kSegBytes + bit);
+            }
           }
           __syncwarp();
+#pragma unroll 1
+          for (uint32_t R = 0; R < th; R += 32) {
+            const bool act = R + lane < th;
+            const uint32_t off = act ? lb[R + lane] : 0u;
+            const uint32_t id = act ? ids[id_slot(off)] : static_cast<uint32_t>(kNoId);
+            const uint32_t peers = __match_any_sync(0xffffffffu, id);
+            uint64_t* dst = nullptr;
+            if (act) dst = S.cptr[id] + hw[id] + __popc(peers & lt);
+            __syncwarp();
+            if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
+            if (act && dst < S.oend[id]) st_stream_u64(dst, cbase + off);   // (duplicates: copied after)
+          }
+          __syncwarp();                                // (lbuf is refilled by the next half)
         }
-        mm = 0;
+        // the ids of the slice's matches go back to kNoId (the next chunk's scan fills them)
+        {
+          uint64_t m2 = M;
+          while (m2) {
+            const uint32_t bit = __ffsll(static_cast<long long>(m2)) - 1;
+            m2 &= m2 - 1;
+            idl[bit] = kNoId;
+          }
+        }
         idx = T;                                      // (the round loop below has nothing left)
       }
-      for (uint32_t R = T > 96 ? T : 0; R < T; R += 32) {
+      for (uint32_t R = T > 32 ? T : 0; R < T; R += 32) {
         while (mm && idx < R + 32) {
           const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
           mm &= mm - 1;
