@@ -617,14 +617,19 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       // each search that asked for that pattern at prefix + rank
       uint16_t* const hw = S.hist[cw];
       {
-        // the slice's count of every pattern (u16 counters, two per 32-bit word)
+        // the slice's count of every pattern (u16 counters, two per 32-bit word); with more than
+        // one round, the first half slice's matches also go to lbuf (see below) on the way
         uint32_t* const hw32 = reinterpret_cast<uint32_t*>(hw);
+        uint16_t* const lb = S.lbuf[cw];
+        const bool fill = T > 32 && lane < 16;
+        uint32_t k = incl - cl;
         uint64_t mm = M;
         while (mm) {
           const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
           mm &= mm - 1;
           const uint32_t id = idl[bit];
           atomicAdd(&hw32[id >> 1], 1u << (16 * (id & 1u)));
+          if (fill) lb[k++] = static_cast<uint16_t>(lane * kSegBytes + bit);
         }
         __syncwarp();
       }
@@ -658,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         for (uint32_t h = 0; h < 2; ++h) {
           const uint32_t hb = h ? t15 : 0u, th = h ? T - t15 : t15;
           if (th == 0) continue;
-          if ((lane >> 4) == h) {
+          if (h == 1 && (lane >> 4) == 1) {              // (half 0: filled with the counts)
             uint32_t k = incl - cl - hb;
             while (mm) {
               const uint32_t bit = __ffsll(static_cast<long long>(mm)) - 1;
@@ -671,24 +676,21 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           for (uint32_t R = 0; R < th; R += 32) {
             const bool act = R + lane < th;
             const uint32_t off = act ? lb[R + lane] : 0u;
-            const uint32_t id = act ? ids[id_slot(off)] : static_cast<uint32_t>(kNoId);
+            uint32_t id = kNoId;
+            if (act) {                                 // (the id slot is reset as it is read)
+              uint8_t* const ip = ids + id_slot(off);
+              id = *ip;
+              *ip = kNoId;
+            }
             const uint32_t peers = __match_any_sync(0xffffffffu, id);
             uint64_t* dst = nullptr;
             if (act) dst = S.cptr[id] + hw[id] + __popc(peers & lt);
             __syncwarp();
             if (act && (peers & lt) == 0) hw[id] = static_cast<uint16_t>(hw[id] + __popc(peers));
             if (act && dst < S.oend[id]) st_stream_u64(dst, cbase + off);   // (duplicates: copied after)
+            __syncwarp();                              // (the next round reads hw)
           }
           __syncwarp();                                // (lbuf is refilled by the next half)
-        }
-        // the ids of the slice's matches go back to kNoId (the next chunk's scan fills them)
-        {
-          uint64_t m2 = M;
-          while (m2) {
-            const uint32_t bit = __ffsll(static_cast<long long>(m2)) - 1;
-            m2 &= m2 - 1;
-            idl[bit] = kNoId;
-          }
         }
         idx = T;                                      // (the round loop below has nothing left)
       }

@@ -334,6 +334,24 @@ def test_group_code_mode(epsm, dev, sigma):
         check(pats, run_group(epsm, pats, td, geom=(m, 0)), t, ("code", sigma, m))
 
 
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_group_code_mode_full_slices(epsm, dev, m):
+    """Code mode at every start matching (2048 matches per 2 KiB slice: pass 3 ranks the slice
+    in two windows of compacted matches) and at about half the starts matching (slices on both
+    sides of the window size), with a few distinct patterns per round."""
+    n = 5 * TILE + 777
+    t = np.tile(np.frombuffer(b"ab", np.uint8), n // 2 + 1)[:n].copy()
+    pats = [(b"ab" * 4)[:m], (b"ba" * 4)[:m], b"b" * m, (b"ab" * 4)[:m]]
+    td = torch.from_numpy(t).to(dev)
+    check(pats, run_group(epsm, pats, td, geom=(m, 0)), t, ("full", m))
+    rng = np.random.default_rng(900 + m)
+    t = rng.integers(0, 2, size=n, dtype=np.uint8)
+    pats = sorted({t[s:s + m].tobytes() for s in range(0, 64)})
+    pats += [pats[0]]
+    td = torch.from_numpy(t).to(dev)
+    check(pats, run_group(epsm, pats, td, geom=(m, 0)), t, ("half", m))
+
+
 def test_group_code_mode_chosen_for_dense_small_alphabets(epsm):
     rng = np.random.default_rng(7)
     t = rng.integers(0, 2, size=1 << 16, dtype=np.uint8)
