@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(CSRC, f) for f in ("epsm.cu", "epsm_sharded.cu", "epsm_multi.cu", "epsm_host.cu", "epsm_long.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("epsm_kernels.cuh", "epsm_multi.cuh", "epsm_ptx.cuh", "epsm_internal.h", "epsm_long.cuh", "epsm_mask.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("epsm_kernels.cuh", "epsm_multi.cuh", "epsm_ptx.cuh", "epsm_internal.h", "epsm_long.cuh", "epsm_mask.cuh", "epsm_code.cuh")] + \
     [os.path.join(ROOT, "include", "epsm.h")]
 OUT = os.path.join(HERE, "libepsm.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

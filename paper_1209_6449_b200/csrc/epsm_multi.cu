@@ -13,9 +13,11 @@
 #include "epsm.h"
 #include "epsm_internal.h"
 #include "epsm_multi.cuh"
+#include "epsm_code.cuh"
 #include "epsm_mask.cuh"
 
 namespace mp = epsm::mp;
+namespace cg = epsm::cg;
 
 namespace {
 
@@ -164,6 +166,7 @@ struct epsm_group_s {
   // 1000 text bytes, dominate; the shared pass gains little there); the rest share the passes
   std::vector<uint32_t> sparse, dense;            // distinct pattern indices
   double sparse_rate = 0;                         // estimated matches per text byte of the sparse ones
+  bool forced_geom = false;                       // epsm_group_set_geometry (tests, A/B)
   std::vector<epsm_plan_t*> dplans;               // plan of dense[i] (one scan, fanned out to its
                                                   // searches: they have the same positions)
 };
@@ -380,6 +383,49 @@ static int set_multi_smem(MKernel fn, bool write) {
   return EPSM_OK;
 }
 
+// EPSM_CODE_CG=0: code-mode groups keep the general group kernels (A/B timing; both exact)
+static bool cg_disabled() {
+  static const bool v = [] {
+    const char* e = getenv("EPSM_CODE_CG");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+
+using CKernel = void (*)(cg::CParams);
+
+template <int M>
+CKernel pick_cg(bool write) {
+  return write ? &cg::cg_write_kernel<M> : &cg::cg_count_kernel<M>;
+}
+
+static CKernel cg_kernel_for(uint32_t m, bool write) {
+  switch (m) {
+    case 1: return pick_cg<1>(write);
+    case 2: return pick_cg<2>(write);
+    case 3: return pick_cg<3>(write);
+    case 4: return pick_cg<4>(write);
+    case 5: return pick_cg<5>(write);
+    case 6: return pick_cg<6>(write);
+    case 7: return pick_cg<7>(write);
+    default: return pick_cg<8>(write);
+  }
+}
+
+static int set_cg_smem(CKernel fn, bool write) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::vector<std::pair<CKernel, int>> done;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), std::make_pair(fn, dev)) != done.end()) return EPSM_OK;
+  const int bytes = static_cast<int>(write ? sizeof(cg::WrSmem) : sizeof(cg::CntSmem));
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(code-mode kernel smem)");
+  done.emplace_back(fn, dev);
+  return EPSM_OK;
+}
+
 // The three launches of one subgroup over d_text[0..nbytes): starts [0, nstarts) reported as
 // start + base.  pos/caps/occ are the caller's batch arrays (indexed by the caller's search).
 static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, uint64_t nbytes, uint64_t nstarts,
@@ -488,12 +534,45 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
     P.jobs = ws->m_jobs;
   }
   const int smem = multi_smem_bytes(false), smem3 = multi_smem_bytes(true);
-  // pass 1: counts per (chunk, distinct pattern), lists of sparse chunks
-  MKernel k1 = multi_kernel_for(S.sk, S.qw, false);
-  rc = set_multi_smem(k1, false);
-  if (rc) return rc;
+  // code-mode groups of <= 127 distinct patterns of length <= 8: the dedicated kernels
+  // (epsm_code.cuh: per-lane counters + staged coalesced write-out instead of match_any rounds)
+  // -- where the chunks overflow the general pass 1's occurrence lists anyway (the lists spare
+  // sparser groups a second read of the text), or where the code mode was forced
+  const bool use_cg = S.sk == 0 && S.D <= static_cast<uint32_t>(cg::kMaxD) && g->m <= static_cast<uint32_t>(cg::kMaxM) &&
+                      !cg_disabled() && (P.direct || g->forced_geom);
+  cg::CParams C;
+  std::memset(&C, 0, sizeof(C));
+  C.text = P.text;
+  C.nbytes = P.nbytes;
+  C.s_lo = P.s_lo;
+  C.s_hi = P.s_hi;
+  C.pos_bias = P.pos_bias;
+  C.nchunks = P.nchunks;
+  C.it_lo = P.it_lo;
+  C.it_hi = P.it_hi;
+  C.cb = P.cb;
+  C.kmask = P.kmask;
+  C.D = P.D;
+  C.desc = P.desc;
+  C.counts = P.counts;
+  C.listlen = P.listlen;
+  C.prefix = P.prefix;
+  C.work = P.work;
+  C.jobs = P.jobs;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(chunks, static_cast<uint64_t>(ws->num_sms)));
-  k1<<<grid, mp::kThreads, smem, s>>>(P);
+  if (use_cg) {
+    // pass 1: counts per (chunk, distinct pattern)
+    CKernel c1 = cg_kernel_for(g->m, false);
+    rc = set_cg_smem(c1, false);
+    if (rc) return rc;
+    c1<<<grid, cg::kCntThreads, sizeof(cg::CntSmem), s>>>(C);
+  } else {
+    // pass 1: counts per (chunk, distinct pattern), lists of sparse chunks
+    MKernel k1 = multi_kernel_for(S.sk, S.qw, false);
+    rc = set_multi_smem(k1, false);
+    if (rc) return rc;
+    k1<<<grid, mp::kThreads, smem, s>>>(P);
+  }
   epsm_count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_kernel (pass 1) launch");
@@ -514,10 +593,17 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_scan_kernel launch");
   if (!search) return EPSM_OK;
   // pass 3: positions of the chunks with occurrences
-  MKernel k3 = multi_kernel_for(S.sk, S.qw, true);
-  rc = set_multi_smem(k3, true);
-  if (rc) return rc;
-  k3<<<ws->num_sms, mp::kThreads, smem3, s>>>(P);
+  if (use_cg) {
+    CKernel c3 = cg_kernel_for(g->m, true);
+    rc = set_cg_smem(c3, true);
+    if (rc) return rc;
+    c3<<<ws->num_sms, cg::kWrThreads, sizeof(cg::WrSmem), s>>>(C);
+  } else {
+    MKernel k3 = multi_kernel_for(S.sk, S.qw, true);
+    rc = set_multi_smem(k3, true);
+    if (rc) return rc;
+    k3<<<ws->num_sms, mp::kThreads, smem3, s>>>(P);
+  }
   epsm_count_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_multi_kernel (pass 3) launch");
@@ -933,6 +1019,7 @@ int epsm_group_set_geometry(epsm_group_t* g, uint32_t q, uint32_t sk) {
     cudaDeviceSynchronize();
   }
   // a forced geometry puts every distinct pattern through the group kernels
+  g->forced_geom = true;
   g->sparse.clear();
   g->dense.clear();
   for (uint32_t d = 0; d < g->D; ++d) g->sparse.push_back(d);
@@ -949,6 +1036,7 @@ int epsm_group_set_dense(epsm_group_t* g, uint32_t log2_rate) {
     cudaDeviceSynchronize();
   }
   group_split(g, log2_rate == 0 ? 4096 : static_cast<int>(log2_rate));
+  g->forced_geom = false;
   return group_partition(g);
 }
 

@@ -46,6 +46,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Polling wait with a back-off for a warp that is idle most of the time (a TMA producer ahead of
+// its consumers): every failed test sleeps ~ns, so the spin takes almost no issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
+}
+
 // Blocking wait for an idle warp: try_wait with a suspend-time hint parks the warp in hardware
 // until the phase completes (no issue slots spent polling).
 __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
