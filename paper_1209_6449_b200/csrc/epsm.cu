@@ -588,6 +588,22 @@ int epsm_launch_jobs(const epsm_job* jobs, uint32_t k, const uint8_t* d_text, ui
 
 // fan-out: occ and positions of a job to its further outputs (identical patterns)
 static int launch_fanout(const epsm_job* jobs, uint32_t k, bool search, cudaStream_t s, epsm_workspace* ws) {
+  // the fan-outs of the launch's searches together (one launch where the buffers allow): every
+  // job's outputs are a run of the same device / host XOut tables
+  int j0 = -1;
+  for (uint32_t j = 0; j < k; ++j)
+    if (jobs[j].nx && jobs[j].xh && (j0 < 0 || jobs[j].xh < jobs[j0].xh)) j0 = static_cast<int>(j);
+  bool tables = j0 >= 0;
+  for (uint32_t j = 0; j < k && tables; ++j)
+    if (jobs[j].nx && !jobs[j].xh) tables = false;
+  if (tables) {
+    std::vector<epsm_rep_req> rq;
+    for (uint32_t j = 0; j < k; ++j)
+      if (jobs[j].nx)
+        rq.push_back(epsm_rep_req{jobs[j].d_pos, jobs[j].cap, jobs[j].d_occ,
+                                  static_cast<uint32_t>(jobs[j].xh - jobs[j0].xh), jobs[j].nx});
+    return epsm_replicate_many(rq.data(), static_cast<uint32_t>(rq.size()), jobs[j0].x, jobs[j0].xh, search, s, ws);
+  }
   for (uint32_t j = 0; j < k; ++j) {
     if (jobs[j].nx == 0) continue;
     int rc = epsm_replicate(jobs[j].d_pos, jobs[j].cap, jobs[j].d_occ, jobs[j].x, jobs[j].nx, search, s, ws);
@@ -627,6 +643,68 @@ int epsm_replicate(const uint64_t* d_pos, uint64_t cap, const unsigned long long
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_replicate_kernel launch");
+  }
+  return EPSM_OK;
+}
+
+int epsm_replicate_many(const epsm_rep_req* r, uint32_t nr, const epsm::XOut* d_x, const epsm::XOut* h_x, bool search,
+                        cudaStream_t s, epsm_workspace* ws) {
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  std::vector<epsm::RepJobD> jobs;
+  for (uint32_t i = 0; i < nr; ++i) {
+    const epsm_rep_req& q = r[i];
+    bool ok = q.nx <= epsm::kRepMultiOut && a16(q.pos);
+    for (uint32_t o = 0; ok && o < q.nx; ++o)
+      if (h_x[q.x0 + o].pos && !a16(h_x[q.x0 + o].pos)) ok = false;
+    if (!ok || !search) {                                          // (the single-source kernel)
+      int rc = epsm_replicate(q.pos, q.cap, q.occ, d_x + q.x0, q.nx, search, s, ws);
+      if (rc) return rc;
+      continue;
+    }
+    jobs.push_back(epsm::RepJobD{q.pos, q.occ, q.cap, q.x0, q.nx});
+  }
+  if (jobs.empty()) return EPSM_OK;
+  cudaError_t e = cudaSuccess;
+  if (ws->num_sms <= 0) {
+    e = cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, ws->device);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  }
+  {                                                                // (per device: the attribute is per device)
+    static std::mutex mu;
+    static std::vector<int> devs;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(devs.begin(), devs.end(), ws->device) == devs.end()) {
+      e = cudaFuncSetAttribute(epsm::epsm_replicate_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(epsm::RepMultiSmem)));
+      if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaFuncSetAttribute(replicate multi)");
+      devs.push_back(ws->device);
+    }
+  }
+  for (size_t a = 0; a < jobs.size(); a += epsm::kRepMaxJobs) {
+    const uint32_t nj = static_cast<uint32_t>(std::min<size_t>(jobs.size() - a, epsm::kRepMaxJobs));
+    if (ws->repjobs_cap < jobs.size()) {
+      if (ws->d_repjobs) {
+        cudaStreamSynchronize(s);
+        cudaFree(ws->d_repjobs);
+        ws->d_repjobs = nullptr;
+        ws->repjobs_cap = 0;
+      }
+      e = cudaMalloc(&ws->d_repjobs, jobs.size() * sizeof(epsm::RepJobD));
+      if (e != cudaSuccess) {
+        epsm_set_error("cudaMalloc(fan-out job table): %s", cudaGetErrorString(e));
+        return EPSM_ENOMEM;
+      }
+      ws->repjobs_cap = jobs.size();
+    }
+    epsm::RepJobD* dj = static_cast<epsm::RepJobD*>(ws->d_repjobs) + a;
+    // (a pageable source is staged before cudaMemcpyAsync returns: the vector may go)
+    e = cudaMemcpyAsync(dj, jobs.data() + a, nj * sizeof(epsm::RepJobD), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out job table)");
+    epsm::epsm_replicate_multi_kernel<<<EPSM_REP_CTAS_PER_SM * ws->num_sms, epsm::kRepThreads,
+                                        sizeof(epsm::RepMultiSmem), s>>>(dj, nj, d_x);
+    epsm_count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_replicate_multi_kernel launch");
   }
   return EPSM_OK;
 }

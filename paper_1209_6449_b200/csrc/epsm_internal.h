@@ -83,6 +83,8 @@ struct epsm_workspace {
   uint64_t l_prefix_cap = 0;
   epsm::XOut* d_xout = nullptr;               // fan-out outputs of a batch call (device)
   uint64_t xout_cap = 0;                      // entries
+  void* d_repjobs = nullptr;                  // job table of the multi-source fan-out (device)
+  uint64_t repjobs_cap = 0;                   // entries
   unsigned long long exit_total[2] = {0, 0};  // CTAs launched so far on each parity
 };
 
@@ -135,6 +137,17 @@ int epsm_upload_pattern(epsm_plan_t* plan, cudaStream_t s);
 // (device XOut table), on stream s
 int epsm_replicate(const uint64_t* d_pos, uint64_t cap, const unsigned long long* d_occ, const epsm::XOut* x,
                    uint32_t nx, bool search, cudaStream_t s, epsm_workspace* ws);
+// Many fan-outs at once: request r copies source pos[r] (capacity cap[r], occ occ[r]) to the
+// outputs d_x[x0 .. x0 + nx) (device table; h_x: the same table on the host, for the alignment
+// check).  Sources and outputs in the 16-byte phase go through one launch, the rest one by one.
+struct epsm_rep_req {
+  const uint64_t* pos;
+  uint64_t cap;
+  const unsigned long long* occ;
+  uint32_t x0, nx;
+};
+int epsm_replicate_many(const epsm_rep_req* r, uint32_t nr, const epsm::XOut* d_x, const epsm::XOut* h_x, bool search,
+                        cudaStream_t s, epsm_workspace* ws);
 
 // Equality-mask index of one text (epsm_eqidx_build_async).
 struct epsm_eqidx_s {

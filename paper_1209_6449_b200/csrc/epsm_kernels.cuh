@@ -1674,6 +1674,112 @@ __global__ void __launch_bounds__(kRepThreads) epsm_replicate_kernel(const uint6
   if (threadIdx.x == 0) bulk_wait0();
 }
 
+// The fan-outs of many searches in ONE launch (a group's duplicate patterns: dozens of copies of
+// a few MB each, which one launch per source spends on ramp and tail): the sources' chunks are
+// numbered one after another (job j's chunks start at cfirst[j], from its occ on the device) and
+// the CTAs stride over that list; the outputs of the job of the current chunk sit in shared
+// memory (reloaded when the job changes).  Only sources and outputs in the 16-byte phase (the
+// library's own buffers; the host routes the rest to epsm_replicate_kernel).
+constexpr int kRepMaxJobs = 256;
+constexpr uint32_t kRepMultiOut = 256;
+struct RepJobD {
+  const uint64_t* src;
+  const unsigned long long* occ;
+  uint64_t cap;
+  uint32_t x0, nx;              // outputs x[x0 .. x0 + nx)
+};
+struct RepMultiSmem {
+  uint64_t buf[kRepStages][kRepChunk / 8];
+  uint64_t* pos[kRepMultiOut];
+  uint64_t cnt[kRepMultiOut];
+  uint64_t cfirst[kRepMaxJobs + 1];
+  uint64_t have[kRepMaxJobs];
+  alignas(8) uint64_t full[kRepStages];
+};
+
+__global__ void __launch_bounds__(kRepThreads) epsm_replicate_multi_kernel(const RepJobD* __restrict__ J, uint32_t nj,
+                                                                           const XOut* __restrict__ x) {
+  extern __shared__ __align__(128) uint8_t rep_raw[];
+  RepMultiSmem& S = *reinterpret_cast<RepMultiSmem*>(rep_raw);
+  for (uint32_t j = threadIdx.x; j < nj; j += blockDim.x) {
+    const unsigned long long occ = *J[j].occ;
+    S.have[j] = J[j].src ? (occ < J[j].cap ? occ : J[j].cap) : 0;
+    if (blockIdx.x == 0)
+      for (uint32_t o = 0; o < J[j].nx; ++o) *x[J[j].x0 + o].occ = occ;
+  }
+  if (threadIdx.x < kRepStages) mbar_init(&S.full[threadIdx.x], 1);
+  fence_mbar_init();
+  __syncthreads();
+  const uint64_t per = kRepChunk / 8;
+  if (threadIdx.x == 0) {
+    uint64_t c = 0;
+    for (uint32_t j = 0; j < nj; ++j) {
+      S.cfirst[j] = c;
+      c += (S.have[j] + per - 1) / per;
+    }
+    S.cfirst[nj] = c;
+  }
+  __syncthreads();
+  const uint64_t total = S.cfirst[nj];
+  uint32_t jf = 0;                                                 // job of the next chunk to fetch
+  auto issue = [&](uint64_t c, int st) {                           // thread 0: chunk c -> stage st
+    while (S.cfirst[jf + 1] <= c) ++jf;
+    const uint64_t e0 = (c - S.cfirst[jf]) * per;
+    const uint64_t ne = S.have[jf] - e0 < per ? S.have[jf] - e0 : per;
+    const uint32_t bytes = static_cast<uint32_t>((ne * 8) & ~15ull);
+    mbar_arrive_expect_tx(&S.full[st], bytes);
+    if (bytes) bulk_g2s_plain(S.buf[st], J[jf].src + e0, bytes, &S.full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int st = 0; st < kRepStages; ++st) {
+      const uint64_t c = blockIdx.x + static_cast<uint64_t>(st) * gridDim.x;
+      if (c < total) issue(c, st);
+    }
+  uint32_t phase = 0, jc = 0, cur = 0xFFFFFFFFu;
+  int st = 0;
+  for (uint64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    while (S.cfirst[jc + 1] <= c) ++jc;                             // (uniform: every thread alike)
+    if (jc != cur) {                                               // the outputs of job jc
+      const uint64_t have = S.have[jc];
+      for (uint32_t o = threadIdx.x; o < J[jc].nx; o += blockDim.x) {
+        const XOut X = x[J[jc].x0 + o];
+        S.pos[o] = X.pos;
+        S.cnt[o] = X.pos ? (X.cap < have ? X.cap : have) : 0;
+      }
+      __syncthreads();
+      cur = jc;
+    }
+    mbar_wait(&S.full[st], phase);
+    const uint64_t e0 = (c - S.cfirst[jc]) * per;
+    const uint64_t ne = S.have[jc] - e0 < per ? S.have[jc] - e0 : per;
+    if (threadIdx.x == 0) {
+      const uint64_t last = (ne & 1u) ? J[jc].src[e0 + ne - 1] : 0;   // (not in the 16-byte bulk part)
+      const uint32_t nx = J[jc].nx;
+      for (uint32_t o = 0; o < nx; ++o) {
+        const uint64_t cnt = S.cnt[o];
+        if (cnt <= e0) continue;
+        uint64_t* d = S.pos[o] + e0;
+        const uint64_t n = cnt - e0 < ne ? cnt - e0 : ne;
+        const uint32_t bytes = static_cast<uint32_t>((n * 8) & ~15ull);
+        if (bytes) bulk_s2g(d, S.buf[st], bytes);
+        if (n & 1u) d[n - 1] = (n == ne) ? last : S.buf[st][n - 1];
+      }
+      bulk_commit();
+    }
+    __syncthreads();                                               // shared-memory reads done
+    if (threadIdx.x == 0) {
+      bulk_wait_read0();                                           // ... and the bulk stores' reads
+      const uint64_t cn = c + static_cast<uint64_t>(kRepStages) * gridDim.x;
+      if (cn < total) issue(cn, st);
+    }
+    if (++st == kRepStages) {
+      st = 0;
+      phase ^= 1u;
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
 constexpr int kMaxPlanes = 256;
 struct IdxParams {
   const uint8_t* text;          // 16-byte aligned

@@ -625,12 +625,15 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
     }
     e = cudaMemcpyAsync(ws->d_xout, S.rep_x.data(), S.rep_x.size() * sizeof(epsm::XOut), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out table)");
-    uint64_t off = 0;
+    // every duplicated pattern's further outputs in one fan-out launch
+    std::vector<epsm_rep_req> rq;
+    uint32_t off = 0;
     for (const RepJob& r : S.rep_jobs) {
-      rc = epsm_replicate(r.pos, r.cap, r.occ, ws->d_xout + off, r.nx, true, s, ws);
-      if (rc) return rc;
+      rq.push_back(epsm_rep_req{r.pos, r.cap, r.occ, off, r.nx});
       off += r.nx;
     }
+    rc = epsm_replicate_many(rq.data(), static_cast<uint32_t>(rq.size()), ws->d_xout, S.rep_x.data(), true, s, ws);
+    if (rc) return rc;
   }
   return EPSM_OK;
 }
@@ -656,7 +659,14 @@ static int group_bind(epsm_group_t* g, const void* dptr) {
   return EPSM_OK;
 }
 
-constexpr uint32_t kMaskMinPatterns = 24;
+// EPSM_MASK_MIN=k: smallest dense set sent through the mask pass (A/B; default 24)
+static uint32_t mask_min_patterns() {
+  static const uint32_t v = [] {
+    const char* e = getenv("EPSM_MASK_MIN");
+    return e ? static_cast<uint32_t>(atoi(e)) : 24u;
+  }();
+  return v;
+}
 
 // EPSM_MASK=0: the dense patterns keep the one-by-one scans (A/B)
 static bool mask_disabled() {
@@ -679,7 +689,7 @@ static int mask_run(epsm_group_t* g, const epsm_eqidx_t* index, const uint8_t* d
   // (only for many dense patterns: a few are faster one by one, their scans write the bulk of
   // their positions with staged 16-byte stores -- sigma=2 m=4, 16 patterns: 4.0 ms either way;
   // sigma=8 m=2, 50 patterns: 2.8 vs 3.8 ms)
-  if (mask_disabled() || D < kMaskMinPatterns || D > static_cast<uint32_t>(mk::kMaxD) ||
+  if (mask_disabled() || D < mask_min_patterns() || D > static_cast<uint32_t>(mk::kMaxD) ||
       g->m > static_cast<uint32_t>(mk::kMaxM))
     return 1;
   if (reinterpret_cast<uintptr_t>(d_text) & 15u) return 1;
@@ -775,12 +785,15 @@ static int mask_run(epsm_group_t* g, const epsm_eqidx_t* index, const uint8_t* d
     }
     cudaError_t e = cudaMemcpyAsync(ws->d_xout, xo.data(), xo.size() * sizeof(epsm::XOut), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out table)");
-    uint64_t off = 0;
+    // every pattern's further outputs in one fan-out launch
+    std::vector<epsm_rep_req> rq;
+    uint32_t off = 0;
     for (const auto& r : rep) {
-      rc = epsm_replicate(P.pos[r.first], P.cap[r.first], P.occ[r.first], ws->d_xout + off, r.second, search, s, ws);
-      if (rc) return rc;
+      rq.push_back(epsm_rep_req{P.pos[r.first], P.cap[r.first], P.occ[r.first], off, r.second});
       off += r.second;
     }
+    rc = epsm_replicate_many(rq.data(), static_cast<uint32_t>(rq.size()), ws->d_xout, xo.data(), search, s, ws);
+    if (rc) return rc;
   }
   return 0;
 }
