@@ -166,10 +166,33 @@ __global__ void __launch_bounds__(1024) epsm_mask_scan_kernel(const __grid_const
   }
 }
 
+// a lane's run of positions: the set bits of M (starts pb + bit) to out[g ..]; cap checked once
+// per run (all of it fits: no per-element test)
+__device__ __forceinline__ void write_run(uint64_t M, uint64_t* out, uint64_t g, uint64_t cap, uint64_t pb, uint32_t c) {
+  uint64_t* o = out + g;
+  if (g + c <= cap) {
+    for (uint32_t lo = static_cast<uint32_t>(M); lo; lo &= lo - 1) st_stream_u64(o++, pb + (__ffs(lo) - 1));
+    for (uint32_t hi = static_cast<uint32_t>(M >> 32); hi; hi &= hi - 1) st_stream_u64(o++, pb + 31 + __ffs(hi));
+  } else {
+    while (M) {
+      const uint32_t bit = __ffsll(static_cast<long long>(M)) - 1;
+      M &= M - 1;
+      if (g < cap) st_stream_u64(out + g, pb + bit);
+      ++g;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) epsm_mask_write_kernel(const __grid_constant__ MaskParams P) {
   __shared__ uint64_t SH[kWarps][kMaxSh][32];
   __shared__ unsigned long long base[kWarps][kMaxD];   // the task's next output slot per pattern
   __shared__ uint8_t shs[kMaxD][kMaxM];
+  __shared__ uint64_t* spos[kMaxD];
+  __shared__ uint64_t scap[kMaxD];
+  for (uint32_t d = threadIdx.x; d < kMaxD; d += blockDim.x) {
+    spos[d] = P.pos[d];
+    scap[d] = P.cap[d];
+  }
   load_sh(P, shs);
   const uint32_t lane = threadIdx.x & 31u, wp = threadIdx.x >> 5;
   bool waited = false;
@@ -184,29 +207,29 @@ __global__ void __launch_bounds__(kThreads) epsm_mask_write_kernel(const __grid_
     for (int r = 0; r < kRounds; ++r) {
       const uint64_t w = stage_round(P, task, r, lane, SH[wp]);
       const uint64_t pb = w * 64 + P.pos_bias;
-      for (uint32_t d = 0; d < P.D; ++d) {
-        uint64_t M = pattern_mask(P, shs, d, w, lane, SH[wp]);
-        const uint32_t c = __popcll(M);
+      for (uint32_t d = 0; d < P.D; d += 2) {
+        // two patterns per warp scan (their counts as the u16 halves of one word: <= 64 per lane,
+        // <= 2048 per round, no carry between the halves)
+        const bool two = d + 1 < P.D;
+        const uint64_t M0 = pattern_mask(P, shs, d, w, lane, SH[wp]);
+        const uint64_t M1 = two ? pattern_mask(P, shs, d + 1, w, lane, SH[wp]) : 0ull;
+        const uint32_t c0 = __popcll(M0), c1 = __popcll(M1);
         // exclusive offset of this lane's matches among the round's (lanes in text order); each
         // lane stores its own run (the runs of consecutive lanes are adjacent in the output)
-        uint32_t incl = c;
+        uint32_t incl = c0 | (c1 << 16);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= static_cast<uint32_t>(o)) incl += y;
         }
-        const unsigned long long b0 = base[wp][d];
-        const uint64_t cap = P.cap[d];
-        uint64_t g = b0 + incl - c;
-        uint64_t* out = P.pos[d];
-        while (M) {
-          const uint32_t bit = __ffsll(static_cast<long long>(M)) - 1;
-          M &= M - 1;
-          if (g < cap) st_stream_u64(out + g, pb + bit);
-          ++g;
-        }
+        const uint32_t i0 = incl & 0xFFFFu, i1 = incl >> 16;
+        write_run(M0, spos[d], base[wp][d] + i0 - c0, scap[d], pb, c0);
+        if (two) write_run(M1, spos[d + 1], base[wp][d + 1] + i1 - c1, scap[d + 1], pb, c1);
         __syncwarp();
-        if (lane == 31) base[wp][d] = b0 + incl;
+        if (lane == 31) {
+          base[wp][d] += i0;
+          if (two) base[wp][d + 1] += i1;
+        }
         __syncwarp();
       }
     }
