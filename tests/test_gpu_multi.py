@@ -412,3 +412,33 @@ def test_group_mask_pass(epsm, dev, sigma, m):
     for j, w in enumerate(wants):
         assert np.array_equal(np.concatenate(parts[j]), w), ("shard", j)
     g.close()
+
+
+@pytest.mark.parametrize("dense", [64, 0])
+def test_group_many_fanout_sources(epsm, dev, dense):
+    """More than 256 duplicated distinct patterns: the multi-source fan-out splits its job table
+    into launches of <= 256 sources (dense=64: every pattern scanned one by one and fanned out
+    by the batch path; dense=0: the group passes, duplicates fanned out after pass 3), with
+    outputs of both 16-byte phases (those sources go through the single-source kernel), odd and
+    zero occurrence counts, and capacities below occ."""
+    rng = np.random.default_rng(4242 + dense)
+    n = 9 * TILE + 333
+    t = rng.integers(0, 32, size=n, dtype=np.uint8)
+    distinct = sorted({t[s:s + 3].tobytes() for s in range(0, n - 2, 97)})[:300]
+    assert len(distinct) == 300
+    pats = distinct + distinct[:280] + [bytes([200, 201, 202])] * 2      # (the last: no occurrence)
+    wants = {p: oracle.search(p, t) for p in set(pats)}
+    g = epsm.group(pats).set_dense(dense)
+    bufs = [torch.full((wants[p].size + 8,), -4, dtype=torch.int64, device=dev) for p in pats]
+    outs = [b[1:] if j % 7 == 3 else b for j, b in enumerate(bufs)]      # some in the other phase
+    caps = [wants[p].size if j % 11 else max(0, wants[p].size - 1) for j, p in enumerate(pats)]
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    g.search_async(torch.from_numpy(t).to(dev), occ, outs=outs, caps=caps)
+    torch.cuda.synchronize()
+    for j, p in enumerate(pats):
+        w = wants[p]
+        assert int(occ[j]) == w.size, j
+        c = min(w.size, caps[j])
+        assert np.array_equal(outs[j][:c].cpu().numpy().astype(np.uint64), w[:c]), j
+        assert int(outs[j][c]) == -4, j
+    g.close()
