@@ -44,6 +44,8 @@ for cfg in a.configs.split(","):
                 p.close()
             if vals:
                 ix = epsm.EqIndex()
+                ix.build_async(text, vals, stream=stream)      # (allocates the planes: not timed)
+                torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 ix.build_async(text, vals, stream=stream)
