@@ -59,6 +59,8 @@ struct CParams {
   uint32_t cb;                  // bits per symbol code
   uint32_t kmask;               // 2^(m * cb) - 1
   uint32_t D;                   // distinct patterns (<= kMaxD)
+  uint32_t invmask;             // code bits that mark a byte outside the alphabet (IDENT: the byte's
+                                // bits above cb; else cmap's 0x80)
   const mp::GroupDesc* desc;    // cmap, key table (overlaying bitmap + boff), dup lists
   uint16_t* counts;             // [D][nchunks]: pass 1 out
   uint32_t* listlen;            // [nchunks]: nonzero <=> the chunk holds a match (pass 1 out)
@@ -142,13 +144,14 @@ __device__ __forceinline__ uint64_t keep_mask(uint64_t ub, const CParams& P) {
 }
 
 // Starts of the lane whose window holds a byte outside the patterns' alphabet (no spare code)
-template <int M>
-__device__ uint64_t invalid_starts(const uint8_t* ts, uint32_t seg, const uint8_t* cmap) {
+template <int M, bool IDENT>
+__device__ uint64_t invalid_starts(const uint8_t* ts, uint32_t seg, const uint8_t* cmap, uint32_t invmask) {
   uint64_t bad = 0;
   int last = -64;
 #pragma unroll 1
   for (int t = 0; t < kSeg + M - 1; ++t) {
-    if (cmap[ts[seg + t]] & 0x80u) last = t;
+    const uint32_t b = ts[seg + t];
+    if ((IDENT ? b : cmap[b]) & invmask) last = t;
     if (t >= M - 1 && t - last < M) bad |= 1ull << (t - (M - 1));
   }
   return bad;
@@ -156,17 +159,22 @@ __device__ uint64_t invalid_starts(const uint8_t* ts, uint32_t seg, const uint8_
 
 // The fast path's id of start s (same arithmetic as the unrolled filters: garbage for windows
 // with an invalid byte, which is exactly what has to be undone)
-template <int M>
+template <int M, bool IDENT>
 __device__ __forceinline__ uint32_t fast_id(const uint8_t* ts, uint32_t st, const uint8_t* cmap, const uint8_t* tab,
                                             uint32_t cb, uint32_t kmask) {
   uint32_t key = 0;
 #pragma unroll
-  for (int j = 0; j < M; ++j) key = ((key << cb) | cmap[ts[st + j]]) & kmask;
+  for (int j = 0; j < M; ++j) {
+    const uint32_t b = ts[st + j];
+    key = ((key << cb) | (IDENT ? b : cmap[b])) & kmask;
+  }
   return tab[key];
 }
 
+// IDENT: every pattern byte is below 2^cb and is its own code (the byte values of small symbol
+// alphabets): no cmap load per start; a byte with a bit at or above cb marks an invalid window.
 // ===================================================================================== pass 1
-template <int M>
+template <int M, bool IDENT>
 __global__ void __launch_bounds__(kCntThreads, 1) cg_count_kernel(const __grid_constant__ CParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   CntSmem& S = *reinterpret_cast<CntSmem*>(smem_raw);
@@ -236,8 +244,10 @@ __global__ void __launch_bounds__(kCntThreads, 1) cg_count_kernel(const __grid_c
 #pragma unroll
     for (int t = 0; t < kSeg / 2 + M - 1; ++t) {
       const int tb = t + kSeg / 2;
-      const uint32_t ca = S.cmap[__byte_perm(W[t >> 2], 0u, 0x4440u | (t & 3))];
-      const uint32_t cbb = S.cmap[__byte_perm(W[tb >> 2], 0u, 0x4440u | (tb & 3))];
+      const uint32_t ba = __byte_perm(W[t >> 2], 0u, 0x4440u | (t & 3));
+      const uint32_t bb = __byte_perm(W[tb >> 2], 0u, 0x4440u | (tb & 3));
+      const uint32_t ca = IDENT ? ba : S.cmap[ba];
+      const uint32_t cbb = IDENT ? bb : S.cmap[bb];
       inv |= ca | cbb;
       ka = ((ka << cb) | ca) & kmask;
       kb = ((kb << cb) | cbb) & kmask;
@@ -250,11 +260,11 @@ __global__ void __launch_bounds__(kCntThreads, 1) cg_count_kernel(const __grid_c
     // holds a byte outside the alphabet (no spare code)
     uint64_t sub = 0;
     if (!(c >= P.it_lo && c < P.it_hi)) sub = ~keep_mask(static_cast<uint64_t>(c) * kTile + seg, P);
-    if (inv & 0x80u) sub |= invalid_starts<M>(ts, seg, S.cmap);
+    if (inv & P.invmask) sub |= invalid_starts<M, IDENT>(ts, seg, S.cmap, P.invmask);
     while (sub) {
       const uint32_t s = __ffsll(static_cast<long long>(sub)) - 1;
       sub &= sub - 1;
-      atomicSub(&h[fast_id<M>(ts, seg + s, S.cmap, S.tab, cb, kmask)], 1u);
+      atomicSub(&h[fast_id<M, IDENT>(ts, seg + s, S.cmap, S.tab, cb, kmask)], 1u);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[stage]);
@@ -285,7 +295,7 @@ __global__ void __launch_bounds__(kCntThreads, 1) cg_count_kernel(const __grid_c
 }
 
 // ===================================================================================== pass 3
-template <int M>
+template <int M, bool IDENT>
 __global__ void __launch_bounds__(kWrThreads, 1) cg_write_kernel(const __grid_constant__ CParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   WrSmem& S = *reinterpret_cast<WrSmem*>(smem_raw);
@@ -389,8 +399,10 @@ __global__ void __launch_bounds__(kWrThreads, 1) cg_write_kernel(const __grid_co
         for (int t = 0; t < kSeg / 2 + M - 1; ++t) {
           // two independent key chains: starts 0..31 (bytes t) and 32..63 (bytes t + 32)
           const int tb = t + kSeg / 2;
-          const uint32_t ca = S.cmap[__byte_perm(W[t >> 2], 0u, 0x4440u | (t & 3))];
-          const uint32_t cbb = S.cmap[__byte_perm(W[tb >> 2], 0u, 0x4440u | (tb & 3))];
+          const uint32_t ba = __byte_perm(W[t >> 2], 0u, 0x4440u | (t & 3));
+          const uint32_t bb = __byte_perm(W[tb >> 2], 0u, 0x4440u | (tb & 3));
+          const uint32_t ca = IDENT ? ba : S.cmap[ba];
+          const uint32_t cbb = IDENT ? bb : S.cmap[bb];
           inv |= ca | cbb;
           ka = ((ka << cb) | ca) & kmask;
           kb = ((kb << cb) | cbb) & kmask;
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(kWrThreads, 1) cg_write_kernel(const __grid_co
       // starts that do not count get 0xFF: outside [s_lo, s_hi), or windows with an invalid byte
       uint64_t drop = 0;
       if (!interior) drop = ~keep_mask(static_cast<uint64_t>(c) * kTile + seg, P);
-      if (inv & 0x80u) drop |= invalid_starts<M>(ts, seg, S.cmap);
+      if (inv & P.invmask) drop |= invalid_starts<M, IDENT>(ts, seg, S.cmap, P.invmask);
       if (drop) {
 #pragma unroll
         for (int w = 0; w < 16; ++w) {

@@ -35,6 +35,7 @@ struct Subgroup {
   int q = 1, sk = 1, qw = 1;           // sk = 0: code mode (every start keyed, exact)
   uint32_t cb = 0;                     // code mode: bits per symbol code
   bool spare = false;                  // code mode: a spare code marks bytes outside the alphabet
+  bool ident = false;                  // code mode: every pattern byte < 2^cb is its own code
   uint32_t qmask = 0xFFu, hmul[4] = {0, 0, 0, 0};
   std::vector<uint32_t> jobs;          // the caller's search index of local search j
   mp::GroupDesc* h_desc = nullptr;
@@ -179,6 +180,15 @@ static bool code_disabled() {
   }();
   return v;
 }
+// EPSM_CODE_IDENT=0: code mode always codes the pattern bytes by rank (A/B; both exact)
+static bool ident_disabled() {
+  static const bool v = [] {
+    const char* e = getenv("EPSM_CODE_IDENT");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+
 // the code mode's cost in the cost model's units (lane instructions per 64 text bytes): 80 key
 // steps of ~10 instructions
 constexpr double kCodeCost = 850.0;
@@ -227,6 +237,20 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
       S.cb = cb + 1;
       S.spare = true;
     }
+    // identity codes where every pattern byte is below 2^cb' and the key still fits the table
+    // (the code-mode kernels then skip the byte -> code load per start); no spare code needed:
+    // a non-pattern byte below 2^cb' is its own code (no pattern key holds it), one above is
+    // invalid
+    uint32_t maxb = 0;
+    for (int c = 0; c < 256; ++c)
+      if (cnt[c]) maxb = static_cast<uint32_t>(c);
+    uint32_t cbi = 1;
+    while ((1u << cbi) <= maxb) ++cbi;
+    if (!wide && m * cbi <= static_cast<uint32_t>(mp::kCodeKeyBits) && !ident_disabled()) {
+      S.cb = cbi;
+      S.spare = false;
+      S.ident = true;
+    }
   } else if (force_q) {
     S.q = force_q;
     S.sk = force_sk;
@@ -253,8 +277,12 @@ static int build_subgroup(const std::vector<std::string>& pats, uint32_t m, Subg
     for (int c = 0; c < 256; ++c) code += cnt[c] ? 1u : 0u;
     std::memset(G.cmap, S.spare ? static_cast<int>(code) : 0x80, sizeof(G.cmap));   // (spare code = sigma')
     code = 0;
-    for (int c = 0; c < 256; ++c)
-      if (cnt[c]) G.cmap[c] = static_cast<uint8_t>(code++);
+    if (S.ident) {
+      for (int c = 0; c < (1 << S.cb); ++c) G.cmap[c] = static_cast<uint8_t>(c);
+    } else {
+      for (int c = 0; c < 256; ++c)
+        if (cnt[c]) G.cmap[c] = static_cast<uint8_t>(code++);
+    }
     uint8_t* lut = reinterpret_cast<uint8_t*>(G.bitmap);
     if (S.sk == 0) std::memset(lut, 0xFF, 1u << mp::kCodeKeyBits);
     else wide_buckets.assign(1u << mp::kBucketLog, {});
@@ -395,20 +423,21 @@ static bool cg_disabled() {
 using CKernel = void (*)(cg::CParams);
 
 template <int M>
-CKernel pick_cg(bool write) {
-  return write ? &cg::cg_write_kernel<M> : &cg::cg_count_kernel<M>;
+CKernel pick_cg(bool write, bool ident) {
+  if (ident) return write ? &cg::cg_write_kernel<M, true> : &cg::cg_count_kernel<M, true>;
+  return write ? &cg::cg_write_kernel<M, false> : &cg::cg_count_kernel<M, false>;
 }
 
-static CKernel cg_kernel_for(uint32_t m, bool write) {
+static CKernel cg_kernel_for(uint32_t m, bool write, bool ident) {
   switch (m) {
-    case 1: return pick_cg<1>(write);
-    case 2: return pick_cg<2>(write);
-    case 3: return pick_cg<3>(write);
-    case 4: return pick_cg<4>(write);
-    case 5: return pick_cg<5>(write);
-    case 6: return pick_cg<6>(write);
-    case 7: return pick_cg<7>(write);
-    default: return pick_cg<8>(write);
+    case 1: return pick_cg<1>(write, ident);
+    case 2: return pick_cg<2>(write, ident);
+    case 3: return pick_cg<3>(write, ident);
+    case 4: return pick_cg<4>(write, ident);
+    case 5: return pick_cg<5>(write, ident);
+    case 6: return pick_cg<6>(write, ident);
+    case 7: return pick_cg<7>(write, ident);
+    default: return pick_cg<8>(write, ident);
   }
 }
 
@@ -553,6 +582,7 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   C.cb = P.cb;
   C.kmask = P.kmask;
   C.D = P.D;
+  C.invmask = S.ident ? (0xFFu & ~((1u << S.cb) - 1u)) : 0x80u;
   C.desc = P.desc;
   C.counts = P.counts;
   C.listlen = P.listlen;
@@ -562,7 +592,7 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(chunks, static_cast<uint64_t>(ws->num_sms)));
   if (use_cg) {
     // pass 1: counts per (chunk, distinct pattern)
-    CKernel c1 = cg_kernel_for(g->m, false);
+    CKernel c1 = cg_kernel_for(g->m, false, S.ident);
     rc = set_cg_smem(c1, false);
     if (rc) return rc;
     c1<<<grid, cg::kCntThreads, sizeof(cg::CntSmem), s>>>(C);
@@ -594,7 +624,7 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   if (!search) return EPSM_OK;
   // pass 3: positions of the chunks with occurrences
   if (use_cg) {
-    CKernel c3 = cg_kernel_for(g->m, true);
+    CKernel c3 = cg_kernel_for(g->m, true, S.ident);
     rc = set_cg_smem(c3, true);
     if (rc) return rc;
     c3<<<ws->num_sms, cg::kWrThreads, sizeof(cg::WrSmem), s>>>(C);
