@@ -42,6 +42,9 @@ constexpr int kCntStages = 4;
 constexpr int kWrStages = 2;
 constexpr int kMaxD = 127;                        // ids 0..126; 0xFF: no pattern
 constexpr int kMaxM = 8;
+#ifndef EPSM_CG_CHAINS
+#define EPSM_CG_CHAINS 2                          // key chains per lane in pass 1
+#endif
 constexpr int kTab = 1 << mp::kCodeKeyBits;       // key table bytes (16 KiB)
 constexpr int kIdsLane = 80;                      // id bytes per lane (16-B aligned, STS.128 conflict-free)
 constexpr int kRows = (kMaxD + 1) / 2;            // counter rows: ids 2r (low half), 2r+1 (high half)
@@ -238,22 +241,26 @@ __global__ void __launch_bounds__(kCntThreads, 1) cg_count_kernel(const __grid_c
     const uint8_t* ts = S.ring[stage];
     uint32_t W[20];
     load_window(ts, seg, lane, W);
-    // every start of the lane: key -> id, counted (no pattern: the dummy counter 255); two
-    // independent key chains (starts 0..31 and 32..63) for instruction-level parallelism
-    uint32_t ka = 0, kb = 0, inv = 0;
+    // every start of the lane: key -> id, counted (no pattern: the dummy counter 255); kChains
+    // independent key chains (starts q*64/kChains ..) for instruction-level parallelism
+    constexpr int kChains = EPSM_CG_CHAINS;
+    constexpr int kPer = kSeg / kChains;
+    uint32_t kc[kChains], inv = 0;
 #pragma unroll
-    for (int t = 0; t < kSeg / 2 + M - 1; ++t) {
-      const int tb = t + kSeg / 2;
-      const uint32_t ba = __byte_perm(W[t >> 2], 0u, 0x4440u | (t & 3));
-      const uint32_t bb = __byte_perm(W[tb >> 2], 0u, 0x4440u | (tb & 3));
-      const uint32_t ca = IDENT ? ba : S.cmap[ba];
-      const uint32_t cbb = IDENT ? bb : S.cmap[bb];
-      inv |= ca | cbb;
-      ka = ((ka << cb) | ca) & kmask;
-      kb = ((kb << cb) | cbb) & kmask;
+    for (int q = 0; q < kChains; ++q) kc[q] = 0;
+#pragma unroll
+    for (int t = 0; t < kPer + M - 1; ++t) {
+#pragma unroll
+      for (int q = 0; q < kChains; ++q) {
+        const int tq = t + q * kPer;
+        const uint32_t bq = __byte_perm(W[tq >> 2], 0u, 0x4440u | (tq & 3));
+        const uint32_t cq = IDENT ? bq : S.cmap[bq];
+        inv |= cq;
+        kc[q] = ((kc[q] << cb) | cq) & kmask;
+      }
       if (t >= M - 1) {
-        atomicAdd(&h[S.tab[ka]], 1u);
-        atomicAdd(&h[S.tab[kb]], 1u);
+#pragma unroll
+        for (int q = 0; q < kChains; ++q) atomicAdd(&h[S.tab[kc[q]]], 1u);
       }
     }
     // undo the starts that do not count: outside [s_lo, s_hi) (the text's ends) or whose window
