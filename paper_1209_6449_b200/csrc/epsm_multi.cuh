@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       const uint32_t c = WRITE ? P.work[1 + w] : w;
       uint32_t len = 0;
       if (WRITE) len = P.listlen[c];
-      mbar_wait(&S.empty[stage], phase ^ 1u);
+      mbar_wait_sleep(&S.empty[stage], phase ^ 1u, 256);
       if (WRITE && len <= static_cast<uint32_t>(kListCap)) {
         // a sparse chunk: its occurrences were listed by pass 1; the text is not needed
         if (lane == 0) {
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         phase ^= 1u;
       }
     }
-    mbar_wait(&S.empty[stage], phase ^ 1u);
+    mbar_wait_sleep(&S.empty[stage], phase ^ 1u, 256);
     if (lane == 0) {
       S.info[stage] = kEnd;
       mbar_arrive(&S.full[stage]);
@@ -557,13 +557,15 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
     }
     // this lane's matches: count and exclusive offset among the warp slice's (text order)
     const uint32_t cl = static_cast<uint32_t>(__popcll(static_cast<long long>(M)));
-    uint32_t incl = cl;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= static_cast<uint32_t>(o)) incl += y;
+    uint32_t incl = cl, T = 0;
+    if (__any_sync(0xffffffffu, cl != 0)) {                       // (most slices of a sparse group:
+#pragma unroll                                                    // none -- no scan chain)
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
+      }
+      T = __shfl_sync(0xffffffffu, incl, 31);                     // matches of the slice
     }
-    const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);       // matches of the slice
     uint8_t* const idl = ids + lane * kIdsLane;
 
     if constexpr (!WRITE) {
