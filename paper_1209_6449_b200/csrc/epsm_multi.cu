@@ -503,6 +503,8 @@ static int subgroup_launch(epsm_group_t* g, Subgroup& S, const uint8_t* d_text, 
   P.kmask = S.sk <= 0 ? (1u << (g->m * S.cb)) - 1u : 0u;
   P.mmask = S.sk <= 0 ? (1u << g->m) - 1u : 0u;
   P.spare = S.sk <= 0 && S.spare ? 1u : 0u;
+  P.ident = S.sk == 0 && S.ident ? 1u : 0u;
+  P.identmask = 0xFFu & ~((1u << S.cb) - 1u);
   // direct counting in pass 1 only where the chunks would overflow their lists anyway (> 256
   // expected matches per 32 KiB chunk); sparser groups keep the lists (pass 3 without the text)
   P.direct = (S.sk <= 0 && g->sparse_rate * mp::kTile > static_cast<double>(mp::kListCap)) ? 1u : 0u;

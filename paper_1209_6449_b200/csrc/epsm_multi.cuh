@@ -103,6 +103,9 @@ struct MParams {
   uint32_t kmask;               // code mode: 2^(m * cb) - 1
   uint32_t mmask;               // code mode: 2^m - 1
   uint32_t spare;               // code mode: bytes outside the alphabet map to a spare code
+  uint32_t ident;               // code mode: every pattern byte < 2^cb is its own code; a byte
+                                // with a bit in identmask (at or above cb) is outside the alphabet
+  uint32_t identmask;
   uint32_t direct;              // code mode, pass 1: count in the scan, no lists (dense groups: the
                                 // chunks overflow their lists anyway and pass 3 re-filters them)
   uint32_t hmul[4];             // key word multipliers of the sample hash
@@ -246,7 +249,7 @@ __device__ __forceinline__ uint32_t code_lookup(const GroupDesc& G, uint32_t key
   }
 }
 
-template <bool DIRECT, bool WIDE, bool SPARE>
+template <bool DIRECT, bool WIDE, bool SPARE, bool IDENT>
 __device__ __forceinline__ uint64_t code_scan_t(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
                                                 uint8_t* idb, uint32_t* cc) {
   const uint32_t m1 = P.m - 1, cb = P.cb, kmask = P.kmask;
@@ -255,14 +258,15 @@ __device__ __forceinline__ uint64_t code_scan_t(const uint32_t (&W)[20], const G
   uint8_t* const ids0 = idb - m1;                // id slot of the start closed by byte t: ids0[t]
 #pragma unroll
   for (int t = 0; t < 80; ++t) {
-    const uint32_t cm = G.cmap[(W[t >> 2] >> (8 * (t & 3))) & 0xFFu];
+    const uint32_t by = (W[t >> 2] >> (8 * (t & 3))) & 0xFFu;
+    const uint32_t cm = IDENT ? by : G.cmap[by];   // (IDENT: the byte is its own code, no load)
     key = ((key << cb) | cm) & kmask;
     uint32_t d;
     if constexpr (SPARE) {
       // bytes outside the alphabet have the spare code: no pattern key holds it (table: 0xFF)
       d = code_lookup<WIDE>(G, key);
     } else {
-      if (cm & 0x80u) last_inv = t;              // (its 0x80 leaves the key within m bytes)
+      if (cm & (IDENT ? P.identmask : 0x80u)) last_inv = t;   // (its high bits leave the key within m bytes)
       d = (t - last_inv > static_cast<int>(m1)) ? code_lookup<WIDE>(G, key) : 0xFFu;
     }
     const uint32_t s0 = static_cast<uint32_t>(t) - m1;
@@ -289,7 +293,9 @@ __device__ __forceinline__ uint64_t code_scan_t(const uint32_t (&W)[20], const G
 template <bool DIRECT, bool WIDE>
 __device__ __forceinline__ uint64_t code_scan(const uint32_t (&W)[20], const GroupDesc& G, const MParams& P,
                                               uint8_t* idb, uint32_t* cc) {
-  return P.spare ? code_scan_t<DIRECT, WIDE, true>(W, G, P, idb, cc) : code_scan_t<DIRECT, WIDE, false>(W, G, P, idb, cc);
+  if (P.ident) return code_scan_t<DIRECT, WIDE, false, true>(W, G, P, idb, cc);
+  return P.spare ? code_scan_t<DIRECT, WIDE, true, false>(W, G, P, idb, cc)
+                 : code_scan_t<DIRECT, WIDE, false, false>(W, G, P, idb, cc);
 }
 
 template <int SK, int QW, bool WRITE>
