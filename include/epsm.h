@@ -433,6 +433,20 @@ const char *epsm_last_error(void);
  * of the library's kernels ran in a timed region. */
 uint64_t epsm_launch_count(void);
 
+/* epsm_ktimer_enable -- benchmark instrumentation of the dominant kernel (the
+ * positions fan-out, epsm_replicate_multi_kernel: DESIGN.md section 6).  While on
+ * (on != 0), every launch of that kernel is bracketed by two CUDA events recorded on
+ * the stream it is launched on, and its jobs (source occ pointer and capacity, the
+ * outputs' capacities) are kept on the host.  Off by default; returns EPSM_OK. */
+int epsm_ktimer_enable(int on);
+
+/* epsm_ktimer_read -- waits for the recorded launches, then returns (each pointer may
+ * be NULL) their number, the sum of their event-timed durations in ms, and their
+ * algorithmic bytes: per job 8 * min(occ, cap) read once plus 8 * min(occ, cap_o)
+ * written per output o, occ read back from the device occ each job names (so those
+ * buffers must still be alive).  Clears the records.  EPSM_ECUDA on a CUDA error. */
+int epsm_ktimer_read(uint64_t *launches, double *ms, double *bytes);
+
 /* epsm_version -- ABI version (major * 10000 + minor * 100 + patch). */
 int epsm_version(void);
 

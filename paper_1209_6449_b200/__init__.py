@@ -8,7 +8,7 @@ from ._lib import (  # noqa: F401
     EPSM_EALIGN, EPSM_ECUDA, EPSM_EINVAL, EPSM_ENCCL, EPSM_ENOMEM, EPSM_EUNSUP, EPSM_OK,
     EXPORTED_SYMBOLS, INDEX_MAX_D, Group, group, LIB_PATH, MAX_M, MAX_M_LONG, MAX_PLANES, EpsmError, EqIndex, Plan, count,
     eq_index, index_values, count_async, count_batch_async, find_all,
-    debug_trace, launch_count, nccl_comm_ptr, plan, search, search_async, search_batch_async, search_host, search_range_async,
+    debug_trace, ktimer_enable, ktimer_read, launch_count, nccl_comm_ptr, plan, search, search_async, search_batch_async, search_host, search_range_async,
     search_range_batch_async, search_text_host, allgatherv_async,
     search_sharded, strerror, version,
 )

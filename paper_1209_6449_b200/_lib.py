@@ -68,6 +68,10 @@ _lib.epsm_last_error.argtypes = []
 _lib.epsm_last_error.restype = ctypes.c_char_p
 _lib.epsm_launch_count.argtypes = []
 _lib.epsm_launch_count.restype = _u64
+_lib.epsm_ktimer_enable.argtypes = [ctypes.c_int]
+_lib.epsm_ktimer_enable.restype = ctypes.c_int
+_lib.epsm_ktimer_read.argtypes = [ctypes.POINTER(_u64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+_lib.epsm_ktimer_read.restype = ctypes.c_int
 _lib.epsm_version.argtypes = []
 _lib.epsm_version.restype = ctypes.c_int
 _lib.epsm_debug_trace.argtypes = [_vp, _u64]
@@ -126,6 +130,7 @@ EXPORTED_SYMBOLS = (
     "epsm_search", "epsm_search_async", "epsm_search_batch_async", "epsm_search_range_batch_async", "epsm_count_batch_async",
     "epsm_search_host", "epsm_search_sharded",
     "epsm_search_range_async", "epsm_strerror", "epsm_last_error", "epsm_launch_count",
+    "epsm_ktimer_enable", "epsm_ktimer_read",
     "epsm_version", "epsm_debug_trace",
     "epsm_eqidx_create", "epsm_eqidx_free", "epsm_eqidx_build_async", "epsm_eqidx_values",
     "epsm_search_batch_index_async", "epsm_count_batch_index_async", "epsm_plan_index_values",
@@ -153,6 +158,18 @@ def strerror(code: int) -> str:
 def launch_count() -> int:
     """Kernels libepsm.so has launched in this process so far."""
     return int(_lib.epsm_launch_count())
+
+
+def ktimer_enable(on: bool) -> None:
+    """Bracket every fan-out kernel launch with CUDA events (benchmark instrumentation)."""
+    _check(_lib.epsm_ktimer_enable(1 if on else 0), "epsm_ktimer_enable")
+
+
+def ktimer_read() -> tuple:
+    """(launches, total ms, algorithmic bytes) of the fan-out launches recorded since the last read."""
+    n, ms, b = _u64(0), ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(_lib.epsm_ktimer_read(ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b)), "epsm_ktimer_read")
+    return int(n.value), float(ms.value), float(b.value)
 
 
 def version() -> int:

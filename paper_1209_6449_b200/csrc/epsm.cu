@@ -48,6 +48,23 @@ unsigned long long* trace_slot(int device) {
   return g_trace + (g_launches.load() % g_trace_slots) * kTraceWordsPerLaunch;
 }
 
+// Diagnostics for benchmarks (epsm_ktimer_enable / epsm_ktimer_read): while on, every launch of
+// the fan-out kernel is bracketed by a pair of CUDA events on its own stream, and the launch's
+// jobs are kept so that its algorithmic bytes (source positions read once, every output's
+// positions written) can be summed from the device occ values once the launches are done.
+struct KtJob {
+  const unsigned long long* occ;
+  uint64_t cap;
+  std::vector<uint64_t> out_caps;              // 0: no output buffer
+};
+struct KtRec {
+  cudaEvent_t ev[2];
+  std::vector<KtJob> jobs;
+};
+std::mutex g_kt_mu;
+std::atomic<bool> g_kt_on{false};
+std::vector<KtRec> g_kt_recs;
+
 using KernelFn = void (*)(epsm::KParams);
 
 template <int F, int F2, int MW, int SK = 0, int SQ = 0>
@@ -700,11 +717,31 @@ int epsm_replicate_many(const epsm_rep_req* r, uint32_t nr, const epsm::XOut* d_
     // (a pageable source is staged before cudaMemcpyAsync returns: the vector may go)
     e = cudaMemcpyAsync(dj, jobs.data() + a, nj * sizeof(epsm::RepJobD), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return epsm_cuda_fail(e, "cudaMemcpyAsync(fan-out job table)");
+    KtRec kt{};
+    const bool timed = g_kt_on.load(std::memory_order_relaxed);
+    if (timed) {
+      for (cudaEvent_t& ev : kt.ev)
+        if ((e = cudaEventCreate(&ev)) != cudaSuccess) return epsm_cuda_fail(e, "cudaEventCreate(ktimer)");
+      for (uint32_t j = a; j < a + nj; ++j) {
+        KtJob kj{jobs[j].occ, jobs[j].src ? jobs[j].cap : 0, {}};
+        for (uint32_t o = 0; o < jobs[j].nx; ++o) {
+          const epsm::XOut& X = h_x[jobs[j].x0 + o];
+          kj.out_caps.push_back(X.pos ? X.cap : 0);
+        }
+        kt.jobs.push_back(std::move(kj));
+      }
+      cudaEventRecord(kt.ev[0], s);
+    }
     epsm::epsm_replicate_multi_kernel<<<EPSM_REP_CTAS_PER_SM * ws->num_sms, epsm::kRepThreads,
                                         sizeof(epsm::RepMultiSmem), s>>>(dj, nj, d_x);
     epsm_count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return epsm_cuda_fail(e, "epsm_replicate_multi_kernel launch");
+    if (timed) {
+      cudaEventRecord(kt.ev[1], s);
+      std::lock_guard<std::mutex> lk(g_kt_mu);
+      g_kt_recs.push_back(std::move(kt));
+    }
   }
   return EPSM_OK;
 }
@@ -1428,6 +1465,43 @@ const char* epsm_last_error(void) { return g_last_error; }
 uint64_t epsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int epsm_version(void) { return 200; }
+
+int epsm_ktimer_enable(int on) {
+  g_kt_on.store(on != 0);
+  return EPSM_OK;
+}
+
+int epsm_ktimer_read(uint64_t* launches, double* ms, double* bytes) {
+  std::vector<KtRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    recs.swap(g_kt_recs);
+  }
+  double t = 0.0, b = 0.0;
+  int rc = EPSM_OK;
+  for (KtRec& r : recs) {
+    if (rc == EPSM_OK) {
+      float f = 0.f;
+      cudaError_t e = cudaEventSynchronize(r.ev[1]);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&f, r.ev[0], r.ev[1]);
+      for (size_t j = 0; e == cudaSuccess && j < r.jobs.size(); ++j) {
+        unsigned long long occ = 0;
+        e = cudaMemcpy(&occ, r.jobs[j].occ, sizeof(occ), cudaMemcpyDeviceToHost);
+        const uint64_t have = occ < r.jobs[j].cap ? occ : r.jobs[j].cap;
+        b += 8.0 * static_cast<double>(have);                       // source read once
+        for (uint64_t oc : r.jobs[j].out_caps) b += 8.0 * static_cast<double>(oc < have ? oc : have);
+      }
+      if (e != cudaSuccess) rc = epsm_cuda_fail(e, "epsm_ktimer_read");
+      t += f;
+    }
+    cudaEventDestroy(r.ev[0]);
+    cudaEventDestroy(r.ev[1]);
+  }
+  if (launches) *launches = recs.size();
+  if (ms) *ms = t;
+  if (bytes) *bytes = b;
+  return rc;
+}
 
 int64_t epsm_debug_trace(uint64_t* h_out, uint64_t max_words) {
   if (!g_trace) return 0;

@@ -442,3 +442,40 @@ def test_group_many_fanout_sources(epsm, dev, dense):
         assert np.array_equal(outs[j][:c].cpu().numpy().astype(np.uint64), w[:c]), j
         assert int(outs[j][c]) == -4, j
     g.close()
+
+
+@pytest.mark.parametrize("dense", [0, 64])
+def test_ktimer_fanout_bytes(epsm, dev, dense):
+    """The benchmark's live timer of the fan-out kernel (epsm_ktimer_*): with every distinct
+    pattern asked k times (outputs 16-byte aligned, capacities >= occ), the recorded algorithmic
+    bytes are exactly sum over patterns of 8 * occ * k (the source read once, k - 1 copies
+    written), occ from the oracle; the records clear on read and nothing is recorded while off."""
+    rng = np.random.default_rng(77 + dense)
+    n = 11 * TILE + 45
+    t = rng.integers(0, 8, size=n, dtype=np.uint8)
+    distinct = [t[s:s + 3].tobytes() for s in (5, 900, 4000, 70000)]
+    ks = [3, 2, 5, 1]
+    pats = [p for p, k in zip(distinct, ks) for _ in range(k)]
+    wants = {p: oracle.search(p, t) for p in distinct}
+    td = torch.from_numpy(t).to(dev)
+    g = epsm.group(pats).set_dense(dense)
+    outs = [torch.full((wants[p].size + 8,), -4, dtype=torch.int64, device=dev) for p in pats]
+    occ = torch.full((len(pats),), -1, dtype=torch.int64, device=dev)
+    epsm.ktimer_read()
+    g.search_async(td, occ, outs=outs)                       # (timer off: not recorded)
+    torch.cuda.synchronize()
+    assert epsm.ktimer_read() == (0, 0.0, 0.0)
+    epsm.ktimer_enable(True)
+    try:
+        g.search_async(td, occ, outs=outs)
+        torch.cuda.synchronize()
+    finally:
+        epsm.ktimer_enable(False)
+    nl, ms, byts = epsm.ktimer_read()
+    for j, p in enumerate(pats):
+        assert int(occ[j]) == wants[p].size
+        assert np.array_equal(outs[j][:wants[p].size].cpu().numpy().astype(np.uint64), wants[p])
+    assert nl >= 1 and ms > 0.0
+    assert byts == sum(8.0 * wants[p].size * k for p, k in zip(distinct, ks) if k > 1)
+    assert epsm.ktimer_read() == (0, 0.0, 0.0)
+    g.close()

@@ -13,7 +13,7 @@ lines = [ln for ln in open(src) if ln.startswith('"')]
 rows = collections.OrderedDict()
 for r in csv.DictReader(lines):
     rows.setdefault((r["ID"], r["Kernel Name"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
-agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0])   # launches, time, read, write, launches > 1 MB
 with open(out_path, "w") as out:
     out.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
               "--clock-control none (cold-cache, serialised launches: shares, not absolutes)\n")
@@ -29,6 +29,7 @@ with open(out_path, "w") as out:
         a[1] += t
         a[2] += rd
         a[3] += wr
+        a[4] += 1 if rd + wr > 1e6 else 0
     tot = sum(a[1] for a in agg.values())
     out.write("\n# per kernel (repo kernels only)\n")
     summ = {"source": out_path, "kernels": {}}
@@ -36,11 +37,15 @@ with open(out_path, "w") as out:
         out.write(f"# {k}: launches {a[0]}, {a[1] / 1e6:.2f} ms ({100 * a[1] / tot:.1f}%), DRAM {a[2] / 1e9:.2f} GB "
                   f"read + {a[3] / 1e9:.2f} GB written, {(a[2] + a[3]) / a[0] / 1e6:.1f} MB per launch\n")
         summ["kernels"][k] = {"launches": a[0], "share": round(a[1] / tot, 4),
-                              "dram_bytes_per_launch": int((a[2] + a[3]) / a[0])}
+                              "dram_bytes_per_launch": int((a[2] + a[3]) / a[0]),
+                              # (launches that moved > 1 MB: the step's launches, not the empty
+                              # fan-outs of the bench's small warm-up / parity calls)
+                              "dram_bytes_per_busy_launch": int((a[2] + a[3]) / max(a[4], 1)), "busy_launches": a[4]}
 dom = max(summ["kernels"].items(), key=lambda x: x[1]["share"])
 summ["dominant"] = dom[0]
-summ["dram_bytes_per_launch"] = dom[1]["dram_bytes_per_launch"]
-summ["unit"] = "DRAM bytes (read + write) per launch of the dominant kernel (" + dom[0] + "), ncu launch list of the bench"
+summ["dram_bytes_per_launch"] = dom[1]["dram_bytes_per_busy_launch"]
+summ["unit"] = ("DRAM bytes (read + write) per launch of the dominant kernel (" + dom[0] + "), ncu launch list of "
+                "the bench, over its launches that moved > 1 MB")
 if tj:
     json.dump(summ, open(tj, "w"), indent=1)
 print(open(out_path).read().split("# per kernel")[1])
