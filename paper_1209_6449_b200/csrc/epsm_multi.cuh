@@ -42,6 +42,9 @@ namespace mp {
 constexpr int kTile = 32768;                      // bytes per chunk (one TMA stage)
 constexpr int kHalo = 32;                         // >= m - 1 (m <= 32)
 constexpr int kStageBytes = kTile + 128;          // tile + halo + unaligned-read slack
+#ifndef EPSM_MULTI_HALO_LDS
+#define EPSM_MULTI_HALO_LDS 1                        // lane's bytes 64..79 loaded, not shuffled
+#endif
 constexpr int kStages = 4;
 constexpr int kConsumerWarps = 16;
 constexpr int kThreads = 32 + 32 * kConsumerWarps;   // producer warp + consumers
@@ -442,6 +445,15 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           W[4 * r + 3] = v.w;
         }
         // bytes 64..79: the next lane's first 16 (lane 31: the next slice / the tile halo)
+#if EPSM_MULTI_HALO_LDS
+        {                                   // (one more independent load: no shuffle waiting on
+          const uint4 v = src[4];           // the first load on every sample chain)
+          W[16] = v.x;
+          W[17] = v.y;
+          W[18] = v.z;
+          W[19] = v.w;
+        }
+#else
 #pragma unroll
         for (int r = 0; r < 4; ++r) W[16 + r] = __shfl_down_sync(0xffffffffu, W[r], 1);
         if (lane == 31) {
@@ -451,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
           W[18] = v.z;
           W[19] = v.w;
         }
+#endif
       }
       if constexpr (SK <= 0) {
         // ---- code mode (dense groups, small pattern alphabets): every start keyed exactly.
