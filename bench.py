@@ -509,16 +509,19 @@ def run_epsm(args, world, rank, local):
             for ti in ixs:
                 us = gev[("ix", ti)][0].elapsed_time(gev[("ix", ti)][1]) * 1e3
                 nb = texts[ti][5].numel()
-                rows.append([texts[ti][0], 0, round(us, 1), None, round(nb * (1 + len(ixv[ti]) / 8) / (us * 1e-6) / 1e9, 1),
-                             len(ixv[ti]), 0])
+                mg = nb * (1 + len(ixv[ti]) / 8) / (us * 1e-6) / 1e9
+                rows.append([texts[ti][0], 0, round(us, 1), None, round(mg, 1), len(ixv[ti]), 0,
+                             round(mg / hbm_peak, 3)])
             for gi, (ti, m, g, plans) in enumerate(G):
                 us = gev[gi][0].elapsed_time(gev[gi][1]) * 1e3
                 nb = texts[ti][5].numel()
                 dense = sum(g.dense_searches()) if args.mode == "group" else None
+                mg = rows_moved[gi] / (us * 1e-6) / 1e9
                 rows.append([texts[ti][0], m, round(us, 1), round(P * nb / (us * 1e-6) / 1e9, 1),
-                             round(rows_moved[gi] / (us * 1e-6) / 1e9, 1), dense, int(occ_l[gi].sum())])
+                             round(mg, 1), dense, int(occ_l[gi].sum()), round(mg / hbm_peak, 3)])
             breakdown = {"cols": ["sigma", "m (0: index build)", "us per group of searches", "text_GBps",
-                                  "moved_GBps", "dense searches (0: index values)", "positions"], "rows": rows}
+                                  "moved_GBps", "dense searches (0: index values)", "positions",
+                                  "moved_frac (moved_GBps / peak)"], "rows": rows}
         else:
             sc = sum(e[0].elapsed_time(e[1]) for e in pev)
             cc = sum(e[1].elapsed_time(e[2]) for e in pev)
