@@ -42,6 +42,12 @@ namespace mp {
 constexpr int kTile = 32768;                      // bytes per chunk (one TMA stage)
 constexpr int kHalo = 32;                         // >= m - 1 (m <= 32)
 constexpr int kStageBytes = kTile + 128;          // tile + halo + unaligned-read slack
+#ifndef EPSM_MULTI_ROT
+#define EPSM_MULTI_ROT 1                             // lane-rotated piece loads of one-word grams
+#endif
+#ifndef EPSM_BLOOM_PRED
+#define EPSM_BLOOM_PRED 1                            // second Bloom probe only where the first hit
+#endif
 #ifndef EPSM_MULTI_HALO_LDS
 #define EPSM_MULTI_HALO_LDS 1                        // lane's bytes 64..79 loaded, not shuffled
 #endif
@@ -173,6 +179,24 @@ __device__ __forceinline__ uint32_t lds_u32_any(const uint8_t* base, uint32_t of
 // the second probe of the sample bitmap: a remix of the gram hash (host and device alike)
 __host__ __device__ __forceinline__ uint32_t bloom2(uint32_t h) { return (h ^ (h >> 15)) * 0x2C1B3C6Du; }
 
+// a shared-memory word loaded only by the lanes with pred != 0 (0 elsewhere): the inactive
+// lanes of the LDS take no bank cycles
+__device__ __forceinline__ uint32_t lds_pred(const uint32_t* p, uint32_t pred) {
+  uint32_t v = 0;
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+      : "+r"(v) : "r"(a), "r"(pred));
+  return v;
+}
+
+// The sample filter's bit for gram hash h: two-probe (Bloom) test, both bits set for every
+// table gram (false positives D*SK/2^16 -> (that)^2: one warp in ~3 instead of every warp walks
+// a bucket per chunk); q <= 2 (bloom2 off): the key itself, one exact probe.  The second probe
+// is loaded only by the lanes whose first probe hit (a few per warp: the random first probes
+// cost ~4 bank cycles per warp, the second ~1).
+// (plain shifts, not the volatile shf asm of __funnelshift_r: the samples' chains interleave)
+__device__ __forceinline__ uint32_t sample_bit(uint32_t h, const GroupDesc& G, const MParams& P);
+
 template <int QW>
 __device__ __forceinline__ uint32_t hash_words(const uint32_t (&k)[4], const MParams& P) {
   uint32_t h = k[0] * P.hmul[0];
@@ -212,6 +236,20 @@ static_assert(sizeof(MSmemT<false>) <= 232448 && sizeof(MSmemT<true>) <= 232448,
               "group kernel fits 227 KB of shared memory");
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 constexpr uint32_t kInfoList = 0x80000000u;
+
+__device__ __forceinline__ uint32_t sample_bit(uint32_t h, const GroupDesc& G, const MParams& P) {
+  uint32_t bit = G.bitmap[h >> (32 - kBitmapLog + 5)] >> ((h >> (32 - kBitmapLog)) & 31u);
+  if (P.bloom2) {
+    const uint32_t h2 = bloom2(h);
+#if EPSM_BLOOM_PRED
+    const uint32_t bw2 = lds_pred(&G.bitmap[h2 >> (32 - kBitmapLog + 5)], bit & 1u);
+#else
+    const uint32_t bw2 = G.bitmap[h2 >> (32 - kBitmapLog + 5)];
+#endif
+    bit &= bw2 >> ((h2 >> (32 - kBitmapLog)) & 31u);
+  }
+  return bit & 1u;
+}
 
 // Naive check of the window at stage offset st against distinct pattern d.
 __device__ __forceinline__ bool verify_window(const uint8_t* ts, uint32_t st, const GroupDesc& G, uint32_t d,
@@ -500,8 +538,33 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
       constexpr int NS = Geo<SK>::kSamples;
       uint64_t hits = 0;
       uint32_t hit64 = 0;                         // the sample at offset 64 (SK > 1)
+      // one-word grams at whole-word strides (q <= 4, SK = 4, 8, 16): the lane reads its four
+      // 16-byte pieces in a lane-rotated order (piece (r + lane/2) mod 4 at step r), so a
+      // quarter-warp's loads hit distinct bank groups instead of one (64-byte lane stride:
+      // 16-way conflicted 32-bit loads); the sample at byte 64 is the next lane's sample 0
+      constexpr bool kRot = EPSM_MULTI_ROT && QW == 1 && SK >= 4 && SK <= 16;
+      if constexpr (kRot) {
+        constexpr int PER = 16 / (kRot ? SK : 16);   // samples per 16-byte piece
+        const uint32_t rot = (lane >> 1) & 3u;
+        const uint8_t* lp = ts + seg;
 #pragma unroll
-      for (int j = 0; j < NS; ++j) {
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t pc = (static_cast<uint32_t>(r) + rot) & 3u;
+          const uint4 v = *reinterpret_cast<const uint4*>(lp + 16u * pc);
+          const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const uint32_t key = vw[u * (SK / 4)] & P.qmask;
+            hits |= static_cast<uint64_t>(sample_bit(key * P.hmul[0], G, P)) << (pc * PER + u);
+          }
+        }
+        // the sample at byte 64: the next lane's sample 0 (lane 31: the next slice / the halo)
+        uint32_t b64 = __shfl_down_sync(0xffffffffu, static_cast<uint32_t>(hits & 1u), 1);
+        if (lane == 31) b64 = sample_bit((*reinterpret_cast<const uint32_t*>(lp + 64) & P.qmask) * P.hmul[0], G, P);
+        hits |= static_cast<uint64_t>(b64) << (4 * PER);
+      }
+#pragma unroll
+      for (int j = 0; j < (kRot ? 0 : NS); ++j) {
         // key words r < QW at the compile-time byte offset j * SK + 4r of the lane's registers
         uint32_t k[4];
 #pragma unroll
@@ -516,14 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) epsm_multi_kernel(const __grid_co
         // two-probe (Bloom) test: both bits set for every table gram (false positives
         // D*SK/2^16 -> (that)^2: one warp in ~3 instead of every warp walks a bucket per chunk)
         // (plain shifts, not the volatile shf asm of __funnelshift_r: the samples' chains interleave)
-        const uint32_t bw = G.bitmap[h >> (32 - kBitmapLog + 5)];
-        uint32_t bit = bw >> ((h >> (32 - kBitmapLog)) & 31u);
-        if (P.bloom2) {                           // (q <= 2: the key itself, exact already)
-          const uint32_t h2 = bloom2(h);
-          const uint32_t bw2 = G.bitmap[h2 >> (32 - kBitmapLog + 5)];
-          bit &= bw2 >> ((h2 >> (32 - kBitmapLog)) & 31u);
-        }
-        bit &= 1u;
+        const uint32_t bit = sample_bit(h, G, P);
         if (j < 64) hits |= static_cast<uint64_t>(bit) << j;
         else hit64 = bit;
       }
