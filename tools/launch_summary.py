@@ -1,7 +1,7 @@
 """Summarise an ncu launch list of bench.py (--metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --csv): per-launch lines of the repo's kernels, per-kernel shares, and
 profiles/traffic.json (DRAM bytes per launch of the dominant kernel, read by bench.py).
-usage: python tools/launch_summary.py launches.csv out.txt [traffic.json]"""
+usage: [LAST_N=n] python tools/launch_summary.py launches.csv out.txt [traffic.json]"""
 import collections
 import csv
 import json
@@ -13,6 +13,11 @@ lines = [ln for ln in open(src) if ln.startswith('"')]
 rows = collections.OrderedDict()
 for r in csv.DictReader(lines):
     rows.setdefault((r["ID"], r["Kernel Name"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+# LAST_N=<n>: keep only the last n launches of the repo's kernels (the steps, not the setup's sizing pass)
+import os
+if os.environ.get("LAST_N"):
+    keep = [k for k in rows if "epsm" in k[1] or "cg::" in k[1]][-int(os.environ["LAST_N"]):]
+    rows = collections.OrderedDict((k, rows[k]) for k in keep)
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0])   # launches, time, read, write, launches > 1 MB
 with open(out_path, "w") as out:
     out.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
